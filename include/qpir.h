@@ -1,0 +1,133 @@
+/*
+ * qpir.h -- C ABI of the B200-native LWE-PIR answer engine (libqpir.so).
+ *
+ * The server side of the PIR of QPADL (arXiv 2510.03631) read as a Regev-LWE
+ * PIR (R1): the spectrum database is a matrix D over Z_p (p = 2^8,
+ * one record byte per entry), a client query is qu in Z_q^m (q = 2^32), and
+ *   answer        ans = D . qu            mod 2^32   (Def. 1 "DB.Query.Response",
+ *                                                     PAPER.md:241; Alg. 1 step 18,
+ *                                                     PAPER.md:591)
+ *   batch answer  ANS = D . Q             mod 2^32   (multi-request form, Alg. 3/4,
+ *                                                     PAPER.md:981)
+ *   hint          H   = D . A             mod 2^32   (offline precomputation,
+ *                                                     PAPER.md:1091-1092; DESIGN R7)
+ * All arithmetic is exact in Z_{2^32} (u32 wrap-around), so every result has a
+ * unique correct value and is bit-identical across GPUs, shards, split factors
+ * and streams.
+ *
+ * Conventions (SPEC.md:204 little-endian u32 elements; SPEC.md:93 DB immutable
+ * after build; SPEC.md:248 output independent of worker count):
+ *   - Geometry (DESIGN R9/R10): theta = cell * n_ch + ch indexes the N =
+ *     n_cells * n_ch records of rec_bytes = d bytes each.  blk = cell / m,
+ *     col = cell % m, row = (blk * n_ch + ch) * d + b holds byte b of record
+ *     theta; ell = ceil(n_cells / m) * n_ch * d rows.  A context owns the row
+ *     shard [row_begin, row_end) of [0, ell) ("ell_local" rows).
+ *   - Buffers: every pointer argument may be host memory (pageable or pinned)
+ *     or device memory of the context's device; the library detects which with
+ *     cudaPointerGetAttributes.  The caller owns every buffer it passes; the
+ *     context owns its device copy of the D shard and its scratch.
+ *   - Lengths: every buffer comes with its element count, which must match the
+ *     geometry exactly, else QPIR_E_DIMENSION and nothing is written.
+ *   - Streams: `stream` is a cudaStream_t (NULL = legacy default stream).  Work
+ *     is enqueued on it.  If any output is host memory the call synchronises
+ *     the stream before returning; with device outputs it returns immediately.
+ *   - Concurrency: calls on one context are serialised by the caller (one
+ *     stream per context); distinct contexts are independent.  The D shard is
+ *     never modified by the answer/hint calls.
+ *   - Errors: functions return QPIR_OK (0) or a QPIR_E_* code; no partial
+ *     outputs on error.  qpir_last_error(ctx) (or qpir_last_error(NULL) for a
+ *     failed qpir_setup) names the offending field, e.g. "m: 8191 != 8192".
+ *
+ * The cross-GPU gather of answer slices is not part of this ABI: each rank
+ * calls it on its own shard and the Python layer gathers over NCCL.
+ */
+#ifndef QPIR_H
+#define QPIR_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define QPIR_OK 0
+#define QPIR_E_PARAM 1     /* unsupported parameter (log_q, log_p, lwe_n, ...) */
+#define QPIR_E_DIMENSION 2 /* a length or the shard geometry does not match     */
+#define QPIR_E_STATE 3     /* call not valid in the context's state             */
+#define QPIR_E_OOM 4       /* device or host allocation failed                  */
+#define QPIR_E_CUDA 5      /* a CUDA runtime call failed (message has details)  */
+
+typedef struct qpir_ctx qpir_ctx;
+
+typedef struct {
+  uint64_t n_cells;   /* location cells (grid (l_x, l_y) flattened) */
+  uint64_t n_ch;      /* channels per cell                                        */
+  uint64_t rec_bytes; /* d: bytes per record (3072 for paper-shaped records)      */
+  uint64_t m;         /* DB columns; 0 means m = n_cells                          */
+  uint32_t lwe_n;     /* LWE dimension n (width of the hint), 1..65536            */
+  uint32_t log_q;     /* must be 32 (q = 2^32, DESIGN R2)                          */
+  uint32_t log_p;     /* must be 8  (p = 2^8,  DESIGN R3)                          */
+  uint32_t reserved0; /* must be 0                                                */
+  uint64_t seed_A;    /* public-matrix seed: A[c][j] = Philox4x32-10(key = seed_A,
+                         ctr = (c, j >> 2, 0, 0x41))[j & 3]  (DESIGN R7)          */
+  uint64_t row_begin; /* this context's shard [row_begin, row_end) of [0, ell);   */
+  uint64_t row_end;   /* row_end = 0 means ell (the whole matrix)                 */
+  int32_t device;     /* CUDA device ordinal                                      */
+  int32_t reserved1;  /* must be 0                                                */
+} qpir_params;
+
+/* Create a context on params->device holding the D shard.  `records` is the
+ * full theta-ordered record array (n_cells * n_ch * rec_bytes bytes, host or
+ * device) or NULL for an all-zero DB to be filled with qpir_db_write.  Only the
+ * records that land in the shard are read.  On success *out owns the device
+ * memory; release it with qpir_destroy.  Parameters are validated before any
+ * CUDA call (QPIR_E_PARAM / QPIR_E_DIMENSION without touching the device).
+ * Setup step a1 "DB pack" (DB.Record). */
+int qpir_setup(const qpir_params *params, const uint8_t *records,
+               uint64_t records_len, void *stream, qpir_ctx **out);
+
+/* Write records theta_begin .. theta_begin + n_records - 1 (n_records * d
+ * bytes, theta order, host or device) into the shard; records outside the
+ * shard's rows are skipped.  Lets a caller stream a DB larger than host or
+ * device memory in chunks.  Not to be called concurrently with answers. */
+int qpir_db_write(qpir_ctx *ctx, uint64_t theta_begin, uint64_t n_records,
+                  const uint8_t *records, uint64_t records_len, void *stream);
+
+/* Geometry: ell (all rows), m (columns), ell_local (= row_end - row_begin),
+ * row_begin.  Any output pointer may be NULL. */
+int qpir_geometry(const qpir_ctx *ctx, uint64_t *ell, uint64_t *m,
+                  uint64_t *ell_local, uint64_t *row_begin);
+
+/* Single query (step a3):
+ *   ans_local[i] = sum_{c < m} D[row_begin + i][c] * qu[c]  mod 2^32.
+ * qu: m u32 (len must equal m).  ans_local: ell_local u32 (len == ell_local). */
+int qpir_answer(qpir_ctx *ctx, const uint32_t *qu, uint64_t len_qu,
+                uint32_t *ans_local, uint64_t len_ans, void *stream);
+
+/* Batch of B queries (step a6):
+ *   ans_local[b * ell_local + i] = sum_c D[row_begin + i][c] * Q[b * m + c] mod 2^32.
+ * Q: B x m u32 query-major (len == B * m); ans_local: B x ell_local (len ==
+ * B * ell_local).  1 <= B <= 4096. */
+int qpir_answer_batch(qpir_ctx *ctx, const uint32_t *Q, uint64_t B,
+                      uint64_t len_Q, uint32_t *ans_local, uint64_t len_ans,
+                      void *stream);
+
+/* Hint (step a7): H_local[i * n + j] = sum_c D[row_begin + i][c] * A[c][j]
+ * mod 2^32 with A expanded from seed_A on the device (n = lwe_n).  H_local:
+ * ell_local x n row-major (len == ell_local * n). */
+int qpir_hint(qpir_ctx *ctx, uint32_t *H_local, uint64_t len_H, void *stream);
+
+/* Number of kernels this context has launched so far (for launch accounting). */
+uint64_t qpir_kernel_launches(const qpir_ctx *ctx);
+
+/* Last error message of ctx, or of the calling thread's last failed
+ * qpir_setup when ctx is NULL.  Never NULL; "" if no error. */
+const char *qpir_last_error(const qpir_ctx *ctx);
+
+/* Free the context and its device memory (NULL is a no-op). */
+void qpir_destroy(qpir_ctx *ctx);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* QPIR_H */

@@ -1,0 +1,276 @@
+/*
+ * qpir_oracle.c -- plain, slow, obviously-correct CPU oracle for the LWE-PIR
+ * answer path of QPADL (arXiv 2510.03631).
+ *
+ * TEST INFRASTRUCTURE ONLY.  Nothing on the product path may link, load or
+ * call this file: only tests/, __graft_entry__.smoke() and bench.py's
+ * cpu_baseline / --impl reference legs.  It shares no code with
+ * paper_2510_03631_b200/ (the CUDA path) and includes none of its headers.
+ *
+ * Citation keys: P:NNN = PAPER.md line, S:NNN = SPEC.md line, SURVEY = SURVEY.md
+ * section, DESIGN = DESIGN.md "Readings" table (R1..R12).
+ *
+ * What is computed (plain definitions, DESIGN R1..R12 for everything the paper
+ * leaves open):
+ *   - the PIR response rho <- PIR.Query.Response(q, DB)  (Def. 1, P:241;
+ *     Alg. 1 step 18) read as the LWE answer ans = D.qu mod 2^32,
+ *     which is the same "q.DB mod q" contraction as Alg. 4 steps 14-15
+ *      with the modulus fixed to q = 2^32 (DESIGN R2);
+ *   - the multi-request form (Alg. 3/4 "multiple requests"):
+ *     ANS[b] = D.Q[b] mod 2^32;
+ *   - the offline precomputation (Offline-online mode) read as
+ *     the LWE hint H = D.A mod 2^32 (DESIGN R7);
+ *   - client side (Def. 1 Client.Query / BlockReconst):
+ *     keygen, query, decode of a Regev-LWE PIR (DESIGN R1, R4-R8).
+ *
+ * Every server-side result is the plain modular matrix product in Z_{2^32};
+ * the loops below are the textbook triple loops in uint32_t arithmetic
+ * (unsigned overflow wraps mod 2^32 by the C standard, C11 6.2.5p9).
+ * No blocking, no reordering beyond an OpenMP split over independent rows.
+ *
+ * Pins (tests/test_oracle_*.py): Philox KATs from Random123; numpy/torch
+ * library matmuls; closed forms (unit, all-ones, all-0xFFFFFFFF, constant,
+ * top-limb queries); linearity; the exact LWE identity; brute-force decode of
+ * every record of the tiny DB; the GF(2) link to Chor PIR (Alg. 3).
+ */
+#include <math.h>
+#include <stddef.h>
+#include <stdint.h>
+#include <string.h>
+#ifdef _OPENMP
+#include <omp.h>
+#endif
+
+/* ------------------------------------------------------------------ */
+/* Philox4x32-10 (Salmon, Moraes, Dror, Shaw, SC'11, "Parallel random   */
+/* numbers: as easy as 1, 2, 3", Fig. 2 / Random123 philox.h).          */
+/* DESIGN R7: the LWE public matrix A and all client randomness are     */
+/* drawn from it.                                                       */
+/* ------------------------------------------------------------------ */
+#define PHILOX_M0 0xD2511F53u
+#define PHILOX_M1 0xCD9E8D57u
+#define PHILOX_W0 0x9E3779B9u
+#define PHILOX_W1 0xBB67AE85u
+
+void qo_philox4x32_10(const uint32_t ctr_in[4], const uint32_t key_in[2],
+                      uint32_t out[4]) {
+  uint32_t c0 = ctr_in[0], c1 = ctr_in[1], c2 = ctr_in[2], c3 = ctr_in[3];
+  uint32_t k0 = key_in[0], k1 = key_in[1];
+  for (int round = 0; round < 10; ++round) {
+    if (round > 0) { /* key schedule: bump before every round but the first */
+      k0 += PHILOX_W0;
+      k1 += PHILOX_W1;
+    }
+    uint64_t p0 = (uint64_t)PHILOX_M0 * (uint64_t)c0;
+    uint64_t p1 = (uint64_t)PHILOX_M1 * (uint64_t)c2;
+    uint32_t hi0 = (uint32_t)(p0 >> 32), lo0 = (uint32_t)p0;
+    uint32_t hi1 = (uint32_t)(p1 >> 32), lo1 = (uint32_t)p1;
+    uint32_t n0 = hi1 ^ c1 ^ k0;
+    uint32_t n1 = lo1;
+    uint32_t n2 = hi0 ^ c3 ^ k1;
+    uint32_t n3 = lo0;
+    c0 = n0; c1 = n1; c2 = n2; c3 = n3;
+  }
+  out[0] = c0; out[1] = c1; out[2] = c2; out[3] = c3;
+}
+
+/* Domain tags in ctr[3] (DESIGN R7): 'A' public matrix, 'S' secret, 'E' error. */
+#define QO_DOMAIN_A 0x41u
+#define QO_DOMAIN_S 0x53u
+#define QO_DOMAIN_E 0x45u
+
+static void key_from_seed(uint64_t seed, uint32_t key[2]) {
+  key[0] = (uint32_t)(seed & 0xFFFFFFFFu);
+  key[1] = (uint32_t)(seed >> 32);
+}
+
+/* A[c][j] = Philox(key = seed_A, ctr = (c, j>>2, 0, 'A'))[j & 3]  (DESIGN R7).
+ * A is m x n, row-major (cell-major): A[c*n + j]. */
+void qo_expand_A(uint64_t seed_A, uint64_t m, uint32_t n, uint32_t *A) {
+  uint32_t key[2];
+  key_from_seed(seed_A, key);
+  for (uint64_t c = 0; c < m; ++c) {
+    for (uint32_t j = 0; j < n; ++j) {
+      uint32_t ctr[4] = {(uint32_t)c, j >> 2, 0u, QO_DOMAIN_A};
+      uint32_t out[4];
+      qo_philox4x32_10(ctr, key, out);
+      A[c * (uint64_t)n + j] = out[j & 3u];
+    }
+  }
+}
+
+/* ------------------------------------------------------------------ */
+/* DB layout (DESIGN R9/R10; "DB is modeled as a matrix", S:51  */
+/* row-major DB.Index, P:1107 multiple-block retrieval).              */
+/* theta = cell * n_ch + ch ;  record bytes rec_theta[0..d)            */
+/* blk = cell / m, col = cell % m, row = (blk * n_ch + ch) * d + b     */
+/* ell = ceil(n_cells / m) * n_ch * d.  Unused slots hold 0.           */
+/* ------------------------------------------------------------------ */
+uint64_t qo_ell(uint64_t n_cells, uint64_t n_ch, uint64_t d, uint64_t m) {
+  uint64_t n_blk = (n_cells + m - 1) / m;
+  return n_blk * n_ch * d;
+}
+
+void qo_position(uint64_t n_ch, uint64_t d, uint64_t m, uint64_t theta,
+                 uint64_t b, uint64_t *row, uint64_t *col) {
+  uint64_t cell = theta / n_ch;
+  uint64_t ch = theta % n_ch;
+  uint64_t blk = cell / m;
+  *col = cell % m;
+  *row = (blk * n_ch + ch) * d + b;
+}
+
+/* D is ell x m, row-major, plain (the oracle's own layout). */
+void qo_pack(const uint8_t *records, uint64_t n_cells, uint64_t n_ch,
+             uint64_t d, uint64_t m, uint8_t *D) {
+  uint64_t ell = qo_ell(n_cells, n_ch, d, m);
+  memset(D, 0, (size_t)(ell * m));
+  uint64_t n_rec = n_cells * n_ch;
+  for (uint64_t theta = 0; theta < n_rec; ++theta) {
+    for (uint64_t b = 0; b < d; ++b) {
+      uint64_t row, col;
+      qo_position(n_ch, d, m, theta, b, &row, &col);
+      D[row * m + col] = records[theta * d + b];
+    }
+  }
+}
+
+/* ------------------------------------------------------------------ */
+/* Server side.                                                        */
+/* ------------------------------------------------------------------ */
+
+/* ans[r] = sum_c D[r][c] * qu[c] mod 2^32, r < rows.  (Def. 1 Response,
+ * P:241; Alg. 4 steps 14-15, modulus 2^32 per DESIGN R2.)
+ * D may be any set of rows (rows x m, row-major). */
+void qo_answer(const uint8_t *D, uint64_t rows, uint64_t m, const uint32_t *qu,
+               uint32_t *ans) {
+  int64_t R = (int64_t)rows;
+#pragma omp parallel for schedule(static)
+  for (int64_t r = 0; r < R; ++r) {
+    uint32_t acc = 0;
+    const uint8_t *Dr = D + (uint64_t)r * m;
+    for (uint64_t c = 0; c < m; ++c) acc += (uint32_t)Dr[c] * qu[c];
+    ans[r] = acc;
+  }
+}
+
+/* ANS[b][r] = sum_c D[r][c] * Q[b][c] mod 2^32.  Q is B x m (query-major),
+ * ANS is B x rows (query-major).  Multi-request form. */
+void qo_answer_batch(const uint8_t *D, uint64_t rows, uint64_t m,
+                     const uint32_t *Q, uint64_t B, uint32_t *ANS) {
+  int64_t R = (int64_t)rows;
+#pragma omp parallel for schedule(static)
+  for (int64_t r = 0; r < R; ++r) {
+    const uint8_t *Dr = D + (uint64_t)r * m;
+    for (uint64_t b = 0; b < B; ++b) {
+      const uint32_t *Qb = Q + b * m;
+      uint32_t acc = 0;
+      for (uint64_t c = 0; c < m; ++c) acc += (uint32_t)Dr[c] * Qb[c];
+      ANS[b * rows + (uint64_t)r] = acc;
+    }
+  }
+}
+
+/* H[r][j] = sum_c D[r][c] * A[c][j] mod 2^32.  A is m x n (cell-major), H is
+ * rows x n row-major.  Offline precomputation, DESIGN R7. */
+void qo_hint(const uint8_t *D, uint64_t rows, uint64_t m, const uint32_t *A,
+             uint32_t n, uint32_t *H) {
+  int64_t R = (int64_t)rows;
+#pragma omp parallel for schedule(static)
+  for (int64_t r = 0; r < R; ++r) {
+    const uint8_t *Dr = D + (uint64_t)r * m;
+    for (uint32_t j = 0; j < n; ++j) {
+      uint32_t acc = 0;
+      for (uint64_t c = 0; c < m; ++c) acc += (uint32_t)Dr[c] * A[c * (uint64_t)n + j];
+      H[(uint64_t)r * n + j] = acc;
+    }
+  }
+}
+
+/* ------------------------------------------------------------------ */
+/* Client side (Def. 1 Client.Query / BlockReconst),     */
+/* Regev-LWE with q = 2^32, p = 2^8, Delta = 2^24 (DESIGN R2-R8).      */
+/* ------------------------------------------------------------------ */
+
+/* s[j] = Philox(key = seed_s, ctr = (j>>2, 0, 0, 'S'))[j & 3]: uniform Z_q^n. */
+void qo_keygen(uint64_t seed_s, uint32_t n, uint32_t *s) {
+  uint32_t key[2];
+  key_from_seed(seed_s, key);
+  for (uint32_t j = 0; j < n; ++j) {
+    uint32_t ctr[4] = {j >> 2, 0u, 0u, QO_DOMAIN_S};
+    uint32_t out[4];
+    qo_philox4x32_10(ctr, key, out);
+    s[j] = out[j & 3u];
+  }
+}
+
+/* e_c = round(sigma * z), z = sqrt(-2 ln u1) cos(2 pi u2) (Box-Muller),
+ * u1 = (w0 + 1) / 2^32 in (0, 1], u2 = w1 / 2^32,
+ * (w0, w1) = Philox(key = seed_e, ctr = (c, qidx, 0, 'E'))[0..1].  DESIGN R5. */
+void qo_sample_error(uint64_t seed_e, uint32_t qidx, uint64_t m, double sigma,
+                     int32_t *e) {
+  uint32_t key[2];
+  key_from_seed(seed_e, key);
+  const double two32 = 4294967296.0;
+  const double two_pi = 6.283185307179586476925286766559;
+  for (uint64_t c = 0; c < m; ++c) {
+    uint32_t ctr[4] = {(uint32_t)c, qidx, 0u, QO_DOMAIN_E};
+    uint32_t out[4];
+    qo_philox4x32_10(ctr, key, out);
+    double u1 = ((double)out[0] + 1.0) / two32;
+    double u2 = (double)out[1] / two32;
+    double z = sqrt(-2.0 * log(u1)) * cos(two_pi * u2);
+    e[c] = (int32_t)llround(sigma * z);
+  }
+}
+
+/* qu[c] = (sum_j A[c][j] s[j] + e_c + Delta * [c == col_star]) mod 2^32.
+ * Client.Query(theta) (Def. 1; Alg. 1 step 7), DESIGN R1.
+ * e is written to e_out (may be NULL) so that tests can check the exact
+ * LWE identity.  A: m x n cell-major. */
+void qo_query(const uint32_t *A, uint64_t m, uint32_t n, const uint32_t *s,
+              uint64_t seed_e, uint32_t qidx, double sigma, uint64_t col_star,
+              uint32_t *qu, int32_t *e_out, int32_t *e_scratch) {
+  int32_t *e = e_out ? e_out : e_scratch;
+  qo_sample_error(seed_e, qidx, m, sigma, e);
+  const uint32_t Delta = 1u << 24;
+  for (uint64_t c = 0; c < m; ++c) {
+    uint32_t acc = 0;
+    for (uint32_t j = 0; j < n; ++j) acc += A[c * (uint64_t)n + j] * s[j];
+    acc += (uint32_t)e[c];
+    if (c == col_star) acc += Delta;
+    qu[c] = acc;
+  }
+}
+
+/* BlockReconst (Def. 1) for a set of rows:
+ * x_r = (ans[r] - sum_j H[r][j] s[j]) mod 2^32, out = ((x_r + 2^23) >> 24) & 0xFF.
+ * rows[i] indexes both ans and H (H row-major, n wide).  DESIGN R8. */
+void qo_decode(const uint32_t *ans, const uint32_t *H, uint32_t n,
+               const uint32_t *s, const uint64_t *rows, uint64_t n_rows,
+               uint8_t *out) {
+  for (uint64_t i = 0; i < n_rows; ++i) {
+    uint64_t r = rows[i];
+    uint32_t hs = 0;
+    for (uint32_t j = 0; j < n; ++j) hs += H[r * n + j] * s[j];
+    uint32_t x = ans[r] - hs;
+    out[i] = (uint8_t)(((x + (1u << 23)) >> 24) & 0xFFu);
+  }
+}
+
+/* Threads the OpenMP loops above use (reported as cpu_baseline.cores). */
+int qo_num_threads(void) {
+#ifdef _OPENMP
+  return omp_get_max_threads();
+#else
+  return 1;
+#endif
+}
+
+void qo_set_num_threads(int t) {
+#ifdef _OPENMP
+  if (t > 0) omp_set_num_threads(t);
+#else
+  (void)t;
+#endif
+}
