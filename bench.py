@@ -1,0 +1,463 @@
+#!/usr/bin/env python3
+"""Benchmark of the LWE-PIR answer path (BASELINE.json metric:
+"PIR answer DB-scan GB/s and queries/sec per GPU at 1/2/4/8 B200 vs HBM roof").
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--workload c2|c3|c4-64|c4-256|c5|c1]
+                    [--impl ours|reference] [--no-cpu-baseline]
+    torchrun --nproc-per-node N bench.py --gpus N ...
+
+A step = one pass of the whole hot path over one batch of synthetic input:
+  c2 (default)  single query on the regional 1.007 GB DB (BASELINE.json configs[1]):
+                GEMV kernel (query ingest + scan + reduction fused) [+ NCCL gather, N>1]
+  c3            single query on the 32.2 GB nationwide DB row-sharded over N GPUs
+  c4-64/256     batch of 64/256 queries on the 8.05 GB DB (limb split + tcgen05 GEMM)
+  c5            hint H = D.A (n = 1024) for one rank's shard of the 32 GB DB
+At N > 1, c2 is weak scaling (each rank holds a 40-channel 1.007 GB slice; the
+DB grows with N), c3 is strong scaling (fixed 32.2 GB).
+value = DB bytes scanned by all ranks / max-over-ranks device time.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+import torch
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "PIR answer DB-scan GB/s and queries/sec per GPU at 1/2/4/8 B200 vs HBM roof"
+FALLBACK_HBM_GBS = 6650.0
+FALLBACK_BF16_TFLOPS = 1590.0
+
+WORKLOADS = {
+    "c1": dict(name="tiny SAS DB 1024 cells x 16 ch x 8 B (BASELINE configs[0])",
+               n_cells=1024, n_ch=16, d=8, kind="answer"),
+    "c2": dict(name="regional SAS DB 8192 cells x 40 ch x 3072 B = 1.007 GB, single query "
+                    "(BASELINE configs[1])", n_cells=8192, n_ch=40, d=3072, kind="answer"),
+    "c3": dict(name="nationwide SAS DB 262144 cells x 40 ch x 3072 B = 32.2 GB row-sharded, "
+                    "single query + NCCL gather (BASELINE configs[2])",
+               n_cells=262144, n_ch=40, d=3072, kind="answer"),
+    "c4-64": dict(name="8.05 GB DB (65536 cells x 40 ch x 3072 B), batch of 64 queries "
+                       "(BASELINE configs[3])", n_cells=65536, n_ch=40, d=3072, kind="batch", B=64),
+    "c4-256": dict(name="8.05 GB DB (65536 cells x 40 ch x 3072 B), batch of 256 queries "
+                        "(BASELINE configs[3])", n_cells=65536, n_ch=40, d=3072, kind="batch", B=256),
+    "c5": dict(name="hint D.A, n=1024, one rank's shard of the 32.2 GB DB at G=8 "
+                    "(BASELINE configs[4])", n_cells=262144, n_ch=40, d=3072, kind="hint", n=1024,
+               shard_of=8),
+}
+
+
+def peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        j = json.load(open(p))
+        return j.get("hbm_gbs", FALLBACK_HBM_GBS), j.get("bf16_tflops", FALLBACK_BF16_TFLOPS), \
+            j.get("bf16_tflops_sustained"), "measured"
+    return FALLBACK_HBM_GBS, FALLBACK_BF16_TFLOPS, None, "fallback"
+
+
+# ---------------------------------------------------------------- clocks
+class ClockSampler:
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+    NAMES = ("hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap")
+
+    def __init__(self, gpu_index: int):
+        self.samples = []
+        self.marks = [None, None]
+        try:
+            self.p = subprocess.Popen(
+                ["nvidia-smi", f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                 "-i", str(gpu_index), "-lms", "50"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.p = None
+
+    def _read(self):
+        for line in self.p.stdout:
+            self.samples.append((time.time(), line.strip()))
+
+    def start(self):
+        self.marks[0] = time.time()
+
+    def stop(self):
+        self.marks[1] = time.time()
+        if self.p:
+            time.sleep(0.12)
+            self.p.terminate()
+            try:
+                self.p.wait(timeout=2)
+            except Exception:
+                self.p.kill()
+
+    def summary(self):
+        if not self.p:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        t0, t1 = self.marks
+        rows = [s for (t, s) in self.samples if t0 - 0.06 <= t <= t1 + 0.06] or \
+               [s for (_, s) in self.samples[-3:]]
+        sm, mx, reasons = [], [], set()
+        for r in rows:
+            f = [x.strip() for x in r.split(",")]
+            try:
+                sm.append(float(f[0]))
+                mx.append(float(f[1]))
+            except (ValueError, IndexError):
+                continue
+            for name, v in zip(self.NAMES, f[4:8]):
+                if v.lower().startswith("active"):
+                    reasons.add(name)
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": max(mx) if mx else None,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+# ---------------------------------------------------------------- helpers
+def dist_env():
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return world, rank, local
+
+
+def physical_gpu(local: int) -> int:
+    vis = os.environ.get("CUDA_VISIBLE_DEVICES")
+    if vis:
+        ids = [x for x in vis.split(",") if x.strip()]
+        if local < len(ids) and ids[local].strip().isdigit():
+            return int(ids[local])
+    return local
+
+
+def build_db(P, wl, n_ch_total, row_begin, row_end, seed, device, lwe_n=1024):
+    """Setup (untimed): stream synthetic records, generated on the device in
+    256 MB theta-ordered chunks, into this rank's shard (rows outside the shard
+    are skipped by the pack kernel)."""
+    import synth
+    n_cells, d = wl["n_cells"], wl["d"]
+    s = P.PirServer(n_cells, n_ch_total, d, lwe_n=lwe_n, seed_A=0x5EED, row_begin=row_begin,
+                    row_end=row_end, device=device)
+    n_rec = n_cells * n_ch_total
+    chunk = max(1, (256 << 20) // d)
+    for t0 in range(0, n_rec, chunk):
+        n = min(chunk, n_rec - t0)
+        rec = synth.records(seed, t0, n, d, n_ch_total, device=f"cuda:{device}")
+        s.db_write(t0, rec)
+    torch.cuda.synchronize(device)
+    return s
+
+
+def cpu_baseline_answer(wl, seed, budget_s=12.0):
+    """The oracle as it stands, on a bounded sample: the first 4 channels of the
+    same DB (4 * d rows x n_cells columns), repeated for ~budget_s seconds."""
+    import synth
+    from oracle import oracle as O
+    n_cells, d = wl["n_cells"], wl["d"]
+    n_ch_s = min(4, wl["n_ch"])
+    # theta = cell * n_ch + ch with the FULL n_ch: gather the first n_ch_s channels
+    theta = (torch.arange(n_cells).unsqueeze(1) * wl["n_ch"] + torch.arange(n_ch_s)).reshape(-1)
+    dev = "cuda" if torch.cuda.is_available() else "cpu"
+    rec = synth.records_at(seed, theta.to(dev), d, wl["n_ch"], 512).cpu().numpy()
+    D = O.pack(rec, n_cells, n_ch_s, d, n_cells)
+    qu = synth.uniform_u32_np(seed + 1, (n_cells,))
+    O.answer(D, qu)  # warm
+    t0 = time.perf_counter()
+    reps = 0
+    while True:
+        O.answer(D, qu)
+        reps += 1
+        if time.perf_counter() - t0 >= budget_s:
+            break
+    dt = time.perf_counter() - t0
+    gbs = reps * D.nbytes / dt / 1e9
+    return {"value": round(gbs, 3), "unit": "GB/s", "cores": O.num_threads(), "kind": "oracle",
+            "sample": f"oracle answer over rows of the first {n_ch_s} channels "
+                      f"({D.shape[0]} rows x {D.shape[1]} cells = {D.nbytes / 1e6:.1f} MB), "
+                      f"{reps} repetitions in {dt:.1f} s"}
+
+
+# ---------------------------------------------------------------- reference arm
+def run_reference(args, wl, world, rank):
+    if rank != 0:
+        return
+    import synth  # noqa: F401
+    from oracle import oracle as O
+    cb = None
+    # each step = oracle answer over a bounded sample (first 4 channels)
+    n_cells, d = wl["n_cells"], wl["d"]
+    n_ch_s = min(4, wl["n_ch"])
+    import synth as S
+    theta = (torch.arange(n_cells).unsqueeze(1) * wl["n_ch"] + torch.arange(n_ch_s)).reshape(-1)
+    dev = "cuda" if torch.cuda.is_available() else "cpu"
+    rec = S.records_at(args.seed, theta.to(dev), d, wl["n_ch"], 512).cpu().numpy()
+    D = O.pack(rec, n_cells, n_ch_s, d, n_cells)
+    qu = S.uniform_u32_np(args.seed + 1, (n_cells,))
+    for _ in range(args.warmup):
+        O.answer(D, qu)
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        O.answer(D, qu)
+    dt = time.perf_counter() - t0
+    gbs = args.steps * D.nbytes / dt / 1e9
+    sample = (f"oracle answer over rows of the first {n_ch_s} channels ({D.shape[0]} rows x "
+              f"{D.shape[1]} cells = {D.nbytes / 1e6:.1f} MB) per step")
+    cb = {"value": round(gbs, 3), "unit": "GB/s", "cores": O.num_threads(), "kind": "oracle",
+          "sample": sample}
+    line = {"impl": "reference", "metric": METRIC, "value": round(gbs, 3), "unit": "GB/s",
+            "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": round(dt / args.steps * 1e3, 4), "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "u8xu32->u32 (mod 2^32)",
+            "data": "synthetic", "config": {"workload": wl["name"], "sample": sample},
+            "cpu_baseline": cb,
+            "e2e": {"value": round(gbs, 3), "unit": "GB/s", "h2d_bytes_per_step": 0,
+                    "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+# ---------------------------------------------------------------- our arm
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=None)
+    ap.add_argument("--warmup", type=int, default=None)
+    ap.add_argument("--workload", default="c2", choices=sorted(WORKLOADS))
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--seed", type=int, default=2025)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    args = ap.parse_args()
+    wl = dict(WORKLOADS[args.workload])
+    world, rank, local = dist_env()
+    if args.impl == "reference":
+        args.steps = args.steps or 20
+        args.warmup = args.warmup if args.warmup is not None else 3
+        return run_reference(args, wl, world, rank)
+
+    default_steps = {"answer": 2000, "batch": 50, "hint": 5}[wl["kind"]]
+    if args.workload == "c3":
+        default_steps = 200
+    args.steps = args.steps or default_steps
+    args.warmup = max(3, args.warmup if args.warmup is not None else 10)
+
+    torch.cuda.set_device(local)
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    import paper_2510_03631_b200 as P
+    from paper_2510_03631_b200.dist import gather_answer, shard_rows
+
+    hbm, bf16, bf16_sus, peak_src = peaks()
+    n_cells, d = wl["n_cells"], wl["d"]
+    kind = wl["kind"]
+    # geometry per rank
+    if args.workload in ("c1", "c2", "c4-64", "c4-256") and world > 1:
+        n_ch_total = wl["n_ch"] * world  # weak scaling: 40-channel slice per rank
+        scaling = "weak"
+    else:
+        n_ch_total = wl["n_ch"]
+        scaling = "weak" if world == 1 else "strong"
+    if kind == "hint":
+        shard_world = wl.get("shard_of", 1)
+        r0, r1 = shard_rows(n_cells, n_ch_total, d, n_cells, shard_world, rank % shard_world)
+        scaling = "weak"
+    else:
+        r0, r1 = shard_rows(n_cells, n_ch_total, d, n_cells, world, rank)
+    sizes = [b - a for a, b in (shard_rows(n_cells, n_ch_total, d, n_cells, world, r)
+                                for r in range(world))] if kind != "hint" else None
+
+    t_setup = time.time()
+    srv = build_db(P, wl, n_ch_total, r0, r1, args.seed, local, lwe_n=wl.get("n", 1024))
+    setup_s = time.time() - t_setup
+    ell_local = srv.ell_local
+    db_bytes_local = ell_local * n_cells
+    import synth
+    dev = torch.device("cuda", local)
+    stream = torch.cuda.current_stream(dev)
+    B = wl.get("B", 1)
+    if kind == "answer":
+        qs = [synth.uniform_u32(args.seed + 100 + i, (n_cells,), device=dev) for i in range(16)]
+        out = torch.empty(ell_local, dtype=torch.int32, device=dev)
+    elif kind == "batch":
+        qs = [synth.uniform_u32(args.seed + 100 + i, (B, n_cells), device=dev) for i in range(2)]
+        out = torch.empty((B, ell_local), dtype=torch.int32, device=dev)
+    else:
+        qs = [None]
+        out = torch.empty((ell_local, wl["n"]), dtype=torch.int32, device=dev)
+
+    def step(i, evs=None):
+        if evs is not None:
+            evs[0].record(stream)
+        if kind == "answer":
+            srv.answer(qs[i % len(qs)], out=out, stream=stream)
+        elif kind == "batch":
+            srv.answer_batch(qs[i % len(qs)], out=out, stream=stream)
+        else:
+            srv.hint(out=out, stream=stream)
+        if evs is not None:
+            evs[1].record(stream)
+        if world > 1 and kind != "hint":
+            gather_answer(out, sizes)
+
+    def barrier():
+        if world > 1:
+            torch.distributed.barrier()
+        torch.cuda.synchronize(dev)
+
+    sampler = ClockSampler(physical_gpu(local))
+    for i in range(args.warmup):
+        step(i)
+    barrier()
+    time.sleep(0.3)  # let the clock sampler come up
+    kev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+           for _ in range(args.steps)]
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    l0 = srv.kernel_launches
+    barrier()
+    sampler.start()
+    e0.record(stream)
+    for i in range(args.steps):
+        step(i, kev[i])
+    e1.record(stream)
+    barrier()
+    sampler.stop()
+    launches = srv.kernel_launches - l0
+    t_ms = e0.elapsed_time(e1)
+    k_ms = sum(a.elapsed_time(b) for a, b in kev) / args.steps
+    if world > 1:
+        tt = torch.tensor([t_ms, k_ms], device=dev, dtype=torch.float64)
+        torch.distributed.all_reduce(tt, op=torch.distributed.ReduceOp.MAX)
+        t_ms, k_ms = tt.tolist()
+    ms_per_step = t_ms / args.steps
+
+    # ---------------------------------------------------------------- e2e
+    e2e = None
+    if not args.no_e2e and kind in ("answer", "batch"):
+        if kind == "answer":
+            h_in = torch.empty(n_cells, dtype=torch.int32).pin_memory()
+            h_in.copy_(qs[0].cpu())
+            h_out = torch.empty(srv.ell if world > 1 else ell_local, dtype=torch.int32).pin_memory()
+        else:
+            h_in = torch.empty((B, n_cells), dtype=torch.int32).pin_memory()
+            h_in.copy_(qs[0].cpu())
+            h_out = torch.empty((B, srv.ell if world > 1 else ell_local), dtype=torch.int32).pin_memory()
+        e2e_steps = max(3, min(args.steps, 200 if kind == "answer" else 10))
+        dev_out = out
+
+        def e2e_step():
+            if kind == "answer":
+                srv.answer(h_in, out=dev_out, stream=stream)  # H2D of qu inside the C call
+            else:
+                srv.answer_batch(h_in, out=dev_out, stream=stream)
+            full = gather_answer(dev_out, sizes) if world > 1 else dev_out
+            h_out.copy_(full, non_blocking=True)
+            stream.synchronize()
+
+        for _ in range(3):
+            e2e_step()
+        barrier()
+        a0 = torch.cuda.Event(enable_timing=True)
+        a1 = torch.cuda.Event(enable_timing=True)
+        a0.record(stream)
+        for _ in range(e2e_steps):
+            e2e_step()
+        a1.record(stream)
+        barrier()
+        te = a0.elapsed_time(a1)
+        if world > 1:
+            tt = torch.tensor([te], device=dev, dtype=torch.float64)
+            torch.distributed.all_reduce(tt, op=torch.distributed.ReduceOp.MAX)
+            te = tt.item()
+        scanned = db_bytes_local * world * B
+        e2e = {"value": round(scanned / (te / e2e_steps / 1e3) / 1e9, 2), "unit": "GB/s",
+               "h2d_bytes_per_step": int(h_in.numel() * 4),
+               "d2h_bytes_per_step": int(h_out.numel() * 4), "steps": e2e_steps,
+               "ms_per_step": round(te / e2e_steps, 4),
+               "path": "qpir_answer with pinned host query (H2D inside the C call) "
+                       + ("+ NCCL all-gather " if world > 1 else "") + "+ D2H of the answer"}
+
+    # ---------------------------------------------------------------- line
+    if rank != 0:
+        if world > 1:
+            torch.distributed.destroy_process_group()
+        return
+    clocks = sampler.summary()
+    if kind == "answer":
+        scanned = db_bytes_local * world
+        value = scanned / (ms_per_step / 1e3) / 1e9
+        alg_bytes = db_bytes_local + 4 * n_cells + 4 * ell_local
+        achieved = alg_bytes / (k_ms / 1e3) / 1e9
+        roof = {"bound": "hbm", "achieved": round(achieved, 1), "peak": hbm, "unit": "GB/s",
+                "frac": round(achieved / hbm, 4), "traffic": None,
+                "kernel": "gemv_u8_u32_kernel", "kernel_ms": round(k_ms, 5),
+                "peak_source": f"{peak_src} hbm_gbs (copy, read+write)",
+                "algorithmic_bytes_per_launch": alg_bytes}
+        qps = world / (ms_per_step / 1e3)
+        unit = "GB/s"
+    elif kind == "batch":
+        scanned = db_bytes_local * world * B
+        value = scanned / (ms_per_step / 1e3) / 1e9
+        ops = 2.0 * ell_local * n_cells * 4 * B
+        achieved = ops / (k_ms / 1e3) / 1e12
+        pk = 2.0 * bf16
+        roof = {"bound": "tensor", "achieved": round(achieved, 1), "peak": pk, "unit": "TFLOP/s",
+                "frac": round(achieved / pk, 4), "traffic": None,
+                "kernel": "limb_split_kernel + mma_u8_limb_kernel (step time, upper bound)",
+                "kernel_ms": round(k_ms, 5),
+                "peak_source": f"{peak_src} bf16_tflops x 2 (nominal int8/bf16 ratio), int8 TOPS",
+                "algorithmic_ops_per_launch": ops}
+        qps = B * world / (ms_per_step / 1e3)
+        unit = "GB/s (query-equivalent)"
+    else:
+        ops = 2.0 * ell_local * n_cells * 4 * wl["n"]
+        value = ops / (ms_per_step / 1e3) / 1e12
+        achieved = value
+        pk = 2.0 * bf16
+        roof = {"bound": "tensor", "achieved": round(achieved, 1), "peak": pk, "unit": "TFLOP/s",
+                "frac": round(achieved / pk, 4), "traffic": None,
+                "kernel": "expand_A_limbs_kernel + mma_u8_limb_kernel (step time)",
+                "kernel_ms": round(k_ms, 5),
+                "peak_source": f"{peak_src} bf16_tflops x 2 (nominal int8/bf16 ratio), int8 TOPS"}
+        qps = None
+        unit = "TOPS (int8)"
+    prof = os.path.join(ROOT, "profiles", f"traffic_{args.workload}.json")
+    if os.path.exists(prof):
+        try:
+            roof["traffic"] = json.load(open(prof)).get("dram_bytes_per_launch")
+        except Exception:
+            pass
+    cpu_base = None
+    if not args.no_cpu_baseline and world == 1 and kind == "answer":
+        cpu_base = cpu_baseline_answer(wl, args.seed)
+    cfg = {"workload": wl["name"], "n_cells": n_cells, "n_ch": n_ch_total, "rec_bytes": d,
+           "ell_local": ell_local, "db_bytes_per_gpu": db_bytes_local,
+           "queries_per_step": B if kind != "hint" else 0,
+           "l2": "inputs larger than L2: D slice per GPU >> 126 MB, no flush needed"
+                 if db_bytes_local > 512e6 else "D slice fits in L2 (latency config)",
+           "setup_s": round(setup_s, 1), "parallelism": f"row-shard x{world}"}
+    line = {"metric": METRIC, "value": round(value, 2), "unit": unit, "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms_per_step, 5),
+            "higher_is_better": True, "scaling": scaling, "vs_baseline": None,
+            "dtype": "u8xu32->u32 (mod 2^32)", "data": "synthetic", "config": cfg,
+            "queries_per_s": round(qps, 1) if qps else None,
+            "roofline": roof, "cpu_baseline": cpu_base, "e2e": e2e, "gpu_launches": launches,
+            "clocks": clocks}
+    print(json.dumps(line), flush=True)
+    srv.close()
+    if world > 1:
+        torch.distributed.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

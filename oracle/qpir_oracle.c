@@ -179,10 +179,13 @@ void qo_hint(const uint8_t *D, uint64_t rows, uint64_t m, const uint32_t *A,
 #pragma omp parallel for schedule(static)
   for (int64_t r = 0; r < R; ++r) {
     const uint8_t *Dr = D + (uint64_t)r * m;
-    for (uint32_t j = 0; j < n; ++j) {
-      uint32_t acc = 0;
-      for (uint64_t c = 0; c < m; ++c) acc += (uint32_t)Dr[c] * A[c * (uint64_t)n + j];
-      H[(uint64_t)r * n + j] = acc;
+    uint32_t *Hr = H + (uint64_t)r * n;
+    for (uint32_t j = 0; j < n; ++j) Hr[j] = 0;
+    /* same sum, c outer so that A is read row by row */
+    for (uint64_t c = 0; c < m; ++c) {
+      const uint32_t dv = Dr[c];
+      const uint32_t *Ac = A + c * (uint64_t)n;
+      for (uint32_t j = 0; j < n; ++j) Hr[j] += dv * Ac[j];
     }
   }
 }

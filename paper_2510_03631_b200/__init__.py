@@ -1,0 +1,91 @@
+"""B200-native LWE-PIR answer engine for QPADL spectrum databases (arXiv 2510.03631).
+
+Public API (thin wrappers over the C ABI in include/qpir.h):
+    PirServer(...)            one rank-local context holding a row shard of D
+        .answer(qu)           ans = D.qu mod 2^32         (GEMV, HBM-bound)
+        .answer_batch(Q)      ANS = D.Q mod 2^32          (tcgen05 int8-limb GEMM)
+        .hint()               H = D.A mod 2^32            (tcgen05 int8-limb GEMM)
+    dist.DistributedPIR       row-sharded over ranks, NCCL gather of answer slices
+u32 values are carried in torch.int32 tensors (same bits); use u32() to view them.
+"""
+from __future__ import annotations
+
+import numpy as np
+import torch
+
+from . import _lib
+from ._lib import QpirError, qpir_params  # noqa: F401
+
+__all__ = ["PirServer", "QpirError", "u32", "qpir_params"]
+
+
+def u32(t) -> np.ndarray:
+    """torch int32 (u32 bit pattern) tensor -> numpy uint32 array (copies to host)."""
+    if isinstance(t, np.ndarray):
+        return t.view(np.uint32)
+    return t.detach().cpu().numpy().view(np.uint32)
+
+
+class PirServer:
+    """A context over rows [row_begin, row_end) of the DB matrix on one GPU."""
+
+    def __init__(self, n_cells: int, n_ch: int, rec_bytes: int, *, m: int = 0,
+                 lwe_n: int = 1024, seed_A: int = 0, row_begin: int = 0, row_end: int = 0,
+                 device: int = 0, records=None, stream=None):
+        p = qpir_params(n_cells=n_cells, n_ch=n_ch, rec_bytes=rec_bytes, m=m, lwe_n=lwe_n,
+                        log_q=32, log_p=8, reserved0=0, seed_A=seed_A, row_begin=row_begin,
+                        row_end=row_end, device=device, reserved1=0)
+        self.device = device
+        self.lwe_n = lwe_n
+        self._ctx = _lib.qpir_setup(p, records, stream)
+        self.ell, self.m, self.ell_local, self.row_begin = _lib.qpir_geometry(self._ctx)
+        self.n_cells, self.n_ch, self.rec_bytes = n_cells, n_ch, rec_bytes
+
+    # ------------------------------------------------------------------ DB
+    def db_write(self, theta_begin: int, records, stream=None) -> None:
+        n = int(records.shape[0]) if records.ndim == 2 else records.numel() // self.rec_bytes
+        _lib.qpir_db_write(self._ctx, theta_begin, records, n, stream)
+
+    # ------------------------------------------------------------------ answers
+    def _dev(self):
+        return torch.device("cuda", self.device)
+
+    def answer(self, qu, out=None, stream=None):
+        if out is None:
+            out = torch.empty(self.ell_local, dtype=torch.int32, device=self._dev())
+        _lib.qpir_answer(self._ctx, qu, out, stream)
+        return out
+
+    def answer_batch(self, Q, out=None, stream=None):
+        B = int(Q.shape[0])
+        if out is None:
+            out = torch.empty((B, self.ell_local), dtype=torch.int32, device=self._dev())
+        _lib.qpir_answer_batch(self._ctx, Q, B, out, stream)
+        return out
+
+    def hint(self, out=None, stream=None):
+        if out is None:
+            out = torch.empty((self.ell_local, self.lwe_n), dtype=torch.int32, device=self._dev())
+        _lib.qpir_hint(self._ctx, out, stream)
+        return out
+
+    @property
+    def kernel_launches(self) -> int:
+        return _lib.qpir_kernel_launches(self._ctx)
+
+    def close(self) -> None:
+        if getattr(self, "_ctx", None):
+            _lib.qpir_destroy(self._ctx)
+            self._ctx = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *exc):
+        self.close()

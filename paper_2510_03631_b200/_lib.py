@@ -1,0 +1,161 @@
+"""Thin ctypes binding of libqpir.so (include/qpir.h) -- argument marshalling only.
+
+Every function here keeps the C name and forwards pointers and lengths; all
+computation happens in the CUDA kernels behind the C ABI.  There is no CPU
+fallback: if libqpir.so is missing this module raises at import.
+Buffers may be torch tensors (CUDA or CPU), numpy arrays, or raw integer
+addresses.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libqpir.so")
+
+QPIR_OK = 0
+QPIR_E_PARAM = 1
+QPIR_E_DIMENSION = 2
+QPIR_E_STATE = 3
+QPIR_E_OOM = 4
+QPIR_E_CUDA = 5
+
+EXPORTS = (
+    "qpir_setup", "qpir_db_write", "qpir_geometry", "qpir_answer", "qpir_answer_batch",
+    "qpir_hint", "qpir_kernel_launches", "qpir_last_error", "qpir_destroy",
+)
+
+
+class qpir_params(ctypes.Structure):
+    _fields_ = [
+        ("n_cells", ctypes.c_uint64),
+        ("n_ch", ctypes.c_uint64),
+        ("rec_bytes", ctypes.c_uint64),
+        ("m", ctypes.c_uint64),
+        ("lwe_n", ctypes.c_uint32),
+        ("log_q", ctypes.c_uint32),
+        ("log_p", ctypes.c_uint32),
+        ("reserved0", ctypes.c_uint32),
+        ("seed_A", ctypes.c_uint64),
+        ("row_begin", ctypes.c_uint64),
+        ("row_end", ctypes.c_uint64),
+        ("device", ctypes.c_int32),
+        ("reserved1", ctypes.c_int32),
+    ]
+
+
+class QpirError(RuntimeError):
+    def __init__(self, code: int, msg: str):
+        super().__init__(f"qpir error {code}: {msg}")
+        self.code = code
+
+
+if not os.path.exists(LIB_PATH):
+    raise ImportError(
+        f"{LIB_PATH} is missing: build it with `python -m paper_2510_03631_b200.build` "
+        "(there is no CPU fallback)"
+    )
+
+_L = ctypes.CDLL(LIB_PATH)
+_vp = ctypes.c_void_p
+_u64 = ctypes.c_uint64
+_L.qpir_setup.argtypes = [ctypes.POINTER(qpir_params), _vp, _u64, _vp, ctypes.POINTER(_vp)]
+_L.qpir_db_write.argtypes = [_vp, _u64, _u64, _vp, _u64, _vp]
+_L.qpir_geometry.argtypes = [_vp, ctypes.POINTER(_u64), ctypes.POINTER(_u64),
+                             ctypes.POINTER(_u64), ctypes.POINTER(_u64)]
+_L.qpir_answer.argtypes = [_vp, _vp, _u64, _vp, _u64, _vp]
+_L.qpir_answer_batch.argtypes = [_vp, _vp, _u64, _u64, _vp, _u64, _vp]
+_L.qpir_hint.argtypes = [_vp, _vp, _u64, _vp]
+_L.qpir_kernel_launches.argtypes = [_vp]
+_L.qpir_kernel_launches.restype = _u64
+_L.qpir_last_error.argtypes = [_vp]
+_L.qpir_last_error.restype = ctypes.c_char_p
+_L.qpir_destroy.argtypes = [_vp]
+for _name in EXPORTS:
+    getattr(_L, _name)
+
+
+def _addr(x) -> int | None:
+    """(address, element count) of a buffer without copying."""
+    if x is None:
+        return None
+    if isinstance(x, int):
+        return x
+    if hasattr(x, "data_ptr"):  # torch.Tensor
+        assert x.is_contiguous(), "qpir buffers must be contiguous"
+        return x.data_ptr()
+    if isinstance(x, np.ndarray):
+        assert x.flags["C_CONTIGUOUS"], "qpir buffers must be C-contiguous"
+        return x.ctypes.data
+    raise TypeError(f"unsupported buffer type {type(x)}")
+
+
+def _numel(x) -> int:
+    if hasattr(x, "numel"):
+        return int(x.numel())
+    return int(np.asarray(x).size)
+
+
+def _stream(stream) -> int | None:
+    if stream is None:
+        return None
+    if isinstance(stream, int):
+        return stream
+    return stream.cuda_stream  # torch.cuda.Stream
+
+
+def _check(rc: int, ctx=None):
+    if rc != QPIR_OK:
+        msg = _L.qpir_last_error(ctx).decode()
+        raise QpirError(rc, msg)
+
+
+# ------------------------------------------------------------ C names
+def qpir_setup(params: qpir_params, records=None, stream=None) -> int:
+    """Returns the context handle (int).  records: full theta-ordered u8 array or None."""
+    out = _vp()
+    rec_len = _numel(records) if records is not None else 0
+    rc = _L.qpir_setup(ctypes.byref(params), _addr(records), rec_len, _stream(stream),
+                       ctypes.byref(out))
+    _check(rc, None)
+    return out.value
+
+
+def qpir_db_write(ctx: int, theta_begin: int, records, n_records: int, stream=None):
+    _check(_L.qpir_db_write(ctx, theta_begin, n_records, _addr(records), _numel(records),
+                            _stream(stream)), ctx)
+
+
+def qpir_geometry(ctx: int):
+    v = [_u64() for _ in range(4)]
+    _check(_L.qpir_geometry(ctx, *[ctypes.byref(x) for x in v]), ctx)
+    return tuple(int(x.value) for x in v)  # ell, m, ell_local, row_begin
+
+
+def qpir_answer(ctx: int, qu, ans_local, stream=None):
+    _check(_L.qpir_answer(ctx, _addr(qu), _numel(qu), _addr(ans_local), _numel(ans_local),
+                          _stream(stream)), ctx)
+
+
+def qpir_answer_batch(ctx: int, Q, B: int, ans_local, stream=None):
+    _check(_L.qpir_answer_batch(ctx, _addr(Q), B, _numel(Q), _addr(ans_local),
+                                _numel(ans_local), _stream(stream)), ctx)
+
+
+def qpir_hint(ctx: int, H_local, stream=None):
+    _check(_L.qpir_hint(ctx, _addr(H_local), _numel(H_local), _stream(stream)), ctx)
+
+
+def qpir_kernel_launches(ctx: int) -> int:
+    return int(_L.qpir_kernel_launches(ctx))
+
+
+def qpir_last_error(ctx: int | None = None) -> str:
+    return _L.qpir_last_error(ctx).decode()
+
+
+def qpir_destroy(ctx: int) -> None:
+    _L.qpir_destroy(ctx)

@@ -1,0 +1,140 @@
+// aux_kernels.cuh -- K-B4 helpers: DB pack (step a1), batch-query limb split
+// (a6 prologue), Philox expansion of the public matrix A into limb planes (a7).
+#pragma once
+#include <cstdint>
+
+namespace qpir {
+
+// ---------------------------------------------------------------- a1 pack
+// Records theta in [theta0, theta0 + n_rec) (theta-ordered, d bytes each) are
+// scattered into the D shard.  Geometry (DESIGN R9/R10; PAPER.md:515 DB matrix,
+// SPEC.md:51 row-major index, PAPER.md:1107 multiple-block retrieval):
+//   theta = cell * n_ch + ch,  blk = cell / m,  col = cell % m,
+//   row = (blk * n_ch + ch) * d + b.
+// One thread = one (local row, 16-column group): read-modify-write of 16 bytes.
+// Lanes walk consecutive rows = consecutive record bytes, so the record reads
+// coalesce and the 16-byte writes are contiguous.
+struct PackArgs {
+  const uint8_t* rec;
+  uint8_t* D;          // [G][L][16]
+  uint64_t theta0, n_rec;
+  uint64_t row_begin;  // global row of local row 0
+  uint32_t ell_local, L;
+  uint32_t n_ch, d, m;
+  uint64_t n_cells;
+  uint32_t g_lo;       // first column group of the launch (grid.x offset)
+};
+
+__global__ void pack_records_kernel(PackArgs a) {
+  const uint32_t rl = blockIdx.y * blockDim.x + threadIdx.x;
+  if (rl >= a.ell_local) return;
+  const uint32_t j = a.g_lo + blockIdx.x;
+  const uint64_t row = a.row_begin + rl;
+  const uint64_t per_blk = (uint64_t)a.n_ch * a.d;
+  const uint64_t blk = row / per_blk;
+  const uint32_t rr = (uint32_t)(row % per_blk);
+  const uint32_t ch = rr / a.d;
+  const uint32_t b = rr % a.d;
+  uint4* dst = reinterpret_cast<uint4*>(a.D + ((size_t)j * a.L + rl) * 16);
+  uint4 v = *dst;
+  uint8_t* bytes = reinterpret_cast<uint8_t*>(&v);
+  bool touched = false;
+#pragma unroll
+  for (int i = 0; i < 16; ++i) {
+    const uint32_t col = j * 16u + i;
+    if (col >= a.m) continue;
+    const uint64_t cell = blk * a.m + col;
+    if (cell >= a.n_cells) continue;
+    const uint64_t theta = cell * a.n_ch + ch;
+    if (theta < a.theta0 || theta >= a.theta0 + a.n_rec) continue;
+    bytes[i] = a.rec[(theta - a.theta0) * a.d + b];
+    touched = true;
+  }
+  if (touched) *dst = v;
+}
+
+// ---------------------------------------------------------------- a6 limbs
+// Q (B x m u32, query-major) -> Q' = byte-limb planes as the MMA B operand,
+// K-major, 16-cell interleaved like D:  Q'[g][n][i] = limb k of Q[j][16g + i],
+// n = 4j + k (k = 0..3), zero for padding (n >= 4B or 16g + i >= m).
+// One thread per (query j, group g): 64 B in, 4 x 16 B out (64 B contiguous).
+__global__ void limb_split_kernel(const uint32_t* __restrict__ Q, uint8_t* __restrict__ Qp,
+                                  uint32_t B, uint32_t m, uint32_t G, uint32_t Npad) {
+  const uint32_t jq = blockIdx.x * blockDim.x + threadIdx.x;  // padded query index
+  const uint32_t g = blockIdx.y;
+  if (jq * 4u >= Npad) return;
+  uint32_t q[16];
+#pragma unroll
+  for (int i = 0; i < 16; ++i) {
+    const uint32_t c = g * 16u + i;
+    q[i] = (jq < B && c < m) ? __ldg(Q + (size_t)jq * m + c) : 0u;
+  }
+  uint4* dst = reinterpret_cast<uint4*>(Qp + ((size_t)g * Npad + jq * 4u) * 16);
+#pragma unroll
+  for (uint32_t k = 0; k < 4; ++k) {
+    uint4 w;
+    w.x = __byte_perm(__byte_perm(q[0], q[1], k | ((k + 4) << 4)),
+                      __byte_perm(q[2], q[3], k | ((k + 4) << 4)), 0x5410);
+    w.y = __byte_perm(__byte_perm(q[4], q[5], k | ((k + 4) << 4)),
+                      __byte_perm(q[6], q[7], k | ((k + 4) << 4)), 0x5410);
+    w.z = __byte_perm(__byte_perm(q[8], q[9], k | ((k + 4) << 4)),
+                      __byte_perm(q[10], q[11], k | ((k + 4) << 4)), 0x5410);
+    w.w = __byte_perm(__byte_perm(q[12], q[13], k | ((k + 4) << 4)),
+                      __byte_perm(q[14], q[15], k | ((k + 4) << 4)), 0x5410);
+    dst[k] = w;
+  }
+}
+
+// ---------------------------------------------------------------- a7 A'
+// Philox4x32-10 (Salmon et al., SC'11), device implementation of the public
+// matrix generator (DESIGN R7): A[c][j] = Philox(key = seed_A,
+// ctr = (c, j >> 2, 0, 0x41))[j & 3].
+__device__ __forceinline__ uint4 philox4x32_10(uint4 ctr, uint2 key) {
+#pragma unroll
+  for (int r = 0; r < 10; ++r) {
+    const uint32_t lo0 = 0xD2511F53u * ctr.x, hi0 = __umulhi(0xD2511F53u, ctr.x);
+    const uint32_t lo1 = 0xCD9E8D57u * ctr.z, hi1 = __umulhi(0xCD9E8D57u, ctr.z);
+    ctr = make_uint4(hi1 ^ ctr.y ^ key.x, lo1, hi0 ^ ctr.w ^ key.y, lo0);
+    key.x += 0x9E3779B9u;
+    key.y += 0xBB67AE85u;
+  }
+  return ctr;
+}
+
+// A' [g][n][i] = limb k of A[16g + i][j], n = 4j + k; one thread per
+// (group g, Philox block jb = j >> 2): 16 Philox calls, 256 contiguous bytes out.
+__global__ void expand_A_limbs_kernel(uint8_t* __restrict__ Ap, uint64_t seed, uint32_t m,
+                                      uint32_t n, uint32_t G, uint32_t Npad) {
+  const uint32_t jb = blockIdx.x * blockDim.x + threadIdx.x;
+  const uint32_t g = blockIdx.y;
+  if (jb * 16u >= Npad) return;
+  const uint2 key = make_uint2((uint32_t)seed, (uint32_t)(seed >> 32));
+  uint32_t a[16][4];
+#pragma unroll
+  for (int i = 0; i < 16; ++i) {
+    const uint32_t c = g * 16u + i;
+    uint4 v = make_uint4(0, 0, 0, 0);
+    if (c < m && jb * 4u < n) v = philox4x32_10(make_uint4(c, jb, 0u, 0x41u), key);
+    a[i][0] = v.x;
+    a[i][1] = (jb * 4u + 1 < n) ? v.y : 0u;
+    a[i][2] = (jb * 4u + 2 < n) ? v.z : 0u;
+    a[i][3] = (jb * 4u + 3 < n) ? v.w : 0u;
+  }
+  uint4* dst = reinterpret_cast<uint4*>(Ap + ((size_t)g * Npad + jb * 16u) * 16);
+#pragma unroll
+  for (int jj = 0; jj < 4; ++jj) {
+#pragma unroll
+    for (uint32_t k = 0; k < 4; ++k) {
+      uint32_t w[4];
+#pragma unroll
+      for (int t = 0; t < 4; ++t) {
+        const uint32_t sel = k | ((k + 4) << 4);
+        w[t] = __byte_perm(__byte_perm(a[4 * t + 0][jj], a[4 * t + 1][jj], sel),
+                           __byte_perm(a[4 * t + 2][jj], a[4 * t + 3][jj], sel), 0x5410);
+      }
+      dst[jj * 4 + k] = make_uint4(w[0], w[1], w[2], w[3]);
+    }
+  }
+}
+
+}  // namespace qpir

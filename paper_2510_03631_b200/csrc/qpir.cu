@@ -1,0 +1,577 @@
+// qpir.cu -- C ABI (include/qpir.h) of the B200-native LWE-PIR answer engine.
+//
+// Host side: parameter validation (before any CUDA call), context + device
+// memory ownership, host/device buffer detection, kernel dispatch.  Every step
+// of the path runs in the kernels of gemv.cuh / mma.cuh / aux_kernels.cuh; there
+// is no CPU fallback -- a missing device is an error.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstdarg>
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
+#include <string>
+
+#include "../../include/qpir.h"
+#include "aux_kernels.cuh"
+#include "gemv.cuh"
+#include "mma.cuh"
+
+using namespace qpir;
+
+namespace {
+
+thread_local std::string g_setup_error;
+
+uint64_t round_up(uint64_t x, uint64_t a) { return (x + a - 1) / a * a; }
+
+struct Geometry {
+  uint64_t n_cells, n_ch, d, m, ell, row_begin, row_end, ell_local;
+  uint64_t m_pad, G, L;
+  uint32_t lwe_n;
+  uint64_t seed_A;
+};
+
+}  // namespace
+
+struct qpir_ctx {
+  Geometry geo;
+  int device = 0;
+  int num_sms = 148;
+  uint8_t* D = nullptr;            // [G][L][16]
+  uint32_t* qu_dev = nullptr;      // m_pad (staging for host / unaligned qu)
+  uint32_t* ans_dev = nullptr;     // ell_local (staging for host answers)
+  uint32_t* partial = nullptr;     // [max_split][L]
+  uint32_t* tickets = nullptr;     // [max row blocks], self-resetting
+  uint32_t max_split = 0, max_rb = 0;
+  uint8_t* rec_stage = nullptr;    // host-record staging for db_write
+  uint64_t rec_stage_bytes = 0;
+  uint8_t* limbs = nullptr;        // Q' or A' limb planes
+  uint64_t limbs_bytes = 0;
+  uint32_t* big_in = nullptr;      // staging for host Q
+  uint64_t big_in_bytes = 0;
+  uint32_t* big_out = nullptr;     // staging for host ANS / H
+  uint64_t big_out_bytes = 0;
+  uint64_t launches = 0;
+  // GEMV tuning (env QPIR_GEMV_U / QPIR_GEMV_SPLIT / QPIR_GEMV_CHUNK)
+  int gemv_u = 2;
+  int gemv_split = 0;  // 0 = auto
+  int gemv_chunk = 512;
+  std::string err;
+};
+
+namespace {
+
+int fail(qpir_ctx* ctx, int code, const char* fmt, ...) {
+  char buf[512];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof buf, fmt, ap);
+  va_end(ap);
+  if (ctx)
+    ctx->err = buf;
+  else
+    g_setup_error = buf;
+  return code;
+}
+
+#define CUDA_TRY(ctx, call)                                                              \
+  do {                                                                                   \
+    cudaError_t e_ = (call);                                                             \
+    if (e_ != cudaSuccess)                                                               \
+      return fail((ctx), e_ == cudaErrorMemoryAllocation ? QPIR_E_OOM : QPIR_E_CUDA,     \
+                  "%s: %s (%s:%d)", #call, cudaGetErrorString(e_), __FILE__, __LINE__); \
+  } while (0)
+
+#define LAUNCH_CHECK(ctx)                                                                 \
+  do {                                                                                    \
+    (ctx)->launches++;                                                                    \
+    cudaError_t e_ = cudaGetLastError();                                                  \
+    if (e_ != cudaSuccess)                                                                \
+      return fail((ctx), QPIR_E_CUDA, "kernel launch: %s (%s:%d)", cudaGetErrorString(e_), \
+                  __FILE__, __LINE__);                                                    \
+  } while (0)
+
+// Restores the caller's current device on scope exit.
+struct DeviceGuard {
+  int prev = -1;
+  explicit DeviceGuard(int dev) {
+    if (cudaGetDevice(&prev) != cudaSuccess) prev = -1;
+    if (prev != dev) cudaSetDevice(dev);
+  }
+  ~DeviceGuard() {
+    int cur;
+    if (prev >= 0 && cudaGetDevice(&cur) == cudaSuccess && cur != prev) cudaSetDevice(prev);
+  }
+};
+
+// 1 = device memory of `dev`, 0 = host memory, -1 = device memory of another device.
+int where(const void* p, int dev) {
+  cudaPointerAttributes at;
+  if (cudaPointerGetAttributes(&at, p) != cudaSuccess) {
+    cudaGetLastError();
+    return 0;
+  }
+  if (at.type == cudaMemoryTypeDevice || at.type == cudaMemoryTypeManaged)
+    return at.device == dev ? 1 : -1;
+  return 0;
+}
+
+int validate(const qpir_params* p, Geometry* g) {
+  if (!p) return fail(nullptr, QPIR_E_PARAM, "params: NULL");
+  if (p->log_q != 32) return fail(nullptr, QPIR_E_PARAM, "log_q: %u != 32", p->log_q);
+  if (p->log_p != 8) return fail(nullptr, QPIR_E_PARAM, "log_p: %u != 8", p->log_p);
+  if (p->reserved0 != 0 || p->reserved1 != 0)
+    return fail(nullptr, QPIR_E_PARAM, "reserved: must be 0");
+  if (p->lwe_n == 0 || p->lwe_n > 65536)
+    return fail(nullptr, QPIR_E_PARAM, "lwe_n: %u not in [1, 65536]", p->lwe_n);
+  if (p->n_cells == 0) return fail(nullptr, QPIR_E_DIMENSION, "n_cells: 0");
+  if (p->n_ch == 0) return fail(nullptr, QPIR_E_DIMENSION, "n_ch: 0");
+  if (p->rec_bytes == 0) return fail(nullptr, QPIR_E_DIMENSION, "rec_bytes: 0");
+  if (p->device < 0) return fail(nullptr, QPIR_E_PARAM, "device: %d < 0", p->device);
+  g->n_cells = p->n_cells;
+  g->n_ch = p->n_ch;
+  g->d = p->rec_bytes;
+  g->m = p->m ? p->m : p->n_cells;
+  if (g->m > (1ull << 30)) return fail(nullptr, QPIR_E_DIMENSION, "m: %llu > 2^30",
+                                       (unsigned long long)g->m);
+  const uint64_t n_blk = (g->n_cells + g->m - 1) / g->m;
+  g->ell = n_blk * g->n_ch * g->d;
+  g->row_begin = p->row_begin;
+  g->row_end = p->row_end ? p->row_end : g->ell;
+  if (g->row_end > g->ell)
+    return fail(nullptr, QPIR_E_DIMENSION, "row_end: %llu > ell %llu",
+                (unsigned long long)g->row_end, (unsigned long long)g->ell);
+  if (g->row_begin >= g->row_end)
+    return fail(nullptr, QPIR_E_DIMENSION, "row_begin: %llu >= row_end %llu",
+                (unsigned long long)g->row_begin, (unsigned long long)g->row_end);
+  g->ell_local = g->row_end - g->row_begin;
+  if (g->ell_local > (1ull << 31) - 4096)
+    return fail(nullptr, QPIR_E_DIMENSION, "ell_local: %llu too large",
+                (unsigned long long)g->ell_local);
+  g->m_pad = round_up(g->m, MMA_BK);
+  g->G = g->m_pad / 16;
+  g->L = round_up(g->ell_local, MMA_BM);
+  g->lwe_n = p->lwe_n;
+  g->seed_A = p->seed_A;
+  return QPIR_OK;
+}
+
+int env_int(const char* name, int dflt) {
+  const char* v = getenv(name);
+  return v ? atoi(v) : dflt;
+}
+
+int ensure(qpir_ctx* ctx, void** buf, uint64_t* have, uint64_t need) {
+  if (*have >= need) return QPIR_OK;
+  if (*buf) cudaFree(*buf);
+  *buf = nullptr;
+  *have = 0;
+  CUDA_TRY(ctx, cudaMalloc(buf, need));
+  *have = need;
+  return QPIR_OK;
+}
+
+int db_write_device(qpir_ctx* ctx, uint64_t theta0, uint64_t n_rec, const uint8_t* rec,
+                    cudaStream_t st) {
+  const Geometry& g = ctx->geo;
+  if (n_rec == 0) return QPIR_OK;
+  // column groups touched: whole range unless the chunk lies in one row block
+  const uint64_t cell_lo = theta0 / g.n_ch, cell_hi = (theta0 + n_rec - 1) / g.n_ch;
+  uint64_t j_lo = 0, j_hi = g.G - 1;
+  if (cell_lo / g.m == cell_hi / g.m) {
+    j_lo = (cell_lo % g.m) / 16;
+    j_hi = (cell_hi % g.m) / 16;
+  }
+  PackArgs a;
+  a.rec = rec;
+  a.D = ctx->D;
+  a.theta0 = theta0;
+  a.n_rec = n_rec;
+  a.row_begin = g.row_begin;
+  a.ell_local = (uint32_t)g.ell_local;
+  a.L = (uint32_t)g.L;
+  a.n_ch = (uint32_t)g.n_ch;
+  a.d = (uint32_t)g.d;
+  a.m = (uint32_t)g.m;
+  a.n_cells = g.n_cells;
+  a.g_lo = (uint32_t)j_lo;
+  const uint32_t rb = (uint32_t)((g.ell_local + 127) / 128);
+  for (uint32_t y0 = 0; y0 < rb; y0 += 65535) {
+    // grid.y is limited to 65535 row blocks per launch
+    PackArgs b = a;
+    const uint32_t ny = std::min<uint32_t>(65535, rb - y0);
+    b.D = ctx->D + (size_t)y0 * 128 * 16;
+    b.row_begin = g.row_begin + (uint64_t)y0 * 128;
+    b.ell_local = (uint32_t)std::min<uint64_t>(g.ell_local - (uint64_t)y0 * 128, (uint64_t)ny * 128);
+    dim3 grid((uint32_t)(j_hi - j_lo + 1), ny);
+    pack_records_kernel<<<grid, 128, 0, st>>>(b);
+    LAUNCH_CHECK(ctx);
+  }
+  return QPIR_OK;
+}
+
+template <int U>
+int launch_gemv(qpir_ctx* ctx, const uint32_t* qu, uint32_t* ans, cudaStream_t st) {
+  const Geometry& g = ctx->geo;
+  constexpr int UNR = 4;
+  const uint32_t rows_per_cta = GEMV_THREADS * U;
+  const uint32_t rb = (uint32_t)((g.L + rows_per_cta - 1) / rows_per_cta);
+  uint32_t S = ctx->gemv_split;
+  if (S == 0) {
+    // enough CTAs for ~6 resident per SM, at least 64 column groups per split
+    const uint32_t want = (uint32_t)(6 * ctx->num_sms);
+    S = (want + rb - 1) / rb;
+    S = std::min<uint32_t>(S, (uint32_t)std::max<uint64_t>(1, g.G / 64));
+  }
+  S = std::max<uint32_t>(1, std::min<uint32_t>(S, (uint32_t)(g.G / UNR)));
+  uint32_t gps = (uint32_t)round_up((g.G + S - 1) / S, UNR);
+  S = (uint32_t)((g.G + gps - 1) / gps);
+  uint32_t chunk = (uint32_t)std::max(UNR, ctx->gemv_chunk / UNR * UNR);
+  chunk = std::min(chunk, gps);
+  if (S > 1 && (S > ctx->max_split || rb > ctx->max_rb)) {
+    if (ctx->partial) cudaFree(ctx->partial);
+    if (ctx->tickets) cudaFree(ctx->tickets);
+    ctx->partial = nullptr;
+    ctx->tickets = nullptr;
+    ctx->max_split = std::max(S, ctx->max_split);
+    ctx->max_rb = std::max(rb, ctx->max_rb);
+    CUDA_TRY(ctx, cudaMalloc(&ctx->partial, (size_t)ctx->max_split * g.L * 4));
+    CUDA_TRY(ctx, cudaMalloc(&ctx->tickets, (size_t)ctx->max_rb * 4));
+    CUDA_TRY(ctx, cudaMemsetAsync(ctx->tickets, 0, (size_t)ctx->max_rb * 4, st));
+  }
+  GemvArgs a;
+  a.D = ctx->D;
+  a.qu = qu;
+  a.ans = ans;
+  a.partial = ctx->partial;
+  a.tickets = ctx->tickets;
+  a.ell_local = (uint32_t)g.ell_local;
+  a.L = (uint32_t)g.L;
+  a.m = (uint32_t)g.m;
+  a.G = (uint32_t)g.G;
+  a.gps = gps;
+  a.chunk = chunk;
+  const size_t smem = (size_t)chunk * 64;
+  auto kern = gemv_u8_u32_kernel<U, UNR>;
+  if (smem > 48 * 1024)
+    CUDA_TRY(ctx, cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  kern<<<dim3(rb, S), GEMV_THREADS, smem, st>>>(a);
+  LAUNCH_CHECK(ctx);
+  return QPIR_OK;
+}
+
+int gemv(qpir_ctx* ctx, const uint32_t* qu, uint32_t* ans, cudaStream_t st) {
+  switch (ctx->gemv_u) {
+    case 1: return launch_gemv<1>(ctx, qu, ans, st);
+    case 4: return launch_gemv<4>(ctx, qu, ans, st);
+    default: return launch_gemv<2>(ctx, qu, ans, st);
+  }
+}
+
+template <uint32_t BN, int MODE>
+int launch_mma_bn(qpir_ctx* ctx, const uint8_t* Bl, uint32_t Npad, uint32_t* out,
+                  uint32_t n_out, uint32_t out_ld, cudaStream_t st) {
+  constexpr uint32_t STAGES = 4;
+  using S = MmaSmem<BN, STAGES>;
+  const Geometry& g = ctx->geo;
+  MmaArgs a;
+  a.A = ctx->D;
+  a.B = Bl;
+  a.out = out;
+  a.L = (uint32_t)g.L;
+  a.Npad = Npad;
+  a.G = (uint32_t)g.G;
+  a.rows = (uint32_t)g.ell_local;
+  a.n_out = n_out;
+  a.out_ld = out_ld;
+  a.m_tiles = (uint32_t)(g.L / MMA_BM);
+  a.n_tiles = Npad / BN;
+  const uint32_t tiles = a.m_tiles * a.n_tiles;
+  const uint32_t grid = std::min<uint32_t>(tiles, (uint32_t)ctx->num_sms);
+  auto kern = mma_u8_limb_kernel<BN, STAGES, MODE>;
+  CUDA_TRY(ctx, cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)S::TOTAL));
+  kern<<<grid, MMA_THREADS, S::TOTAL, st>>>(a);
+  LAUNCH_CHECK(ctx);
+  return QPIR_OK;
+}
+
+uint32_t pick_bn(uint64_t ncols) {
+  if (ncols <= 16) return 16;
+  if (ncols <= 32) return 32;
+  if (ncols <= 64) return 64;
+  if (ncols <= 128) return 128;
+  return 256;
+}
+
+template <int MODE>
+int launch_mma(qpir_ctx* ctx, uint32_t BN, const uint8_t* Bl, uint32_t Npad, uint32_t* out,
+               uint32_t n_out, uint32_t out_ld, cudaStream_t st) {
+  switch (BN) {
+    case 16: return launch_mma_bn<16, MODE>(ctx, Bl, Npad, out, n_out, out_ld, st);
+    case 32: return launch_mma_bn<32, MODE>(ctx, Bl, Npad, out, n_out, out_ld, st);
+    case 64: return launch_mma_bn<64, MODE>(ctx, Bl, Npad, out, n_out, out_ld, st);
+    case 128: return launch_mma_bn<128, MODE>(ctx, Bl, Npad, out, n_out, out_ld, st);
+    default: return launch_mma_bn<256, MODE>(ctx, Bl, Npad, out, n_out, out_ld, st);
+  }
+}
+
+bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
+
+}  // namespace
+
+extern "C" {
+
+int qpir_setup(const qpir_params* params, const uint8_t* records, uint64_t records_len,
+               void* stream, qpir_ctx** out) {
+  g_setup_error.clear();
+  if (!out) return fail(nullptr, QPIR_E_PARAM, "out: NULL");
+  *out = nullptr;
+  Geometry g;
+  int rc = validate(params, &g);
+  if (rc) return rc;
+  const uint64_t n_rec = g.n_cells * g.n_ch;
+  if (records && records_len != n_rec * g.d)
+    return fail(nullptr, QPIR_E_DIMENSION, "records_len: %llu != %llu",
+                (unsigned long long)records_len, (unsigned long long)(n_rec * g.d));
+  int ndev = 0;
+  if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0) {
+    cudaGetLastError();
+    return fail(nullptr, QPIR_E_CUDA, "device: no CUDA device available");
+  }
+  if (params->device >= ndev)
+    return fail(nullptr, QPIR_E_PARAM, "device: %d >= device count %d", params->device, ndev);
+  DeviceGuard dg(params->device);
+  cudaDeviceProp prop;
+  if (cudaGetDeviceProperties(&prop, params->device) != cudaSuccess)
+    return fail(nullptr, QPIR_E_CUDA, "cudaGetDeviceProperties failed");
+  if (prop.major != 10)
+    return fail(nullptr, QPIR_E_CUDA, "device: compute capability %d.%d, need 10.x (sm_100a)",
+                prop.major, prop.minor);
+  qpir_ctx* ctx = new qpir_ctx();
+  ctx->geo = g;
+  ctx->device = params->device;
+  ctx->num_sms = prop.multiProcessorCount;
+  ctx->gemv_u = env_int("QPIR_GEMV_U", 2);
+  ctx->gemv_split = env_int("QPIR_GEMV_SPLIT", 0);
+  ctx->gemv_chunk = env_int("QPIR_GEMV_CHUNK", 512);
+  cudaStream_t st = (cudaStream_t)stream;
+  auto bail = [&](int code) {
+    g_setup_error = ctx->err;
+    qpir_destroy(ctx);
+    return code;
+  };
+  const size_t dbytes = (size_t)g.m_pad * g.L;
+  if (cudaMalloc(&ctx->D, dbytes) != cudaSuccess) {
+    cudaGetLastError();
+    fail(ctx, QPIR_E_OOM, "D: cudaMalloc(%zu) failed", dbytes);
+    return bail(QPIR_E_OOM);
+  }
+  if (cudaMalloc(&ctx->qu_dev, g.m_pad * 4) != cudaSuccess ||
+      cudaMalloc(&ctx->ans_dev, g.L * 4) != cudaSuccess) {
+    cudaGetLastError();
+    fail(ctx, QPIR_E_OOM, "scratch: cudaMalloc failed");
+    return bail(QPIR_E_OOM);
+  }
+  if (cudaMemsetAsync(ctx->D, 0, dbytes, st) != cudaSuccess ||
+      cudaMemsetAsync(ctx->qu_dev, 0, g.m_pad * 4, st) != cudaSuccess) {
+    fail(ctx, QPIR_E_CUDA, "memset failed");
+    return bail(QPIR_E_CUDA);
+  }
+  if (records) {
+    rc = qpir_db_write(ctx, 0, n_rec, records, records_len, stream);
+    if (rc) return bail(rc);
+  }
+  if (cudaStreamSynchronize(st) != cudaSuccess) {
+    fail(ctx, QPIR_E_CUDA, "setup: %s", cudaGetErrorString(cudaGetLastError()));
+    return bail(QPIR_E_CUDA);
+  }
+  *out = ctx;
+  return QPIR_OK;
+}
+
+int qpir_db_write(qpir_ctx* ctx, uint64_t theta_begin, uint64_t n_records,
+                  const uint8_t* records, uint64_t records_len, void* stream) {
+  if (!ctx) return fail(nullptr, QPIR_E_STATE, "ctx: NULL");
+  const Geometry& g = ctx->geo;
+  const uint64_t n_all = g.n_cells * g.n_ch;
+  if (theta_begin > n_all || n_records > n_all - theta_begin)
+    return fail(ctx, QPIR_E_DIMENSION, "theta range: [%llu, +%llu) exceeds %llu records",
+                (unsigned long long)theta_begin, (unsigned long long)n_records,
+                (unsigned long long)n_all);
+  if (records_len != n_records * g.d)
+    return fail(ctx, QPIR_E_DIMENSION, "records_len: %llu != %llu",
+                (unsigned long long)records_len, (unsigned long long)(n_records * g.d));
+  if (n_records == 0) return QPIR_OK;
+  if (!records) return fail(ctx, QPIR_E_PARAM, "records: NULL");
+  DeviceGuard dg(ctx->device);
+  cudaStream_t st = (cudaStream_t)stream;
+  const int w = where(records, ctx->device);
+  if (w < 0) return fail(ctx, QPIR_E_PARAM, "records: device memory of another device");
+  if (w == 1) return db_write_device(ctx, theta_begin, n_records, records, st);
+  // host records: stream through a device staging buffer in chunks
+  const uint64_t chunk_rec = std::max<uint64_t>(1, (64ull << 20) / g.d);
+  int rc = ensure(ctx, (void**)&ctx->rec_stage, &ctx->rec_stage_bytes,
+                  std::min(n_records, chunk_rec) * g.d);
+  if (rc) return rc;
+  for (uint64_t t = 0; t < n_records; t += chunk_rec) {
+    const uint64_t n = std::min(chunk_rec, n_records - t);
+    CUDA_TRY(ctx, cudaMemcpyAsync(ctx->rec_stage, records + t * g.d, n * g.d,
+                                  cudaMemcpyHostToDevice, st));
+    rc = db_write_device(ctx, theta_begin + t, n, ctx->rec_stage, st);
+    if (rc) return rc;
+  }
+  CUDA_TRY(ctx, cudaStreamSynchronize(st));
+  return QPIR_OK;
+}
+
+int qpir_geometry(const qpir_ctx* ctx, uint64_t* ell, uint64_t* m, uint64_t* ell_local,
+                  uint64_t* row_begin) {
+  if (!ctx) return QPIR_E_STATE;
+  if (ell) *ell = ctx->geo.ell;
+  if (m) *m = ctx->geo.m;
+  if (ell_local) *ell_local = ctx->geo.ell_local;
+  if (row_begin) *row_begin = ctx->geo.row_begin;
+  return QPIR_OK;
+}
+
+int qpir_answer(qpir_ctx* ctx, const uint32_t* qu, uint64_t len_qu, uint32_t* ans_local,
+                uint64_t len_ans, void* stream) {
+  if (!ctx) return fail(nullptr, QPIR_E_STATE, "ctx: NULL");
+  const Geometry& g = ctx->geo;
+  if (!qu || !ans_local) return fail(ctx, QPIR_E_PARAM, "qu/ans_local: NULL");
+  if (len_qu != g.m)
+    return fail(ctx, QPIR_E_DIMENSION, "m: %llu != %llu", (unsigned long long)len_qu,
+                (unsigned long long)g.m);
+  if (len_ans != g.ell_local)
+    return fail(ctx, QPIR_E_DIMENSION, "ell_local: %llu != %llu", (unsigned long long)len_ans,
+                (unsigned long long)g.ell_local);
+  DeviceGuard dg(ctx->device);
+  cudaStream_t st = (cudaStream_t)stream;
+  const int wq = where(qu, ctx->device), wa = where(ans_local, ctx->device);
+  if (wq < 0 || wa < 0) return fail(ctx, QPIR_E_PARAM, "qu/ans_local: memory of another device");
+  const uint32_t* qd = qu;
+  if (wq == 0 || !aligned16(qu)) {
+    CUDA_TRY(ctx, cudaMemcpyAsync(ctx->qu_dev, qu, g.m * 4,
+                                  wq ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, st));
+    qd = ctx->qu_dev;
+  }
+  uint32_t* ad = wa ? ans_local : ctx->ans_dev;
+  int rc = gemv(ctx, qd, ad, st);
+  if (rc) return rc;
+  if (!wa) {
+    CUDA_TRY(ctx, cudaMemcpyAsync(ans_local, ad, g.ell_local * 4, cudaMemcpyDeviceToHost, st));
+    CUDA_TRY(ctx, cudaStreamSynchronize(st));
+  }
+  return QPIR_OK;
+}
+
+int qpir_answer_batch(qpir_ctx* ctx, const uint32_t* Q, uint64_t B, uint64_t len_Q,
+                      uint32_t* ans_local, uint64_t len_ans, void* stream) {
+  if (!ctx) return fail(nullptr, QPIR_E_STATE, "ctx: NULL");
+  const Geometry& g = ctx->geo;
+  if (!Q || !ans_local) return fail(ctx, QPIR_E_PARAM, "Q/ans_local: NULL");
+  if (B == 0 || B > 4096) return fail(ctx, QPIR_E_PARAM, "B: %llu not in [1, 4096]",
+                                      (unsigned long long)B);
+  if (len_Q != B * g.m)
+    return fail(ctx, QPIR_E_DIMENSION, "len_Q: %llu != B*m %llu", (unsigned long long)len_Q,
+                (unsigned long long)(B * g.m));
+  if (len_ans != B * g.ell_local)
+    return fail(ctx, QPIR_E_DIMENSION, "len_ans: %llu != B*ell_local %llu",
+                (unsigned long long)len_ans, (unsigned long long)(B * g.ell_local));
+  DeviceGuard dg(ctx->device);
+  cudaStream_t st = (cudaStream_t)stream;
+  const int wq = where(Q, ctx->device), wa = where(ans_local, ctx->device);
+  if (wq < 0 || wa < 0) return fail(ctx, QPIR_E_PARAM, "Q/ans_local: memory of another device");
+  const uint64_t ncols = 4 * B;
+  const uint32_t BN = pick_bn(ncols);
+  const uint32_t Npad = (uint32_t)round_up(ncols, BN);
+  int rc = ensure(ctx, (void**)&ctx->limbs, &ctx->limbs_bytes, (uint64_t)Npad * g.m_pad);
+  if (rc) return rc;
+  const uint32_t* Qd = Q;
+  if (wq == 0) {
+    rc = ensure(ctx, (void**)&ctx->big_in, &ctx->big_in_bytes, len_Q * 4);
+    if (rc) return rc;
+    CUDA_TRY(ctx, cudaMemcpyAsync(ctx->big_in, Q, len_Q * 4, cudaMemcpyHostToDevice, st));
+    Qd = ctx->big_in;
+  }
+  uint32_t* out = ans_local;
+  if (wa == 0) {
+    rc = ensure(ctx, (void**)&ctx->big_out, &ctx->big_out_bytes, len_ans * 4);
+    if (rc) return rc;
+    out = ctx->big_out;
+  }
+  {
+    const uint32_t nq = Npad / 4;  // padded query slots
+    dim3 grid((nq + 127) / 128, (uint32_t)g.G);
+    limb_split_kernel<<<grid, 128, 0, st>>>(Qd, ctx->limbs, (uint32_t)B, (uint32_t)g.m,
+                                            (uint32_t)g.G, Npad);
+    LAUNCH_CHECK(ctx);
+  }
+  rc = launch_mma<OUT_QUERY_MAJOR>(ctx, BN, ctx->limbs, Npad, out, (uint32_t)B,
+                                   (uint32_t)g.ell_local, st);
+  if (rc) return rc;
+  if (wa == 0) {
+    CUDA_TRY(ctx, cudaMemcpyAsync(ans_local, out, len_ans * 4, cudaMemcpyDeviceToHost, st));
+    CUDA_TRY(ctx, cudaStreamSynchronize(st));
+  }
+  return QPIR_OK;
+}
+
+int qpir_hint(qpir_ctx* ctx, uint32_t* H_local, uint64_t len_H, void* stream) {
+  if (!ctx) return fail(nullptr, QPIR_E_STATE, "ctx: NULL");
+  const Geometry& g = ctx->geo;
+  if (!H_local) return fail(ctx, QPIR_E_PARAM, "H_local: NULL");
+  if (len_H != g.ell_local * g.lwe_n)
+    return fail(ctx, QPIR_E_DIMENSION, "len_H: %llu != ell_local*n %llu",
+                (unsigned long long)len_H, (unsigned long long)(g.ell_local * g.lwe_n));
+  DeviceGuard dg(ctx->device);
+  cudaStream_t st = (cudaStream_t)stream;
+  const int wh = where(H_local, ctx->device);
+  if (wh < 0) return fail(ctx, QPIR_E_PARAM, "H_local: memory of another device");
+  const uint64_t ncols = 4ull * g.lwe_n;
+  const uint32_t BN = pick_bn(ncols);
+  const uint32_t Npad = (uint32_t)round_up(ncols, BN);
+  int rc = ensure(ctx, (void**)&ctx->limbs, &ctx->limbs_bytes, (uint64_t)Npad * g.m_pad);
+  if (rc) return rc;
+  uint32_t* out = H_local;
+  if (wh == 0 || !aligned16(H_local)) {
+    rc = ensure(ctx, (void**)&ctx->big_out, &ctx->big_out_bytes, len_H * 4);
+    if (rc) return rc;
+    out = ctx->big_out;
+  }
+  {
+    const uint32_t nb = Npad / 16;  // Philox blocks (4 outputs x 4 limbs)
+    dim3 grid((nb + 127) / 128, (uint32_t)g.G);
+    expand_A_limbs_kernel<<<grid, 128, 0, st>>>(ctx->limbs, g.seed_A, (uint32_t)g.m, g.lwe_n,
+                                                (uint32_t)g.G, Npad);
+    LAUNCH_CHECK(ctx);
+  }
+  rc = launch_mma<OUT_ROW_MAJOR>(ctx, BN, ctx->limbs, Npad, out, g.lwe_n, g.lwe_n, st);
+  if (rc) return rc;
+  if (out != H_local) {
+    CUDA_TRY(ctx, cudaMemcpyAsync(H_local, out, len_H * 4,
+                                  wh ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost, st));
+    if (!wh) CUDA_TRY(ctx, cudaStreamSynchronize(st));
+  }
+  return QPIR_OK;
+}
+
+uint64_t qpir_kernel_launches(const qpir_ctx* ctx) { return ctx ? ctx->launches : 0; }
+
+const char* qpir_last_error(const qpir_ctx* ctx) {
+  return ctx ? ctx->err.c_str() : g_setup_error.c_str();
+}
+
+void qpir_destroy(qpir_ctx* ctx) {
+  if (!ctx) return;
+  DeviceGuard dg(ctx->device);
+  void* bufs[] = {ctx->D,         ctx->qu_dev, ctx->ans_dev, ctx->partial, ctx->tickets,
+                  ctx->rec_stage, ctx->limbs,  ctx->big_in,  ctx->big_out};
+  for (void* b : bufs)
+    if (b) cudaFree(b);
+  delete ctx;
+}
+
+}  // extern "C"

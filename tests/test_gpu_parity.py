@@ -1,0 +1,297 @@
+"""GPU parity: the CUDA path (through the C ABI) against the CPU oracle.
+
+Bar (DESIGN "Parity"): bit-exact u32 equality -- every result is a unique value
+in Z_{2^32}.  Expected values come only from oracle/ (or closed forms); inputs
+come only from synth/ (or the oracle's client for LWE queries).
+"""
+import numpy as np
+import pytest
+import torch
+
+import synth
+from oracle import oracle as O
+
+pytestmark = pytest.mark.gpu
+M32 = (1 << 32) - 1
+
+
+def _srv():
+    import paper_2510_03631_b200 as P
+    return P
+
+
+def _u32(t):
+    return _srv().u32(t)
+
+
+def _db(n_cells, n_ch, d, m=0, seed=1):
+    rec = synth.records_np(seed, n_cells * n_ch, d, n_ch)
+    D = O.pack(rec, n_cells, n_ch, d, m or n_cells)
+    return rec, D
+
+
+# ------------------------------------------------------------------ GEMV (a3)
+def test_answer_tiny_host_and_device(cuda_ok):
+    P = _srv()
+    n_cells, n_ch, d = 1024, 16, 8  # BASELINE.json configs[0]
+    rec, D = _db(n_cells, n_ch, d)
+    qu = synth.uniform_u32_np(2, (n_cells,))
+    want = O.answer(D, qu)
+    with P.PirServer(n_cells, n_ch, d, records=rec) as s:  # host records
+        out = np.empty(s.ell_local, np.uint32)
+        s.answer(qu, out=out)  # host in, host out
+        assert (out == want).all()
+        got = s.answer(torch.from_numpy(qu.view(np.int32)).cuda())  # device in/out
+        assert (_u32(got) == want).all()
+        assert s.kernel_launches >= 2
+    with P.PirServer(n_cells, n_ch, d, records=torch.from_numpy(rec).cuda()) as s:  # device records
+        assert (_u32(s.answer(qu)) == want).all()
+
+
+RAGGED = [
+    # n_cells, n_ch, d, m   (m=0 -> n_cells)
+    (1000, 3, 5, 0),      # m not a multiple of 16/128, ell = 15 rows
+    (333, 7, 11, 100),    # cells wrap into 4 row blocks (SimplePIR packing)
+    (17, 1, 1, 0),        # single tiny row
+    (4096, 40, 64, 0),    # 2560 rows, 4096 columns
+    (2500, 9, 37, 640),   # several blocks, ragged everything
+]
+
+
+@pytest.mark.parametrize("geo", RAGGED)
+@pytest.mark.parametrize("cfg", [dict(), dict(QPIR_GEMV_U="1", QPIR_GEMV_SPLIT="3", QPIR_GEMV_CHUNK="8"),
+                                 dict(QPIR_GEMV_U="4", QPIR_GEMV_SPLIT="1", QPIR_GEMV_CHUNK="4")])
+def test_answer_ragged(cuda_ok, geo, cfg, monkeypatch):
+    for k, v in cfg.items():
+        monkeypatch.setenv(k, v)
+    P = _srv()
+    n_cells, n_ch, d, m = geo
+    rec, D = _db(n_cells, n_ch, d, m, seed=3)
+    with P.PirServer(n_cells, n_ch, d, m=m, records=rec) as s:
+        assert s.ell == D.shape[0] and s.m == D.shape[1]
+        for seed in (4, 5):
+            qu = synth.uniform_u32_np(seed, (s.m,))
+            assert (_u32(s.answer(qu)) == O.answer(D, qu)).all()
+        # closed form: all-0xFFFFFFFF query -> -row sums
+        qf = np.full(s.m, M32, np.uint32)
+        want = (-D.astype(np.int64).sum(1)) & M32
+        assert (_u32(s.answer(qf)).astype(np.int64) == want).all()
+
+
+def test_shards_concatenate(cuda_ok):
+    """P6: row shards answered separately concatenate to the unsharded answer."""
+    P = _srv()
+    n_cells, n_ch, d = 2048, 8, 24
+    rec, D = _db(n_cells, n_ch, d, seed=6)
+    qu = synth.uniform_u32_np(7, (n_cells,))
+    want = O.answer(D, qu)
+    rec_dev = torch.from_numpy(rec).cuda()
+    from paper_2510_03631_b200.dist import shard_rows
+    for world in (1, 2, 3, 8):
+        parts = []
+        for r in range(world):
+            r0, r1 = shard_rows(n_cells, n_ch, d, n_cells, world, r)
+            with P.PirServer(n_cells, n_ch, d, row_begin=r0, row_end=r1, records=rec_dev) as s:
+                assert s.ell_local == r1 - r0
+                parts.append(_u32(s.answer(qu)))
+        assert (np.concatenate(parts) == want).all()
+
+
+def test_db_write_streaming(cuda_ok):
+    """Streaming the DB in odd-sized chunks gives the same D as one-shot setup."""
+    P = _srv()
+    n_cells, n_ch, d = 1500, 5, 12
+    rec, D = _db(n_cells, n_ch, d, m=512, seed=8)
+    qu = synth.uniform_u32_np(9, (512,))
+    with P.PirServer(n_cells, n_ch, d, m=512) as s:
+        n = n_cells * n_ch
+        t = 0
+        for k, step in enumerate((1, 7, 333, 1000, 5000)):
+            chunk = rec[t:t + step]
+            src = torch.from_numpy(chunk).cuda() if k % 2 else chunk
+            s.db_write(t, src)
+            t += chunk.shape[0]
+        s.db_write(t, rec[t:n])
+        assert (_u32(s.answer(qu)) == O.answer(D, qu)).all()
+
+
+def test_wraparound_kat_gemv_and_tc(cuda_ok):
+    """P9: all-0xFF D times all-0xFFFFFFFF queries, K = 65536: every byte-limb sum
+    is 255*255*65536 = 4,261,478,400 > 2^31, so the GEMV's dp4a accumulators and
+    the tensor-core s32 accumulators must wrap (not saturate).  Expected value in
+    closed form: sum_c 255 * (2^32 - 1) = -255 * m mod 2^32."""
+    P = _srv()
+    n_cells, n_ch, d = 65536, 1, 128
+    rec = np.full((n_cells * n_ch, d), 255, np.uint8)
+    want = (-255 * n_cells) & M32
+    with P.PirServer(n_cells, n_ch, d, records=rec) as s:
+        qf = np.full(n_cells, M32, np.uint32)
+        assert (_u32(s.answer(qf)) == want).all()
+        Q = np.full((4, n_cells), M32, np.uint32)
+        ans = _u32(s.answer_batch(Q))
+        assert (ans == want).all()
+
+
+# ------------------------------------------------------------------ batch (a6)
+@pytest.mark.parametrize("B", [1, 3, 8, 64, 65, 200])
+def test_answer_batch_small(cuda_ok, B):
+    P = _srv()
+    n_cells, n_ch, d, m = 1200, 6, 30, 0
+    rec, D = _db(n_cells, n_ch, d, m, seed=10)
+    Q = synth.uniform_u32_np(11 + B, (B, n_cells))
+    want = O.answer_batch(D, Q)
+    with P.PirServer(n_cells, n_ch, d, records=rec) as s:
+        got = _u32(s.answer_batch(Q))
+        assert got.shape == want.shape
+        assert (got == want).all()
+        # P6: column j of the batch == single answer of query j (host in/out too)
+        out = np.empty((B, s.ell_local), np.uint32)
+        s.answer_batch(Q, out=out)
+        assert (out == want).all()
+        j = B // 2
+        assert (_u32(s.answer(Q[j])) == got[j]).all()
+
+
+def test_answer_batch_ragged_shard(cuda_ok):
+    P = _srv()
+    n_cells, n_ch, d, m = 999, 5, 33, 333
+    rec, D = _db(n_cells, n_ch, d, m, seed=12)
+    Q = synth.uniform_u32_np(13, (37, m))
+    r0, r1 = 31, 401
+    with P.PirServer(n_cells, n_ch, d, m=m, row_begin=r0, row_end=r1, records=rec) as s:
+        assert (_u32(s.answer_batch(Q)) == O.answer_batch(D[r0:r1], Q)).all()
+
+
+# ------------------------------------------------------------------ hint (a7)
+@pytest.mark.parametrize("n", [4, 9, 64, 1024])
+def test_hint_small(cuda_ok, n):
+    P = _srv()
+    n_cells, n_ch, d = 700, 4, 20
+    rec, D = _db(n_cells, n_ch, d, seed=14)
+    seed_A = 0xDEADBEEF12345678
+    A = O.expand_A(seed_A, n_cells, n)
+    want = O.hint(D, A)
+    with P.PirServer(n_cells, n_ch, d, lwe_n=n, seed_A=seed_A, records=rec) as s:
+        got = _u32(s.hint())
+        assert got.shape == want.shape
+        assert (got == want).all()
+        host = np.empty((s.ell_local, n), np.uint32)
+        s.hint(out=host)
+        assert (host == want).all()
+
+
+# ------------------------------------------------------------------ LWE end to end
+def test_lwe_end_to_end_tiny_bruteforce(cuda_ok):
+    """P1 through the GPU path: hint and answers from the CUDA kernels, queries
+    and decode from the oracle client; every one of the 16384 records of the
+    tiny DB (BASELINE.json configs[0]) must decode exactly."""
+    P = _srv()
+    n_cells, n_ch, d, n = 1024, 16, 8, 1024
+    rec, D = _db(n_cells, n_ch, d, seed=15)
+    seed_A = 77
+    A = O.expand_A(seed_A, n_cells, n)
+    s_key = O.keygen(78, n)
+    Q = np.stack([O.query(A, s_key, 79, c, 6.4, c)[0] for c in range(n_cells)])
+    with P.PirServer(n_cells, n_ch, d, lwe_n=n, seed_A=seed_A, records=rec) as s:
+        H = _u32(s.hint())
+        assert (H == O.hint(D, A)).all()
+        ANS = _u32(s.answer_batch(Q))  # all 1024 queries in one batch
+        for c in (0, 511, 1023):
+            assert (_u32(s.answer(Q[c])) == ANS[c]).all()
+    rows = np.arange(n_ch * d, dtype=np.uint64)
+    bad = 0
+    for c in range(n_cells):
+        got = O.decode(ANS[c], H, s_key, rows).reshape(n_ch, d)
+        bad += int((got != rec[c * n_ch:(c + 1) * n_ch]).sum())
+    assert bad == 0
+
+
+# ------------------------------------------------------------------ full sizes
+def _setup_synth_db(P, n_cells, n_ch, d, seed, chunk_cells=2048, **kw):
+    s = P.PirServer(n_cells, n_ch, d, **kw)
+    for c0 in range(0, n_cells, chunk_cells):
+        nc = min(chunk_cells, n_cells - c0)
+        r = synth.records(seed, c0 * n_ch, nc * n_ch, d, n_ch, device="cuda")
+        s.db_write(c0 * n_ch, r)
+    torch.cuda.synchronize()
+    return s
+
+
+def _sampled_rows(seed, rows, n_cells, n_ch, d):
+    """Rows of D (m = n_cells) regenerated from synth, for sampled exact checks."""
+    cells = torch.arange(n_cells, dtype=torch.int64)
+    out = np.empty((len(rows), n_cells), np.uint8)
+    for i, r in enumerate(rows):
+        ch, b = divmod(int(r), d)
+        out[i] = synth.byte_column(seed, cells * n_ch + ch, b, d, n_ch).numpy()
+    return out
+
+
+def test_c2_regional_full(cuda_ok):
+    """BASELINE.json configs[1]: 8192 cells x 40 ch x 3072 B = 1.007 GB, exact
+    full answer vs the oracle."""
+    P = _srv()
+    n_cells, n_ch, d = 8192, 40, 3072
+    seed = 21
+    s = _setup_synth_db(P, n_cells, n_ch, d, seed)
+    rec = synth.records(seed, 0, n_cells * n_ch, d, n_ch, device="cuda").cpu().numpy()
+    D = O.pack(rec, n_cells, n_ch, d, n_cells)
+    del rec
+    qu = synth.uniform_u32_np(22, (n_cells,))
+    assert (_u32(s.answer(qu)) == O.answer(D, qu)).all()
+    s.close()
+
+
+@pytest.mark.slow
+def test_c3_nationwide_sampled(cuda_ok):
+    """configs[2] on one GPU: 262144 cells x 40 x 3072 = 32.2 GB; 48 sampled rows exact."""
+    P = _srv()
+    n_cells, n_ch, d = 262144, 40, 3072
+    seed = 23
+    s = _setup_synth_db(P, n_cells, n_ch, d, seed)
+    qu = synth.uniform_u32_np(24, (n_cells,))
+    got = _u32(s.answer(qu))
+    rng = np.random.default_rng(0)
+    rows = np.concatenate([[0, 1, s.ell - 1], rng.choice(s.ell, 45, replace=False)])
+    Dr = _sampled_rows(seed, rows, n_cells, n_ch, d)
+    assert (got[rows] == O.answer(Dr, qu)).all()
+    s.close()
+
+
+@pytest.mark.slow
+@pytest.mark.parametrize("B", [64, 256])
+def test_c4_batch_sampled(cuda_ok, B):
+    """configs[3]: 65536 cells x 40 x 3072 = 8.05 GB, B concurrent queries;
+    24 sampled rows exact for all B queries, + 2 columns == single answers."""
+    P = _srv()
+    n_cells, n_ch, d = 65536, 40, 3072
+    seed = 25
+    s = _setup_synth_db(P, n_cells, n_ch, d, seed)
+    Q = synth.uniform_u32_np(26, (B, n_cells))
+    ANS = _u32(s.answer_batch(Q))
+    rng = np.random.default_rng(1)
+    rows = np.concatenate([[0, s.ell - 1], rng.choice(s.ell, 22, replace=False)])
+    Dr = _sampled_rows(seed, rows, n_cells, n_ch, d)
+    assert (ANS[:, rows] == O.answer_batch(Dr, Q)).all()
+    for j in (0, B - 1):
+        assert (_u32(s.answer(Q[j])) == ANS[j]).all()
+    s.close()
+
+
+@pytest.mark.slow
+def test_c5_hint_shard_sampled(cuda_ok):
+    """configs[4], one rank's shard at G = 8: rows [0, 15360) of the 32 GB DB,
+    n = 1024; 12 sampled rows of H exact against the oracle's D.A."""
+    P = _srv()
+    n_cells, n_ch, d, n = 262144, 40, 3072, 1024
+    seed, seed_A = 27, 0x5EED
+    from paper_2510_03631_b200.dist import shard_rows
+    r0, r1 = shard_rows(n_cells, n_ch, d, n_cells, 8, 0)
+    s = _setup_synth_db(P, n_cells, n_ch, d, seed, lwe_n=n, seed_A=seed_A, row_begin=r0, row_end=r1)
+    H = _u32(s.hint())
+    rng = np.random.default_rng(2)
+    rows = np.concatenate([[0, r1 - r0 - 1], rng.choice(r1 - r0, 10, replace=False)])
+    Dr = _sampled_rows(seed, rows + r0, n_cells, n_ch, d)
+    A = O.expand_A(seed_A, n_cells, n)
+    assert (H[rows] == O.hint(Dr, A)).all()
+    s.close()
