@@ -1,0 +1,77 @@
+"""Multi-rank host logic on CPU (gloo, world_size 2): whole-channel row
+shards and the answer gather reassemble the unsharded answer exactly.  The
+per-rank slice answers come from the oracle here (no GPU); on the GPU box the
+same gather runs over NCCL on the kernels' slices (bench.py, N > 1)."""
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+from paper_2510_03631_b200.dist import gather_answer, shard_rows
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def _worker(rank, world, port, geo, B, q):
+    import synth
+    from oracle import oracle as O
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        n_cells, n_ch, d, m = geo
+        rec = synth.records_np(3, n_cells * n_ch, d, n_ch)
+        D = O.pack(rec, n_cells, n_ch, d, m)
+        bounds = [shard_rows(n_cells, n_ch, d, m, world, r) for r in range(world)]
+        sizes = [b - a for a, b in bounds]
+        r0, r1 = bounds[rank]
+        Q = synth.uniform_u32_np(4, (B, m))
+        local = O.answer_batch(D[r0:r1], Q)              # [B, ell_local]
+        t = torch.from_numpy(local.view(np.int32))
+        if B == 1:
+            t = t[0]
+        full = gather_answer(t, sizes).numpy().view(np.uint32)
+        want = O.answer_batch(D, Q)
+        ok = bool((full == (want[0] if B == 1 else want)).all())
+        q.put((rank, ok, sizes))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("geo,B", [((64, 4, 6, 64), 1), ((50, 3, 5, 16), 1), ((40, 5, 4, 40), 3)])
+def test_gather_reassembles_answer(geo, B):
+    world = 2
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker, args=(r, world, port, geo, B, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = [q.get(timeout=120) for _ in range(world)]
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    assert all(ok for _, ok, _ in res), res
+
+
+def test_shard_rows_whole_channels():
+    # 122880 rows = 40 channels x 3072 B: whole channels per rank for G = 1..8
+    for world in (1, 2, 4, 8):
+        b = [shard_rows(262144, 40, 3072, 262144, world, r) for r in range(world)]
+        assert b[0][0] == 0 and b[-1][1] == 40 * 3072
+        assert all(x[1] == y[0] for x, y in zip(b, b[1:]))
+        assert all((e - s) % 3072 == 0 and (e - s) == 122880 // world for s, e in b)
+    # uneven: 3 channel units over 2 ranks -> 2 + 1
+    assert [shard_rows(10, 3, 5, 10, 2, r) for r in range(2)] == [(0, 10), (10, 15)]
+    with pytest.raises(ValueError):
+        shard_rows(10, 1, 5, 10, 2, 0)
