@@ -16,13 +16,14 @@ namespace qpir {
 // coalesce and the 16-byte writes are contiguous.
 struct PackArgs {
   const uint8_t* rec;
-  uint8_t* D;          // [G][L][16]
+  uint8_t* D;          // 128-row panels: [L/128][G][128][16]
   uint64_t theta0, n_rec;
   uint64_t row_begin;  // global row of local row 0
   uint32_t ell_local, L;
   uint32_t n_ch, d, m;
   uint64_t n_cells;
   uint32_t g_lo;       // first column group of the launch (grid.x offset)
+  uint32_t G;          // column groups per panel
 };
 
 __global__ void pack_records_kernel(PackArgs a) {
@@ -35,7 +36,8 @@ __global__ void pack_records_kernel(PackArgs a) {
   const uint32_t rr = (uint32_t)(row % per_blk);
   const uint32_t ch = rr / a.d;
   const uint32_t b = rr % a.d;
-  uint4* dst = reinterpret_cast<uint4*>(a.D + ((size_t)j * a.L + rl) * 16);
+  uint4* dst = reinterpret_cast<uint4*>(a.D + ((size_t)(rl >> 7) * a.G + j) * 2048 +
+                                        (rl & 127u) * 16);
   uint4 v = *dst;
   uint8_t* bytes = reinterpret_cast<uint8_t*>(&v);
   bool touched = false;
@@ -55,11 +57,19 @@ __global__ void pack_records_kernel(PackArgs a) {
 
 // ---------------------------------------------------------------- a6 limbs
 // Q (B x m u32, query-major) -> Q' = byte-limb planes as the MMA B operand,
-// K-major, 16-cell interleaved like D:  Q'[g][n][i] = limb k of Q[j][16g + i],
-// n = 4j + k (k = 0..3), zero for padding (n >= 4B or 16g + i >= m).
-// One thread per (query j, group g): 64 B in, 4 x 16 B out (64 B contiguous).
+// K-major, 16-cell interleaved like D, in BN-column panels:
+//   byte i of (limb column n, group g) at ((n / BN) * G + g) * BN * 16 + (n % BN) * 16 + i
+//   = limb k of Q[j][16g + i], n = 4j + k (k = 0..3); zero for padding
+// (n >= 4B or 16g + i >= m).  One MMA B tile (BN columns x 8 groups) is then
+// BN * 128 contiguous bytes.  One thread per (query j, group g): 64 B in,
+// 4 x 16 B out (64 B contiguous).
+__device__ __forceinline__ size_t limb_off(uint32_t n, uint32_t g, uint32_t G, uint32_t BN) {
+  return (((size_t)(n / BN) * G + g) * BN + (n % BN)) * 16;
+}
+
 __global__ void limb_split_kernel(const uint32_t* __restrict__ Q, uint8_t* __restrict__ Qp,
-                                  uint32_t B, uint32_t m, uint32_t G, uint32_t Npad) {
+                                  uint32_t B, uint32_t m, uint32_t G, uint32_t Npad,
+                                  uint32_t BN) {
   const uint32_t jq = blockIdx.x * blockDim.x + threadIdx.x;  // padded query index
   const uint32_t g = blockIdx.y;
   if (jq * 4u >= Npad) return;
@@ -69,7 +79,7 @@ __global__ void limb_split_kernel(const uint32_t* __restrict__ Q, uint8_t* __res
     const uint32_t c = g * 16u + i;
     q[i] = (jq < B && c < m) ? __ldg(Q + (size_t)jq * m + c) : 0u;
   }
-  uint4* dst = reinterpret_cast<uint4*>(Qp + ((size_t)g * Npad + jq * 4u) * 16);
+  uint4* dst = reinterpret_cast<uint4*>(Qp + limb_off(jq * 4u, g, G, BN));
 #pragma unroll
   for (uint32_t k = 0; k < 4; ++k) {
     uint4 w;
@@ -101,10 +111,10 @@ __device__ __forceinline__ uint4 philox4x32_10(uint4 ctr, uint2 key) {
   return ctr;
 }
 
-// A' [g][n][i] = limb k of A[16g + i][j], n = 4j + k; one thread per
+// A' (same panel layout as Q') = limb k of A[16g + i][j], n = 4j + k; one thread per
 // (group g, Philox block jb = j >> 2): 16 Philox calls, 256 contiguous bytes out.
 __global__ void expand_A_limbs_kernel(uint8_t* __restrict__ Ap, uint64_t seed, uint32_t m,
-                                      uint32_t n, uint32_t G, uint32_t Npad) {
+                                      uint32_t n, uint32_t G, uint32_t Npad, uint32_t BN) {
   const uint32_t jb = blockIdx.x * blockDim.x + threadIdx.x;
   const uint32_t g = blockIdx.y;
   if (jb * 16u >= Npad) return;
@@ -120,7 +130,7 @@ __global__ void expand_A_limbs_kernel(uint8_t* __restrict__ Ap, uint64_t seed, u
     a[i][2] = (jb * 4u + 2 < n) ? v.z : 0u;
     a[i][3] = (jb * 4u + 3 < n) ? v.w : 0u;
   }
-  uint4* dst = reinterpret_cast<uint4*>(Ap + ((size_t)g * Npad + jb * 16u) * 16);
+  uint4* dst = reinterpret_cast<uint4*>(Ap + limb_off(jb * 16u, g, G, BN));
 #pragma unroll
   for (int jj = 0; jj < 4; ++jj) {
 #pragma unroll

@@ -3,10 +3,12 @@
 // contraction of Alg. 4 steps 14-15, with q = 2^32).
 //
 // HBM-bound: every byte of the D shard is read exactly once per query.
-// D layout in HBM (DESIGN "Data layout"): 16-cell interleaved column groups,
-//   D[r][c] at ((c >> 4) * L + r) * 16 + (c & 15),   L = padded row count,
-// so one thread's 128-bit load holds 16 consecutive cells of one row and a
-// warp's load covers 32 consecutive rows = 512 contiguous bytes.
+// D layout in HBM (DESIGN "Data layout"): 128-row panels of 16-cell interleaved
+// column groups,
+//   D[r][c] at ((r >> 7) * G + (c >> 4)) * 2048 + (r & 127) * 16 + (c & 15),
+// so one thread's 128-bit load holds 16 consecutive cells of one row, a warp's
+// load covers 32 consecutive rows = 512 contiguous bytes, and each panel is one
+// contiguous stream of G * 2 KB that a CTA walks front to back.
 //
 // Query ingest (a2) is fused: each CTA splits its slice of qu into 4 byte-limb
 // planes in shared memory, laid out so that one 32-bit word holds limb k of 4
@@ -93,7 +95,7 @@ __device__ __forceinline__ void dp4a_group(const uint4& d, const uint4& l0, cons
 }
 
 struct GemvArgs {
-  const uint8_t* D;     // [G][L][16]
+  const uint8_t* D;     // [L/128][G][128][16]
   const uint32_t* qu;   // m (device)
   uint32_t* ans;        // ell_local (device)
   uint32_t* partial;    // [S][L] scratch (S > 1)
@@ -104,6 +106,7 @@ struct GemvArgs {
   uint32_t G;           // column groups (multiple of UNR)
   uint32_t gps;         // groups per split (multiple of UNR)
   uint32_t chunk;       // groups staged in smem at a time (multiple of UNR)
+  uint32_t split_major; // 1: blockIdx.x = split, blockIdx.y = row block (page-local order)
 };
 
 // U rows per thread (rows r, r + 128, ...); UNR column groups per iteration.
@@ -111,8 +114,12 @@ template <int U, int UNR>
 __global__ void __launch_bounds__(GEMV_THREADS) gemv_u8_u32_kernel(GemvArgs a) {
   extern __shared__ uint4 sL[];
   const uint32_t tid = threadIdx.x;
-  const uint32_t row0 = blockIdx.x * (GEMV_THREADS * U) + tid;
-  const uint32_t split = blockIdx.y;
+  // Grid order: with split_major the CTAs that run at the same time walk
+  // adjacent K ranges of the same row panels, i.e. few distinct 2 MB pages.
+  const uint32_t rblk = a.split_major ? blockIdx.y : blockIdx.x;
+  const uint32_t split = a.split_major ? blockIdx.x : blockIdx.y;
+  const uint32_t nsplit = a.split_major ? gridDim.x : gridDim.y;
+  const uint32_t row0 = rblk * (GEMV_THREADS * U) + tid;
   const uint32_t gb = split * a.gps;
   const uint32_t ge = min(a.G, gb + a.gps);
 
@@ -125,10 +132,10 @@ __global__ void __launch_bounds__(GEMV_THREADS) gemv_u8_u32_kernel(GemvArgs a) {
 #pragma unroll
   for (int u = 0; u < U; ++u) {
     const uint32_t r = row0 + u * GEMV_THREADS;
-    live[u] = r < a.L;
-    Drow[u] = a.D + (size_t)r * 16;
+    live[u] = r < a.ell_local;  // rows >= ell_local are zero padding: skip
+    Drow[u] = a.D + (size_t)(r >> 7) * a.G * 2048 + (r & 127u) * 16;
   }
-  const size_t gstride = (size_t)a.L * 16;
+  constexpr size_t gstride = 2048;
 
   for (uint32_t cb = gb; cb < ge; cb += a.chunk) {
     const uint32_t ce = min(ge, cb + a.chunk);
@@ -159,7 +166,7 @@ __global__ void __launch_bounds__(GEMV_THREADS) gemv_u8_u32_kernel(GemvArgs a) {
   for (int u = 0; u < U; ++u)
     out[u] = acc[u][0] + (acc[u][1] << 8) + (acc[u][2] << 16) + (acc[u][3] << 24);
 
-  if (gridDim.y == 1) {
+  if (nsplit == 1) {
 #pragma unroll
     for (int u = 0; u < U; ++u) {
       const uint32_t r = row0 + u * GEMV_THREADS;
@@ -178,8 +185,8 @@ __global__ void __launch_bounds__(GEMV_THREADS) gemv_u8_u32_kernel(GemvArgs a) {
   __shared__ uint32_t s_last;
   __syncthreads();
   if (tid == 0) {
-    const uint32_t t = atomicAdd(&a.tickets[blockIdx.x], 1u);
-    s_last = (t == gridDim.y - 1) ? 1u : 0u;
+    const uint32_t t = atomicAdd(&a.tickets[rblk], 1u);
+    s_last = (t == nsplit - 1) ? 1u : 0u;
   }
   __syncthreads();
   if (!s_last) return;
@@ -189,11 +196,11 @@ __global__ void __launch_bounds__(GEMV_THREADS) gemv_u8_u32_kernel(GemvArgs a) {
     const uint32_t r = row0 + u * GEMV_THREADS;
     if (r < a.ell_local) {
       uint32_t s = 0;
-      for (uint32_t k = 0; k < gridDim.y; ++k) s += __ldcg(a.partial + (size_t)k * a.L + r);
+      for (uint32_t k = 0; k < nsplit; ++k) s += __ldcg(a.partial + (size_t)k * a.L + r);
       a.ans[r] = s;
     }
   }
-  if (tid == 0) a.tickets[blockIdx.x] = 0u;
+  if (tid == 0) a.tickets[rblk] = 0u;
 }
 
 }  // namespace qpir

@@ -8,19 +8,21 @@
 // accumulation (no saturation: the idesc saturate bit is 0, sums wrap mod 2^32)
 // and the epilogue recombines  ANS[:, j] = sum_k 2^{8k} C[:, 4j + k]  mod 2^32.
 //
-// Structure (one CTA per SM, persistent over output tiles):
-//   warp 0     : producer -- 1-D bulk async copies (TMA engine) of the A tile
-//                (128 rows of D) and the B tile (BN limb columns) per K-block of
-//                128 bytes into a STAGES-deep smem ring, mbarrier complete_tx.
+// Structure (one CTA per SM, persistent over work units = tile x K-split):
+//   warp 0     : producer -- per K-block of 128 cells, one 1-D bulk async copy
+//                (TMA engine, SASS UBLKCP) per 128-row D panel (16 KB each) and
+//                one for the B tile (BN x 128 B), into a STAGES-deep smem ring;
+//                mbarrier complete_tx.
 //   warp 1     : TMEM allocator + MMA issuer -- one thread issues
-//                tcgen05.mma.cta_group::1.kind::i8 (M=128, N=BN, K=32) x 4 per
-//                K-block into a double-buffered TMEM accumulator, tcgen05.commit
-//                frees smem stages and signals the epilogue.
+//                tcgen05.mma.cta_group::1.kind::i8 (M = 128, N = BN, K = 32),
+//                MT x 4 per K-block (MT row panels share each B tile), into a
+//                TMEM accumulator (double-buffered when 2 * MT * BN <= 512 cols);
+//                tcgen05.commit frees smem stages and signals the epilogue.
 //   warps 2..5 : epilogue -- tcgen05.ld 32 lanes x 16 columns, limb recombine,
-//                coalesced u32 stores; then release the accumulator buffer.
-// Shared-memory operand layout = the global layout (16-cell interleave):
-// [8 groups][rows][16 B], i.e. the canonical no-swizzle K-major layout with
-// core matrices of 8 rows x 16 B contiguous (SBO = 128 B between 8-row core
+//                coalesced u32 stores (red.add when K is split), release TMEM.
+// The smem operand layout equals the global layout (16-cell interleave):
+// [8 groups][rows][16 B] = the canonical no-swizzle K-major layout, core
+// matrices of 8 rows x 16 B contiguous (SBO = 128 B between 8-row core
 // matrices, LBO = rows * 16 B between the two 16-byte K chunks of one MMA).
 #pragma once
 #include <cstdint>
@@ -29,42 +31,50 @@
 
 namespace qpir {
 
-constexpr uint32_t MMA_BM = 128;      // rows of D per tile (UMMA M)
-constexpr uint32_t MMA_BK = 128;      // K bytes (cells) per pipeline stage
-constexpr uint32_t MMA_GPB = MMA_BK / 16;  // column groups per stage (8)
+constexpr uint32_t MMA_BM = 128;           // rows of D per UMMA (M)
+constexpr uint32_t MMA_BK = 128;           // K padding unit of D (cells)
 constexpr uint32_t MMA_THREADS = 192;
 
 enum : int { OUT_QUERY_MAJOR = 0, OUT_ROW_MAJOR = 1 };
 
 struct MmaArgs {
-  const uint8_t* A;   // D shard [G][L][16]
-  const uint8_t* B;   // limbs   [G][Npad][16]
+  const uint8_t* A;   // D shard, 128-row panels [L/128][G][128][16]
+  const uint8_t* B;   // limbs, BN-column panels [Npad/BN][G][BN][16]
   uint32_t* out;
-  uint32_t L;         // padded rows of D (multiple of 128)
-  uint32_t Npad;      // padded limb columns (multiple of BN)
   uint32_t G;         // column groups (multiple of 8)
   uint32_t rows;      // valid output rows (ell_local)
   uint32_t n_out;     // valid outputs along N (queries B, or hint width n)
   uint32_t out_ld;    // query-major: ell_local; row-major: n
-  uint32_t m_tiles, n_tiles;
+  uint32_t m_tiles, n_tiles, splits, kps;  // work units = m_tiles * n_tiles * splits
 };
 
-template <uint32_t BN, uint32_t STAGES>
-struct MmaSmem {
-  static constexpr uint32_t A_BYTES = MMA_BM * MMA_BK;  // 16 KB
-  static constexpr uint32_t B_BYTES = BN * MMA_BK;
+// GPB = 16-cell column groups per pipeline stage (K-block = 16 * GPB cells).
+template <uint32_t BN, uint32_t MT, uint32_t GPB>
+struct MmaCfg {
+  static constexpr uint32_t KB_CELLS = 16 * GPB;
+  static constexpr uint32_t PANEL_BYTES = MMA_BM * KB_CELLS;  // one 128-row panel x one K-block
+  static constexpr uint32_t A_BYTES = MT * PANEL_BYTES;
+  static constexpr uint32_t B_BYTES = BN * KB_CELLS;
   static constexpr uint32_t STAGE_BYTES = A_BYTES + B_BYTES;
+  static constexpr uint32_t STAGES_RAW = (200u * 1024u) / STAGE_BYTES;
+  static constexpr uint32_t STAGES = STAGES_RAW > 12 ? 12 : STAGES_RAW;
+  static constexpr uint32_t ACC_COLS = MT * BN;  // one accumulator buffer
+  static constexpr uint32_t ACC_BUFS = (2 * ACC_COLS <= 512) ? 2 : 1;
+  static constexpr uint32_t NEED_COLS = ACC_BUFS * ACC_COLS;
+  static constexpr uint32_t TMEM_COLS =
+      NEED_COLS <= 32 ? 32 : NEED_COLS <= 64 ? 64 : NEED_COLS <= 128 ? 128 : NEED_COLS <= 256 ? 256 : 512;
   static constexpr uint32_t BAR_OFF = STAGES * STAGE_BYTES;
   // full[STAGES], empty[STAGES], tfull[2], tempty[2], tmem addr
   static constexpr uint32_t TOTAL = BAR_OFF + (2 * STAGES + 4) * 8 + 16;
-  static constexpr uint32_t TMEM_COLS = (2 * BN < 32) ? 32 : 2 * BN;
+  static_assert(ACC_COLS <= 512, "accumulator exceeds TMEM");
 };
 
-template <uint32_t BN, uint32_t STAGES, int OUT_MODE>
+template <uint32_t BN, uint32_t MT, uint32_t GPB, int OUT_MODE>
 __global__ void __launch_bounds__(MMA_THREADS, 1) mma_u8_limb_kernel(MmaArgs a) {
-  using S = MmaSmem<BN, STAGES>;
+  using C = MmaCfg<BN, MT, GPB>;
+  constexpr uint32_t STAGES = C::STAGES;
   extern __shared__ __align__(1024) uint8_t smem[];
-  uint64_t* full = reinterpret_cast<uint64_t*>(smem + S::BAR_OFF);
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + C::BAR_OFF);
   uint64_t* empty = full + STAGES;
   uint64_t* tfull = empty + STAGES;
   uint64_t* tempty = tfull + 2;
@@ -72,8 +82,8 @@ __global__ void __launch_bounds__(MMA_THREADS, 1) mma_u8_limb_kernel(MmaArgs a) 
 
   const uint32_t warp = threadIdx.x / 32;
   const uint32_t lane = threadIdx.x % 32;
-  const uint32_t num_tiles = a.m_tiles * a.n_tiles;
-  const uint32_t kblocks = a.G / MMA_GPB;
+  const uint32_t num_units = a.m_tiles * a.n_tiles * a.splits;
+  const uint32_t kblocks = a.G / GPB;
 
   if (threadIdx.x == 0) {
     for (uint32_t s = 0; s < STAGES; ++s) {
@@ -86,31 +96,45 @@ __global__ void __launch_bounds__(MMA_THREADS, 1) mma_u8_limb_kernel(MmaArgs a) 
     }
     fence_mbarrier_init();
   }
-  if (warp == 1) tmem_alloc(tmem_slot, S::TMEM_COLS);
+  if (warp == 1) tmem_alloc(tmem_slot, C::TMEM_COLS);
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
 
+  // unit -> (m tile, n tile, split); n and split fastest so that CTAs running
+  // at the same time share the D panels of one m tile through L2.
+  auto decode = [&](uint32_t u, uint32_t& mt, uint32_t& nt, uint32_t& kb0, uint32_t& kb1) {
+    const uint32_t per_m = a.n_tiles * a.splits;
+    mt = u / per_m;
+    const uint32_t r = u % per_m;
+    nt = r / a.splits;
+    const uint32_t s = r % a.splits;
+    kb0 = s * a.kps;
+    kb1 = min(kblocks, kb0 + a.kps);
+  };
+
   if (warp == 0) {
     // ------------------------------------------------------------ producer
     if (lane == 0) {
       uint32_t stage = 0, phase = 0;
-      for (uint32_t tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
-        const uint32_t mt = tile / a.n_tiles, nt = tile % a.n_tiles;
-        const uint8_t* srcA = a.A + (size_t)mt * MMA_BM * 16;
-        const uint8_t* srcB = a.B + (size_t)nt * BN * 16;
-        for (uint32_t kb = 0; kb < kblocks; ++kb) {
+      for (uint32_t u = blockIdx.x; u < num_units; u += gridDim.x) {
+        uint32_t mt, nt, kb0, kb1;
+        decode(u, mt, nt, kb0, kb1);
+        for (uint32_t kb = kb0; kb < kb1; ++kb) {
           mbar_wait(&empty[stage], phase ^ 1);
-          mbar_arrive_expect_tx(&full[stage], S::STAGE_BYTES);
-          uint8_t* dA = smem + stage * S::STAGE_BYTES;
-          uint8_t* dB = dA + S::A_BYTES;
+          mbar_arrive_expect_tx(&full[stage], C::STAGE_BYTES);
+          uint8_t* dst = smem + stage * C::STAGE_BYTES;
 #pragma unroll
-          for (uint32_t i = 0; i < MMA_GPB; ++i) {
-            const size_t g = (size_t)kb * MMA_GPB + i;
-            bulk_g2s(dA + i * (MMA_BM * 16), srcA + g * a.L * 16, MMA_BM * 16, &full[stage]);
-            bulk_g2s(dB + i * (BN * 16), srcB + g * a.Npad * 16, BN * 16, &full[stage]);
+          for (uint32_t p = 0; p < MT; ++p) {
+            const size_t panel = (size_t)mt * MT + p;
+            bulk_g2s(dst + p * C::PANEL_BYTES,
+                     a.A + (panel * a.G + (size_t)kb * GPB) * 2048, C::PANEL_BYTES,
+                     &full[stage]);
           }
+          bulk_g2s(dst + C::A_BYTES,
+                   a.B + ((size_t)nt * a.G + (size_t)kb * GPB) * (BN * 16), C::B_BYTES,
+                   &full[stage]);
           if (++stage == STAGES) { stage = 0; phase ^= 1; }
         }
       }
@@ -119,69 +143,96 @@ __global__ void __launch_bounds__(MMA_THREADS, 1) mma_u8_limb_kernel(MmaArgs a) 
     // ------------------------------------------------------------ MMA issuer
     constexpr uint32_t idesc = idesc_i8_u8u8_s32(MMA_BM, BN);
     uint32_t stage = 0, phase = 0, acc = 0, acc_phase = 0;
-    for (uint32_t tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
+    for (uint32_t u = blockIdx.x; u < num_units; u += gridDim.x) {
+      uint32_t mt, nt, kb0, kb1;
+      decode(u, mt, nt, kb0, kb1);
       mbar_wait(&tempty[acc], acc_phase ^ 1);
       tc_fence_after();
-      const uint32_t d_tmem = tmem_base + acc * BN;
-      for (uint32_t kb = 0; kb < kblocks; ++kb) {
+      const uint32_t d_tmem = tmem_base + acc * C::ACC_COLS;
+      for (uint32_t kb = kb0; kb < kb1; ++kb) {
         mbar_wait(&full[stage], phase);
         tc_fence_after();
         if (lane == 0) {
-          const uint32_t sA = smem_u32(smem + stage * S::STAGE_BYTES);
-          const uint32_t sB = sA + S::A_BYTES;
+          const uint32_t sA = smem_u32(smem + stage * C::STAGE_BYTES);
+          const uint32_t sB = sA + C::A_BYTES;
 #pragma unroll
-          for (uint32_t k = 0; k < MMA_BK / 32; ++k) {
-            const uint64_t da = smem_desc_noswizzle(sA + k * 2 * (MMA_BM * 16), MMA_BM * 16, 128);
+          for (uint32_t k = 0; k < C::KB_CELLS / 32; ++k) {
             const uint64_t db = smem_desc_noswizzle(sB + k * 2 * (BN * 16), BN * 16, 128);
-            mma_i8_ss(d_tmem, da, db, idesc, (kb | k) != 0u);
+#pragma unroll
+            for (uint32_t p = 0; p < MT; ++p) {
+              const uint64_t da = smem_desc_noswizzle(
+                  sA + p * C::PANEL_BYTES + k * 2 * (MMA_BM * 16), MMA_BM * 16, 128);
+              mma_i8_ss(d_tmem + p * BN, da, db, idesc, (kb > kb0 || k > 0) ? 1u : 0u);
+            }
           }
           mma_commit(&empty[stage]);
-          if (kb + 1 == kblocks) mma_commit(&tfull[acc]);
+          if (kb + 1 == kb1) mma_commit(&tfull[acc]);
         }
         __syncwarp();
         if (++stage == STAGES) { stage = 0; phase ^= 1; }
       }
-      if (++acc == 2) { acc = 0; acc_phase ^= 1; }
+      if (++acc == C::ACC_BUFS) { acc = 0; acc_phase ^= 1; }
     }
   } else {
     // ------------------------------------------------------------ epilogue
     const uint32_t q = warp & 3;  // TMEM lane quarter this warp may access
+    const bool split = a.splits > 1;
     uint32_t acc = 0, acc_phase = 0;
-    for (uint32_t tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
-      const uint32_t mt = tile / a.n_tiles, nt = tile % a.n_tiles;
+    for (uint32_t u = blockIdx.x; u < num_units; u += gridDim.x) {
+      uint32_t mt, nt, kb0, kb1;
+      decode(u, mt, nt, kb0, kb1);
       mbar_wait(&tfull[acc], acc_phase);
       tc_fence_after();
-      const uint32_t row = mt * MMA_BM + q * 32 + lane;
-      const uint32_t taddr = tmem_base + ((q * 32u) << 16) + acc * BN;
 #pragma unroll 1
-      for (uint32_t c0 = 0; c0 < BN; c0 += 16) {
-        uint32_t v[16];
-        tmem_ld_32x32b_x16(taddr + c0, v);
-        const uint32_t j0 = (nt * BN + c0) / 4;  // first output (query / hint column)
-        uint32_t o[4];
+      for (uint32_t p = 0; p < MT; ++p) {
+        const uint32_t row = (mt * MT + p) * MMA_BM + q * 32 + lane;
+        const uint32_t taddr = tmem_base + ((q * 32u) << 16) + acc * C::ACC_COLS + p * BN;
+        constexpr uint32_t CH = BN < 64 ? BN : 64;  // columns per TMEM wait
+#pragma unroll 1
+        for (uint32_t cb = 0; cb < BN; cb += CH) {
+          uint32_t v[CH];
 #pragma unroll
-        for (int jj = 0; jj < 4; ++jj)
-          o[jj] = v[4 * jj] + (v[4 * jj + 1] << 8) + (v[4 * jj + 2] << 16) + (v[4 * jj + 3] << 24);
-        if (row < a.rows) {
-          if (OUT_MODE == OUT_QUERY_MAJOR) {
+          for (uint32_t t = 0; t < CH / 16; ++t)
+            tmem_ld_32x32b_x16_nowait(taddr + cb + 16 * t, *reinterpret_cast<uint32_t(*)[16]>(v + 16 * t));
+          tmem_ld_wait();
 #pragma unroll
-            for (int jj = 0; jj < 4; ++jj)
-              if (j0 + jj < a.n_out) a.out[(size_t)(j0 + jj) * a.out_ld + row] = o[jj];
-          } else {
-            uint32_t* dst = a.out + (size_t)row * a.out_ld + j0;
-            if (j0 + 4 <= a.n_out && (a.out_ld & 3u) == 0) {
-              *reinterpret_cast<uint4*>(dst) = make_uint4(o[0], o[1], o[2], o[3]);
-            } else {
+          for (uint32_t t = 0; t < CH / 16; ++t) {
+            const uint32_t c0 = cb + 16 * t;
+            const uint32_t j0 = (nt * BN + c0) / 4;  // first output (query / hint column)
+            uint32_t o[4];
 #pragma unroll
-              for (int jj = 0; jj < 4; ++jj)
-                if (j0 + jj < a.n_out) dst[jj] = o[jj];
+            for (int jj = 0; jj < 4; ++jj) {
+              const uint32_t* w = v + 16 * t + 4 * jj;
+              o[jj] = w[0] + (w[1] << 8) + (w[2] << 16) + (w[3] << 24);
+            }
+            if (row < a.rows) {
+              if (OUT_MODE == OUT_QUERY_MAJOR) {
+#pragma unroll
+                for (int jj = 0; jj < 4; ++jj) {
+                  if (j0 + jj < a.n_out) {
+                    uint32_t* dst = a.out + (size_t)(j0 + jj) * a.out_ld + row;
+                    if (split) atomicAdd(dst, o[jj]); else *dst = o[jj];
+                  }
+                }
+              } else {
+                uint32_t* dst = a.out + (size_t)row * a.out_ld + j0;
+                if (!split && j0 + 4 <= a.n_out && (a.out_ld & 3u) == 0) {
+                  *reinterpret_cast<uint4*>(dst) = make_uint4(o[0], o[1], o[2], o[3]);
+                } else {
+#pragma unroll
+                  for (int jj = 0; jj < 4; ++jj)
+                    if (j0 + jj < a.n_out) {
+                      if (split) atomicAdd(dst + jj, o[jj]); else dst[jj] = o[jj];
+                    }
+                }
+              }
             }
           }
         }
       }
       tc_fence_before();
       mbar_arrive(&tempty[acc]);
-      if (++acc == 2) { acc = 0; acc_phase ^= 1; }
+      if (++acc == C::ACC_BUFS) { acc = 0; acc_phase ^= 1; }
     }
   }
 
@@ -189,7 +240,7 @@ __global__ void __launch_bounds__(MMA_THREADS, 1) mma_u8_limb_kernel(MmaArgs a) 
   __syncthreads();
   if (warp == 1) {
     tc_fence_after();
-    tmem_dealloc(tmem_base, S::TMEM_COLS);
+    tmem_dealloc(tmem_base, C::TMEM_COLS);
   }
 }
 

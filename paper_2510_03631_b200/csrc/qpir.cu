@@ -39,7 +39,7 @@ struct qpir_ctx {
   Geometry geo;
   int device = 0;
   int num_sms = 148;
-  uint8_t* D = nullptr;            // [G][L][16]
+  uint8_t* D = nullptr;            // 128-row panels [L/128][G][128][16]
   uint32_t* qu_dev = nullptr;      // m_pad (staging for host / unaligned qu)
   uint32_t* ans_dev = nullptr;     // ell_local (staging for host answers)
   uint32_t* partial = nullptr;     // [max_split][L]
@@ -58,6 +58,11 @@ struct qpir_ctx {
   int gemv_u = 2;
   int gemv_split = 0;  // 0 = auto
   int gemv_chunk = 512;
+  int gemv_unroll = 4;
+  int gemv_order = 0;  // env QPIR_GEMV_ORDER (1 = split-major grid)
+  int mma_mt = 2;      // env QPIR_MMA_MT (1 or 2 row panels per CTA tile)
+  int mma_split = 0;   // env QPIR_MMA_SPLIT (0 = auto)
+  int mma_gpb = 8;     // env QPIR_MMA_GPB (column groups per pipeline stage: 4 or 8)
   std::string err;
 };
 
@@ -152,7 +157,7 @@ int validate(const qpir_params* p, Geometry* g) {
                 (unsigned long long)g->ell_local);
   g->m_pad = round_up(g->m, MMA_BK);
   g->G = g->m_pad / 16;
-  g->L = round_up(g->ell_local, MMA_BM);
+  g->L = round_up(g->ell_local, 2 * MMA_BM);  // whole pairs of 128-row panels
   g->lwe_n = p->lwe_n;
   g->seed_A = p->seed_A;
   return QPIR_OK;
@@ -197,12 +202,13 @@ int db_write_device(qpir_ctx* ctx, uint64_t theta0, uint64_t n_rec, const uint8_
   a.m = (uint32_t)g.m;
   a.n_cells = g.n_cells;
   a.g_lo = (uint32_t)j_lo;
+  a.G = (uint32_t)g.G;
   const uint32_t rb = (uint32_t)((g.ell_local + 127) / 128);
   for (uint32_t y0 = 0; y0 < rb; y0 += 65535) {
     // grid.y is limited to 65535 row blocks per launch
     PackArgs b = a;
     const uint32_t ny = std::min<uint32_t>(65535, rb - y0);
-    b.D = ctx->D + (size_t)y0 * 128 * 16;
+    b.D = ctx->D + (size_t)y0 * g.G * 2048;  // y0 panels of 128 rows
     b.row_begin = g.row_begin + (uint64_t)y0 * 128;
     b.ell_local = (uint32_t)std::min<uint64_t>(g.ell_local - (uint64_t)y0 * 128, (uint64_t)ny * 128);
     dim3 grid((uint32_t)(j_hi - j_lo + 1), ny);
@@ -212,18 +218,21 @@ int db_write_device(qpir_ctx* ctx, uint64_t theta0, uint64_t n_rec, const uint8_
   return QPIR_OK;
 }
 
-template <int U>
+template <int U, int UNR>
 int launch_gemv(qpir_ctx* ctx, const uint32_t* qu, uint32_t* ans, cudaStream_t st) {
   const Geometry& g = ctx->geo;
-  constexpr int UNR = 4;
   const uint32_t rows_per_cta = GEMV_THREADS * U;
-  const uint32_t rb = (uint32_t)((g.L + rows_per_cta - 1) / rows_per_cta);
+  const uint32_t rb = (uint32_t)((g.ell_local + rows_per_cta - 1) / rows_per_cta);
   uint32_t S = ctx->gemv_split;
   if (S == 0) {
-    // enough CTAs for ~6 resident per SM, at least 64 column groups per split
-    const uint32_t want = (uint32_t)(6 * ctx->num_sms);
-    S = (want + rb - 1) / rb;
-    S = std::min<uint32_t>(S, (uint32_t)std::max<uint64_t>(1, g.G / 64));
+    // Many short CTAs beat one wave of long ones (measured on B200, DESIGN 6):
+    // about 256 column groups (1 MB of D at U = 2) per CTA, and at least ~8
+    // waves of ~6 resident CTAs per SM so the tail stays small; at least 16
+    // groups per split.
+    const uint32_t by_work = (uint32_t)((g.G + 255) / 256);
+    const uint32_t by_waves = (uint32_t)((8u * 6u * ctx->num_sms + rb - 1) / rb);
+    S = std::max(by_work, by_waves);
+    S = std::min<uint32_t>(S, (uint32_t)std::max<uint64_t>(1, g.G / 16));
   }
   S = std::max<uint32_t>(1, std::min<uint32_t>(S, (uint32_t)(g.G / UNR)));
   uint32_t gps = (uint32_t)round_up((g.G + S - 1) / S, UNR);
@@ -253,46 +262,72 @@ int launch_gemv(qpir_ctx* ctx, const uint32_t* qu, uint32_t* ans, cudaStream_t s
   a.G = (uint32_t)g.G;
   a.gps = gps;
   a.chunk = chunk;
+  a.split_major = (ctx->gemv_order == 1 && rb <= 65535) ? 1u : 0u;
   const size_t smem = (size_t)chunk * 64;
   auto kern = gemv_u8_u32_kernel<U, UNR>;
   if (smem > 48 * 1024)
     CUDA_TRY(ctx, cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-  kern<<<dim3(rb, S), GEMV_THREADS, smem, st>>>(a);
+  const dim3 grid = a.split_major ? dim3(S, rb) : dim3(rb, S);
+  kern<<<grid, GEMV_THREADS, smem, st>>>(a);
   LAUNCH_CHECK(ctx);
   return QPIR_OK;
 }
 
 int gemv(qpir_ctx* ctx, const uint32_t* qu, uint32_t* ans, cudaStream_t st) {
+  const bool u8 = ctx->gemv_unroll == 8;
   switch (ctx->gemv_u) {
-    case 1: return launch_gemv<1>(ctx, qu, ans, st);
-    case 4: return launch_gemv<4>(ctx, qu, ans, st);
-    default: return launch_gemv<2>(ctx, qu, ans, st);
+    case 1: return u8 ? launch_gemv<1, 8>(ctx, qu, ans, st) : launch_gemv<1, 4>(ctx, qu, ans, st);
+    case 4: return u8 ? launch_gemv<4, 8>(ctx, qu, ans, st) : launch_gemv<4, 4>(ctx, qu, ans, st);
+    default: return u8 ? launch_gemv<2, 8>(ctx, qu, ans, st) : launch_gemv<2, 4>(ctx, qu, ans, st);
   }
 }
 
-template <uint32_t BN, int MODE>
-int launch_mma_bn(qpir_ctx* ctx, const uint8_t* Bl, uint32_t Npad, uint32_t* out,
-                  uint32_t n_out, uint32_t out_ld, cudaStream_t st) {
-  constexpr uint32_t STAGES = 4;
-  using S = MmaSmem<BN, STAGES>;
+// Split K so that work units fill the SMs evenly (a few % tail at most);
+// partial tiles are added with u32 atomics (exact: addition mod 2^32 commutes).
+uint32_t choose_splits(uint32_t tiles, uint32_t kblocks, uint32_t sms, int forced) {
+  if (forced > 0) return std::max<uint32_t>(1, std::min<uint32_t>((uint32_t)forced, kblocks));
+  auto eff = [&](uint32_t units) {
+    const uint32_t waves = (units + sms - 1) / sms;
+    return (double)units / ((double)waves * sms);
+  };
+  uint32_t best = 1;
+  double best_eff = eff(tiles);
+  for (uint32_t s = 2; s <= 8; ++s) {
+    if (kblocks / s < 16) break;
+    const double e = eff(tiles * s);
+    if (e > best_eff + 0.02) {
+      best = s;
+      best_eff = e;
+    }
+  }
+  return best;
+}
+
+template <uint32_t BN, uint32_t MT, uint32_t GPB, int MODE>
+int launch_mma_cfg(qpir_ctx* ctx, const uint8_t* Bl, uint32_t Npad, uint32_t* out,
+                   uint32_t n_out, uint32_t out_ld, uint64_t out_elems, cudaStream_t st) {
+  using C = MmaCfg<BN, MT, GPB>;
   const Geometry& g = ctx->geo;
   MmaArgs a;
   a.A = ctx->D;
   a.B = Bl;
   a.out = out;
-  a.L = (uint32_t)g.L;
-  a.Npad = Npad;
   a.G = (uint32_t)g.G;
   a.rows = (uint32_t)g.ell_local;
   a.n_out = n_out;
   a.out_ld = out_ld;
-  a.m_tiles = (uint32_t)(g.L / MMA_BM);
+  a.m_tiles = (uint32_t)(g.L / (MMA_BM * MT));
   a.n_tiles = Npad / BN;
-  const uint32_t tiles = a.m_tiles * a.n_tiles;
-  const uint32_t grid = std::min<uint32_t>(tiles, (uint32_t)ctx->num_sms);
-  auto kern = mma_u8_limb_kernel<BN, STAGES, MODE>;
-  CUDA_TRY(ctx, cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)S::TOTAL));
-  kern<<<grid, MMA_THREADS, S::TOTAL, st>>>(a);
+  const uint32_t kblocks = (uint32_t)(g.G / GPB);
+  a.splits = choose_splits(a.m_tiles * a.n_tiles, kblocks, (uint32_t)ctx->num_sms, ctx->mma_split);
+  a.kps = (kblocks + a.splits - 1) / a.splits;
+  a.splits = (kblocks + a.kps - 1) / a.kps;  // no empty split
+  if (a.splits > 1) CUDA_TRY(ctx, cudaMemsetAsync(out, 0, out_elems * 4, st));
+  const uint32_t units = a.m_tiles * a.n_tiles * a.splits;
+  const uint32_t grid = std::min<uint32_t>(units, (uint32_t)ctx->num_sms);
+  auto kern = mma_u8_limb_kernel<BN, MT, GPB, MODE>;
+  CUDA_TRY(ctx, cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::TOTAL));
+  kern<<<grid, MMA_THREADS, C::TOTAL, st>>>(a);
   LAUNCH_CHECK(ctx);
   return QPIR_OK;
 }
@@ -307,14 +342,25 @@ uint32_t pick_bn(uint64_t ncols) {
 
 template <int MODE>
 int launch_mma(qpir_ctx* ctx, uint32_t BN, const uint8_t* Bl, uint32_t Npad, uint32_t* out,
-               uint32_t n_out, uint32_t out_ld, cudaStream_t st) {
+               uint32_t n_out, uint32_t out_ld, uint64_t out_elems, cudaStream_t st) {
+  const bool mt2 = ctx->mma_mt != 1;
+  const bool g4 = ctx->mma_gpb == 4;
+#define QPIR_MMA_CASE(BNV)                                                                     \
+  case BNV:                                                                                    \
+    if (g4)                                                                                    \
+      return mt2 ? launch_mma_cfg<BNV, 2, 4, MODE>(ctx, Bl, Npad, out, n_out, out_ld, out_elems, st) \
+                 : launch_mma_cfg<BNV, 1, 4, MODE>(ctx, Bl, Npad, out, n_out, out_ld, out_elems, st); \
+    return mt2 ? launch_mma_cfg<BNV, 2, 8, MODE>(ctx, Bl, Npad, out, n_out, out_ld, out_elems, st)   \
+               : launch_mma_cfg<BNV, 1, 8, MODE>(ctx, Bl, Npad, out, n_out, out_ld, out_elems, st);
   switch (BN) {
-    case 16: return launch_mma_bn<16, MODE>(ctx, Bl, Npad, out, n_out, out_ld, st);
-    case 32: return launch_mma_bn<32, MODE>(ctx, Bl, Npad, out, n_out, out_ld, st);
-    case 64: return launch_mma_bn<64, MODE>(ctx, Bl, Npad, out, n_out, out_ld, st);
-    case 128: return launch_mma_bn<128, MODE>(ctx, Bl, Npad, out, n_out, out_ld, st);
-    default: return launch_mma_bn<256, MODE>(ctx, Bl, Npad, out, n_out, out_ld, st);
+    QPIR_MMA_CASE(16)
+    QPIR_MMA_CASE(32)
+    QPIR_MMA_CASE(64)
+    QPIR_MMA_CASE(128)
+    default:
+      QPIR_MMA_CASE(256)
   }
+#undef QPIR_MMA_CASE
 }
 
 bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
@@ -356,6 +402,11 @@ int qpir_setup(const qpir_params* params, const uint8_t* records, uint64_t recor
   ctx->gemv_u = env_int("QPIR_GEMV_U", 2);
   ctx->gemv_split = env_int("QPIR_GEMV_SPLIT", 0);
   ctx->gemv_chunk = env_int("QPIR_GEMV_CHUNK", 512);
+  ctx->gemv_unroll = env_int("QPIR_GEMV_UNROLL", 4);
+  ctx->gemv_order = env_int("QPIR_GEMV_ORDER", 0);
+  ctx->mma_mt = env_int("QPIR_MMA_MT", 2);
+  ctx->mma_split = env_int("QPIR_MMA_SPLIT", 0);
+  ctx->mma_gpb = env_int("QPIR_MMA_GPB", 8);
   cudaStream_t st = (cudaStream_t)stream;
   auto bail = [&](int code) {
     g_setup_error = ctx->err;
@@ -506,11 +557,11 @@ int qpir_answer_batch(qpir_ctx* ctx, const uint32_t* Q, uint64_t B, uint64_t len
     const uint32_t nq = Npad / 4;  // padded query slots
     dim3 grid((nq + 127) / 128, (uint32_t)g.G);
     limb_split_kernel<<<grid, 128, 0, st>>>(Qd, ctx->limbs, (uint32_t)B, (uint32_t)g.m,
-                                            (uint32_t)g.G, Npad);
+                                            (uint32_t)g.G, Npad, BN);
     LAUNCH_CHECK(ctx);
   }
   rc = launch_mma<OUT_QUERY_MAJOR>(ctx, BN, ctx->limbs, Npad, out, (uint32_t)B,
-                                   (uint32_t)g.ell_local, st);
+                                   (uint32_t)g.ell_local, len_ans, st);
   if (rc) return rc;
   if (wa == 0) {
     CUDA_TRY(ctx, cudaMemcpyAsync(ans_local, out, len_ans * 4, cudaMemcpyDeviceToHost, st));
@@ -545,10 +596,10 @@ int qpir_hint(qpir_ctx* ctx, uint32_t* H_local, uint64_t len_H, void* stream) {
     const uint32_t nb = Npad / 16;  // Philox blocks (4 outputs x 4 limbs)
     dim3 grid((nb + 127) / 128, (uint32_t)g.G);
     expand_A_limbs_kernel<<<grid, 128, 0, st>>>(ctx->limbs, g.seed_A, (uint32_t)g.m, g.lwe_n,
-                                                (uint32_t)g.G, Npad);
+                                                (uint32_t)g.G, Npad, BN);
     LAUNCH_CHECK(ctx);
   }
-  rc = launch_mma<OUT_ROW_MAJOR>(ctx, BN, ctx->limbs, Npad, out, g.lwe_n, g.lwe_n, st);
+  rc = launch_mma<OUT_ROW_MAJOR>(ctx, BN, ctx->limbs, Npad, out, g.lwe_n, g.lwe_n, len_H, st);
   if (rc) return rc;
   if (out != H_local) {
     CUDA_TRY(ctx, cudaMemcpyAsync(H_local, out, len_H * 4,

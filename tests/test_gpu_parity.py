@@ -60,7 +60,9 @@ RAGGED = [
 
 @pytest.mark.parametrize("geo", RAGGED)
 @pytest.mark.parametrize("cfg", [dict(), dict(QPIR_GEMV_U="1", QPIR_GEMV_SPLIT="3", QPIR_GEMV_CHUNK="8"),
-                                 dict(QPIR_GEMV_U="4", QPIR_GEMV_SPLIT="1", QPIR_GEMV_CHUNK="4")])
+                                 dict(QPIR_GEMV_U="4", QPIR_GEMV_SPLIT="1", QPIR_GEMV_CHUNK="4"),
+                                 dict(QPIR_GEMV_ORDER="1", QPIR_GEMV_SPLIT="5", QPIR_GEMV_UNROLL="8"),
+                                 dict(QPIR_MMA_MT="1", QPIR_MMA_SPLIT="3")])
 def test_answer_ragged(cuda_ok, geo, cfg, monkeypatch):
     for k, v in cfg.items():
         monkeypatch.setenv(k, v)
@@ -76,6 +78,9 @@ def test_answer_ragged(cuda_ok, geo, cfg, monkeypatch):
         qf = np.full(s.m, M32, np.uint32)
         want = (-D.astype(np.int64).sum(1)) & M32
         assert (_u32(s.answer(qf)).astype(np.int64) == want).all()
+        # the tensor-core batch path on the same ragged geometry
+        Q = synth.uniform_u32_np(6, (5, s.m))
+        assert (_u32(s.answer_batch(Q)) == O.answer_batch(D, Q)).all()
 
 
 def test_shards_concatenate(cuda_ok):
