@@ -60,6 +60,10 @@ def lib():
         L.qo_query.argtypes = [_u32p, _u64, _u32, _u32p, _u64, _u32, ctypes.c_double, _u64,
                                _u32p, _i32p, _i32p]
         L.qo_decode.argtypes = [_u32p, _u32p, _u32, _u32p, _u64p, _u64, _u8p]
+        L.qo_ens_query.argtypes = [_u64, _u64, _u32, _u64, _u8p]
+        L.qo_ens_respond.argtypes = [_u8p, _u64, _u64, _u8p, _u8p]
+        L.qo_ens_respond_batch.argtypes = [_u8p, _u64, _u64, _u8p, _u64, _u8p]
+        L.qo_ens_reconstruct.argtypes = [_u8p, _u32, _u64, _u8p]
         L.qo_num_threads.restype = ctypes.c_int
         L.qo_set_num_threads.argtypes = [ctypes.c_int]
         _lib = L
@@ -184,6 +188,43 @@ def decode(ans: np.ndarray, H: np.ndarray, s: np.ndarray, rows) -> np.ndarray:
 def record_rows(theta: int, n_ch: int, d: int, m: int) -> np.ndarray:
     """Rows of D holding record theta's d bytes (all in one column)."""
     return np.array([position(n_ch, d, m, theta, b)[0] for b in range(d)], np.uint64)
+
+
+# ---------------------------------------------------------------- ENS (Chor, NEXT-1)
+def ens_query(theta: int, r: int, l: int, seed: int) -> np.ndarray:
+    """l shares of r bits (l x ceil(r/8) bytes, bit t at byte t>>3, bit t&7)."""
+    sh = np.empty((l, (r + 7) // 8), np.uint8)
+    lib().qo_ens_query(theta, r, l, seed, _p(sh, _u8p))
+    return sh
+
+
+def ens_respond(records: np.ndarray, share: np.ndarray) -> np.ndarray:
+    rec = _c(records, np.uint8)
+    r, d = rec.shape
+    sh = _c(share, np.uint8)
+    assert sh.shape == ((r + 7) // 8,)
+    out = np.empty(d, np.uint8)
+    lib().qo_ens_respond(_p(rec, _u8p), r, d, _p(sh, _u8p), _p(out, _u8p))
+    return out
+
+
+def ens_respond_batch(records: np.ndarray, Q: np.ndarray) -> np.ndarray:
+    rec = _c(records, np.uint8)
+    r, d = rec.shape
+    Q = _c(Q, np.uint8)
+    B = Q.shape[0]
+    assert Q.shape == (B, (r + 7) // 8)
+    out = np.empty((B, d), np.uint8)
+    lib().qo_ens_respond_batch(_p(rec, _u8p), r, d, _p(Q, _u8p), B, _p(out, _u8p))
+    return out
+
+
+def ens_reconstruct(resp: np.ndarray) -> np.ndarray:
+    resp = _c(resp, np.uint8)
+    l, d = resp.shape
+    out = np.empty(d, np.uint8)
+    lib().qo_ens_reconstruct(_p(resp, _u8p), l, d, _p(out, _u8p))
+    return out
 
 
 def num_threads() -> int:

@@ -277,3 +277,66 @@ void qo_set_num_threads(int t) {
   (void)t;
 #endif
 }
+
+/* ------------------------------------------------------------------ */
+/* NEXT-1: QPADL-ENS = Chor et al. multi-server XOR PIR (P:736;        */
+/* Lemma 1 proof; Alg. 3 "Multi-request Parallel Chor-PIR",    */
+/* P:972-1000).  DB = r records (rows) of d bytes = b = 8d bits over   */
+/* GF(2).  Bit t of an r-bit vector lives at byte t >> 3, bit t & 7.   */
+/* ------------------------------------------------------------------ */
+#define QO_DOMAIN_C 0x43u
+
+/* Client.Query (Lemma 1 proof): rho_1..rho_{l-1} uniform r-bit strings,
+ * rho_l = XOR_{i<l} rho_i XOR e_theta.  Share i's byte w is byte (w & 3) of
+ * word 0 of Philox(key = seed, ctr = (w >> 2, i, theta_lo, 'C')) (DESIGN R15);
+ * bits at positions >= r are 0.  shares: l x ceil(r/8) bytes. */
+void qo_ens_query(uint64_t theta, uint64_t r, uint32_t l, uint64_t seed, uint8_t *shares) {
+  uint64_t nb = (r + 7) / 8;
+  uint32_t key[2];
+  key_from_seed(seed, key);
+  uint8_t *last = shares + (uint64_t)(l - 1) * nb;
+  memset(last, 0, (size_t)nb);
+  for (uint32_t i = 0; i + 1 < l; ++i) {
+    uint8_t *sh = shares + (uint64_t)i * nb;
+    for (uint64_t w = 0; w < nb; ++w) {
+      uint32_t ctr[4] = {(uint32_t)(w >> 2), i, (uint32_t)theta, QO_DOMAIN_C};
+      uint32_t out[4];
+      qo_philox4x32_10(ctr, key, out);
+      sh[w] = (uint8_t)((out[0] >> (8 * (w & 3))) & 0xFFu);
+    }
+    if (r % 8) sh[nb - 1] &= (uint8_t)((1u << (r % 8)) - 1u);
+    for (uint64_t w = 0; w < nb; ++w) last[w] ^= sh[w];
+  }
+  last[theta >> 3] ^= (uint8_t)(1u << (theta & 7));
+}
+
+/* DB.Query.Response (Def. 1; Alg. 3 steps 8-9): out = XOR of the rows
+ * theta whose share bit is 1.  records: r x d, row-major. */
+void qo_ens_respond(const uint8_t *records, uint64_t r, uint64_t d, const uint8_t *share,
+                    uint8_t *out) {
+  memset(out, 0, (size_t)d);
+  for (uint64_t t = 0; t < r; ++t) {
+    if ((share[t >> 3] >> (t & 7)) & 1u) {
+      const uint8_t *row = records + t * d;
+      for (uint64_t j = 0; j < d; ++j) out[j] ^= row[j];
+    }
+  }
+}
+
+/* Multi-request form (Alg. 3): B shares (B x ceil(r/8)) -> B x d. */
+void qo_ens_respond_batch(const uint8_t *records, uint64_t r, uint64_t d, const uint8_t *Q,
+                          uint64_t B, uint8_t *out) {
+  uint64_t nb = (r + 7) / 8;
+  int64_t BB = (int64_t)B;
+#pragma omp parallel for schedule(static)
+  for (int64_t b = 0; b < BB; ++b)
+    qo_ens_respond(records, r, d, Q + (uint64_t)b * nb, out + (uint64_t)b * d);
+}
+
+/* BlockReconst (Def. 1; Lemma 1 proof -- read as the XOR of the l
+ * responses, DESIGN R16): out = XOR_i resp_i.  resp: l x d. */
+void qo_ens_reconstruct(const uint8_t *resp, uint32_t l, uint64_t d, uint8_t *out) {
+  memset(out, 0, (size_t)d);
+  for (uint32_t i = 0; i < l; ++i)
+    for (uint64_t j = 0; j < d; ++j) out[j] ^= resp[(uint64_t)i * d + j];
+}

@@ -46,9 +46,11 @@ def gather_answer(ans_local: torch.Tensor, shard_sizes, group=None) -> torch.Ten
         buf = torch.empty((world, *lead, mx), dtype=ans_local.dtype, device=ans_local.device)
         dist.all_gather_into_tensor(buf, ans_local.unsqueeze(0), group=group)
         slices = [buf[r] for r in range(world)]
-    else:  # gloo (CPU tests): list all_gather
-        slices = [torch.empty_like(ans_local) for _ in range(world)]
-        dist.all_gather(slices, ans_local, group=group)
+    else:  # gloo (CPU tests, single-GPU functional runs): list all_gather on host
+        host = ans_local.cpu()
+        slices = [torch.empty_like(host) for _ in range(world)]
+        dist.all_gather(slices, host, group=group)
+        slices = [t.to(ans_local.device) for t in slices]
     parts = [slices[r][..., : shard_sizes[r]] for r in range(world)]
     return torch.cat(parts, dim=-1)
 
