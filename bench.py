@@ -49,6 +49,11 @@ WORKLOADS = {
                        "(BASELINE configs[3])", n_cells=65536, n_ch=40, d=3072, kind="batch", B=64),
     "c4-256": dict(name="8.05 GB DB (65536 cells x 40 ch x 3072 B), batch of 256 queries "
                         "(BASELINE configs[3])", n_cells=65536, n_ch=40, d=3072, kind="batch", B=256),
+    "ens-c2": dict(name="QPADL-ENS (Chor XOR PIR, NEXT-1): 327680 paper-shaped 3 KB records "
+                        "= 1.007 GB, one uniform r-bit share", n_cells=8192, n_ch=40, d=3072,
+                   kind="ens"),
+    "ens-c2-b128": dict(name="QPADL-ENS multi-request (Alg. 3): 1.007 GB, 128 shares",
+                        n_cells=8192, n_ch=40, d=3072, kind="ens_batch", B=128),
     "c5": dict(name="hint D.A, n=1024, one rank's shard of the 32.2 GB DB at G=8 "
                     "(BASELINE configs[4])", n_cells=262144, n_ch=40, d=3072, kind="hint", n=1024,
                shard_of=8),
@@ -225,6 +230,108 @@ def run_reference(args, wl, world, rank):
     print(json.dumps(line), flush=True)
 
 
+# ---------------------------------------------------------------- ENS (NEXT-1)
+def run_ens(args, wl, world, rank, local):
+    """QPADL-ENS single / multi-request scan.  Every rank runs an independent
+    replica (no data-path collective; weak scaling)."""
+    import synth
+    import paper_2510_03631_b200 as P
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    stream = torch.cuda.current_stream(dev)
+    n_cells, n_ch, d = wl["n_cells"], wl["n_ch"], wl["d"]
+    r = n_cells * n_ch
+    t0 = time.time()
+    srv = P.EnsServer(r, d, device=local)
+    chunk = max(1, (256 << 20) // d)
+    for a in range(0, r, chunk):
+        srv.db_write(a, synth.records(args.seed, a, min(chunk, r - a), d, n_ch, device=dev))
+    torch.cuda.synchronize(dev)
+    setup_s = time.time() - t0
+    nb = (r + 7) // 8
+    B = wl.get("B", 1)
+    shares = [(synth.uniform_u32(args.seed + 7 + i, ((B * nb + 3) // 4,), device=dev)
+               .view(torch.uint8)[: B * nb].reshape(B, nb).contiguous()) for i in range(4)]
+    out = torch.empty((B, d), dtype=torch.uint8, device=dev)
+
+    def step(i):
+        if B == 1:
+            srv.answer(shares[i % 4][0], out=out[0], stream=stream)
+        else:
+            srv.answer_batch(shares[i % 4], out=out, stream=stream)
+
+    sampler = ClockSampler(physical_gpu(local))
+    for i in range(args.warmup):
+        step(i)
+    torch.cuda.synchronize(dev)
+    time.sleep(0.3)
+    l0 = srv.kernel_launches
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    sampler.start()
+    e0.record(stream)
+    for i in range(args.steps):
+        step(i)
+    e1.record(stream)
+    torch.cuda.synchronize(dev)
+    sampler.stop()
+    ms = e0.elapsed_time(e1) / args.steps
+    launches = srv.kernel_launches - l0
+    if world > 1:
+        tt = torch.tensor([ms], device=dev, dtype=torch.float64)
+        torch.distributed.all_reduce(tt, op=torch.distributed.ReduceOp.MAX)
+        ms = tt.item()
+    # e2e: share from pinned host, response back to pinned host
+    h_in = torch.empty((B, nb), dtype=torch.uint8).pin_memory()
+    h_in.copy_(shares[0].cpu())
+    h_out = torch.empty((B, d), dtype=torch.uint8).pin_memory()
+    n_e2e = max(3, min(args.steps, 100))
+    for _ in range(3):
+        (srv.answer(h_in[0], out=h_out[0], stream=stream) if B == 1
+         else srv.answer_batch(h_in, out=h_out, stream=stream))
+    a0 = time.perf_counter()
+    for _ in range(n_e2e):
+        (srv.answer(h_in[0], out=h_out[0], stream=stream) if B == 1
+         else srv.answer_batch(h_in, out=h_out, stream=stream))
+    torch.cuda.synchronize(dev)
+    te = (time.perf_counter() - a0) / n_e2e * 1e3
+    if rank != 0:
+        return
+    hbm, _, _, peak_src = peaks()
+    db = r * d
+    value = world * db * B / (ms / 1e3) / 1e9
+    nnz_frac = float(np.unpackbits(shares[0].cpu().numpy().reshape(-1)[: nb]).mean())
+    touched = nnz_frac * db  # rows actually read (Alg. 3 step 9 skips unselected rows)
+    achieved = (touched + nb + d) / (ms / 1e3) / 1e9 if B == 1 else None
+    roof = ({"bound": "hbm", "achieved": round(achieved, 1), "peak": hbm, "unit": "GB/s",
+             "frac": round(achieved / hbm, 4), "traffic": None, "kernel": "ens_scan_kernel",
+             "kernel_ms": round(ms, 5), "peak_source": f"{peak_src} hbm_gbs",
+             "algorithmic_bytes_per_launch": touched + nb + d,
+             "note": "selected rows only (nnz(q) * d), P:968"} if B == 1 else
+            {"bound": "alu", "achieved": round(B * r * d / 4 / (ms / 1e3) / 1e12, 3),
+             "unit": "T word-XOR/s", "peak": round(148 * 64 * 1.965e9 / 1e12, 2),
+             "frac": round(B * r * d / 4 / (ms / 1e3) / (148 * 64 * 1.965e9), 4),
+             "traffic": None, "kernel": "ens_transpose_bits_kernel + ens_batch_kernel",
+             "kernel_ms": round(ms, 5),
+             "peak_source": "148 SMs x 64 LOP3 lanes/clk x 1965 MHz (guide unit counts)"})
+    line = {"metric": METRIC, "value": round(value, 2),
+            "unit": "GB/s" if B == 1 else "GB/s (query-equivalent)", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms, 5),
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+            "dtype": "u8 (GF(2) XOR)", "data": "synthetic",
+            "config": {"workload": wl["name"], "n_records": r, "rec_bytes": d,
+                       "queries_per_step": B, "selected_row_fraction": round(nnz_frac, 4),
+                       "setup_s": round(setup_s, 1),
+                       "l2": "inputs larger than L2 (1.007 GB records)"},
+            "queries_per_s": round(world * B / (ms / 1e3), 1), "roofline": roof,
+            "cpu_baseline": None,
+            "e2e": {"value": round(world * db * B / (te / 1e3) / 1e9, 2), "unit": "GB/s",
+                    "h2d_bytes_per_step": B * nb, "d2h_bytes_per_step": B * d,
+                    "ms_per_step": round(te, 4), "timing": "host wall clock per synchronous call"},
+            "gpu_launches": launches, "clocks": sampler.summary()}
+    print(json.dumps(line), flush=True)
+
+
 # ---------------------------------------------------------------- our arm
 def main():
     ap = argparse.ArgumentParser()
@@ -248,6 +355,14 @@ def main():
         args.warmup = args.warmup if args.warmup is not None else 3
         return run_reference(args, wl, world, rank)
 
+    if wl["kind"] in ("ens", "ens_batch"):
+        args.steps = args.steps or (1000 if wl["kind"] == "ens" else 50)
+        args.warmup = max(3, args.warmup if args.warmup is not None else 5)
+        if world > 1:
+            import torch.distributed as dist
+            dist.init_process_group(args.backend)
+        return run_ens(args, wl, world, rank,
+                       local if args.device_override is None else args.device_override)
     default_steps = {"answer": 2000, "batch": 300, "hint": 40}[wl["kind"]]
     if args.workload == "c3":
         default_steps = 200

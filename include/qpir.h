@@ -127,6 +127,47 @@ const char *qpir_last_error(const qpir_ctx *ctx);
 /* Free the context and its device memory (NULL is a no-op). */
 void qpir_destroy(qpir_ctx *ctx);
 
+/* ===================================================================== */
+/* QPADL-ENS: Chor multi-server XOR PIR (Lemma 1 proof,     */
+/* PAPER.md:1227; Alg. 3 "Multi-request Parallel Chor-PIR"). */
+/* The DB is r records of d bytes (b = 8d bits over GF(2)), theta-major.   */
+/* A share is an r-bit vector, bit t at byte t >> 3, bit (t & 7); bits at  */
+/* positions >= r are ignored.  The response to a share is the XOR of the  */
+/* records whose bit is 1 (rho = q . DB over GF(2)); a client XORs the l   */
+/* responses of l servers to rebuild its record.  Same buffer, length,     */
+/* stream and error conventions as above.                                  */
+/* ===================================================================== */
+typedef struct qpir_ens_ctx qpir_ens_ctx;
+
+typedef struct {
+  uint64_t n_records; /* r                                       */
+  uint64_t rec_bytes; /* d, 1..16384                             */
+  int32_t device;     /* CUDA device ordinal                     */
+  int32_t reserved;   /* must be 0                               */
+} qpir_ens_params;
+
+/* Create an ENS context holding all r records (records may be NULL: zero DB). */
+int qpir_ens_setup(const qpir_ens_params *params, const uint8_t *records,
+                   uint64_t records_len, void *stream, qpir_ens_ctx **out);
+
+/* Overwrite records theta_begin .. theta_begin + n_records - 1. */
+int qpir_ens_db_write(qpir_ens_ctx *ctx, uint64_t theta_begin, uint64_t n_records,
+                      const uint8_t *records, uint64_t records_len, void *stream);
+
+/* Response to one share (len_share == ceil(r/8)) -> out: d bytes (len_out == d). */
+int qpir_ens_answer(qpir_ens_ctx *ctx, const uint8_t *share, uint64_t len_share,
+                    uint8_t *out, uint64_t len_out, void *stream);
+
+/* Responses to B shares (B x ceil(r/8), share-major) -> out: B x d bytes.
+ * 1 <= B <= 65536. */
+int qpir_ens_answer_batch(qpir_ens_ctx *ctx, const uint8_t *shares, uint64_t B,
+                          uint64_t len_shares, uint8_t *out, uint64_t len_out,
+                          void *stream);
+
+uint64_t qpir_ens_kernel_launches(const qpir_ens_ctx *ctx);
+const char *qpir_ens_last_error(const qpir_ens_ctx *ctx);
+void qpir_ens_destroy(qpir_ens_ctx *ctx);
+
 #ifdef __cplusplus
 }
 #endif

@@ -5,6 +5,9 @@ Public API (thin wrappers over the C ABI in include/qpir.h):
         .answer(qu)           ans = D.qu mod 2^32         (GEMV, HBM-bound)
         .answer_batch(Q)      ANS = D.Q mod 2^32          (tcgen05 int8-limb GEMM)
         .hint()               H = D.A mod 2^32            (tcgen05 int8-limb GEMM)
+    EnsServer(...)            QPADL-ENS (Chor XOR PIR, NEXT-1): records theta-major
+        .answer(share)        XOR of the selected records (HBM scan, sparse rows skipped)
+        .answer_batch(Q)      multi-request form (Alg. 3)
     dist.DistributedPIR       row-sharded over ranks, NCCL gather of answer slices
 u32 values are carried in torch.int32 tensors (same bits); use u32() to view them.
 """
@@ -16,7 +19,7 @@ import torch
 from . import _lib
 from ._lib import QpirError, qpir_params  # noqa: F401
 
-__all__ = ["PirServer", "QpirError", "u32", "qpir_params"]
+__all__ = ["PirServer", "EnsServer", "QpirError", "u32", "qpir_params"]
 
 
 def u32(t) -> np.ndarray:
@@ -76,6 +79,58 @@ class PirServer:
     def close(self) -> None:
         if getattr(self, "_ctx", None):
             _lib.qpir_destroy(self._ctx)
+            self._ctx = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *exc):
+        self.close()
+
+
+class EnsServer:
+    """QPADL-ENS server (Chor XOR PIR): r records of d bytes on one GPU."""
+
+    def __init__(self, n_records: int, rec_bytes: int, *, device: int = 0, records=None,
+                 stream=None):
+        p = _lib.qpir_ens_params(n_records=n_records, rec_bytes=rec_bytes, device=device,
+                                 reserved=0)
+        self.device = device
+        self.r, self.d = n_records, rec_bytes
+        self.share_bytes = (n_records + 7) // 8
+        self._ctx = _lib.qpir_ens_setup(p, records, stream)
+
+    def db_write(self, theta_begin: int, records, stream=None) -> None:
+        n = int(records.shape[0]) if records.ndim == 2 else records.numel() // self.d
+        _lib.qpir_ens_db_write(self._ctx, theta_begin, records, n, stream)
+
+    def answer(self, share, out=None, stream=None):
+        if out is None:
+            out = torch.empty(self.d, dtype=torch.uint8, device=torch.device("cuda", self.device))
+        _lib.qpir_ens_answer(self._ctx, share, out, stream)
+        return out
+
+    def answer_batch(self, shares, out=None, stream=None):
+        B = int(shares.shape[0])
+        if out is None:
+            out = torch.empty((B, self.d), dtype=torch.uint8,
+                              device=torch.device("cuda", self.device))
+        _lib.qpir_ens_answer_batch(self._ctx, shares, B, out, stream)
+        return out
+
+    @property
+    def kernel_launches(self) -> int:
+        return _lib.qpir_ens_kernel_launches(self._ctx)
+
+    def close(self) -> None:
+        if getattr(self, "_ctx", None):
+            _lib.qpir_ens_destroy(self._ctx)
             self._ctx = None
 
     def __del__(self):

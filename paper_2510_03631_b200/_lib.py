@@ -26,6 +26,8 @@ QPIR_E_CUDA = 5
 EXPORTS = (
     "qpir_setup", "qpir_db_write", "qpir_geometry", "qpir_answer", "qpir_answer_batch",
     "qpir_hint", "qpir_kernel_launches", "qpir_last_error", "qpir_destroy",
+    "qpir_ens_setup", "qpir_ens_db_write", "qpir_ens_answer", "qpir_ens_answer_batch",
+    "qpir_ens_kernel_launches", "qpir_ens_last_error", "qpir_ens_destroy",
 )
 
 
@@ -44,6 +46,15 @@ class qpir_params(ctypes.Structure):
         ("row_end", ctypes.c_uint64),
         ("device", ctypes.c_int32),
         ("reserved1", ctypes.c_int32),
+    ]
+
+
+class qpir_ens_params(ctypes.Structure):
+    _fields_ = [
+        ("n_records", ctypes.c_uint64),
+        ("rec_bytes", ctypes.c_uint64),
+        ("device", ctypes.c_int32),
+        ("reserved", ctypes.c_int32),
     ]
 
 
@@ -74,6 +85,15 @@ _L.qpir_kernel_launches.restype = _u64
 _L.qpir_last_error.argtypes = [_vp]
 _L.qpir_last_error.restype = ctypes.c_char_p
 _L.qpir_destroy.argtypes = [_vp]
+_L.qpir_ens_setup.argtypes = [ctypes.POINTER(qpir_ens_params), _vp, _u64, _vp, ctypes.POINTER(_vp)]
+_L.qpir_ens_db_write.argtypes = [_vp, _u64, _u64, _vp, _u64, _vp]
+_L.qpir_ens_answer.argtypes = [_vp, _vp, _u64, _vp, _u64, _vp]
+_L.qpir_ens_answer_batch.argtypes = [_vp, _vp, _u64, _u64, _vp, _u64, _vp]
+_L.qpir_ens_kernel_launches.argtypes = [_vp]
+_L.qpir_ens_kernel_launches.restype = _u64
+_L.qpir_ens_last_error.argtypes = [_vp]
+_L.qpir_ens_last_error.restype = ctypes.c_char_p
+_L.qpir_ens_destroy.argtypes = [_vp]
 for _name in EXPORTS:
     getattr(_L, _name)
 
@@ -111,6 +131,11 @@ def _check(rc: int, ctx=None):
     if rc != QPIR_OK:
         msg = _L.qpir_last_error(ctx).decode()
         raise QpirError(rc, msg)
+
+
+def _check_ens(rc: int, ctx=None):
+    if rc != QPIR_OK:
+        raise QpirError(rc, _L.qpir_ens_last_error(ctx).decode())
 
 
 # ------------------------------------------------------------ C names
@@ -159,3 +184,40 @@ def qpir_last_error(ctx: int | None = None) -> str:
 
 def qpir_destroy(ctx: int) -> None:
     _L.qpir_destroy(ctx)
+
+
+# ------------------------------------------------------------ ENS (Chor XOR PIR)
+def qpir_ens_setup(params: qpir_ens_params, records=None, stream=None) -> int:
+    out = _vp()
+    rec_len = _numel(records) if records is not None else 0
+    rc = _L.qpir_ens_setup(ctypes.byref(params), _addr(records), rec_len, _stream(stream),
+                           ctypes.byref(out))
+    _check_ens(rc, None)
+    return out.value
+
+
+def qpir_ens_db_write(ctx: int, theta_begin: int, records, n_records: int, stream=None):
+    _check_ens(_L.qpir_ens_db_write(ctx, theta_begin, n_records, _addr(records),
+                                    _numel(records), _stream(stream)), ctx)
+
+
+def qpir_ens_answer(ctx: int, share, out, stream=None):
+    _check_ens(_L.qpir_ens_answer(ctx, _addr(share), _numel(share), _addr(out), _numel(out),
+                                  _stream(stream)), ctx)
+
+
+def qpir_ens_answer_batch(ctx: int, shares, B: int, out, stream=None):
+    _check_ens(_L.qpir_ens_answer_batch(ctx, _addr(shares), B, _numel(shares), _addr(out),
+                                        _numel(out), _stream(stream)), ctx)
+
+
+def qpir_ens_kernel_launches(ctx: int) -> int:
+    return int(_L.qpir_ens_kernel_launches(ctx))
+
+
+def qpir_ens_last_error(ctx: int | None = None) -> str:
+    return _L.qpir_ens_last_error(ctx).decode()
+
+
+def qpir_ens_destroy(ctx: int) -> None:
+    _L.qpir_ens_destroy(ctx)

@@ -16,15 +16,15 @@
 #include "../../include/qpir.h"
 #include "aux_kernels.cuh"
 #include "gemv.cuh"
+#include "host_common.h"
 #include "mma.cuh"
 
 using namespace qpir;
+using namespace qpir_host;
 
 namespace {
 
 thread_local std::string g_setup_error;
-
-uint64_t round_up(uint64_t x, uint64_t a) { return (x + a - 1) / a * a; }
 
 struct Geometry {
   uint64_t n_cells, n_ch, d, m, ell, row_begin, row_end, ell_local;
@@ -98,31 +98,6 @@ int fail(qpir_ctx* ctx, int code, const char* fmt, ...) {
                   __FILE__, __LINE__);                                                    \
   } while (0)
 
-// Restores the caller's current device on scope exit.
-struct DeviceGuard {
-  int prev = -1;
-  explicit DeviceGuard(int dev) {
-    if (cudaGetDevice(&prev) != cudaSuccess) prev = -1;
-    if (prev != dev) cudaSetDevice(dev);
-  }
-  ~DeviceGuard() {
-    int cur;
-    if (prev >= 0 && cudaGetDevice(&cur) == cudaSuccess && cur != prev) cudaSetDevice(prev);
-  }
-};
-
-// 1 = device memory of `dev`, 0 = host memory, -1 = device memory of another device.
-int where(const void* p, int dev) {
-  cudaPointerAttributes at;
-  if (cudaPointerGetAttributes(&at, p) != cudaSuccess) {
-    cudaGetLastError();
-    return 0;
-  }
-  if (at.type == cudaMemoryTypeDevice || at.type == cudaMemoryTypeManaged)
-    return at.device == dev ? 1 : -1;
-  return 0;
-}
-
 int validate(const qpir_params* p, Geometry* g) {
   if (!p) return fail(nullptr, QPIR_E_PARAM, "params: NULL");
   if (p->log_q != 32) return fail(nullptr, QPIR_E_PARAM, "log_q: %u != 32", p->log_q);
@@ -161,11 +136,6 @@ int validate(const qpir_params* p, Geometry* g) {
   g->lwe_n = p->lwe_n;
   g->seed_A = p->seed_A;
   return QPIR_OK;
-}
-
-int env_int(const char* name, int dflt) {
-  const char* v = getenv(name);
-  return v ? atoi(v) : dflt;
 }
 
 int ensure(qpir_ctx* ctx, void** buf, uint64_t* have, uint64_t need) {
@@ -362,8 +332,6 @@ int launch_mma(qpir_ctx* ctx, uint32_t BN, const uint8_t* Bl, uint32_t Npad, uin
   }
 #undef QPIR_MMA_CASE
 }
-
-bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
 
 }  // namespace
 

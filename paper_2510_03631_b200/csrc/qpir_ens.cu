@@ -1,0 +1,285 @@
+// qpir_ens.cu -- C ABI for QPADL-ENS (Chor XOR PIR; NEXT-1), include/qpir.h.
+// Host side only: validation, device memory, dispatch to ens.cuh kernels.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <string>
+
+#include "../../include/qpir.h"
+#include "ens.cuh"
+#include "host_common.h"
+
+using namespace qpir;
+using namespace qpir_host;
+
+namespace {
+thread_local std::string g_ens_setup_error;
+}
+
+struct qpir_ens_ctx {
+  uint64_t r = 0, d = 0, dp = 0;
+  int device = 0, num_sms = 148;
+  uint8_t* R = nullptr;       // [r][dp]
+  uint8_t* q_dev = nullptr;   // staging for one share (ceil(r/8))
+  uint32_t* acc = nullptr;    // [max_B][dp/4] XOR accumulators
+  uint64_t acc_B = 0;
+  uint8_t* Q_dev = nullptr;   // staging for a batch of shares
+  uint64_t Q_bytes = 0;
+  uint32_t* Qt = nullptr;     // transposed selector bits
+  uint64_t Qt_bytes = 0;
+  uint64_t launches = 0;
+  int rows_per_cta = 0;       // env QPIR_ENS_ROWS (0 = auto)
+  int ur = 16;                // env QPIR_ENS_UR (rows in flight per thread: 4, 8, 16)
+  std::string err;
+};
+
+#define ENS_FAIL(ctx, code, ...) set_error(&(ctx)->err, code, __VA_ARGS__)
+#define ENS_CUDA(ctx, call)                                                                  \
+  do {                                                                                       \
+    cudaError_t e_ = (call);                                                                 \
+    if (e_ != cudaSuccess)                                                                   \
+      return ENS_FAIL(ctx, e_ == cudaErrorMemoryAllocation ? QPIR_E_OOM : QPIR_E_CUDA,      \
+                      "%s: %s", #call, cudaGetErrorString(e_));                              \
+  } while (0)
+#define ENS_LAUNCHED(ctx)                                                                    \
+  do {                                                                                       \
+    (ctx)->launches++;                                                                       \
+    cudaError_t e_ = cudaGetLastError();                                                     \
+    if (e_ != cudaSuccess)                                                                   \
+      return ENS_FAIL(ctx, QPIR_E_CUDA, "kernel launch: %s", cudaGetErrorString(e_));       \
+  } while (0)
+
+namespace {
+
+int grow(qpir_ens_ctx* ctx, void** buf, uint64_t* have, uint64_t need) {
+  if (*have >= need) return QPIR_OK;
+  if (*buf) cudaFree(*buf);
+  *buf = nullptr;
+  *have = 0;
+  ENS_CUDA(ctx, cudaMalloc(buf, need));
+  *have = need;
+  return QPIR_OK;
+}
+
+// Stage a possibly-host input of `bytes` into a device buffer; returns the device pointer.
+int stage_in(qpir_ens_ctx* ctx, const uint8_t* src, uint64_t bytes, uint8_t* staging,
+             const uint8_t** dev, cudaStream_t st) {
+  const int w = where(src, ctx->device);
+  if (w < 0) return ENS_FAIL(ctx, QPIR_E_PARAM, "input: memory of another device");
+  if (w == 1) {
+    *dev = src;
+    return QPIR_OK;
+  }
+  ENS_CUDA(ctx, cudaMemcpyAsync(staging, src, bytes, cudaMemcpyHostToDevice, st));
+  *dev = staging;
+  return QPIR_OK;
+}
+
+// Copy B rows of d bytes out of the dp-strided accumulator into `out`.
+int copy_out(qpir_ens_ctx* ctx, uint8_t* out, uint64_t B, cudaStream_t st) {
+  const int w = where(out, ctx->device);
+  if (w < 0) return ENS_FAIL(ctx, QPIR_E_PARAM, "out: memory of another device");
+  ENS_CUDA(ctx, cudaMemcpy2DAsync(out, ctx->d, ctx->acc, ctx->dp, ctx->d, B,
+                                  w ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost, st));
+  if (!w) ENS_CUDA(ctx, cudaStreamSynchronize(st));
+  return QPIR_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+int qpir_ens_setup(const qpir_ens_params* p, const uint8_t* records, uint64_t records_len,
+                   void* stream, qpir_ens_ctx** out) {
+  g_ens_setup_error.clear();
+  if (!out) return set_error(&g_ens_setup_error, QPIR_E_PARAM, "out: NULL");
+  *out = nullptr;
+  if (!p) return set_error(&g_ens_setup_error, QPIR_E_PARAM, "params: NULL");
+  if (p->reserved != 0) return set_error(&g_ens_setup_error, QPIR_E_PARAM, "reserved: must be 0");
+  if (p->n_records == 0) return set_error(&g_ens_setup_error, QPIR_E_DIMENSION, "n_records: 0");
+  if (p->rec_bytes == 0 || p->rec_bytes > 16384)
+    return set_error(&g_ens_setup_error, QPIR_E_DIMENSION, "rec_bytes: %llu not in [1, 16384]",
+                     (unsigned long long)p->rec_bytes);
+  if (records && records_len != p->n_records * p->rec_bytes)
+    return set_error(&g_ens_setup_error, QPIR_E_DIMENSION, "records_len: %llu != %llu",
+                     (unsigned long long)records_len,
+                     (unsigned long long)(p->n_records * p->rec_bytes));
+  if (p->device < 0) return set_error(&g_ens_setup_error, QPIR_E_PARAM, "device: < 0");
+  int sms = 148;
+  std::string e = check_device(p->device, &sms);
+  if (!e.empty()) return set_error(&g_ens_setup_error, QPIR_E_CUDA, "%s", e.c_str());
+  DeviceGuard dg(p->device);
+  qpir_ens_ctx* ctx = new qpir_ens_ctx();
+  ctx->r = p->n_records;
+  ctx->d = p->rec_bytes;
+  ctx->dp = round_up(p->rec_bytes, 16);
+  ctx->device = p->device;
+  ctx->num_sms = sms;
+  ctx->rows_per_cta = env_int("QPIR_ENS_ROWS", 0);
+  ctx->ur = env_int("QPIR_ENS_UR", 16);
+  cudaStream_t st = (cudaStream_t)stream;
+  const uint64_t nb = (ctx->r + 7) / 8;
+  if (cudaMalloc(&ctx->R, ctx->r * ctx->dp) != cudaSuccess ||
+      cudaMalloc(&ctx->q_dev, nb) != cudaSuccess) {
+    cudaGetLastError();
+    g_ens_setup_error = "records: cudaMalloc failed";
+    qpir_ens_destroy(ctx);
+    return QPIR_E_OOM;
+  }
+  int rc = QPIR_OK;
+  if (cudaMemsetAsync(ctx->R, 0, ctx->r * ctx->dp, st) != cudaSuccess) rc = QPIR_E_CUDA;
+  if (!rc && records) rc = qpir_ens_db_write(ctx, 0, ctx->r, records, records_len, stream);
+  if (!rc && cudaStreamSynchronize(st) != cudaSuccess) rc = QPIR_E_CUDA;
+  if (rc) {
+    g_ens_setup_error = ctx->err.empty() ? "setup failed" : ctx->err;
+    qpir_ens_destroy(ctx);
+    return rc;
+  }
+  *out = ctx;
+  return QPIR_OK;
+}
+
+int qpir_ens_db_write(qpir_ens_ctx* ctx, uint64_t theta_begin, uint64_t n_records,
+                      const uint8_t* records, uint64_t records_len, void* stream) {
+  if (!ctx) return QPIR_E_STATE;
+  if (theta_begin > ctx->r || n_records > ctx->r - theta_begin)
+    return ENS_FAIL(ctx, QPIR_E_DIMENSION, "theta range: [%llu, +%llu) exceeds %llu records",
+                    (unsigned long long)theta_begin, (unsigned long long)n_records,
+                    (unsigned long long)ctx->r);
+  if (records_len != n_records * ctx->d)
+    return ENS_FAIL(ctx, QPIR_E_DIMENSION, "records_len: %llu != %llu",
+                    (unsigned long long)records_len, (unsigned long long)(n_records * ctx->d));
+  if (n_records == 0) return QPIR_OK;
+  DeviceGuard dg(ctx->device);
+  const int w = where(records, ctx->device);
+  if (w < 0) return ENS_FAIL(ctx, QPIR_E_PARAM, "records: memory of another device");
+  cudaStream_t st = (cudaStream_t)stream;
+  ENS_CUDA(ctx, cudaMemcpy2DAsync(ctx->R + theta_begin * ctx->dp, ctx->dp, records, ctx->d,
+                                  ctx->d, n_records,
+                                  w ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, st));
+  if (!w) ENS_CUDA(ctx, cudaStreamSynchronize(st));
+  return QPIR_OK;
+}
+
+int qpir_ens_answer(qpir_ens_ctx* ctx, const uint8_t* share, uint64_t len_share, uint8_t* out,
+                    uint64_t len_out, void* stream) {
+  if (!ctx) return QPIR_E_STATE;
+  const uint64_t nb = (ctx->r + 7) / 8;
+  if (!share || !out) return ENS_FAIL(ctx, QPIR_E_PARAM, "share/out: NULL");
+  if (len_share != nb)
+    return ENS_FAIL(ctx, QPIR_E_DIMENSION, "len_share: %llu != %llu", (unsigned long long)len_share,
+                    (unsigned long long)nb);
+  if (len_out != ctx->d)
+    return ENS_FAIL(ctx, QPIR_E_DIMENSION, "len_out: %llu != d %llu", (unsigned long long)len_out,
+                    (unsigned long long)ctx->d);
+  DeviceGuard dg(ctx->device);
+  cudaStream_t st = (cudaStream_t)stream;
+  int rc = grow(ctx, (void**)&ctx->acc, &ctx->acc_B, ctx->dp);
+  if (rc) return rc;
+  const uint8_t* qd = nullptr;
+  rc = stage_in(ctx, share, nb, ctx->q_dev, &qd, st);
+  if (rc) return rc;
+  ENS_CUDA(ctx, cudaMemsetAsync(ctx->acc, 0, ctx->dp, st));
+  EnsArgs a;
+  a.R = ctx->R;
+  a.q = qd;
+  a.out = ctx->acc;
+  a.r = ctx->r;
+  a.dp = (uint32_t)ctx->dp;
+  a.W = (uint32_t)(ctx->dp / 16);
+  const uint32_t R = std::max<uint32_t>(1, 256 / a.W);
+  const uint32_t threads = a.W * R;
+  const int UR = ctx->ur == 8 ? 8 : ctx->ur == 4 ? 4 : 16;
+  uint64_t rows = ctx->rows_per_cta;
+  if (rows == 0) {
+    // ~1.5 MB of records per CTA (measured best on B200 at d = 3072: 512 rows),
+    // at least one full unrolled step
+    rows = std::max<uint64_t>((1536u << 10) / ctx->dp, (uint64_t)R * UR);
+  }
+  rows = round_up(rows, (uint64_t)R * UR);
+  a.rows_per_cta = rows;
+  const uint64_t grid = (ctx->r + rows - 1) / rows;
+  const size_t smem = R > 1 ? threads * 16 : 0;
+  if (UR == 16)
+    ens_scan_kernel<16><<<(uint32_t)grid, threads, smem, st>>>(a);
+  else if (UR == 4)
+    ens_scan_kernel<4><<<(uint32_t)grid, threads, smem, st>>>(a);
+  else
+    ens_scan_kernel<8><<<(uint32_t)grid, threads, smem, st>>>(a);
+  ENS_LAUNCHED(ctx);
+  return copy_out(ctx, out, 1, st);
+}
+
+int qpir_ens_answer_batch(qpir_ens_ctx* ctx, const uint8_t* shares, uint64_t B,
+                          uint64_t len_shares, uint8_t* out, uint64_t len_out, void* stream) {
+  if (!ctx) return QPIR_E_STATE;
+  const uint64_t nb = (ctx->r + 7) / 8;
+  if (!shares || !out) return ENS_FAIL(ctx, QPIR_E_PARAM, "shares/out: NULL");
+  if (B == 0 || B > 65536) return ENS_FAIL(ctx, QPIR_E_PARAM, "B: %llu not in [1, 65536]",
+                                           (unsigned long long)B);
+  if (len_shares != B * nb)
+    return ENS_FAIL(ctx, QPIR_E_DIMENSION, "len_shares: %llu != B*ceil(r/8) %llu",
+                    (unsigned long long)len_shares, (unsigned long long)(B * nb));
+  if (len_out != B * ctx->d)
+    return ENS_FAIL(ctx, QPIR_E_DIMENSION, "len_out: %llu != B*d %llu", (unsigned long long)len_out,
+                    (unsigned long long)(B * ctx->d));
+  DeviceGuard dg(ctx->device);
+  cudaStream_t st = (cudaStream_t)stream;
+  int rc = grow(ctx, (void**)&ctx->acc, &ctx->acc_B, B * ctx->dp);
+  if (rc) return rc;
+  const uint32_t QW = (uint32_t)((B + 31) / 32);
+  rc = grow(ctx, (void**)&ctx->Qt, &ctx->Qt_bytes, ctx->r * QW * 4);
+  if (rc) return rc;
+  const uint8_t* Qd = shares;
+  if (where(shares, ctx->device) != 1) {
+    rc = grow(ctx, (void**)&ctx->Q_dev, &ctx->Q_bytes, B * nb);
+    if (rc) return rc;
+    rc = stage_in(ctx, shares, B * nb, ctx->Q_dev, &Qd, st);
+    if (rc) return rc;
+  }
+  ENS_CUDA(ctx, cudaMemsetAsync(ctx->acc, 0, B * ctx->dp, st));
+  {
+    dim3 grid((uint32_t)((ctx->r + 255) / 256), QW);
+    ens_transpose_bits_kernel<<<grid, 256, 0, st>>>(Qd, ctx->Qt, ctx->r, nb, (uint32_t)B, QW);
+    ENS_LAUNCHED(ctx);
+  }
+  EnsBatchArgs a;
+  a.R = ctx->R;
+  a.Qt = ctx->Qt;
+  a.out = ctx->acc;
+  a.r = ctx->r;
+  a.dp = (uint32_t)ctx->dp;
+  a.W = (uint32_t)(ctx->dp / 16);
+  a.QW = QW;
+  a.B = (uint32_t)B;
+  const uint32_t slices = (a.W + ENS_CW - 1) / ENS_CW;
+  const uint32_t qblocks = (uint32_t)((B + ENS_QG * ENS_QB - 1) / (ENS_QG * ENS_QB));
+  // enough CTAs for ~8 per SM, rows split evenly
+  const uint64_t want = 8ull * ctx->num_sms;
+  uint64_t splits = std::max<uint64_t>(1, (want + slices * qblocks - 1) / (slices * qblocks));
+  uint64_t rows = ctx->rows_per_cta ? (uint64_t)ctx->rows_per_cta
+                                    : std::min<uint64_t>(256, (ctx->r + splits - 1) / splits);
+  rows = round_up(std::max<uint64_t>(rows, 4), 4);
+  a.rows_per_cta = rows;
+  dim3 grid((uint32_t)((ctx->r + rows - 1) / rows), slices, qblocks);
+  ens_batch_kernel<<<grid, ENS_CW * ENS_QB, 0, st>>>(a);
+  ENS_LAUNCHED(ctx);
+  return copy_out(ctx, out, B, st);
+}
+
+uint64_t qpir_ens_kernel_launches(const qpir_ens_ctx* ctx) { return ctx ? ctx->launches : 0; }
+
+const char* qpir_ens_last_error(const qpir_ens_ctx* ctx) {
+  return ctx ? ctx->err.c_str() : g_ens_setup_error.c_str();
+}
+
+void qpir_ens_destroy(qpir_ens_ctx* ctx) {
+  if (!ctx) return;
+  DeviceGuard dg(ctx->device);
+  void* bufs[] = {ctx->R, ctx->q_dev, ctx->acc, ctx->Q_dev, ctx->Qt};
+  for (void* b : bufs)
+    if (b) cudaFree(b);
+  delete ctx;
+}
+
+}  // extern "C"

@@ -1,0 +1,86 @@
+"""GPU parity for QPADL-ENS (Chor XOR PIR, NEXT-1) through the C ABI against
+the oracle (bit-exact bytes)."""
+import numpy as np
+import pytest
+import torch
+
+import synth
+from oracle import oracle as O
+
+pytestmark = pytest.mark.gpu
+
+
+def _P():
+    import paper_2510_03631_b200 as P
+    return P
+
+
+def _share(seed, r):
+    q = synth.uniform_u8_np(seed, ((r + 7) // 8,))
+    if r % 8:
+        q[-1] &= (1 << (r % 8)) - 1
+    return q
+
+
+@pytest.mark.parametrize("r,d", [(1000, 24), (77, 5), (4099, 100), (513, 3072), (20000, 16)])
+@pytest.mark.parametrize("rows", ["0", "8", "96"])
+def test_ens_answer_matches_oracle(cuda_ok, r, d, rows, monkeypatch):
+    monkeypatch.setenv("QPIR_ENS_ROWS", rows)
+    P = _P()
+    rec = synth.uniform_u8_np(r + d, (r, d))
+    with P.EnsServer(r, d, records=rec) as s:
+        nb = (r + 7) // 8
+        assert (s.answer(np.zeros(nb, np.uint8)).cpu().numpy() == 0).all()
+        for j in (0, r // 2, r - 1):
+            e = np.zeros(nb, np.uint8)
+            e[j >> 3] = 1 << (j & 7)
+            assert (s.answer(e).cpu().numpy() == rec[j]).all()
+        for seed in (1, 2):
+            q = _share(seed, r)
+            want = O.ens_respond(rec, q)
+            out = np.empty(d, np.uint8)
+            s.answer(q, out=out)  # host in / host out
+            assert (out == want).all()
+            got = s.answer(torch.from_numpy(q).cuda())  # device in / device out
+            assert (got.cpu().numpy() == want).all()
+
+
+@pytest.mark.parametrize("B", [1, 7, 64, 130])
+def test_ens_batch_matches_oracle(cuda_ok, B):
+    P = _P()
+    r, d = 3001, 200
+    rec = synth.uniform_u8_np(5, (r, d))
+    Q = np.stack([_share(100 + b, r) for b in range(B)])
+    want = O.ens_respond_batch(rec, Q)
+    with P.EnsServer(r, d, records=torch.from_numpy(rec).cuda()) as s:
+        got = s.answer_batch(Q).cpu().numpy()
+        assert (got == want).all()
+        assert (s.answer(Q[B // 2]).cpu().numpy() == want[B // 2]).all()
+
+
+def test_ens_bruteforce_reconstruct(cuda_ok):
+    """Lemma 1: XOR of the l GPU responses == record theta, every theta."""
+    P = _P()
+    r, d, l = 384, 40, 3
+    rec = synth.uniform_u8_np(6, (r, d))
+    with P.EnsServer(r, d, records=rec) as s:
+        shares = np.concatenate([O.ens_query(t, r, l, 500 + t) for t in range(r)])  # (r*l, nb)
+        resp = s.answer_batch(shares).cpu().numpy().reshape(r, l, d)
+    for t in range(r):
+        assert (O.ens_reconstruct(resp[t]) == rec[t]).all()
+
+
+def test_ens_db_write_and_c2_scale(cuda_ok):
+    """configs[1]-sized ENS DB (327680 paper-shaped 3 KB records = 1.007 GB)."""
+    P = _P()
+    n_cells, n_ch, d = 8192, 40, 3072
+    r = n_cells * n_ch
+    with P.EnsServer(r, d) as s:
+        chunk = 65536
+        for t0 in range(0, r, chunk):
+            s.db_write(t0, synth.records(31, t0, min(chunk, r - t0), d, n_ch, device="cuda"))
+        rec = synth.records(31, 0, r, d, n_ch, device="cuda").cpu().numpy()
+        q = _share(32, r)
+        assert (s.answer(q).cpu().numpy() == O.ens_respond(rec, q)).all()
+        Q = np.stack([_share(40 + b, r) for b in range(3)])
+        assert (s.answer_batch(Q).cpu().numpy() == O.ens_respond_batch(rec, Q)).all()
