@@ -64,6 +64,11 @@ def lib():
         L.qo_ens_respond.argtypes = [_u8p, _u64, _u64, _u8p, _u8p]
         L.qo_ens_respond_batch.argtypes = [_u8p, _u64, _u64, _u8p, _u64, _u8p]
         L.qo_ens_reconstruct.argtypes = [_u8p, _u32, _u64, _u8p]
+        L.qo_ftr_query.argtypes = [_u64, _u64, _u32, _u32, _u32, _u64, _u32p]
+        L.qo_ftr_respond.argtypes = [_u8p, _u64, _u64, _u32p, _u32, _u32p]
+        L.qo_ftr_respond_batch.argtypes = [_u8p, _u64, _u64, _u32p, _u64, _u32, _u32p]
+        L.qo_ftr_reconstruct.argtypes = [_u32p, _u32p, _u32, _u64, _u32, _u32p]
+        L.qo_ftr_reconstruct.restype = ctypes.c_int
         L.qo_num_threads.restype = ctypes.c_int
         L.qo_set_num_threads.argtypes = [ctypes.c_int]
         _lib = L
@@ -224,6 +229,50 @@ def ens_reconstruct(resp: np.ndarray) -> np.ndarray:
     l, d = resp.shape
     out = np.empty(d, np.uint8)
     lib().qo_ens_reconstruct(_p(resp, _u8p), l, d, _p(out, _u8p))
+    return out
+
+
+# ---------------------------------------------------------------- FTR (Goldberg, NEXT-2)
+FTR_P = 65537
+
+
+def ftr_query(theta: int, r: int, l: int, t: int, seed: int, p: int = FTR_P) -> np.ndarray:
+    """l shares (l x r u32); server i evaluates at alpha_i = i + 1."""
+    sh = np.empty((l, r), np.uint32)
+    lib().qo_ftr_query(theta, r, l, t, p, seed, _p(sh, _u32p))
+    return sh
+
+
+def ftr_respond(records: np.ndarray, rho: np.ndarray, p: int = FTR_P) -> np.ndarray:
+    rec = _c(records, np.uint8)
+    r, s_ = rec.shape
+    rho = _c(rho, np.uint32)
+    assert rho.shape == (r,)
+    out = np.empty(s_, np.uint32)
+    lib().qo_ftr_respond(_p(rec, _u8p), r, s_, _p(rho, _u32p), p, _p(out, _u32p))
+    return out
+
+
+def ftr_respond_batch(records: np.ndarray, Q: np.ndarray, p: int = FTR_P) -> np.ndarray:
+    rec = _c(records, np.uint8)
+    r, s_ = rec.shape
+    Q = _c(Q, np.uint32)
+    B = Q.shape[0]
+    assert Q.shape == (B, r)
+    out = np.empty((B, s_), np.uint32)
+    lib().qo_ftr_respond_batch(_p(rec, _u8p), r, s_, _p(Q, _u32p), B, p, _p(out, _u32p))
+    return out
+
+
+def ftr_reconstruct(resp: np.ndarray, alpha, p: int = FTR_P) -> np.ndarray:
+    resp = _c(resp, np.uint32)
+    k, s_ = resp.shape
+    al = _c(alpha, np.uint32)
+    assert al.shape == (k,)
+    out = np.empty(s_, np.uint32)
+    rc = lib().qo_ftr_reconstruct(_p(resp, _u32p), _p(al, _u32p), k, s_, p, _p(out, _u32p))
+    if rc != 0:
+        raise ValueError("evaluation points must be distinct")
     return out
 
 

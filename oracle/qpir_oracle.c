@@ -340,3 +340,95 @@ void qo_ens_reconstruct(const uint8_t *resp, uint32_t l, uint64_t d, uint8_t *ou
   for (uint32_t i = 0; i < l; ++i)
     for (uint64_t j = 0; j < d; ++j) out[j] ^= resp[(uint64_t)i * d + j];
 }
+
+/* ------------------------------------------------------------------ */
+/* NEXT-2: QPADL-FTR = Goldberg robust multi-server PIR over a prime    */
+/* field F_p (Lemma 1 proof; Alg. 4 "Multi-request       */
+/* Parallel Goldberg-PIR").  DB = r records x s words;     */
+/* one word = one record byte (DESIGN R17), p = 65537 by default        */
+/* (SPEC S:196).  Server i evaluates at alpha_i = i + 1.   */
+/* ------------------------------------------------------------------ */
+#define QO_DOMAIN_F 0x46u
+
+static uint64_t mulmod(uint64_t a, uint64_t b, uint64_t p) { return (a * b) % p; }
+
+static uint64_t powmod(uint64_t a, uint64_t e, uint64_t p) {
+  uint64_t r = 1 % p;
+  a %= p;
+  while (e) {
+    if (e & 1) r = mulmod(r, a, p);
+    a = mulmod(a, a, p);
+    e >>= 1;
+  }
+  return r;
+}
+
+/* Client.Query (Lemma 1 proof): for each record index j a random
+ * polynomial f_j of degree t with f_j(0) = e_theta[j]; server i receives
+ * rho_i[j] = f_j(alpha_i), alpha_i = i + 1.  Coefficient a_k of f_j
+ * (k = 1..t) = Philox(key = seed, ctr = (j, k, theta, 'F'))[0] mod p
+ * (DESIGN R18).  shares: l x r u32.  p < 2^31 so products fit in u64. */
+void qo_ftr_query(uint64_t theta, uint64_t r, uint32_t l, uint32_t t, uint32_t p,
+                  uint64_t seed, uint32_t *shares) {
+  uint32_t key[2];
+  key_from_seed(seed, key);
+  for (uint64_t j = 0; j < r; ++j) {
+    for (uint32_t i = 0; i < l; ++i) {
+      uint64_t x = (uint64_t)i + 1;
+      uint64_t val = (j == theta) ? 1u : 0u; /* f_j(0) = e_theta[j] */
+      uint64_t xk = 1;
+      for (uint32_t k = 1; k <= t; ++k) {
+        uint32_t ctr[4] = {(uint32_t)j, k, (uint32_t)theta, QO_DOMAIN_F};
+        uint32_t out[4];
+        qo_philox4x32_10(ctr, key, out);
+        xk = mulmod(xk, x, p);
+        val = (val + mulmod(out[0] % p, xk, p)) % p;
+      }
+      shares[(uint64_t)i * r + j] = (uint32_t)val;
+    }
+  }
+}
+
+/* DB.Query.Response (Lemma 1 proof "R_j := rho_j . DB"; Alg. 4 steps
+ * 14-15): out[b] = sum_j rho[j] * DB[j][b] mod p.  records: r x s bytes. */
+void qo_ftr_respond(const uint8_t *records, uint64_t r, uint64_t s, const uint32_t *rho,
+                    uint32_t p, uint32_t *out) {
+  for (uint64_t b = 0; b < s; ++b) {
+    uint64_t acc = 0;
+    for (uint64_t j = 0; j < r; ++j)
+      acc = (acc + (uint64_t)rho[j] * records[j * s + b]) % p;
+    out[b] = (uint32_t)acc;
+  }
+}
+
+void qo_ftr_respond_batch(const uint8_t *records, uint64_t r, uint64_t s, const uint32_t *Q,
+                          uint64_t B, uint32_t p, uint32_t *out) {
+  int64_t BB = (int64_t)B;
+#pragma omp parallel for schedule(static)
+  for (int64_t b = 0; b < BB; ++b)
+    qo_ftr_respond(records, r, s, Q + (uint64_t)b * r, p, out + (uint64_t)b * s);
+}
+
+/* BlockReconst (Def. 1): Lagrange interpolation at 0 of k responses
+ * with evaluation points alpha (k distinct nonzero elements):
+ * out[b] = sum_i lambda_i * resp[i][b] mod p,
+ * lambda_i = prod_{m != i} alpha_m / (alpha_m - alpha_i).  Modular inverse by
+ * Fermat's little theorem (p prime).  Returns -1 if two alphas coincide. */
+int qo_ftr_reconstruct(const uint32_t *resp, const uint32_t *alpha, uint32_t k, uint64_t s,
+                       uint32_t p, uint32_t *out) {
+  for (uint64_t b = 0; b < s; ++b) out[b] = 0;
+  for (uint32_t i = 0; i < k; ++i) {
+    uint64_t num = 1, den = 1;
+    for (uint32_t m = 0; m < k; ++m) {
+      if (m == i) continue;
+      uint64_t am = alpha[m] % p, ai = alpha[i] % p;
+      if (am == ai) return -1;
+      num = mulmod(num, am, p);
+      den = mulmod(den, (am + p - ai) % p, p);
+    }
+    uint64_t lam = mulmod(num, powmod(den, p - 2, p), p);
+    for (uint64_t b = 0; b < s; ++b)
+      out[b] = (uint32_t)((out[b] + mulmod(lam, resp[(uint64_t)i * s + b], p)) % p);
+  }
+  return 0;
+}
