@@ -54,6 +54,9 @@ WORKLOADS = {
                    kind="ens"),
     "ens-c2-b128": dict(name="QPADL-ENS multi-request (Alg. 3): 1.007 GB, 128 shares",
                         n_cells=8192, n_ch=40, d=3072, kind="ens_batch", B=128),
+    "ftr-c2-b128": dict(name="QPADL-FTR (Goldberg PIR over F_65537, NEXT-2; Alg. 4): 327680 "
+                             "paper-shaped 3 KB records = 1.007 GB, 128 Shamir-share queries",
+                        n_cells=327680, n_ch=1, d=3072, kind="batch", B=128, modp=65537),
     "c5": dict(name="hint D.A, n=1024, one rank's shard of the 32.2 GB DB at G=8 "
                     "(BASELINE configs[4])", n_cells=262144, n_ch=40, d=3072, kind="hint", n=1024,
                shard_of=8),
@@ -424,6 +427,8 @@ def main():
             evs[0].record(stream)
         if kind == "answer":
             srv.answer(qs[i % len(qs)], out=out, stream=stream)
+        elif kind == "batch" and wl.get("modp"):
+            srv.answer_batch_modp(qs[i % len(qs)], wl["modp"], out=out, stream=stream)
         elif kind == "batch":
             srv.answer_batch(qs[i % len(qs)], out=out, stream=stream)
         else:
@@ -482,6 +487,8 @@ def main():
         def e2e_step():
             if kind == "answer":
                 srv.answer(h_in, out=dev_out, stream=stream)  # H2D of qu inside the C call
+            elif wl.get("modp"):
+                srv.answer_batch_modp(h_in, wl["modp"], out=dev_out, stream=stream)
             else:
                 srv.answer_batch(h_in, out=dev_out, stream=stream)
             full = gather_answer(dev_out, sizes) if world > 1 else dev_out

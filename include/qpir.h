@@ -112,6 +112,17 @@ int qpir_answer_batch(qpir_ctx *ctx, const uint32_t *Q, uint64_t B,
                       uint64_t len_Q, uint32_t *ans_local, uint64_t len_ans,
                       void *stream);
 
+/* Batch over a prime field (NEXT-2, QPADL-FTR: Goldberg robust PIR,
+ * PAPER.md:740; the "q . DB mod q" GEMM of Alg. 4):
+ *   ans_local[b * ell_local + i] = (sum_c D[row_begin + i][c] * Q[b * m + c]) mod p,
+ * exact for any u32 Q entries and any 2 <= p < 2^32 (results < p).  With
+ * n_ch = 1 and n_cells = r records, row b of D is byte b of every record, so
+ * row i of the answer is word i of the FTR response rho . DB (one word = one
+ * record byte, DESIGN R17).  Same buffers and B range as qpir_answer_batch. */
+int qpir_answer_batch_modp(qpir_ctx *ctx, const uint32_t *Q, uint64_t B,
+                           uint64_t len_Q, uint32_t p, uint32_t *ans_local,
+                           uint64_t len_ans, void *stream);
+
 /* Hint (step a7): H_local[i * n + j] = sum_c D[row_begin + i][c] * A[c][j]
  * mod 2^32 with A expanded from seed_A on the device (n = lwe_n).  H_local:
  * ell_local x n row-major (len == ell_local * n). */

@@ -8,6 +8,8 @@ Public API (thin wrappers over the C ABI in include/qpir.h):
     EnsServer(...)            QPADL-ENS (Chor XOR PIR, NEXT-1): records theta-major
         .answer(share)        XOR of the selected records (HBM scan, sparse rows skipped)
         .answer_batch(Q)      multi-request form (Alg. 3)
+    FtrServer(...)            QPADL-FTR (Goldberg PIR over F_p, NEXT-2): rho . DB mod p
+        .answer_batch(Q)      on the tcgen05 limb engine with a mod-p epilogue (Alg. 4)
     dist.DistributedPIR       row-sharded over ranks, NCCL gather of answer slices
 u32 values are carried in torch.int32 tensors (same bits); use u32() to view them.
 """
@@ -19,7 +21,7 @@ import torch
 from . import _lib
 from ._lib import QpirError, qpir_params  # noqa: F401
 
-__all__ = ["PirServer", "EnsServer", "QpirError", "u32", "qpir_params"]
+__all__ = ["PirServer", "EnsServer", "FtrServer", "QpirError", "u32", "qpir_params"]
 
 
 def u32(t) -> np.ndarray:
@@ -64,6 +66,13 @@ class PirServer:
         if out is None:
             out = torch.empty((B, self.ell_local), dtype=torch.int32, device=self._dev())
         _lib.qpir_answer_batch(self._ctx, Q, B, out, stream)
+        return out
+
+    def answer_batch_modp(self, Q, p: int, out=None, stream=None):
+        B = int(Q.shape[0])
+        if out is None:
+            out = torch.empty((B, self.ell_local), dtype=torch.int32, device=self._dev())
+        _lib.qpir_answer_batch_modp(self._ctx, Q, B, p, out, stream)
         return out
 
     def hint(self, out=None, stream=None):
@@ -138,6 +147,44 @@ class EnsServer:
             self.close()
         except Exception:
             pass
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *exc):
+        self.close()
+
+
+class FtrServer:
+    """QPADL-FTR server (Goldberg Shamir-share PIR over F_p): r records of s byte-words.
+
+    The records are the columns of a PirServer with n_ch = 1 (row b = byte b of
+    every record), so the response rho . DB mod p is the field-mode batch GEMM."""
+
+    P_DEFAULT = 65537
+
+    def __init__(self, n_records: int, rec_bytes: int, *, p: int = P_DEFAULT, device: int = 0,
+                 records=None, stream=None):
+        self.p = p
+        self.r, self.s = n_records, rec_bytes
+        self.server = PirServer(n_records, 1, rec_bytes, lwe_n=4, device=device,
+                                records=records, stream=stream)
+
+    def db_write(self, theta_begin: int, records, stream=None) -> None:
+        self.server.db_write(theta_begin, records, stream)
+
+    def answer_batch(self, Q, out=None, stream=None):
+        return self.server.answer_batch_modp(Q, self.p, out, stream)
+
+    def answer(self, rho, stream=None):
+        return self.answer_batch(rho.reshape(1, -1), stream=stream)[0]
+
+    @property
+    def kernel_launches(self) -> int:
+        return self.server.kernel_launches
+
+    def close(self) -> None:
+        self.server.close()
 
     def __enter__(self):
         return self

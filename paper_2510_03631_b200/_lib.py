@@ -26,7 +26,7 @@ QPIR_E_CUDA = 5
 EXPORTS = (
     "qpir_setup", "qpir_db_write", "qpir_geometry", "qpir_answer", "qpir_answer_batch",
     "qpir_hint", "qpir_kernel_launches", "qpir_last_error", "qpir_destroy",
-    "qpir_ens_setup", "qpir_ens_db_write", "qpir_ens_answer", "qpir_ens_answer_batch",
+    "qpir_answer_batch_modp", "qpir_ens_setup", "qpir_ens_db_write", "qpir_ens_answer", "qpir_ens_answer_batch",
     "qpir_ens_kernel_launches", "qpir_ens_last_error", "qpir_ens_destroy",
 )
 
@@ -80,6 +80,7 @@ _L.qpir_geometry.argtypes = [_vp, ctypes.POINTER(_u64), ctypes.POINTER(_u64),
 _L.qpir_answer.argtypes = [_vp, _vp, _u64, _vp, _u64, _vp]
 _L.qpir_answer_batch.argtypes = [_vp, _vp, _u64, _u64, _vp, _u64, _vp]
 _L.qpir_hint.argtypes = [_vp, _vp, _u64, _vp]
+_L.qpir_answer_batch_modp.argtypes = [_vp, _vp, _u64, _u64, ctypes.c_uint32, _vp, _u64, _vp]
 _L.qpir_kernel_launches.argtypes = [_vp]
 _L.qpir_kernel_launches.restype = _u64
 _L.qpir_last_error.argtypes = [_vp]
@@ -168,6 +169,11 @@ def qpir_answer(ctx: int, qu, ans_local, stream=None):
 def qpir_answer_batch(ctx: int, Q, B: int, ans_local, stream=None):
     _check(_L.qpir_answer_batch(ctx, _addr(Q), B, _numel(Q), _addr(ans_local),
                                 _numel(ans_local), _stream(stream)), ctx)
+
+
+def qpir_answer_batch_modp(ctx: int, Q, B: int, p: int, ans_local, stream=None):
+    _check(_L.qpir_answer_batch_modp(ctx, _addr(Q), B, _numel(Q), p, _addr(ans_local),
+                                     _numel(ans_local), _stream(stream)), ctx)
 
 
 def qpir_hint(ctx: int, H_local, stream=None):

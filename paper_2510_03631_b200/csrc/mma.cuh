@@ -35,7 +35,11 @@ constexpr uint32_t MMA_BM = 128;           // rows of D per UMMA (M)
 constexpr uint32_t MMA_BK = 128;           // K padding unit of D (cells)
 constexpr uint32_t MMA_THREADS = 192;
 
-enum : int { OUT_QUERY_MAJOR = 0, OUT_ROW_MAJOR = 1 };
+// OUT_MODP (NEXT-2, FTR over F_p): query-major, each K-split's exact limb sums
+// (u32-exact while the split covers <= 66051 cells) are folded to
+// sum_k 2^{8k} C_k mod p in 64-bit and added into a u64 scratch; a fixup
+// kernel reduces mod p again.
+enum : int { OUT_QUERY_MAJOR = 0, OUT_ROW_MAJOR = 1, OUT_MODP = 2 };
 
 struct MmaArgs {
   const uint8_t* A;   // D shard, 128-row panels [L/128][G][128][16]
@@ -46,6 +50,8 @@ struct MmaArgs {
   uint32_t n_out;     // valid outputs along N (queries B, or hint width n)
   uint32_t out_ld;    // query-major: ell_local; row-major: n
   uint32_t m_tiles, n_tiles, splits, kps;  // work units = m_tiles * n_tiles * splits
+  uint32_t p;         // OUT_MODP modulus
+  unsigned long long* out64;  // OUT_MODP accumulator [n_out][out_ld]
 };
 
 // GPB = 16-cell column groups per pipeline stage (K-block = 16 * GPB cells).
@@ -199,6 +205,21 @@ __global__ void __launch_bounds__(MMA_THREADS, 1) mma_u8_limb_kernel(MmaArgs a) 
           for (uint32_t t = 0; t < CH / 16; ++t) {
             const uint32_t c0 = cb + 16 * t;
             const uint32_t j0 = (nt * BN + c0) / 4;  // first output (query / hint column)
+            if (OUT_MODE == OUT_MODP) {
+              if (row < a.rows) {
+#pragma unroll
+                for (int jj = 0; jj < 4; ++jj) {
+                  const uint32_t* w = v + 16 * t + 4 * jj;
+                  const unsigned long long x = (unsigned long long)w[0] +
+                                               ((unsigned long long)w[1] << 8) +
+                                               ((unsigned long long)w[2] << 16) +
+                                               ((unsigned long long)w[3] << 24);
+                  if (j0 + jj < a.n_out)
+                    atomicAdd(a.out64 + (size_t)(j0 + jj) * a.out_ld + row, x % a.p);
+                }
+              }
+              continue;
+            }
             uint32_t o[4];
 #pragma unroll
             for (int jj = 0; jj < 4; ++jj) {
@@ -244,4 +265,14 @@ __global__ void __launch_bounds__(MMA_THREADS, 1) mma_u8_limb_kernel(MmaArgs a) 
   }
 }
 
+}  // namespace qpir
+
+namespace qpir {
+// out[i] = acc[i] mod p (u64 -> u32), after the OUT_MODP GEMM.
+__global__ void modp_fixup_kernel(const unsigned long long* __restrict__ acc, uint32_t* __restrict__ out,
+                                  uint64_t n, uint32_t p) {
+  for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (uint64_t)gridDim.x * blockDim.x)
+    out[i] = (uint32_t)(acc[i] % p);
+}
 }  // namespace qpir

@@ -53,6 +53,8 @@ struct qpir_ctx {
   uint64_t big_in_bytes = 0;
   uint32_t* big_out = nullptr;     // staging for host ANS / H
   uint64_t big_out_bytes = 0;
+  unsigned long long* acc64 = nullptr;  // OUT_MODP accumulator
+  uint64_t acc64_bytes = 0;
   uint64_t launches = 0;
   // GEMV tuning (env QPIR_GEMV_U / QPIR_GEMV_SPLIT / QPIR_GEMV_CHUNK)
   int gemv_u = 2;
@@ -254,15 +256,17 @@ int gemv(qpir_ctx* ctx, const uint32_t* qu, uint32_t* ans, cudaStream_t st) {
 
 // Split K so that work units fill the SMs evenly (a few % tail at most);
 // partial tiles are added with u32 atomics (exact: addition mod 2^32 commutes).
-uint32_t choose_splits(uint32_t tiles, uint32_t kblocks, uint32_t sms, int forced) {
-  if (forced > 0) return std::max<uint32_t>(1, std::min<uint32_t>((uint32_t)forced, kblocks));
+uint32_t choose_splits(uint32_t tiles, uint32_t kblocks, uint32_t sms, int forced,
+                       uint32_t min_splits = 1) {
+  if (forced > 0)
+    return std::max<uint32_t>(min_splits, std::min<uint32_t>((uint32_t)forced, kblocks));
   auto eff = [&](uint32_t units) {
     const uint32_t waves = (units + sms - 1) / sms;
     return (double)units / ((double)waves * sms);
   };
-  uint32_t best = 1;
-  double best_eff = eff(tiles);
-  for (uint32_t s = 2; s <= 8; ++s) {
+  uint32_t best = min_splits;
+  double best_eff = eff(tiles * min_splits);
+  for (uint32_t s = min_splits + 1; s <= min_splits + 8; ++s) {
     if (kblocks / s < 16) break;
     const double e = eff(tiles * s);
     if (e > best_eff + 0.02) {
@@ -275,7 +279,8 @@ uint32_t choose_splits(uint32_t tiles, uint32_t kblocks, uint32_t sms, int force
 
 template <uint32_t BN, uint32_t MT, uint32_t GPB, int MODE>
 int launch_mma_cfg(qpir_ctx* ctx, const uint8_t* Bl, uint32_t Npad, uint32_t* out,
-                   uint32_t n_out, uint32_t out_ld, uint64_t out_elems, cudaStream_t st) {
+                   uint32_t n_out, uint32_t out_ld, uint64_t out_elems, cudaStream_t st,
+                   uint32_t p = 0, unsigned long long* out64 = nullptr) {
   using C = MmaCfg<BN, MT, GPB>;
   const Geometry& g = ctx->geo;
   MmaArgs a;
@@ -289,16 +294,30 @@ int launch_mma_cfg(qpir_ctx* ctx, const uint8_t* Bl, uint32_t Npad, uint32_t* ou
   a.m_tiles = (uint32_t)(g.L / (MMA_BM * MT));
   a.n_tiles = Npad / BN;
   const uint32_t kblocks = (uint32_t)(g.G / GPB);
-  a.splits = choose_splits(a.m_tiles * a.n_tiles, kblocks, (uint32_t)ctx->num_sms, ctx->mma_split);
-  a.kps = (kblocks + a.splits - 1) / a.splits;
+  // OUT_MODP: each split's limb sums must stay exact in u32 (<= 66051 cells)
+  const uint32_t max_kps = MODE == OUT_MODP ? 66048u / (16u * GPB) : kblocks;
+  const uint32_t min_splits = (kblocks + max_kps - 1) / max_kps;
+  a.splits = choose_splits(a.m_tiles * a.n_tiles, kblocks, (uint32_t)ctx->num_sms, ctx->mma_split,
+                           min_splits);
+  a.kps = std::min((kblocks + a.splits - 1) / a.splits, max_kps);
   a.splits = (kblocks + a.kps - 1) / a.kps;  // no empty split
-  if (a.splits > 1) CUDA_TRY(ctx, cudaMemsetAsync(out, 0, out_elems * 4, st));
+  a.p = p;
+  a.out64 = out64;
+  if (MODE == OUT_MODP)
+    CUDA_TRY(ctx, cudaMemsetAsync(out64, 0, out_elems * 8, st));
+  else if (a.splits > 1)
+    CUDA_TRY(ctx, cudaMemsetAsync(out, 0, out_elems * 4, st));
   const uint32_t units = a.m_tiles * a.n_tiles * a.splits;
   const uint32_t grid = std::min<uint32_t>(units, (uint32_t)ctx->num_sms);
   auto kern = mma_u8_limb_kernel<BN, MT, GPB, MODE>;
   CUDA_TRY(ctx, cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::TOTAL));
   kern<<<grid, MMA_THREADS, C::TOTAL, st>>>(a);
   LAUNCH_CHECK(ctx);
+  if (MODE == OUT_MODP) {
+    const uint32_t blocks = (uint32_t)std::min<uint64_t>((out_elems + 255) / 256, 4096);
+    modp_fixup_kernel<<<blocks, 256, 0, st>>>(out64, out, out_elems, p);
+    LAUNCH_CHECK(ctx);
+  }
   return QPIR_OK;
 }
 
@@ -312,16 +331,17 @@ uint32_t pick_bn(uint64_t ncols) {
 
 template <int MODE>
 int launch_mma(qpir_ctx* ctx, uint32_t BN, const uint8_t* Bl, uint32_t Npad, uint32_t* out,
-               uint32_t n_out, uint32_t out_ld, uint64_t out_elems, cudaStream_t st) {
+               uint32_t n_out, uint32_t out_ld, uint64_t out_elems, cudaStream_t st,
+               uint32_t p = 0, unsigned long long* out64 = nullptr) {
   const bool mt2 = ctx->mma_mt != 1;
   const bool g4 = ctx->mma_gpb == 4;
 #define QPIR_MMA_CASE(BNV)                                                                     \
   case BNV:                                                                                    \
     if (g4)                                                                                    \
-      return mt2 ? launch_mma_cfg<BNV, 2, 4, MODE>(ctx, Bl, Npad, out, n_out, out_ld, out_elems, st) \
-                 : launch_mma_cfg<BNV, 1, 4, MODE>(ctx, Bl, Npad, out, n_out, out_ld, out_elems, st); \
-    return mt2 ? launch_mma_cfg<BNV, 2, 8, MODE>(ctx, Bl, Npad, out, n_out, out_ld, out_elems, st)   \
-               : launch_mma_cfg<BNV, 1, 8, MODE>(ctx, Bl, Npad, out, n_out, out_ld, out_elems, st);
+      return mt2 ? launch_mma_cfg<BNV, 2, 4, MODE>(ctx, Bl, Npad, out, n_out, out_ld, out_elems, st, p, out64) \
+                 : launch_mma_cfg<BNV, 1, 4, MODE>(ctx, Bl, Npad, out, n_out, out_ld, out_elems, st, p, out64); \
+    return mt2 ? launch_mma_cfg<BNV, 2, 8, MODE>(ctx, Bl, Npad, out, n_out, out_ld, out_elems, st, p, out64)   \
+               : launch_mma_cfg<BNV, 1, 8, MODE>(ctx, Bl, Npad, out, n_out, out_ld, out_elems, st, p, out64);
   switch (BN) {
     QPIR_MMA_CASE(16)
     QPIR_MMA_CASE(32)
@@ -486,8 +506,8 @@ int qpir_answer(qpir_ctx* ctx, const uint32_t* qu, uint64_t len_qu, uint32_t* an
   return QPIR_OK;
 }
 
-int qpir_answer_batch(qpir_ctx* ctx, const uint32_t* Q, uint64_t B, uint64_t len_Q,
-                      uint32_t* ans_local, uint64_t len_ans, void* stream) {
+static int answer_batch_impl(qpir_ctx* ctx, const uint32_t* Q, uint64_t B, uint64_t len_Q,
+                             uint32_t* ans_local, uint64_t len_ans, void* stream, uint32_t p) {
   if (!ctx) return fail(nullptr, QPIR_E_STATE, "ctx: NULL");
   const Geometry& g = ctx->geo;
   if (!Q || !ans_local) return fail(ctx, QPIR_E_PARAM, "Q/ans_local: NULL");
@@ -528,14 +548,33 @@ int qpir_answer_batch(qpir_ctx* ctx, const uint32_t* Q, uint64_t B, uint64_t len
                                             (uint32_t)g.G, Npad, BN);
     LAUNCH_CHECK(ctx);
   }
-  rc = launch_mma<OUT_QUERY_MAJOR>(ctx, BN, ctx->limbs, Npad, out, (uint32_t)B,
-                                   (uint32_t)g.ell_local, len_ans, st);
+  if (p == 0) {
+    rc = launch_mma<OUT_QUERY_MAJOR>(ctx, BN, ctx->limbs, Npad, out, (uint32_t)B,
+                                     (uint32_t)g.ell_local, len_ans, st);
+  } else {
+    rc = ensure(ctx, (void**)&ctx->acc64, &ctx->acc64_bytes, len_ans * 8);
+    if (rc) return rc;
+    rc = launch_mma<OUT_MODP>(ctx, BN, ctx->limbs, Npad, out, (uint32_t)B,
+                              (uint32_t)g.ell_local, len_ans, st, p, ctx->acc64);
+  }
   if (rc) return rc;
   if (wa == 0) {
     CUDA_TRY(ctx, cudaMemcpyAsync(ans_local, out, len_ans * 4, cudaMemcpyDeviceToHost, st));
     CUDA_TRY(ctx, cudaStreamSynchronize(st));
   }
   return QPIR_OK;
+}
+
+int qpir_answer_batch(qpir_ctx* ctx, const uint32_t* Q, uint64_t B, uint64_t len_Q,
+                      uint32_t* ans_local, uint64_t len_ans, void* stream) {
+  return answer_batch_impl(ctx, Q, B, len_Q, ans_local, len_ans, stream, 0);
+}
+
+int qpir_answer_batch_modp(qpir_ctx* ctx, const uint32_t* Q, uint64_t B, uint64_t len_Q,
+                           uint32_t p, uint32_t* ans_local, uint64_t len_ans, void* stream) {
+  if (!ctx) return fail(nullptr, QPIR_E_STATE, "ctx: NULL");
+  if (p < 2) return fail(ctx, QPIR_E_PARAM, "p: %u < 2", p);
+  return answer_batch_impl(ctx, Q, B, len_Q, ans_local, len_ans, stream, p);
 }
 
 int qpir_hint(qpir_ctx* ctx, uint32_t* H_local, uint64_t len_H, void* stream) {
@@ -587,7 +626,7 @@ void qpir_destroy(qpir_ctx* ctx) {
   if (!ctx) return;
   DeviceGuard dg(ctx->device);
   void* bufs[] = {ctx->D,         ctx->qu_dev, ctx->ans_dev, ctx->partial, ctx->tickets,
-                  ctx->rec_stage, ctx->limbs,  ctx->big_in,  ctx->big_out};
+                  ctx->rec_stage, ctx->limbs,  ctx->big_in,  ctx->big_out, ctx->acc64};
   for (void* b : bufs)
     if (b) cudaFree(b);
   delete ctx;

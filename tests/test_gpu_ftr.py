@@ -1,0 +1,56 @@
+"""GPU parity for QPADL-FTR (Goldberg PIR over F_p, NEXT-2): the tcgen05 limb
+GEMM with the mod-p epilogue (qpir_answer_batch_modp) against the oracle."""
+import numpy as np
+import pytest
+import torch
+
+import synth
+from oracle import oracle as O
+
+pytestmark = pytest.mark.gpu
+P = 65537
+
+
+def _P():
+    import paper_2510_03631_b200 as Pk
+    return Pk
+
+
+@pytest.mark.parametrize("r,s,B", [(700, 33, 1), (1000, 24, 5), (3001, 200, 64), (70000, 16, 9)])
+def test_ftr_batch_matches_oracle(cuda_ok, r, s, B):
+    Pk = _P()
+    rec = synth.uniform_u8_np(r + s, (r, s))
+    Q = synth.uniform_u32_np(B + 3, (B, r)) % P
+    want = O.ftr_respond_batch(rec, Q)
+    with Pk.FtrServer(r, s, records=rec) as srv:
+        got = Pk.u32(srv.answer_batch(Q))
+        assert got.shape == want.shape
+        assert (got == want).all()
+        assert (Pk.u32(srv.answer(torch.from_numpy(Q[0].view(np.int32)).cuda())) == want[0]).all()
+
+
+def test_ftr_any_u32_and_other_primes(cuda_ok):
+    """Exact for any u32 query entries and any modulus: compare with int64 numpy."""
+    Pk = _P()
+    r, s = 70001, 8  # > 66051 cells: forces several exact K-splits
+    rec = np.full((r, s), 255, np.uint8)
+    rec[::7] = synth.uniform_u8_np(9, rec[::7].shape)
+    Q = synth.uniform_u32_np(10, (3, r))
+    for p in (2, 65537, 2147483647, 4294967291):
+        want = ((Q.astype(object) @ rec.astype(object)) % p).astype(np.uint32)
+        with Pk.FtrServer(r, s, p=p, records=rec) as srv:
+            assert (Pk.u32(srv.answer_batch(Q)) == want).all(), p
+
+
+def test_ftr_end_to_end_reconstruct(cuda_ok):
+    """Lemma 1: Lagrange interpolation of t + 1 GPU responses recovers record theta."""
+    Pk = _P()
+    r, s, l, t = 512, 40, 4, 2
+    rec = synth.uniform_u8_np(11, (r, s))
+    thetas = [0, 17, 255, 511]
+    Q = np.concatenate([O.ftr_query(th, r, l, t, seed=50 + th) for th in thetas])  # (len*l, r)
+    with Pk.FtrServer(r, s, records=rec) as srv:
+        resp = Pk.u32(srv.answer_batch(Q)).reshape(len(thetas), l, s)
+    for i, th in enumerate(thetas):
+        got = O.ftr_reconstruct(resp[i][1:t + 2], [2, 3, 4])  # servers 2..4
+        assert (got == rec[th]).all()
