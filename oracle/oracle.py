@@ -69,6 +69,9 @@ def lib():
         L.qo_ftr_respond_batch.argtypes = [_u8p, _u64, _u64, _u32p, _u64, _u32, _u32p]
         L.qo_ftr_reconstruct.argtypes = [_u32p, _u32p, _u32, _u64, _u32, _u32p]
         L.qo_ftr_reconstruct.restype = ctypes.c_int
+        L.qo_oop_preprocess.argtypes = [_u8p, _u64, _u64, _u32, _u32, _u64, _u8p]
+        L.qo_oop_query.argtypes = [_u64, _u64, _u32, _u64p, _u8p]
+        L.qo_oop_respond.argtypes = [_u8p, _u64, _u64, _u32, _u32, _u8p, _u8p, _u8p]
         L.qo_num_threads.restype = ctypes.c_int
         L.qo_set_num_threads.argtypes = [ctypes.c_int]
         _lib = L
@@ -273,6 +276,34 @@ def ftr_reconstruct(resp: np.ndarray, alpha, p: int = FTR_P) -> np.ndarray:
     rc = lib().qo_ftr_reconstruct(_p(resp, _u32p), _p(al, _u32p), k, s_, p, _p(out, _u32p))
     if rc != 0:
         raise ValueError("evaluation points must be distinct")
+    return out
+
+
+# ---------------------------------------------------------------- OOP (CIP-PIR, NEXT-3)
+def oop_preprocess(records: np.ndarray, n: int, i: int, seed: int) -> np.ndarray:
+    rec = _c(records, np.uint8)
+    B, d = rec.shape
+    assert B % n == 0
+    A = np.empty(d, np.uint8)
+    lib().qo_oop_preprocess(_p(rec, _u8p), B, d, n, i, seed, _p(A, _u8p))
+    return A
+
+
+def oop_query(theta: int, B: int, n: int, seeds) -> np.ndarray:
+    sd = _c(seeds, np.uint64)
+    assert sd.shape == (n,) and B % n == 0
+    q = np.empty((n, (B // n + 7) // 8), np.uint8)
+    lib().qo_oop_query(theta, B, n, _p(sd, _u64p), _p(q, _u8p))
+    return q
+
+
+def oop_respond(records: np.ndarray, n: int, i: int, q_i: np.ndarray, A_i: np.ndarray) -> np.ndarray:
+    rec = _c(records, np.uint8)
+    B, d = rec.shape
+    q = _c(q_i, np.uint8)
+    A = _c(A_i, np.uint8)
+    out = np.empty(d, np.uint8)
+    lib().qo_oop_respond(_p(rec, _u8p), B, d, n, i, _p(q, _u8p), _p(A, _u8p), _p(out, _u8p))
     return out
 
 

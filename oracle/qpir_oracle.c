@@ -432,3 +432,80 @@ int qo_ftr_reconstruct(const uint32_t *resp, const uint32_t *alpha, uint32_t k, 
   }
   return 0;
 }
+
+/* ------------------------------------------------------------------ */
+/* NEXT-3: QPADL-OOP = CIP-PIR offline-online (P:930-942;       */
+/* Lemma 2 proof).  B blocks (records of d bytes) in n chunks  */
+/* of k = B / n blocks; full replication t = n; server i's */
+/* flip chunk is chunk i, its non-flip chunks in rotated order          */
+/* chunk_{i+1}, ..., chunk_{i+n-1} (DESIGN R19).                        */
+/* ------------------------------------------------------------------ */
+#define QO_DOMAIN_O 0x4Fu
+
+/* PRG(S, nbits) (DESIGN R19): bit p = bit (p & 31) of word w = p >> 5,
+ * word w = Philox(key = S, ctr = (w >> 2, 0, 0, 'O'))[w & 3]. */
+static uint32_t oop_prg_bit(uint64_t seed, uint64_t p) {
+  uint32_t key[2];
+  key_from_seed(seed, key);
+  uint64_t w = p >> 5;
+  uint32_t ctr[4] = {(uint32_t)(w >> 2), 0u, 0u, QO_DOMAIN_O};
+  uint32_t out[4];
+  qo_philox4x32_10(ctr, key, out);
+  return (out[w & 3] >> (p & 31)) & 1u;
+}
+
+/* Non-flip position p in [0, k(n-1)) of server i -> block index theta. */
+static uint64_t oop_nonflip_block(uint64_t p, uint64_t k, uint32_t n, uint32_t i) {
+  uint64_t chunk = (i + 1 + p / k) % n;
+  return chunk * k + p % k;
+}
+
+/* Offline preprocessing of server i (P:930 steps 1-3): q = PRG(S, k(n-1)),
+ * A = XOR of the non-flip blocks whose bit in q is set.  out: d bytes. */
+void qo_oop_preprocess(const uint8_t *records, uint64_t B, uint64_t d, uint32_t n, uint32_t i,
+                       uint64_t seed, uint8_t *A) {
+  uint64_t k = B / n;
+  memset(A, 0, (size_t)d);
+  for (uint64_t p = 0; p < k * (n - 1); ++p) {
+    if (oop_prg_bit(seed, p)) {
+      const uint8_t *row = records + oop_nonflip_block(p, k, n, i) * d;
+      for (uint64_t j = 0; j < d; ++j) A[j] ^= row[j];
+    }
+  }
+}
+
+/* Client query: Q = e_theta (B bits); for every server j, XOR
+ * PRG(S_j, k(n-1)) into the positions of j's non-flip blocks; q_j = Q
+ * restricted to chunk j.  seeds: n; q: n x ceil(k/8) bytes (bit b of q_j =
+ * block j*k + b). */
+void qo_oop_query(uint64_t theta, uint64_t B, uint32_t n, const uint64_t *seeds, uint8_t *q) {
+  uint64_t k = B / n, kb = (k + 7) / 8;
+  memset(q, 0, (size_t)(n * kb));
+  /* Q as one bit per block, built plainly */
+  for (uint64_t blk = 0; blk < B; ++blk) {
+    uint32_t bit = (blk == theta) ? 1u : 0u;
+    for (uint32_t j = 0; j < n; ++j) {
+      if (blk / k == j) continue; /* flip chunk of server j */
+      uint64_t rot = (blk / k + n - j - 1) % n; /* position of this chunk in j's non-flip order */
+      uint64_t p = rot * k + blk % k;
+      bit ^= oop_prg_bit(seeds[j], p);
+    }
+    uint64_t owner = blk / k;
+    uint64_t b = blk % k;
+    if (bit) q[owner * kb + (b >> 3)] |= (uint8_t)(1u << (b & 7));
+  }
+}
+
+/* Online response of server i (Lemma 2: R_i := A_i XOR q_i . chunk_flip):
+ * touches only chunk i (1/n of the DB).  out: d bytes. */
+void qo_oop_respond(const uint8_t *records, uint64_t B, uint64_t d, uint32_t n, uint32_t i,
+                    const uint8_t *q_i, const uint8_t *A_i, uint8_t *out) {
+  uint64_t k = B / n;
+  memcpy(out, A_i, (size_t)d);
+  for (uint64_t b = 0; b < k; ++b) {
+    if ((q_i[b >> 3] >> (b & 7)) & 1u) {
+      const uint8_t *row = records + ((uint64_t)i * k + b) * d;
+      for (uint64_t j = 0; j < d; ++j) out[j] ^= row[j];
+    }
+  }
+}
