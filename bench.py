@@ -52,6 +52,9 @@ WORKLOADS = {
     "ens-c2": dict(name="QPADL-ENS (Chor XOR PIR, NEXT-1): 327680 paper-shaped 3 KB records "
                         "= 1.007 GB, one uniform r-bit share", n_cells=8192, n_ch=40, d=3072,
                    kind="ens"),
+    "oop-c2": dict(name="QPADL-OOP (CIP-PIR, NEXT-3) online answer of one of n = 4 servers on "
+                        "1.007 GB (touches its 1/4 flip chunk) + offline queue of 128 (S, A)",
+                   n_cells=8192, n_ch=40, d=3072, kind="oop", n_chunks=4),
     "ens-c2-b128": dict(name="QPADL-ENS multi-request (Alg. 3): 1.007 GB, 128 shares",
                         n_cells=8192, n_ch=40, d=3072, kind="ens_batch", B=128),
     "ftr-c2-b128": dict(name="QPADL-FTR (Goldberg PIR over F_65537, NEXT-2; Alg. 4): 327680 "
@@ -335,6 +338,73 @@ def run_ens(args, wl, world, rank, local):
     print(json.dumps(line), flush=True)
 
 
+def run_oop(args, wl, rank, local):
+    """QPADL-OOP: online answer (1/n of the DB) timed per step; the offline
+    preprocessing of a 128-entry (S, A) queue timed once and reported beside it."""
+    import synth
+    import paper_2510_03631_b200 as P
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    stream = torch.cuda.current_stream(dev)
+    n_cells, n_ch, d, n = wl["n_cells"], wl["n_ch"], wl["d"], wl["n_chunks"]
+    r = n_cells * n_ch
+    srv = P.EnsServer(r, d, device=local)
+    chunk = max(1, (256 << 20) // d)
+    for a in range(0, r, chunk):
+        srv.db_write(a, synth.records(args.seed, a, min(chunk, r - a), d, n_ch, device=dev))
+    k = r // n
+    kb = (k + 7) // 8
+    seeds = torch.arange(1, 129, dtype=torch.int64, device=dev) * 7919
+    # offline queue (timed once, after a warm-up call)
+    srv.oop_preprocess(n, 0, seeds[:2], stream=stream)
+    o0 = torch.cuda.Event(enable_timing=True)
+    o1 = torch.cuda.Event(enable_timing=True)
+    o0.record(stream)
+    A = srv.oop_preprocess(n, 0, seeds, stream=stream)
+    o1.record(stream)
+    torch.cuda.synchronize(dev)
+    off_ms = o0.elapsed_time(o1)
+    qs = [synth.uniform_u32(args.seed + 3 + i, ((kb + 3) // 4,), device=dev).view(torch.uint8)[:kb]
+          .contiguous() for i in range(4)]
+    out = torch.empty(d, dtype=torch.uint8, device=dev)
+    sampler = ClockSampler(physical_gpu(local))
+    for i in range(args.warmup):
+        srv.oop_answer(n, 0, qs[i % 4], A[i % 128], out=out, stream=stream)
+    torch.cuda.synchronize(dev)
+    time.sleep(0.3)
+    l0 = srv.kernel_launches
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    sampler.start()
+    e0.record(stream)
+    for i in range(args.steps):
+        srv.oop_answer(n, 0, qs[i % 4], A[i % 128], out=out, stream=stream)
+    e1.record(stream)
+    torch.cuda.synchronize(dev)
+    sampler.stop()
+    ms = e0.elapsed_time(e1) / args.steps
+    if rank != 0:
+        return
+    hbm, _, _, peak_src = peaks()
+    touched = 0.5 * k * d
+    achieved = (touched + kb + 2 * d) / (ms / 1e3) / 1e9
+    line = {"metric": METRIC, "value": round(r * d / (ms / 1e3) / 1e9, 2),
+            "unit": "GB/s (whole-DB equivalent: the online step reads 1/n of it)", "n_gpus": 1,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms, 5),
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+            "dtype": "u8 (GF(2) XOR)", "data": "synthetic",
+            "config": {"workload": wl["name"], "n_records": r, "rec_bytes": d, "n_chunks": n,
+                       "offline_queue": 128, "offline_ms_for_128": round(off_ms, 3)},
+            "queries_per_s": round(1e3 / ms, 1),
+            "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": hbm, "unit": "GB/s",
+                         "frac": round(achieved / hbm, 4), "traffic": None,
+                         "kernel": "ens_scan_kernel (flip chunk)", "kernel_ms": round(ms, 5),
+                         "peak_source": f"{peak_src} hbm_gbs"},
+            "cpu_baseline": None, "e2e": None,
+            "gpu_launches": srv.kernel_launches - l0, "clocks": sampler.summary()}
+    print(json.dumps(line), flush=True)
+
+
 # ---------------------------------------------------------------- our arm
 def main():
     ap = argparse.ArgumentParser()
@@ -358,6 +428,10 @@ def main():
         args.warmup = args.warmup if args.warmup is not None else 3
         return run_reference(args, wl, world, rank)
 
+    if wl["kind"] == "oop":
+        args.steps = args.steps or 1000
+        args.warmup = max(3, args.warmup if args.warmup is not None else 5)
+        return run_oop(args, wl, rank, local if args.device_override is None else args.device_override)
     if wl["kind"] in ("ens", "ens_batch"):
         args.steps = args.steps or (1000 if wl["kind"] == "ens" else 50)
         args.warmup = max(3, args.warmup if args.warmup is not None else 5)

@@ -175,6 +175,24 @@ int qpir_ens_answer_batch(qpir_ens_ctx *ctx, const uint8_t *shares, uint64_t B,
                           uint64_t len_shares, uint8_t *out, uint64_t len_out,
                           void *stream);
 
+/* QPADL-OOP = CIP-PIR offline-online on the same context (NEXT-3; PAPER.md:744,
+ * PAPER.md:930-942; Lemma 2 proof).  The r records form n_chunks
+ * chunks of k = r / n_chunks blocks (n_chunks must divide r); full replication,
+ * server i's flip chunk is chunk i, its non-flip chunks in rotated order
+ * chunk_{i+1}, ..., chunk_{i+n-1} (DESIGN R19).
+ * Offline: for each seed S, q = PRG(S, k(n-1)) over the non-flip blocks,
+ *   A = XOR of the selected blocks (A_out: n_seeds x d bytes).  PRG word w =
+ *   Philox4x32-10(key = S, ctr = (w >> 2, 0, 0, 0x4F))[w & 3], bit p of the
+ *   stream = bit (p & 31) of word p >> 5.
+ * Online: R_i = A_i XOR q_i . chunk_i, q_i: k bits (ceil(k/8) bytes), touching
+ *   only chunk i (1/n of the DB). */
+int qpir_oop_preprocess(qpir_ens_ctx *ctx, uint32_t n_chunks, uint32_t server,
+                        const uint64_t *seeds, uint64_t n_seeds, uint8_t *A_out,
+                        uint64_t len_A, void *stream);
+int qpir_oop_answer(qpir_ens_ctx *ctx, uint32_t n_chunks, uint32_t server,
+                    const uint8_t *q, uint64_t len_q, const uint8_t *A, uint64_t len_A,
+                    uint8_t *out, uint64_t len_out, void *stream);
+
 uint64_t qpir_ens_kernel_launches(const qpir_ens_ctx *ctx);
 const char *qpir_ens_last_error(const qpir_ens_ctx *ctx);
 void qpir_ens_destroy(qpir_ens_ctx *ctx);

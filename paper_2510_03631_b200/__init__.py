@@ -133,6 +133,22 @@ class EnsServer:
         _lib.qpir_ens_answer_batch(self._ctx, shares, B, out, stream)
         return out
 
+    # ---- NEXT-3: OOP / CIP-PIR offline-online on the same records
+    def oop_preprocess(self, n_chunks: int, server: int, seeds, out=None, stream=None):
+        """Offline: A = PRG(S).(non-flip chunks) for each seed (n_seeds x d bytes)."""
+        n = int(seeds.shape[0])
+        if out is None:
+            out = torch.empty((n, self.d), dtype=torch.uint8, device=torch.device("cuda", self.device))
+        _lib.qpir_oop_preprocess(self._ctx, n_chunks, server, seeds, out, stream)
+        return out
+
+    def oop_answer(self, n_chunks: int, server: int, q, A, out=None, stream=None):
+        """Online: R_i = A_i XOR q_i . chunk_i (touches 1/n of the DB)."""
+        if out is None:
+            out = torch.empty(self.d, dtype=torch.uint8, device=torch.device("cuda", self.device))
+        _lib.qpir_oop_answer(self._ctx, n_chunks, server, q, A, out, stream)
+        return out
+
     @property
     def kernel_launches(self) -> int:
         return _lib.qpir_ens_kernel_launches(self._ctx)

@@ -28,6 +28,7 @@ EXPORTS = (
     "qpir_hint", "qpir_kernel_launches", "qpir_last_error", "qpir_destroy",
     "qpir_answer_batch_modp", "qpir_ens_setup", "qpir_ens_db_write", "qpir_ens_answer", "qpir_ens_answer_batch",
     "qpir_ens_kernel_launches", "qpir_ens_last_error", "qpir_ens_destroy",
+    "qpir_oop_preprocess", "qpir_oop_answer",
 )
 
 
@@ -95,6 +96,9 @@ _L.qpir_ens_kernel_launches.restype = _u64
 _L.qpir_ens_last_error.argtypes = [_vp]
 _L.qpir_ens_last_error.restype = ctypes.c_char_p
 _L.qpir_ens_destroy.argtypes = [_vp]
+_L.qpir_oop_preprocess.argtypes = [_vp, ctypes.c_uint32, ctypes.c_uint32, _vp, _u64, _vp, _u64, _vp]
+_L.qpir_oop_answer.argtypes = [_vp, ctypes.c_uint32, ctypes.c_uint32, _vp, _u64, _vp, _u64, _vp,
+                               _u64, _vp]
 for _name in EXPORTS:
     getattr(_L, _name)
 
@@ -227,3 +231,14 @@ def qpir_ens_last_error(ctx: int | None = None) -> str:
 
 def qpir_ens_destroy(ctx: int) -> None:
     _L.qpir_ens_destroy(ctx)
+
+
+# ------------------------------------------------------------ OOP (CIP-PIR offline-online)
+def qpir_oop_preprocess(ctx: int, n_chunks: int, server: int, seeds, A_out, stream=None):
+    _check_ens(_L.qpir_oop_preprocess(ctx, n_chunks, server, _addr(seeds), _numel(seeds),
+                                      _addr(A_out), _numel(A_out), _stream(stream)), ctx)
+
+
+def qpir_oop_answer(ctx: int, n_chunks: int, server: int, q, A, out, stream=None):
+    _check_ens(_L.qpir_oop_answer(ctx, n_chunks, server, _addr(q), _numel(q), _addr(A), _numel(A),
+                                  _addr(out), _numel(out), _stream(stream)), ctx)

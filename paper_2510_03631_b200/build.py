@@ -1,6 +1,7 @@
 """Build libqpir.so (sm_100a) in-tree with nvcc.
 
-    python -m paper_2510_03631_b200.build [--verbose]
+    python paper_2510_03631_b200/build.py [--verbose]
+(run it as a file: importing the package would load the library it builds)
 """
 from __future__ import annotations
 

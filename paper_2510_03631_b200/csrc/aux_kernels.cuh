@@ -3,6 +3,8 @@
 #pragma once
 #include <cstdint>
 
+#include "philox.cuh"
+
 namespace qpir {
 
 // ---------------------------------------------------------------- a1 pack
@@ -96,21 +98,6 @@ __global__ void limb_split_kernel(const uint32_t* __restrict__ Q, uint8_t* __res
 }
 
 // ---------------------------------------------------------------- a7 A'
-// Philox4x32-10 (Salmon et al., SC'11), device implementation of the public
-// matrix generator (DESIGN R7): A[c][j] = Philox(key = seed_A,
-// ctr = (c, j >> 2, 0, 0x41))[j & 3].
-__device__ __forceinline__ uint4 philox4x32_10(uint4 ctr, uint2 key) {
-#pragma unroll
-  for (int r = 0; r < 10; ++r) {
-    const uint32_t lo0 = 0xD2511F53u * ctr.x, hi0 = __umulhi(0xD2511F53u, ctr.x);
-    const uint32_t lo1 = 0xCD9E8D57u * ctr.z, hi1 = __umulhi(0xCD9E8D57u, ctr.z);
-    ctr = make_uint4(hi1 ^ ctr.y ^ key.x, lo1, hi0 ^ ctr.w ^ key.y, lo0);
-    key.x += 0x9E3779B9u;
-    key.y += 0xBB67AE85u;
-  }
-  return ctr;
-}
-
 // A' (same panel layout as Q') = limb k of A[16g + i][j], n = 4j + k; one thread per
 // (group g, Philox block jb = j >> 2): 16 Philox calls, 256 contiguous bytes out.
 __global__ void expand_A_limbs_kernel(uint8_t* __restrict__ Ap, uint64_t seed, uint32_t m,

@@ -22,15 +22,16 @@
 #pragma once
 #include <cstdint>
 
+#include "philox.cuh"
 #include "ptx.cuh"
 
 namespace qpir {
 
 struct EnsArgs {
   const uint8_t* R;     // records [r][dp]
-  const uint8_t* q;     // selector bits, bit t at byte t >> 3, bit t & 7
-  uint32_t* out;        // dp / 4 words, zeroed, atomicXor target
-  uint64_t r;           // rows
+  const uint8_t* q;     // selector bits for rows [row_lo, row_hi): bit (t - row_lo)
+  uint32_t* out;        // dp / 4 words, pre-initialised (zero, or OOP's A), atomicXor target
+  uint64_t row_lo, row_hi;  // scanned row range (whole DB: [0, r))
   uint32_t dp;          // row stride (multiple of 16)
   uint32_t W;           // 16-byte chunks per row
   uint64_t rows_per_cta;
@@ -42,10 +43,12 @@ __global__ void __launch_bounds__(1024) ens_scan_kernel(EnsArgs a) {
   const uint32_t w = threadIdx.x % a.W;
   const uint32_t lr = threadIdx.x / a.W;
   const uint32_t R = blockDim.x / a.W;
+  // t counts rows relative to row_lo (= the selector bit index)
+  const uint64_t n_rows = a.row_hi - a.row_lo;
   const uint64_t t0 = (uint64_t)blockIdx.x * a.rows_per_cta;
-  const uint64_t t1 = min(a.r, t0 + a.rows_per_cta);
+  const uint64_t t1 = min(n_rows, t0 + a.rows_per_cta);
   uint4 acc = make_uint4(0, 0, 0, 0);
-  const uint8_t* base = a.R + (size_t)w * 16;
+  const uint8_t* base = a.R + (size_t)a.row_lo * a.dp + (size_t)w * 16;
   for (uint64_t t = t0 + lr; t < t1; t += (uint64_t)R * UR) {
     // all selector bytes first (L1 hits), then all row loads, predicated
     uint32_t qb[UR];
@@ -167,4 +170,41 @@ __global__ void __launch_bounds__(ENS_CW* ENS_QB) ens_batch_kernel(EnsBatchArgs 
   }
 }
 
+}  // namespace qpir
+
+namespace qpir {
+// ---------------------------------------------------------------- NEXT-3 OOP
+// CIP-PIR offline expansion (P:930 steps 1-2; DESIGN R19): for each seed S,
+// the full B-bit selector over the DB: 0 on server i's flip chunk, and on the
+// non-flip chunks (rotated order chunk_{i+1}, ..., chunk_{i+n-1}) bit p of
+// PRG(S) -- word w of PRG(S) = Philox(key = S, ctr = (w >> 2, 0, 0, 'O'))[w & 3].
+// One thread per (seed, output byte).  Output: n_seeds x ceil(B/8) bytes, the
+// shares of the ENS batch kernel that then computes A = q . DB.
+__global__ void oop_expand_kernel(const unsigned long long* __restrict__ seeds, uint8_t* __restrict__ out,
+                                  uint64_t B, uint64_t k, uint32_t n, uint32_t i, uint64_t nb) {
+  const uint64_t byte = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const uint32_t sidx = blockIdx.y;
+  if (byte >= nb) return;
+  const unsigned long long seed = seeds[sidx];
+  const uint2 key = make_uint2((uint32_t)seed, (uint32_t)(seed >> 32));
+  uint32_t v = 0;
+  uint64_t cached_blk = ~0ull;
+  uint4 words = make_uint4(0, 0, 0, 0);
+  for (uint32_t b = 0; b < 8; ++b) {
+    const uint64_t blk = byte * 8 + b;
+    if (blk >= B) break;
+    const uint64_t chunk = blk / k;
+    if (chunk == i) continue;                        // flip chunk: online only
+    const uint64_t rot = (chunk + n - i - 1) % n;    // position among non-flip chunks
+    const uint64_t p = rot * k + blk % k;
+    const uint64_t w = p >> 5;
+    if ((w >> 2) != cached_blk) {
+      cached_blk = w >> 2;
+      words = philox4x32_10(make_uint4((uint32_t)cached_blk, 0u, 0u, 0x4Fu), key);
+    }
+    const uint32_t word = (w & 3) == 0 ? words.x : (w & 3) == 1 ? words.y : (w & 3) == 2 ? words.z : words.w;
+    v |= ((word >> (p & 31)) & 1u) << b;
+  }
+  out[(size_t)sidx * nb + byte] = (uint8_t)v;
+}
 }  // namespace qpir

@@ -205,7 +205,7 @@ __global__ void __launch_bounds__(MMA_THREADS, 1) mma_u8_limb_kernel(MmaArgs a) 
           for (uint32_t t = 0; t < CH / 16; ++t) {
             const uint32_t c0 = cb + 16 * t;
             const uint32_t j0 = (nt * BN + c0) / 4;  // first output (query / hint column)
-            if (OUT_MODE == OUT_MODP) {
+            if constexpr (OUT_MODE == OUT_MODP) {
               if (row < a.rows) {
 #pragma unroll
                 for (int jj = 0; jj < 4; ++jj) {
@@ -218,8 +218,7 @@ __global__ void __launch_bounds__(MMA_THREADS, 1) mma_u8_limb_kernel(MmaArgs a) 
                     atomicAdd(a.out64 + (size_t)(j0 + jj) * a.out_ld + row, x % a.p);
                 }
               }
-              continue;
-            }
+            } else {
             uint32_t o[4];
 #pragma unroll
             for (int jj = 0; jj < 4; ++jj) {
@@ -248,6 +247,7 @@ __global__ void __launch_bounds__(MMA_THREADS, 1) mma_u8_limb_kernel(MmaArgs a) 
                 }
               }
             }
+            }  // OUT_MODE != OUT_MODP
           }
         }
       }

@@ -27,6 +27,8 @@ struct qpir_ens_ctx {
   uint64_t Q_bytes = 0;
   uint32_t* Qt = nullptr;     // transposed selector bits
   uint64_t Qt_bytes = 0;
+  uint8_t* seed_dev = nullptr;  // OOP seeds
+  uint64_t seed_bytes = 0;
   uint64_t launches = 0;
   int rows_per_cta = 0;       // env QPIR_ENS_ROWS (0 = auto)
   int ur = 16;                // env QPIR_ENS_UR (rows in flight per thread: 4, 8, 16)
@@ -161,6 +163,42 @@ int qpir_ens_db_write(qpir_ens_ctx* ctx, uint64_t theta_begin, uint64_t n_record
   return QPIR_OK;
 }
 
+static int scan_range(qpir_ens_ctx* ctx, const uint8_t* share_dev, uint64_t row_lo,
+                      uint64_t row_hi, cudaStream_t st) {
+  EnsArgs a;
+  a.R = ctx->R;
+  a.q = share_dev;
+  a.out = ctx->acc;
+  a.row_lo = row_lo;
+  a.row_hi = row_hi;
+  a.dp = (uint32_t)ctx->dp;
+  a.W = (uint32_t)(ctx->dp / 16);
+  const uint32_t R = std::max<uint32_t>(1, 256 / a.W);
+  const uint32_t threads = a.W * R;
+  const int UR = ctx->ur == 8 ? 8 : ctx->ur == 4 ? 4 : 16;
+  uint64_t rows = ctx->rows_per_cta;
+  if (rows == 0) {
+    // ~1.5 MB of records per CTA (measured best on B200 at d = 3072: 512 rows),
+    // but at least ~4 CTAs per SM for short ranges (OOP flip chunks), and at
+    // least one full unrolled step
+    const uint64_t by_bytes = (1536u << 10) / ctx->dp;
+    const uint64_t by_occ = (row_hi - row_lo + 4ull * ctx->num_sms - 1) / (4ull * ctx->num_sms);
+    rows = std::max<uint64_t>(std::min(by_bytes, by_occ), (uint64_t)R * UR);
+  }
+  rows = round_up(rows, (uint64_t)R * UR);
+  a.rows_per_cta = rows;
+  const uint64_t grid = (row_hi - row_lo + rows - 1) / rows;
+  const size_t smem = R > 1 ? threads * 16 : 0;
+  if (UR == 16)
+    ens_scan_kernel<16><<<(uint32_t)grid, threads, smem, st>>>(a);
+  else if (UR == 4)
+    ens_scan_kernel<4><<<(uint32_t)grid, threads, smem, st>>>(a);
+  else
+    ens_scan_kernel<8><<<(uint32_t)grid, threads, smem, st>>>(a);
+  ENS_LAUNCHED(ctx);
+  return QPIR_OK;
+}
+
 int qpir_ens_answer(qpir_ens_ctx* ctx, const uint8_t* share, uint64_t len_share, uint8_t* out,
                     uint64_t len_out, void* stream) {
   if (!ctx) return QPIR_E_STATE;
@@ -180,34 +218,78 @@ int qpir_ens_answer(qpir_ens_ctx* ctx, const uint8_t* share, uint64_t len_share,
   rc = stage_in(ctx, share, nb, ctx->q_dev, &qd, st);
   if (rc) return rc;
   ENS_CUDA(ctx, cudaMemsetAsync(ctx->acc, 0, ctx->dp, st));
-  EnsArgs a;
-  a.R = ctx->R;
-  a.q = qd;
-  a.out = ctx->acc;
-  a.r = ctx->r;
-  a.dp = (uint32_t)ctx->dp;
-  a.W = (uint32_t)(ctx->dp / 16);
-  const uint32_t R = std::max<uint32_t>(1, 256 / a.W);
-  const uint32_t threads = a.W * R;
-  const int UR = ctx->ur == 8 ? 8 : ctx->ur == 4 ? 4 : 16;
-  uint64_t rows = ctx->rows_per_cta;
-  if (rows == 0) {
-    // ~1.5 MB of records per CTA (measured best on B200 at d = 3072: 512 rows),
-    // at least one full unrolled step
-    rows = std::max<uint64_t>((1536u << 10) / ctx->dp, (uint64_t)R * UR);
-  }
-  rows = round_up(rows, (uint64_t)R * UR);
-  a.rows_per_cta = rows;
-  const uint64_t grid = (ctx->r + rows - 1) / rows;
-  const size_t smem = R > 1 ? threads * 16 : 0;
-  if (UR == 16)
-    ens_scan_kernel<16><<<(uint32_t)grid, threads, smem, st>>>(a);
-  else if (UR == 4)
-    ens_scan_kernel<4><<<(uint32_t)grid, threads, smem, st>>>(a);
-  else
-    ens_scan_kernel<8><<<(uint32_t)grid, threads, smem, st>>>(a);
-  ENS_LAUNCHED(ctx);
+  rc = scan_range(ctx, qd, 0, ctx->r, st);
+  if (rc) return rc;
   return copy_out(ctx, out, 1, st);
+}
+
+int qpir_oop_answer(qpir_ens_ctx* ctx, uint32_t n_chunks, uint32_t server, const uint8_t* q,
+                    uint64_t len_q, const uint8_t* A, uint64_t len_A, uint8_t* out,
+                    uint64_t len_out, void* stream) {
+  if (!ctx) return QPIR_E_STATE;
+  if (n_chunks < 2 || ctx->r % n_chunks != 0)
+    return ENS_FAIL(ctx, QPIR_E_PARAM, "n_chunks: %u must be >= 2 and divide r = %llu", n_chunks,
+                    (unsigned long long)ctx->r);
+  if (server >= n_chunks) return ENS_FAIL(ctx, QPIR_E_PARAM, "server: %u >= n_chunks", server);
+  const uint64_t k = ctx->r / n_chunks, kb = (k + 7) / 8;
+  if (!q || !A || !out) return ENS_FAIL(ctx, QPIR_E_PARAM, "q/A/out: NULL");
+  if (len_q != kb)
+    return ENS_FAIL(ctx, QPIR_E_DIMENSION, "len_q: %llu != ceil(k/8) %llu", (unsigned long long)len_q,
+                    (unsigned long long)kb);
+  if (len_A != ctx->d || len_out != ctx->d)
+    return ENS_FAIL(ctx, QPIR_E_DIMENSION, "len_A/len_out: must equal d %llu",
+                    (unsigned long long)ctx->d);
+  DeviceGuard dg(ctx->device);
+  cudaStream_t st = (cudaStream_t)stream;
+  int rc = grow(ctx, (void**)&ctx->acc, &ctx->acc_B, ctx->dp);
+  if (rc) return rc;
+  const uint8_t* qd = nullptr;
+  rc = stage_in(ctx, q, kb, ctx->q_dev, &qd, st);
+  if (rc) return rc;
+  // R_i := A_i XOR q_i . chunk_i (Lemma 2): start the accumulator at A_i
+  const int wA = where(A, ctx->device);
+  if (wA < 0) return ENS_FAIL(ctx, QPIR_E_PARAM, "A: memory of another device");
+  ENS_CUDA(ctx, cudaMemsetAsync(ctx->acc, 0, ctx->dp, st));
+  ENS_CUDA(ctx, cudaMemcpyAsync(ctx->acc, A, ctx->d,
+                                wA ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, st));
+  rc = scan_range(ctx, qd, (uint64_t)server * k, (uint64_t)(server + 1) * k, st);
+  if (rc) return rc;
+  return copy_out(ctx, out, 1, st);
+}
+
+int qpir_oop_preprocess(qpir_ens_ctx* ctx, uint32_t n_chunks, uint32_t server,
+                        const uint64_t* seeds, uint64_t n_seeds, uint8_t* A_out, uint64_t len_A,
+                        void* stream) {
+  if (!ctx) return QPIR_E_STATE;
+  if (n_chunks < 2 || ctx->r % n_chunks != 0)
+    return ENS_FAIL(ctx, QPIR_E_PARAM, "n_chunks: %u must be >= 2 and divide r = %llu", n_chunks,
+                    (unsigned long long)ctx->r);
+  if (server >= n_chunks) return ENS_FAIL(ctx, QPIR_E_PARAM, "server: %u >= n_chunks", server);
+  if (!seeds || !A_out) return ENS_FAIL(ctx, QPIR_E_PARAM, "seeds/A_out: NULL");
+  if (n_seeds == 0 || n_seeds > 65536)
+    return ENS_FAIL(ctx, QPIR_E_PARAM, "n_seeds: %llu not in [1, 65536]", (unsigned long long)n_seeds);
+  if (len_A != n_seeds * ctx->d)
+    return ENS_FAIL(ctx, QPIR_E_DIMENSION, "len_A: %llu != n_seeds*d %llu", (unsigned long long)len_A,
+                    (unsigned long long)(n_seeds * ctx->d));
+  DeviceGuard dg(ctx->device);
+  cudaStream_t st = (cudaStream_t)stream;
+  const uint64_t nb = (ctx->r + 7) / 8;
+  int rc = grow(ctx, (void**)&ctx->Q_dev, &ctx->Q_bytes, n_seeds * nb);
+  if (rc) return rc;
+  rc = grow(ctx, (void**)&ctx->seed_dev, &ctx->seed_bytes, n_seeds * 8);
+  if (rc) return rc;
+  const int ws = where(seeds, ctx->device);
+  if (ws < 0) return ENS_FAIL(ctx, QPIR_E_PARAM, "seeds: memory of another device");
+  ENS_CUDA(ctx, cudaMemcpyAsync(ctx->seed_dev, seeds, n_seeds * 8,
+                                ws ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, st));
+  {
+    dim3 grid((uint32_t)((nb + 255) / 256), (uint32_t)n_seeds);
+    oop_expand_kernel<<<grid, 256, 0, st>>>((const unsigned long long*)ctx->seed_dev, ctx->Q_dev,
+                                            ctx->r, ctx->r / n_chunks, n_chunks, server, nb);
+    ENS_LAUNCHED(ctx);
+  }
+  // A = q . DB for every seed: the ENS multi-request kernel on the expanded shares
+  return qpir_ens_answer_batch(ctx, ctx->Q_dev, n_seeds, n_seeds * nb, A_out, len_A, stream);
 }
 
 int qpir_ens_answer_batch(qpir_ens_ctx* ctx, const uint8_t* shares, uint64_t B,
@@ -276,7 +358,7 @@ const char* qpir_ens_last_error(const qpir_ens_ctx* ctx) {
 void qpir_ens_destroy(qpir_ens_ctx* ctx) {
   if (!ctx) return;
   DeviceGuard dg(ctx->device);
-  void* bufs[] = {ctx->R, ctx->q_dev, ctx->acc, ctx->Q_dev, ctx->Qt};
+  void* bufs[] = {ctx->R, ctx->q_dev, ctx->acc, ctx->Q_dev, ctx->Qt, ctx->seed_dev};
   for (void* b : bufs)
     if (b) cudaFree(b);
   delete ctx;

@@ -14,8 +14,8 @@ HEADER = os.path.join(ROOT, "include", "qpir.h")
 
 @pytest.fixture(scope="module")
 def L():
-    from paper_2510_03631_b200 import build
-    build.build()
+    import __graft_entry__
+    __graft_entry__._load_builder().build()
     from paper_2510_03631_b200 import _lib
     return _lib
 
