@@ -35,6 +35,9 @@ struct EnsArgs {
   uint32_t dp;          // row stride (multiple of 16)
   uint32_t W;           // 16-byte chunks per row
   uint64_t rows_per_cta;
+  uint4* partial;       // [gridDim.x][W] CTA partials (group reduction), or nullptr
+  uint32_t* tickets;    // [ceil(grid / group)] zero-initialised, self-resetting
+  uint32_t group;       // CTAs per reduction group
 };
 
 template <int UR>
@@ -71,18 +74,50 @@ __global__ void __launch_bounds__(1024) ens_scan_kernel(EnsArgs a) {
       acc.w ^= v[u].w;
     }
   }
+  const bool owner = lr == 0;  // one thread per 16-byte chunk keeps the CTA result
   if (R > 1) {
     s_part[threadIdx.x] = acc;
     __syncthreads();
-    if (lr != 0) return;
-    for (uint32_t k = 1; k < R; ++k) {
-      const uint4 p = s_part[k * a.W + w];
-      acc.x ^= p.x;
-      acc.y ^= p.y;
-      acc.z ^= p.z;
-      acc.w ^= p.w;
+    if (owner) {
+      for (uint32_t k = 1; k < R; ++k) {
+        const uint4 p = s_part[k * a.W + w];
+        acc.x ^= p.x;
+        acc.y ^= p.y;
+        acc.z ^= p.z;
+        acc.w ^= p.w;
+      }
     }
   }
+  if (a.partial != nullptr) {
+    // two-level reduction: publish the CTA partial; the last CTA of each group
+    // of `group` CTAs folds the group's partials and does the atomics.
+    __shared__ uint32_t s_last;
+    if (owner) a.partial[(size_t)blockIdx.x * a.W + w] = acc;
+    __threadfence();
+    __syncthreads();
+    const uint32_t grp = blockIdx.x / a.group;
+    const uint32_t g0 = grp * a.group;
+    const uint32_t g1 = min(gridDim.x, g0 + a.group);
+    if (threadIdx.x == 0) {
+      const uint32_t t = atomicAdd(&a.tickets[grp], 1u);
+      s_last = (t == g1 - g0 - 1) ? 1u : 0u;
+    }
+    __syncthreads();
+    if (!s_last) return;
+    __threadfence();
+    if (owner) {
+      acc = make_uint4(0, 0, 0, 0);
+      for (uint32_t c = g0; c < g1; ++c) {
+        const uint4 p = __ldcg(a.partial + (size_t)c * a.W + w);
+        acc.x ^= p.x;
+        acc.y ^= p.y;
+        acc.z ^= p.z;
+        acc.w ^= p.w;
+      }
+    }
+    if (threadIdx.x == 0) a.tickets[grp] = 0u;
+  }
+  if (!owner) return;
   uint32_t* o = a.out + (size_t)w * 4;
   if (acc.x) atomicXor(o + 0, acc.x);
   if (acc.y) atomicXor(o + 1, acc.y);

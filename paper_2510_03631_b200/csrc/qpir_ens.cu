@@ -29,6 +29,11 @@ struct qpir_ens_ctx {
   uint64_t Qt_bytes = 0;
   uint8_t* seed_dev = nullptr;  // OOP seeds
   uint64_t seed_bytes = 0;
+  uint8_t* partial = nullptr;   // scan CTA partials
+  uint64_t partial_bytes = 0;
+  uint32_t* tickets = nullptr;  // scan group tickets (self-resetting)
+  uint64_t tickets_bytes = 0;
+  int group = 0;                // env QPIR_ENS_GROUP (0 = auto 32; 1 = atomics only)
   uint64_t launches = 0;
   int rows_per_cta = 0;       // env QPIR_ENS_ROWS (0 = auto)
   int ur = 16;                // env QPIR_ENS_UR (rows in flight per thread: 4, 8, 16)
@@ -119,6 +124,7 @@ int qpir_ens_setup(const qpir_ens_params* p, const uint8_t* records, uint64_t re
   ctx->num_sms = sms;
   ctx->rows_per_cta = env_int("QPIR_ENS_ROWS", 0);
   ctx->ur = env_int("QPIR_ENS_UR", 16);
+  ctx->group = env_int("QPIR_ENS_GROUP", 0);
   cudaStream_t st = (cudaStream_t)stream;
   const uint64_t nb = (ctx->r + 7) / 8;
   if (cudaMalloc(&ctx->R, ctx->r * ctx->dp) != cudaSuccess ||
@@ -178,16 +184,35 @@ static int scan_range(qpir_ens_ctx* ctx, const uint8_t* share_dev, uint64_t row_
   const int UR = ctx->ur == 8 ? 8 : ctx->ur == 4 ? 4 : 16;
   uint64_t rows = ctx->rows_per_cta;
   if (rows == 0) {
-    // ~1.5 MB of records per CTA (measured best on B200 at d = 3072: 512 rows),
-    // but at least ~4 CTAs per SM for short ranges (OOP flip chunks), and at
-    // least one full unrolled step
-    const uint64_t by_bytes = (1536u << 10) / ctx->dp;
+    // ~192 KB of records per CTA (measured best on B200 at d = 3072: 64 rows
+    // with the two-level reduction, profiles/r01_sweep_run10.log), at least
+    // ~4 CTAs per SM for short ranges (OOP flip chunks), and at least one full
+    // unrolled step
+    const uint64_t by_bytes = (192u << 10) / ctx->dp;
     const uint64_t by_occ = (row_hi - row_lo + 4ull * ctx->num_sms - 1) / (4ull * ctx->num_sms);
     rows = std::max<uint64_t>(std::min(by_bytes, by_occ), (uint64_t)R * UR);
   }
   rows = round_up(rows, (uint64_t)R * UR);
   a.rows_per_cta = rows;
   const uint64_t grid = (row_hi - row_lo + rows - 1) / rows;
+  a.partial = nullptr;
+  a.tickets = nullptr;
+  a.group = 1;
+  const uint32_t group = ctx->group > 0 ? (uint32_t)ctx->group : 32;
+  if (grid > 4ull * ctx->num_sms && group > 1) {
+    // many small CTAs: two-level XOR reduction instead of grid x W atomics
+    const uint64_t ngroups = (grid + group - 1) / group;
+    int rc = grow(ctx, (void**)&ctx->partial, &ctx->partial_bytes, grid * a.W * 16);
+    if (rc) return rc;
+    if (ngroups * 4 > ctx->tickets_bytes) {
+      rc = grow(ctx, (void**)&ctx->tickets, &ctx->tickets_bytes, ngroups * 4);
+      if (rc) return rc;
+      ENS_CUDA(ctx, cudaMemsetAsync(ctx->tickets, 0, ctx->tickets_bytes, st));
+    }
+    a.partial = reinterpret_cast<uint4*>(ctx->partial);
+    a.tickets = ctx->tickets;
+    a.group = group;
+  }
   const size_t smem = R > 1 ? threads * 16 : 0;
   if (UR == 16)
     ens_scan_kernel<16><<<(uint32_t)grid, threads, smem, st>>>(a);
@@ -358,7 +383,8 @@ const char* qpir_ens_last_error(const qpir_ens_ctx* ctx) {
 void qpir_ens_destroy(qpir_ens_ctx* ctx) {
   if (!ctx) return;
   DeviceGuard dg(ctx->device);
-  void* bufs[] = {ctx->R, ctx->q_dev, ctx->acc, ctx->Q_dev, ctx->Qt, ctx->seed_dev};
+  void* bufs[] = {ctx->R,  ctx->q_dev, ctx->acc, ctx->Q_dev, ctx->Qt, ctx->seed_dev,
+                  ctx->partial, ctx->tickets};
   for (void* b : bufs)
     if (b) cudaFree(b);
   delete ctx;

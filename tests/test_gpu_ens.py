@@ -23,9 +23,10 @@ def _share(seed, r):
 
 
 @pytest.mark.parametrize("r,d", [(1000, 24), (77, 5), (4099, 100), (513, 3072), (20000, 16)])
-@pytest.mark.parametrize("rows", ["0", "8", "96"])
-def test_ens_answer_matches_oracle(cuda_ok, r, d, rows, monkeypatch):
+@pytest.mark.parametrize("rows,group", [("0", "0"), ("8", "0"), ("8", "3"), ("8", "1"), ("96", "0")])
+def test_ens_answer_matches_oracle(cuda_ok, r, d, rows, group, monkeypatch):
     monkeypatch.setenv("QPIR_ENS_ROWS", rows)
+    monkeypatch.setenv("QPIR_ENS_GROUP", group)
     P = _P()
     rec = synth.uniform_u8_np(r + d, (r, d))
     with P.EnsServer(r, d, records=rec) as s:
