@@ -3,6 +3,7 @@
 #pragma once
 #include <cstdint>
 
+#include "layout.cuh"
 #include "philox.cuh"
 
 namespace qpir {
@@ -65,10 +66,6 @@ __global__ void pack_records_kernel(PackArgs a) {
 // (n >= 4B or 16g + i >= m).  One MMA B tile (BN columns x 8 groups) is then
 // BN * 128 contiguous bytes.  One thread per (query j, group g): 64 B in,
 // 4 x 16 B out (64 B contiguous).
-__device__ __forceinline__ size_t limb_off(uint32_t n, uint32_t g, uint32_t G, uint32_t BN) {
-  return (((size_t)(n / BN) * G + g) * BN + (n % BN)) * 16;
-}
-
 __global__ void limb_split_kernel(const uint32_t* __restrict__ Q, uint8_t* __restrict__ Qp,
                                   uint32_t B, uint32_t m, uint32_t G, uint32_t Npad,
                                   uint32_t BN) {

@@ -22,6 +22,7 @@
 #pragma once
 #include <cstdint>
 
+#include "layout.cuh"
 #include "philox.cuh"
 #include "ptx.cuh"
 
@@ -241,5 +242,77 @@ __global__ void oop_expand_kernel(const unsigned long long* __restrict__ seeds, 
     v |= ((word >> (p & 31)) & 1u) << b;
   }
   out[(size_t)sidx * nb + byte] = (uint8_t)v;
+}
+}  // namespace qpir
+
+namespace qpir {
+// ---------------------------------------------------------------- ENS on tensor cores
+// Bit-plane operand for the GF(2) multi-request product (NEXT-1, DESIGN 6):
+// Dbits[8j + k][theta] = bit k of byte j of record theta, in the engine's
+// 128-row panel layout ((row >> 7) * G + (theta >> 4)) * 2048 + (row & 127) * 16
+// + (theta & 15).  One thread per (panel, 16-record group): 16 x 16-byte record
+// loads in, one contiguous 2 KB panel block out.
+__device__ __forceinline__ uint32_t gather_byte(uint32_t a, uint32_t b, uint32_t c, uint32_t e,
+                                                uint32_t k) {
+  const uint32_t sel = k | ((k + 4u) << 4);
+  return __byte_perm(__byte_perm(a, b, sel), __byte_perm(c, e, sel), 0x5410);
+}
+
+__device__ __forceinline__ uint32_t u4_word(const uint4& v, uint32_t i) {
+  return i == 0 ? v.x : i == 1 ? v.y : i == 2 ? v.z : v.w;
+}
+
+__global__ void ens_bitplane_pack_kernel(const uint8_t* __restrict__ R, uint64_t r, uint32_t dp,
+                                         uint8_t* __restrict__ Dbits, uint32_t G) {
+  const uint32_t g = blockIdx.x * blockDim.x + threadIdx.x;
+  const uint32_t pnl = blockIdx.y;  // record bytes 16 * pnl .. 16 * pnl + 15
+  if (g >= G) return;
+  uint4 rec[16];
+#pragma unroll
+  for (int i = 0; i < 16; ++i) {
+    const uint64_t th = (uint64_t)g * 16 + i;
+    rec[i] = (th < r && pnl * 16u < dp)
+                 ? __ldg(reinterpret_cast<const uint4*>(R + th * dp + (size_t)pnl * 16))
+                 : make_uint4(0, 0, 0, 0);
+  }
+  uint4* dst = reinterpret_cast<uint4*>(Dbits + ((size_t)pnl * G + g) * 2048);
+#pragma unroll 1
+  for (uint32_t jj = 0; jj < 16; ++jj) {
+    const uint32_t wsel = jj >> 2, bsel = jj & 3;
+    uint32_t X[4];  // byte jj of records 4t .. 4t+3
+#pragma unroll
+    for (int t = 0; t < 4; ++t)
+      X[t] = gather_byte(u4_word(rec[4 * t + 0], wsel), u4_word(rec[4 * t + 1], wsel),
+                         u4_word(rec[4 * t + 2], wsel), u4_word(rec[4 * t + 3], wsel), bsel);
+#pragma unroll
+    for (uint32_t k = 0; k < 8; ++k)
+      dst[jj * 8 + k] = make_uint4((X[0] >> k) & 0x01010101u, (X[1] >> k) & 0x01010101u,
+                                   (X[2] >> k) & 0x01010101u, (X[3] >> k) & 0x01010101u);
+  }
+}
+
+// Shares as the B operand: byte (share q, record theta) = bit theta of share q
+// (0/1), BN-column panels like the LWE limbs.  One thread per (q, 16-record group).
+__global__ void ens_share_expand_kernel(const uint8_t* __restrict__ Q, uint32_t B, uint64_t r,
+                                        uint64_t nb, uint8_t* __restrict__ Qb, uint32_t G,
+                                        uint32_t Npad, uint32_t BN) {
+  const uint32_t q = blockIdx.x * blockDim.x + threadIdx.x;
+  const uint32_t g = blockIdx.y;
+  if (q >= Npad) return;
+  uint32_t bits = 0;
+  if (q < B) {
+    const uint64_t b0 = (uint64_t)g * 2;
+    if (b0 < nb) bits = __ldg(Q + (size_t)q * nb + b0);
+    if (b0 + 1 < nb) bits |= (uint32_t)__ldg(Q + (size_t)q * nb + b0 + 1) << 8;
+    const uint64_t t0 = (uint64_t)g * 16;
+    if (t0 + 16 > r) bits &= (t0 >= r) ? 0u : ((1u << (r - t0)) - 1u);
+  }
+  uint32_t w[4];
+#pragma unroll
+  for (int t = 0; t < 4; ++t) {
+    const uint32_t nib = (bits >> (4 * t)) & 0xFu;
+    w[t] = (nib & 1u) | ((nib >> 1) & 1u) << 8 | ((nib >> 2) & 1u) << 16 | ((nib >> 3) & 1u) << 24;
+  }
+  *reinterpret_cast<uint4*>(Qb + limb_off(q, g, G, BN)) = make_uint4(w[0], w[1], w[2], w[3]);
 }
 }  // namespace qpir

@@ -39,7 +39,12 @@ constexpr uint32_t MMA_THREADS = 192;
 // (u32-exact while the split covers <= 66051 cells) are folded to
 // sum_k 2^{8k} C_k mod p in 64-bit and added into a u64 scratch; a fixup
 // kernel reduces mod p again.
-enum : int { OUT_QUERY_MAJOR = 0, OUT_ROW_MAJOR = 1, OUT_MODP = 2 };
+// OUT_PARITY (NEXT-1 ENS on tensor cores): A = bit-planes of the records (rows
+// 8j + k = bit k of byte j, values 0/1), B = shares as 0/1 bytes; the GF(2)
+// response bit is the parity of the s32 count, 32 consecutive bit-rows (one
+// warp's TMEM lanes) pack into one u32 of the response with __ballot_sync;
+// K-split partials combine with atomicXor.
+enum : int { OUT_QUERY_MAJOR = 0, OUT_ROW_MAJOR = 1, OUT_MODP = 2, OUT_PARITY = 3 };
 
 struct MmaArgs {
   const uint8_t* A;   // D shard, 128-row panels [L/128][G][128][16]
@@ -205,7 +210,19 @@ __global__ void __launch_bounds__(MMA_THREADS, 1) mma_u8_limb_kernel(MmaArgs a) 
           for (uint32_t t = 0; t < CH / 16; ++t) {
             const uint32_t c0 = cb + 16 * t;
             const uint32_t j0 = (nt * BN + c0) / 4;  // first output (query / hint column)
-            if constexpr (OUT_MODE == OUT_MODP) {
+            if constexpr (OUT_MODE == OUT_PARITY) {
+              const uint32_t row0 = (mt * MT + p) * MMA_BM + q * 32;  // first bit-row of the warp
+              const uint32_t widx = row0 >> 5;                       // its u32 in the response
+#pragma unroll
+              for (uint32_t cc = 0; cc < 16; ++cc) {
+                const uint32_t word = __ballot_sync(0xffffffffu, v[16 * t + cc] & 1u);
+                const uint32_t col = nt * BN + c0 + cc;  // share index
+                if (lane == cc && col < a.n_out && widx < a.out_ld) {
+                  uint32_t* dst = a.out + (size_t)col * a.out_ld + widx;
+                  if (split) atomicXor(dst, word); else *dst = word;
+                }
+              }
+            } else if constexpr (OUT_MODE == OUT_MODP) {
               if (row < a.rows) {
 #pragma unroll
                 for (int jj = 0; jj < 4; ++jj) {
@@ -269,7 +286,7 @@ __global__ void __launch_bounds__(MMA_THREADS, 1) mma_u8_limb_kernel(MmaArgs a) 
 
 namespace qpir {
 // out[i] = acc[i] mod p (u64 -> u32), after the OUT_MODP GEMM.
-__global__ void modp_fixup_kernel(const unsigned long long* __restrict__ acc, uint32_t* __restrict__ out,
+static __global__ void modp_fixup_kernel(const unsigned long long* __restrict__ acc, uint32_t* __restrict__ out,
                                   uint64_t n, uint32_t p) {
   for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
        i += (uint64_t)gridDim.x * blockDim.x)

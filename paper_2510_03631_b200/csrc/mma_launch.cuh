@@ -1,0 +1,132 @@
+// mma_launch.cuh -- host-side launcher of the tcgen05 limb engine (mma.cuh),
+// shared by the C-ABI translation units (LWE answer/batch/hint, FTR mod p,
+// ENS GF(2) bit-plane batch).
+#pragma once
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstdint>
+
+#include "mma.cuh"
+
+namespace qpir {
+
+struct MmaJob {
+  const uint8_t* A;  // 128-row panels [L/128][G][128][16]
+  uint32_t L;        // padded rows (multiple of 256)
+  uint32_t G;        // column groups (multiple of 8)
+  uint32_t rows;     // valid output rows
+  const uint8_t* B;  // BN-column panels [Npad/BN][G][BN][16]
+  uint32_t Npad, BN;
+  uint32_t* out;
+  uint32_t n_out, out_ld;
+  uint64_t out_elems;
+  uint32_t p = 0;                       // OUT_MODP modulus
+  unsigned long long* out64 = nullptr;  // OUT_MODP accumulator
+  int num_sms = 148;
+  int forced_split = 0;  // 0 = auto
+  int mt = 2;            // row panels per CTA tile (1 or 2)
+  int gpb = 8;           // column groups per pipeline stage (4 or 8)
+};
+
+inline uint32_t mma_pick_bn(uint64_t ncols) {
+  if (ncols <= 16) return 16;
+  if (ncols <= 32) return 32;
+  if (ncols <= 64) return 64;
+  if (ncols <= 128) return 128;
+  return 256;
+}
+
+// Split K so that work units fill the SMs evenly (a few % tail at most); split
+// partials are combined with commutative atomics (exact for u32 add / XOR).
+inline uint32_t mma_choose_splits(uint32_t tiles, uint32_t kblocks, uint32_t sms, int forced,
+                                  uint32_t min_splits) {
+  if (forced > 0)
+    return std::max<uint32_t>(min_splits, std::min<uint32_t>((uint32_t)forced, kblocks));
+  auto eff = [&](uint32_t units) {
+    const uint32_t waves = (units + sms - 1) / sms;
+    return (double)units / ((double)waves * sms);
+  };
+  uint32_t best = min_splits;
+  double best_eff = eff(tiles * min_splits);
+  for (uint32_t s = min_splits + 1; s <= min_splits + 8; ++s) {
+    if (kblocks / s < 16) break;
+    const double e = eff(tiles * s);
+    if (e > best_eff + 0.02) {
+      best = s;
+      best_eff = e;
+    }
+  }
+  return best;
+}
+
+template <uint32_t BN, uint32_t MT, uint32_t GPB, int MODE>
+cudaError_t mma_launch_cfg(const MmaJob& j, cudaStream_t st, uint64_t* launches) {
+  using C = MmaCfg<BN, MT, GPB>;
+  MmaArgs a;
+  a.A = j.A;
+  a.B = j.B;
+  a.out = j.out;
+  a.G = j.G;
+  a.rows = j.rows;
+  a.n_out = j.n_out;
+  a.out_ld = j.out_ld;
+  a.m_tiles = j.L / (MMA_BM * MT);
+  a.n_tiles = j.Npad / BN;
+  const uint32_t kblocks = j.G / GPB;
+  // OUT_MODP: each split's limb sums must stay exact in u32 (<= 66051 cells)
+  const uint32_t max_kps = MODE == OUT_MODP ? 66048u / (16u * GPB) : kblocks;
+  const uint32_t min_splits = (kblocks + max_kps - 1) / max_kps;
+  a.splits = mma_choose_splits(a.m_tiles * a.n_tiles, kblocks, (uint32_t)j.num_sms,
+                               j.forced_split, min_splits);
+  a.kps = std::min((kblocks + a.splits - 1) / a.splits, max_kps);
+  a.splits = (kblocks + a.kps - 1) / a.kps;  // no empty split
+  a.p = j.p;
+  a.out64 = j.out64;
+  cudaError_t e = cudaSuccess;
+  if (MODE == OUT_MODP)
+    e = cudaMemsetAsync(j.out64, 0, j.out_elems * 8, st);
+  else if (a.splits > 1)
+    e = cudaMemsetAsync(j.out, 0, j.out_elems * 4, st);
+  if (e != cudaSuccess) return e;
+  const uint32_t units = a.m_tiles * a.n_tiles * a.splits;
+  const uint32_t grid = std::min<uint32_t>(units, (uint32_t)j.num_sms);
+  auto kern = mma_u8_limb_kernel<BN, MT, GPB, MODE>;
+  e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::TOTAL);
+  if (e != cudaSuccess) return e;
+  kern<<<grid, MMA_THREADS, C::TOTAL, st>>>(a);
+  ++*launches;
+  e = cudaGetLastError();
+  if (e != cudaSuccess) return e;
+  if (MODE == OUT_MODP) {
+    const uint32_t blocks = (uint32_t)std::min<uint64_t>((j.out_elems + 255) / 256, 4096);
+    modp_fixup_kernel<<<blocks, 256, 0, st>>>(j.out64, j.out, j.out_elems, j.p);
+    ++*launches;
+    e = cudaGetLastError();
+  }
+  return e;
+}
+
+template <int MODE>
+cudaError_t mma_launch(const MmaJob& j, cudaStream_t st, uint64_t* launches) {
+  const bool mt2 = j.mt != 1;
+  const bool g4 = j.gpb == 4;
+#define QPIR_MMA_CASE(BNV)                                                           \
+  case BNV:                                                                          \
+    if (g4)                                                                          \
+      return mt2 ? mma_launch_cfg<BNV, 2, 4, MODE>(j, st, launches)                  \
+                 : mma_launch_cfg<BNV, 1, 4, MODE>(j, st, launches);                 \
+    return mt2 ? mma_launch_cfg<BNV, 2, 8, MODE>(j, st, launches)                    \
+               : mma_launch_cfg<BNV, 1, 8, MODE>(j, st, launches);
+  switch (j.BN) {
+    QPIR_MMA_CASE(16)
+    QPIR_MMA_CASE(32)
+    QPIR_MMA_CASE(64)
+    QPIR_MMA_CASE(128)
+    default:
+      QPIR_MMA_CASE(256)
+  }
+#undef QPIR_MMA_CASE
+}
+
+}  // namespace qpir

@@ -17,7 +17,7 @@
 #include "aux_kernels.cuh"
 #include "gemv.cuh"
 #include "host_common.h"
-#include "mma.cuh"
+#include "mma_launch.cuh"
 
 using namespace qpir;
 using namespace qpir_host;
@@ -254,103 +254,34 @@ int gemv(qpir_ctx* ctx, const uint32_t* qu, uint32_t* ans, cudaStream_t st) {
   }
 }
 
-// Split K so that work units fill the SMs evenly (a few % tail at most);
-// partial tiles are added with u32 atomics (exact: addition mod 2^32 commutes).
-uint32_t choose_splits(uint32_t tiles, uint32_t kblocks, uint32_t sms, int forced,
-                       uint32_t min_splits = 1) {
-  if (forced > 0)
-    return std::max<uint32_t>(min_splits, std::min<uint32_t>((uint32_t)forced, kblocks));
-  auto eff = [&](uint32_t units) {
-    const uint32_t waves = (units + sms - 1) / sms;
-    return (double)units / ((double)waves * sms);
-  };
-  uint32_t best = min_splits;
-  double best_eff = eff(tiles * min_splits);
-  for (uint32_t s = min_splits + 1; s <= min_splits + 8; ++s) {
-    if (kblocks / s < 16) break;
-    const double e = eff(tiles * s);
-    if (e > best_eff + 0.02) {
-      best = s;
-      best_eff = e;
-    }
-  }
-  return best;
-}
-
-template <uint32_t BN, uint32_t MT, uint32_t GPB, int MODE>
-int launch_mma_cfg(qpir_ctx* ctx, const uint8_t* Bl, uint32_t Npad, uint32_t* out,
-                   uint32_t n_out, uint32_t out_ld, uint64_t out_elems, cudaStream_t st,
-                   uint32_t p = 0, unsigned long long* out64 = nullptr) {
-  using C = MmaCfg<BN, MT, GPB>;
-  const Geometry& g = ctx->geo;
-  MmaArgs a;
-  a.A = ctx->D;
-  a.B = Bl;
-  a.out = out;
-  a.G = (uint32_t)g.G;
-  a.rows = (uint32_t)g.ell_local;
-  a.n_out = n_out;
-  a.out_ld = out_ld;
-  a.m_tiles = (uint32_t)(g.L / (MMA_BM * MT));
-  a.n_tiles = Npad / BN;
-  const uint32_t kblocks = (uint32_t)(g.G / GPB);
-  // OUT_MODP: each split's limb sums must stay exact in u32 (<= 66051 cells)
-  const uint32_t max_kps = MODE == OUT_MODP ? 66048u / (16u * GPB) : kblocks;
-  const uint32_t min_splits = (kblocks + max_kps - 1) / max_kps;
-  a.splits = choose_splits(a.m_tiles * a.n_tiles, kblocks, (uint32_t)ctx->num_sms, ctx->mma_split,
-                           min_splits);
-  a.kps = std::min((kblocks + a.splits - 1) / a.splits, max_kps);
-  a.splits = (kblocks + a.kps - 1) / a.kps;  // no empty split
-  a.p = p;
-  a.out64 = out64;
-  if (MODE == OUT_MODP)
-    CUDA_TRY(ctx, cudaMemsetAsync(out64, 0, out_elems * 8, st));
-  else if (a.splits > 1)
-    CUDA_TRY(ctx, cudaMemsetAsync(out, 0, out_elems * 4, st));
-  const uint32_t units = a.m_tiles * a.n_tiles * a.splits;
-  const uint32_t grid = std::min<uint32_t>(units, (uint32_t)ctx->num_sms);
-  auto kern = mma_u8_limb_kernel<BN, MT, GPB, MODE>;
-  CUDA_TRY(ctx, cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::TOTAL));
-  kern<<<grid, MMA_THREADS, C::TOTAL, st>>>(a);
-  LAUNCH_CHECK(ctx);
-  if (MODE == OUT_MODP) {
-    const uint32_t blocks = (uint32_t)std::min<uint64_t>((out_elems + 255) / 256, 4096);
-    modp_fixup_kernel<<<blocks, 256, 0, st>>>(out64, out, out_elems, p);
-    LAUNCH_CHECK(ctx);
-  }
-  return QPIR_OK;
-}
-
-uint32_t pick_bn(uint64_t ncols) {
-  if (ncols <= 16) return 16;
-  if (ncols <= 32) return 32;
-  if (ncols <= 64) return 64;
-  if (ncols <= 128) return 128;
-  return 256;
-}
-
 template <int MODE>
 int launch_mma(qpir_ctx* ctx, uint32_t BN, const uint8_t* Bl, uint32_t Npad, uint32_t* out,
                uint32_t n_out, uint32_t out_ld, uint64_t out_elems, cudaStream_t st,
                uint32_t p = 0, unsigned long long* out64 = nullptr) {
-  const bool mt2 = ctx->mma_mt != 1;
-  const bool g4 = ctx->mma_gpb == 4;
-#define QPIR_MMA_CASE(BNV)                                                                     \
-  case BNV:                                                                                    \
-    if (g4)                                                                                    \
-      return mt2 ? launch_mma_cfg<BNV, 2, 4, MODE>(ctx, Bl, Npad, out, n_out, out_ld, out_elems, st, p, out64) \
-                 : launch_mma_cfg<BNV, 1, 4, MODE>(ctx, Bl, Npad, out, n_out, out_ld, out_elems, st, p, out64); \
-    return mt2 ? launch_mma_cfg<BNV, 2, 8, MODE>(ctx, Bl, Npad, out, n_out, out_ld, out_elems, st, p, out64)   \
-               : launch_mma_cfg<BNV, 1, 8, MODE>(ctx, Bl, Npad, out, n_out, out_ld, out_elems, st, p, out64);
-  switch (BN) {
-    QPIR_MMA_CASE(16)
-    QPIR_MMA_CASE(32)
-    QPIR_MMA_CASE(64)
-    QPIR_MMA_CASE(128)
-    default:
-      QPIR_MMA_CASE(256)
-  }
-#undef QPIR_MMA_CASE
+  const Geometry& g = ctx->geo;
+  MmaJob j;
+  j.A = ctx->D;
+  j.L = (uint32_t)g.L;
+  j.G = (uint32_t)g.G;
+  j.rows = (uint32_t)g.ell_local;
+  j.B = Bl;
+  j.Npad = Npad;
+  j.BN = BN;
+  j.out = out;
+  j.n_out = n_out;
+  j.out_ld = out_ld;
+  j.out_elems = out_elems;
+  j.p = p;
+  j.out64 = out64;
+  j.num_sms = ctx->num_sms;
+  j.forced_split = ctx->mma_split;
+  j.mt = ctx->mma_mt;
+  j.gpb = ctx->mma_gpb;
+  const cudaError_t e = mma_launch<MODE>(j, st, &ctx->launches);
+  if (e != cudaSuccess)
+    return fail(ctx, e == cudaErrorMemoryAllocation ? QPIR_E_OOM : QPIR_E_CUDA,
+                "tcgen05 GEMM launch: %s", cudaGetErrorString(e));
+  return QPIR_OK;
 }
 
 }  // namespace
@@ -524,7 +455,7 @@ static int answer_batch_impl(qpir_ctx* ctx, const uint32_t* Q, uint64_t B, uint6
   const int wq = where(Q, ctx->device), wa = where(ans_local, ctx->device);
   if (wq < 0 || wa < 0) return fail(ctx, QPIR_E_PARAM, "Q/ans_local: memory of another device");
   const uint64_t ncols = 4 * B;
-  const uint32_t BN = pick_bn(ncols);
+  const uint32_t BN = mma_pick_bn(ncols);
   const uint32_t Npad = (uint32_t)round_up(ncols, BN);
   int rc = ensure(ctx, (void**)&ctx->limbs, &ctx->limbs_bytes, (uint64_t)Npad * g.m_pad);
   if (rc) return rc;
@@ -589,7 +520,7 @@ int qpir_hint(qpir_ctx* ctx, uint32_t* H_local, uint64_t len_H, void* stream) {
   const int wh = where(H_local, ctx->device);
   if (wh < 0) return fail(ctx, QPIR_E_PARAM, "H_local: memory of another device");
   const uint64_t ncols = 4ull * g.lwe_n;
-  const uint32_t BN = pick_bn(ncols);
+  const uint32_t BN = mma_pick_bn(ncols);
   const uint32_t Npad = (uint32_t)round_up(ncols, BN);
   int rc = ensure(ctx, (void**)&ctx->limbs, &ctx->limbs_bytes, (uint64_t)Npad * g.m_pad);
   if (rc) return rc;

@@ -8,6 +8,7 @@
 #include "../../include/qpir.h"
 #include "ens.cuh"
 #include "host_common.h"
+#include "mma_launch.cuh"
 
 using namespace qpir;
 using namespace qpir_host;
@@ -34,6 +35,14 @@ struct qpir_ens_ctx {
   uint32_t* tickets = nullptr;  // scan group tickets (self-resetting)
   uint64_t tickets_bytes = 0;
   int group = 0;                // env QPIR_ENS_GROUP (0 = auto 32; 1 = atomics only)
+  // tensor-core multi-request path (bit-planes, 8x the record bytes)
+  uint8_t* bitD = nullptr;
+  uint64_t bitD_bytes = 0;
+  bool bitD_valid = false;
+  uint8_t* Qb = nullptr;        // shares as 0/1 bytes (B operand)
+  uint64_t Qb_bytes = 0;
+  int tc = -1;                  // env QPIR_ENS_TC: -1 auto, 0 CUDA cores, 1 tensor cores
+  int mma_split = 0;
   uint64_t launches = 0;
   int rows_per_cta = 0;       // env QPIR_ENS_ROWS (0 = auto)
   int ur = 16;                // env QPIR_ENS_UR (rows in flight per thread: 4, 8, 16)
@@ -125,6 +134,8 @@ int qpir_ens_setup(const qpir_ens_params* p, const uint8_t* records, uint64_t re
   ctx->rows_per_cta = env_int("QPIR_ENS_ROWS", 0);
   ctx->ur = env_int("QPIR_ENS_UR", 16);
   ctx->group = env_int("QPIR_ENS_GROUP", 0);
+  ctx->tc = env_int("QPIR_ENS_TC", -1);
+  ctx->mma_split = env_int("QPIR_MMA_SPLIT", 0);
   cudaStream_t st = (cudaStream_t)stream;
   const uint64_t nb = (ctx->r + 7) / 8;
   if (cudaMalloc(&ctx->R, ctx->r * ctx->dp) != cudaSuccess ||
@@ -161,6 +172,7 @@ int qpir_ens_db_write(qpir_ens_ctx* ctx, uint64_t theta_begin, uint64_t n_record
   DeviceGuard dg(ctx->device);
   const int w = where(records, ctx->device);
   if (w < 0) return ENS_FAIL(ctx, QPIR_E_PARAM, "records: memory of another device");
+  ctx->bitD_valid = false;  // the tensor-core bit-planes are rebuilt on next use
   cudaStream_t st = (cudaStream_t)stream;
   ENS_CUDA(ctx, cudaMemcpy2DAsync(ctx->R + theta_begin * ctx->dp, ctx->dp, records, ctx->d,
                                   ctx->d, n_records,
@@ -317,6 +329,62 @@ int qpir_oop_preprocess(qpir_ens_ctx* ctx, uint32_t n_chunks, uint32_t server,
   return qpir_ens_answer_batch(ctx, ctx->Q_dev, n_seeds, n_seeds * nb, A_out, len_A, stream);
 }
 
+// Multi-request GF(2) product on tensor cores (DESIGN 6): the records'
+// bit-planes (8 x r x d bytes of 0/1, built once per DB version) times the
+// shares as 0/1 bytes, s32 counts, parity packed by the OUT_PARITY epilogue.
+static int ens_batch_tc(qpir_ens_ctx* ctx, const uint8_t* Qd, uint64_t B, cudaStream_t st,
+                        bool* used) {
+  *used = false;
+  const uint64_t Lbits = round_up(8 * ctx->dp, 256);
+  const uint64_t m_pad = round_up(ctx->r, 128);
+  const uint64_t G = m_pad / 16;
+  if (G > 0xFFFFFFFFull || Lbits > 0x7FFFFFFFull) return QPIR_OK;
+  if (!ctx->bitD) {
+    if (cudaMalloc(&ctx->bitD, Lbits * m_pad) != cudaSuccess) {
+      cudaGetLastError();
+      ctx->bitD = nullptr;
+      return QPIR_OK;  // not enough HBM for the bit-planes: CUDA-core path
+    }
+    ctx->bitD_bytes = Lbits * m_pad;
+    ctx->bitD_valid = false;
+  }
+  if (!ctx->bitD_valid) {
+    dim3 grid((uint32_t)((G + 127) / 128), (uint32_t)(Lbits / 128));
+    ens_bitplane_pack_kernel<<<grid, 128, 0, st>>>(ctx->R, ctx->r, (uint32_t)ctx->dp, ctx->bitD,
+                                                   (uint32_t)G);
+    ENS_LAUNCHED(ctx);
+    ctx->bitD_valid = true;
+  }
+  const uint32_t BN = mma_pick_bn(B);
+  const uint64_t Npad = round_up(B, BN);
+  int rc = grow(ctx, (void**)&ctx->Qb, &ctx->Qb_bytes, Npad * m_pad);
+  if (rc) return rc;
+  {
+    dim3 grid((uint32_t)((Npad + 127) / 128), (uint32_t)G);
+    ens_share_expand_kernel<<<grid, 128, 0, st>>>(Qd, (uint32_t)B, ctx->r, (ctx->r + 7) / 8,
+                                                  ctx->Qb, (uint32_t)G, (uint32_t)Npad, BN);
+    ENS_LAUNCHED(ctx);
+  }
+  MmaJob j;
+  j.A = ctx->bitD;
+  j.L = (uint32_t)Lbits;
+  j.G = (uint32_t)G;
+  j.rows = (uint32_t)(8 * ctx->dp);
+  j.B = ctx->Qb;
+  j.Npad = (uint32_t)Npad;
+  j.BN = BN;
+  j.out = ctx->acc;
+  j.n_out = (uint32_t)B;
+  j.out_ld = (uint32_t)(ctx->dp / 4);
+  j.out_elems = B * (ctx->dp / 4);
+  j.num_sms = ctx->num_sms;
+  j.forced_split = ctx->mma_split;
+  const cudaError_t e = mma_launch<OUT_PARITY>(j, st, &ctx->launches);
+  if (e != cudaSuccess) return ENS_FAIL(ctx, QPIR_E_CUDA, "tcgen05 GF(2) GEMM: %s", cudaGetErrorString(e));
+  *used = true;
+  return QPIR_OK;
+}
+
 int qpir_ens_answer_batch(qpir_ens_ctx* ctx, const uint8_t* shares, uint64_t B,
                           uint64_t len_shares, uint8_t* out, uint64_t len_out, void* stream) {
   if (!ctx) return QPIR_E_STATE;
@@ -343,6 +411,14 @@ int qpir_ens_answer_batch(qpir_ens_ctx* ctx, const uint8_t* shares, uint64_t B,
     if (rc) return rc;
     rc = stage_in(ctx, shares, B * nb, ctx->Q_dev, &Qd, st);
     if (rc) return rc;
+  }
+  // tensor cores for larger batches when the bit-planes fit in HBM
+  const bool want_tc = ctx->tc == 1 || (ctx->tc < 0 && B >= 32);
+  if (want_tc) {
+    bool used = false;
+    rc = ens_batch_tc(ctx, Qd, B, st, &used);
+    if (rc) return rc;
+    if (used) return copy_out(ctx, out, B, st);
   }
   ENS_CUDA(ctx, cudaMemsetAsync(ctx->acc, 0, B * ctx->dp, st));
   {
@@ -383,8 +459,8 @@ const char* qpir_ens_last_error(const qpir_ens_ctx* ctx) {
 void qpir_ens_destroy(qpir_ens_ctx* ctx) {
   if (!ctx) return;
   DeviceGuard dg(ctx->device);
-  void* bufs[] = {ctx->R,  ctx->q_dev, ctx->acc, ctx->Q_dev, ctx->Qt, ctx->seed_dev,
-                  ctx->partial, ctx->tickets};
+  void* bufs[] = {ctx->R,       ctx->q_dev,   ctx->acc,  ctx->Q_dev, ctx->Qt,
+                  ctx->seed_dev, ctx->partial, ctx->tickets, ctx->bitD, ctx->Qb};
   for (void* b : bufs)
     if (b) cudaFree(b);
   delete ctx;

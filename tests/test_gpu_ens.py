@@ -47,7 +47,11 @@ def test_ens_answer_matches_oracle(cuda_ok, r, d, rows, group, monkeypatch):
 
 
 @pytest.mark.parametrize("B", [1, 7, 64, 130])
-def test_ens_batch_matches_oracle(cuda_ok, B):
+@pytest.mark.parametrize("tc", ["0", "1"])
+def test_ens_batch_matches_oracle(cuda_ok, B, tc, monkeypatch):
+    """tc = 1: GF(2) product on tcgen05 over bit-planes (OUT_PARITY epilogue);
+    tc = 0: CUDA-core predicated-XOR kernel."""
+    monkeypatch.setenv("QPIR_ENS_TC", tc)
     P = _P()
     r, d = 3001, 200
     rec = synth.uniform_u8_np(5, (r, d))
@@ -69,6 +73,25 @@ def test_ens_bruteforce_reconstruct(cuda_ok):
         resp = s.answer_batch(shares).cpu().numpy().reshape(r, l, d)
     for t in range(r):
         assert (O.ens_reconstruct(resp[t]) == rec[t]).all()
+
+
+@pytest.mark.parametrize("split", ["0", "3"])
+def test_ens_tc_ragged_and_split(cuda_ok, split, monkeypatch):
+    """Ragged r / d (d not a multiple of 16, r not of 128) and forced K-splits
+    (parities combined with atomicXor) on the tensor-core path."""
+    monkeypatch.setenv("QPIR_ENS_TC", "1")
+    monkeypatch.setenv("QPIR_MMA_SPLIT", split)
+    P = _P()
+    for r, d, B in [(70001, 5, 33), (1000, 37, 40), (4097, 3072, 17)]:
+        rec = synth.uniform_u8_np(r * 3 + d, (r, d))
+        Q = np.stack([_share(700 + b, r) for b in range(B)])
+        with P.EnsServer(r, d, records=rec) as s:
+            assert (s.answer_batch(Q).cpu().numpy() == O.ens_respond_batch(rec, Q)).all()
+            # DB update invalidates the bit-planes
+            rec2 = rec.copy()
+            rec2[5] ^= 0xFF
+            s.db_write(5, rec2[5:6])
+            assert (s.answer_batch(Q).cpu().numpy() == O.ens_respond_batch(rec2, Q)).all()
 
 
 def test_ens_db_write_and_c2_scale(cuda_ok):
