@@ -174,6 +174,7 @@ def cpu_baseline_answer(wl, seed, budget_s=12.0):
     same DB (4 * d rows x n_cells columns), repeated for ~budget_s seconds."""
     import synth
     from oracle import oracle as O
+    O.set_num_threads(os.cpu_count() or 1)  # torchrun defaults OMP_NUM_THREADS to 1
     n_cells, d = wl["n_cells"], wl["d"]
     n_ch_s = min(4, wl["n_ch"])
     # theta = cell * n_ch + ch with the FULL n_ch: gather the first n_ch_s channels
@@ -204,6 +205,7 @@ def run_reference(args, wl, world, rank):
         return
     import synth  # noqa: F401
     from oracle import oracle as O
+    O.set_num_threads(os.cpu_count() or 1)  # torchrun defaults OMP_NUM_THREADS to 1
     cb = None
     # each step = oracle answer over a bounded sample (first 4 channels)
     n_cells, d = wl["n_cells"], wl["d"]
@@ -509,21 +511,43 @@ def main():
         qs = [None]
         out = torch.empty((ell_local, wl["n"]), dtype=torch.int32, device=dev)
 
+    # N > 1: the NCCL gather of query i runs on a side stream, overlapped with the
+    # scan of query i + 1 (double-buffered answer slices); device-side ordering
+    # only, no host syncs inside the timed region.
+    pipelined = world > 1 and kind != "hint"
+    comm = torch.cuda.Stream(dev) if pipelined else None
+    outs = [out, torch.empty_like(out)] if pipelined else [out]
+    kdone = [torch.cuda.Event() for _ in outs]
+    gdone = [torch.cuda.Event() for _ in outs]
+    used = [False for _ in outs]
+
     def step(i, evs=None):
+        b = i % len(outs)
+        if pipelined and used[b]:
+            stream.wait_event(gdone[b])  # slice b's previous gather has read it
         if evs is not None:
             evs[0].record(stream)
         if kind == "answer":
-            srv.answer(qs[i % len(qs)], out=out, stream=stream)
+            srv.answer(qs[i % len(qs)], out=outs[b], stream=stream)
         elif kind == "batch" and wl.get("modp"):
-            srv.answer_batch_modp(qs[i % len(qs)], wl["modp"], out=out, stream=stream)
+            srv.answer_batch_modp(qs[i % len(qs)], wl["modp"], out=outs[b], stream=stream)
         elif kind == "batch":
-            srv.answer_batch(qs[i % len(qs)], out=out, stream=stream)
+            srv.answer_batch(qs[i % len(qs)], out=outs[b], stream=stream)
         else:
-            srv.hint(out=out, stream=stream)
+            srv.hint(out=outs[b], stream=stream)
         if evs is not None:
             evs[1].record(stream)
-        if world > 1 and kind != "hint":
-            gather_answer(out, sizes)
+        if pipelined:
+            kdone[b].record(stream)
+            comm.wait_event(kdone[b])
+            with torch.cuda.stream(comm):
+                gather_answer(outs[b], sizes)
+                gdone[b].record(comm)
+            used[b] = True
+
+    def drain():
+        if pipelined:
+            stream.wait_stream(comm)
 
     def barrier():
         if world > 1:
@@ -533,6 +557,7 @@ def main():
     sampler = ClockSampler(physical_gpu(local))
     for i in range(args.warmup):
         step(i)
+    drain()
     barrier()
     time.sleep(0.3)  # let the clock sampler come up
     kev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
@@ -545,6 +570,7 @@ def main():
     e0.record(stream)
     for i in range(args.steps):
         step(i, kev[i])
+    drain()
     e1.record(stream)
     barrier()
     sampler.stop()

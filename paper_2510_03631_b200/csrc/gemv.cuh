@@ -113,6 +113,11 @@ struct GemvArgs {
 template <int U, int UNR>
 __global__ void __launch_bounds__(GEMV_THREADS) gemv_u8_u32_kernel(GemvArgs a) {
   extern __shared__ uint4 sL[];
+  // Programmatic dependent launch: let the next query's GEMV start streaming D
+  // while this grid drains.  Only reads (D, qu) happen before griddepcontrol.wait;
+  // every global write (partials, tickets, ans) comes after it, so back-to-back
+  // answers never race on the shared scratch or output buffers.
+  asm volatile("griddepcontrol.launch_dependents;");
   const uint32_t tid = threadIdx.x;
   // Grid order: with split_major the CTAs that run at the same time walk
   // adjacent K ranges of the same row panels, i.e. few distinct 2 MB pages.
@@ -165,6 +170,7 @@ __global__ void __launch_bounds__(GEMV_THREADS) gemv_u8_u32_kernel(GemvArgs a) {
 #pragma unroll
   for (int u = 0; u < U; ++u)
     out[u] = acc[u][0] + (acc[u][1] << 8) + (acc[u][2] << 16) + (acc[u][3] << 24);
+  asm volatile("griddepcontrol.wait;" ::: "memory");  // previous grid complete + visible
 
   if (nsplit == 1) {
 #pragma unroll

@@ -62,6 +62,7 @@ struct qpir_ctx {
   int gemv_chunk = 512;
   int gemv_unroll = 4;
   int gemv_order = 0;  // env QPIR_GEMV_ORDER (1 = split-major grid)
+  int gemv_pdl = 1;    // env QPIR_GEMV_PDL (programmatic dependent launch of back-to-back GEMVs)
   int mma_mt = 2;      // env QPIR_MMA_MT (1 or 2 row panels per CTA tile)
   int mma_split = 0;   // env QPIR_MMA_SPLIT (0 = auto)
   int mma_gpb = 8;     // env QPIR_MMA_GPB (column groups per pipeline stage: 4 or 8)
@@ -240,7 +241,17 @@ int launch_gemv(qpir_ctx* ctx, const uint32_t* qu, uint32_t* ans, cudaStream_t s
   if (smem > 48 * 1024)
     CUDA_TRY(ctx, cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   const dim3 grid = a.split_major ? dim3(S, rb) : dim3(rb, S);
-  kern<<<grid, GEMV_THREADS, smem, st>>>(a);
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = dim3(GEMV_THREADS);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = ctx->gemv_pdl ? 1 : 0;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  CUDA_TRY(ctx, cudaLaunchKernelEx(&cfg, kern, a));
   LAUNCH_CHECK(ctx);
   return QPIR_OK;
 }
@@ -323,6 +334,7 @@ int qpir_setup(const qpir_params* params, const uint8_t* records, uint64_t recor
   ctx->gemv_chunk = env_int("QPIR_GEMV_CHUNK", 512);
   ctx->gemv_unroll = env_int("QPIR_GEMV_UNROLL", 4);
   ctx->gemv_order = env_int("QPIR_GEMV_ORDER", 0);
+  ctx->gemv_pdl = env_int("QPIR_GEMV_PDL", 1);
   ctx->mma_mt = env_int("QPIR_MMA_MT", 2);
   ctx->mma_split = env_int("QPIR_MMA_SPLIT", 0);
   ctx->mma_gpb = env_int("QPIR_MMA_GPB", 8);

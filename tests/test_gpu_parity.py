@@ -300,3 +300,28 @@ def test_c5_hint_shard_sampled(cuda_ok):
     A = O.expand_A(seed_A, n_cells, n)
     assert (H[rows] == O.hint(Dr, A)).all()
     s.close()
+
+
+@pytest.mark.parametrize("cfg", [dict(), dict(QPIR_GEMV_SPLIT="7"), dict(QPIR_GEMV_PDL="0")])
+def test_back_to_back_answers_pdl(cuda_ok, cfg, monkeypatch):
+    """Back-to-back GEMVs on one stream overlap under programmatic dependent
+    launch; split-K scratch and outputs must not race (every answer exact)."""
+    for k, v in cfg.items():
+        monkeypatch.setenv(k, v)
+    P = _srv()
+    n_cells, n_ch, d = 4096, 8, 64
+    rec, D = _db(n_cells, n_ch, d, seed=40)
+    Qs = [synth.uniform_u32_np(41 + i, (n_cells,)) for i in range(24)]
+    with P.PirServer(n_cells, n_ch, d, records=torch.from_numpy(rec).cuda()) as s:
+        qd = [torch.from_numpy(q.view(np.int32)).cuda() for q in Qs]
+        same = torch.empty(s.ell_local, dtype=torch.int32, device="cuda")
+        outs = []
+        for i, q in enumerate(qd):
+            if i % 3 == 2:
+                s.answer(q, out=same)  # reuse one output buffer (WAW across launches)
+            else:
+                outs.append((i, s.answer(q)))
+        torch.cuda.synchronize()
+        for i, o in outs:
+            assert (_u32(o) == O.answer(D, Qs[i])).all(), i
+        assert (_u32(same) == O.answer(D, Qs[23])).all()
