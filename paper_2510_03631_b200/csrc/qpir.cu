@@ -206,6 +206,13 @@ int launch_gemv(qpir_ctx* ctx, const uint32_t* qu, uint32_t* ans, cudaStream_t s
     const uint32_t by_waves = (uint32_t)((8u * 6u * ctx->num_sms + rb - 1) / rb);
     S = std::max(by_work, by_waves);
     S = std::min<uint32_t>(S, (uint32_t)std::max<uint64_t>(1, g.G / 16));
+    // prefer a split count that divides the K range into equal pieces
+    const uint32_t units = (uint32_t)(g.G / UNR);
+    for (uint32_t c = S; c <= 2 * S && c <= units; ++c)
+      if (units % c == 0) {
+        S = c;
+        break;
+      }
   }
   S = std::max<uint32_t>(1, std::min<uint32_t>(S, (uint32_t)(g.G / UNR)));
   uint32_t gps = (uint32_t)round_up((g.G + S - 1) / S, UNR);
