@@ -88,3 +88,87 @@ class DistributedPIR:
         if not gather:
             return h
         return gather_answer(h.t().contiguous(), self.sizes, self.group).t()
+
+
+# ---------------------------------------------------------------- NEXT rows
+def shard_records(r: int, world: int, rank: int, align: int = 1):
+    """Contiguous record shard [t0, t1) of rank (whole multiples of `align`)."""
+    units = -(-r // align)
+    base, extra = divmod(units, world)
+    u0 = rank * base + min(rank, extra)
+    u1 = u0 + base + (1 if rank < extra else 0)
+    return min(r, u0 * align), min(r, u1 * align)
+
+
+def xor_combine(part: torch.Tensor, group=None) -> torch.Tensor:
+    """XOR of every rank's uint8 partial response (NCCL has no XOR reduction:
+    all-gather the d-byte partials and fold them; the payload is a few KB)."""
+    world = dist.get_world_size(group)
+    if dist.get_backend(group) == "nccl":
+        buf = torch.empty((world, *part.shape), dtype=part.dtype, device=part.device)
+        dist.all_gather_into_tensor(buf, part.contiguous().unsqueeze(0), group=group)
+        parts = list(buf)
+    else:
+        host = part.contiguous().cpu()
+        parts = [torch.empty_like(host) for _ in range(world)]
+        dist.all_gather(parts, host, group=group)
+    out = parts[0].clone()
+    for t in parts[1:]:
+        out ^= t.to(out.device)
+    return out.to(part.device)
+
+
+def sum_mod_p(part_u32: torch.Tensor, p: int, group=None) -> torch.Tensor:
+    """Sum of every rank's partial F_p response (values < p) mod p, exactly:
+    all-reduce in int64 (world * p < 2^63), then reduce."""
+    acc = part_u32.to(torch.int64) & 0xFFFFFFFF
+    dist.all_reduce(acc, op=dist.ReduceOp.SUM, group=group)
+    return (acc % p).to(torch.int64)
+
+
+class DistributedEns:
+    """QPADL-ENS with the records sharded over ranks: each GPU XORs the selected
+    records of its shard; the d-byte partials are XOR-combined."""
+
+    def __init__(self, n_records: int, rec_bytes: int, *, device: int | None = None,
+                 records=None, group=None):
+        from . import EnsServer
+
+        self.group = group
+        self.world = dist.get_world_size(group)
+        self.rank = dist.get_rank(group)
+        self.r, self.d = n_records, rec_bytes
+        self.t0, self.t1 = shard_records(n_records, self.world, self.rank, align=8)
+        dev = torch.cuda.current_device() if device is None else device
+        local = None if records is None else records[self.t0:self.t1]
+        self.server = EnsServer(self.t1 - self.t0, rec_bytes, device=dev, records=local)
+
+    def local_share(self, share_bits: torch.Tensor) -> torch.Tensor:
+        """Slice of a full r-bit share for this shard (shards start on byte boundaries)."""
+        nb = (self.t1 - self.t0 + 7) // 8
+        return share_bits[..., self.t0 // 8: self.t0 // 8 + nb].contiguous()
+
+    def answer(self, share_bits):
+        return xor_combine(self.server.answer(self.local_share(share_bits)), self.group)
+
+
+class DistributedFtr:
+    """QPADL-FTR with the records sharded over ranks: partial rho . DB mod p per
+    shard, summed across ranks mod p."""
+
+    def __init__(self, n_records: int, rec_bytes: int, *, p: int = 65537,
+                 device: int | None = None, records=None, group=None):
+        from . import FtrServer
+
+        self.group = group
+        self.world = dist.get_world_size(group)
+        self.rank = dist.get_rank(group)
+        self.p = p
+        self.t0, self.t1 = shard_records(n_records, self.world, self.rank)
+        dev = torch.cuda.current_device() if device is None else device
+        local = None if records is None else records[self.t0:self.t1]
+        self.server = FtrServer(self.t1 - self.t0, rec_bytes, p=p, device=dev, records=local)
+
+    def answer_batch(self, Q):
+        part = self.server.answer_batch(Q[:, self.t0:self.t1].contiguous())
+        return sum_mod_p(part, self.p, self.group)

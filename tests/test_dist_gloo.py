@@ -75,3 +75,45 @@ def test_shard_rows_whole_channels():
     assert [shard_rows(10, 3, 5, 10, 2, r) for r in range(2)] == [(0, 10), (10, 15)]
     with pytest.raises(ValueError):
         shard_rows(10, 1, 5, 10, 2, 0)
+
+
+def _worker_next(rank, world, port, q):
+    import synth
+    from oracle import oracle as O
+    from paper_2510_03631_b200.dist import shard_records, sum_mod_p, xor_combine
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        r, d, p = 203, 17, 65537
+        rec = synth.uniform_u8_np(9, (r, d))
+        # ENS: shards on byte boundaries of the share, partials XOR-combined
+        t0, t1 = shard_records(r, world, rank, align=8)
+        share = synth.uniform_u8_np(10, ((r + 7) // 8,))
+        share[-1] &= (1 << (r % 8)) - 1
+        local = share[t0 // 8:(t1 + 7) // 8]
+        part = torch.from_numpy(O.ens_respond(rec[t0:t1], local))
+        ok_ens = bool((xor_combine(part).numpy() == O.ens_respond(rec, share)).all())
+        # FTR: contiguous shards, partial sums mod p combined exactly
+        f0, f1 = shard_records(r, world, rank)
+        Q = synth.uniform_u32_np(11, (3, r)) % p
+        partf = torch.from_numpy(O.ftr_respond_batch(rec[f0:f1], Q[:, f0:f1]).view(np.int32))
+        ok_ftr = bool((sum_mod_p(partf, p).numpy() == O.ftr_respond_batch(rec, Q)).all())
+        q.put((rank, ok_ens, ok_ftr))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_next_rows_shard_and_combine(world):
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker_next, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = [q.get(timeout=120) for _ in range(world)]
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    assert all(e and f for _, e, f in res), res

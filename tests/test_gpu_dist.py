@@ -1,0 +1,49 @@
+"""Device glue of the multi-GPU layer with a one-rank NCCL group (the pool gives
+one GPU per call; multi-rank combining logic is covered by test_dist_gloo.py)."""
+import socket
+
+import numpy as np
+import pytest
+import torch
+import torch.distributed as dist
+
+import synth
+from oracle import oracle as O
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture
+def nccl1(cuda_ok):
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    dist.init_process_group("nccl", init_method=f"tcp://127.0.0.1:{port}", rank=0, world_size=1,
+                            device_id=torch.device("cuda", 0))
+    yield
+    dist.destroy_process_group()
+
+
+def test_distributed_pir_ens_ftr_one_rank(nccl1):
+    from paper_2510_03631_b200.dist import DistributedEns, DistributedFtr, DistributedPIR
+    n_cells, n_ch, d = 1024, 8, 24
+    rec = synth.uniform_u8_np(3, (n_cells * n_ch, d))
+    D = O.pack(rec, n_cells, n_ch, d, n_cells)
+    pir = DistributedPIR(n_cells, n_ch, d, records=torch.from_numpy(rec).cuda())
+    qu = synth.uniform_u32_np(4, (n_cells,))
+    got = pir.answer(torch.from_numpy(qu.view(np.int32)).cuda())
+    assert (got.cpu().numpy().view(np.uint32) == O.answer(D, qu)).all()
+    Q = synth.uniform_u32_np(5, (3, n_cells))
+    got = pir.answer_batch(torch.from_numpy(Q.view(np.int32)).cuda())
+    assert (got.cpu().numpy().view(np.uint32) == O.answer_batch(D, Q)).all()
+
+    r = rec.shape[0]
+    ens = DistributedEns(r, d, records=torch.from_numpy(rec).cuda())
+    share = synth.uniform_u8_np(6, ((r + 7) // 8,))
+    assert (ens.answer(torch.from_numpy(share).cuda()).cpu().numpy() == O.ens_respond(rec, share)).all()
+
+    ftr = DistributedFtr(r, d, records=torch.from_numpy(rec).cuda())
+    Qf = synth.uniform_u32_np(7, (2, r)) % 65537
+    got = ftr.answer_batch(torch.from_numpy(Qf.view(np.int32)).cuda())
+    assert (got.cpu().numpy() == O.ftr_respond_batch(rec, Qf)).all()
