@@ -31,9 +31,11 @@
  *   - Streams: `stream` is a cudaStream_t (NULL = legacy default stream).  Work
  *     is enqueued on it.  If any output is host memory the call synchronises
  *     the stream before returning; with device outputs it returns immediately.
- *   - Concurrency: calls on one context are serialised by the caller (one
- *     stream per context); distinct contexts are independent.  The D shard is
- *     never modified by the answer/hint calls.
+ *   - Concurrency: answer / batch / hint calls on one context may run
+ *     concurrently on different streams (each stream gets its own scratch
+ *     arena: staging buffers, split-K partials, tickets); calls on one stream
+ *     are ordered by that stream.  qpir_db_write must not overlap any other
+ *     call on the context.  The D shard is never modified by answer/hint calls.
  *   - Errors: functions return QPIR_OK (0) or a QPIR_E_* code; no partial
  *     outputs on error.  qpir_last_error(ctx) (or qpir_last_error(NULL) for a
  *     failed qpir_setup) names the offending field, e.g. "m: 8191 != 8192".

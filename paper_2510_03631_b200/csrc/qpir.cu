@@ -8,6 +8,8 @@
 
 #include <algorithm>
 #include <cstdarg>
+#include <map>
+#include <mutex>
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
@@ -35,18 +37,18 @@ struct Geometry {
 
 }  // namespace
 
-struct qpir_ctx {
-  Geometry geo;
-  int device = 0;
-  int num_sms = 148;
-  uint8_t* D = nullptr;            // 128-row panels [L/128][G][128][16]
-  uint32_t* qu_dev = nullptr;      // m_pad (staging for host / unaligned qu)
-  uint32_t* ans_dev = nullptr;     // ell_local (staging for host answers)
-  uint32_t* partial = nullptr;     // [max_split][L]
-  uint32_t* tickets = nullptr;     // [max row blocks], self-resetting
-  uint32_t max_split = 0, max_rb = 0;
-  uint8_t* rec_stage = nullptr;    // host-record staging for db_write
-  uint64_t rec_stage_bytes = 0;
+// Per-stream scratch: calls on different streams of one context may run
+// concurrently (each stream owns its staging buffers, split-K partials and
+// tickets); calls on one stream are ordered by the stream.
+struct Arena {
+  uint32_t* qu_dev = nullptr;      // staging for host / unaligned qu
+  uint64_t qu_bytes = 0;
+  uint32_t* ans_dev = nullptr;     // staging for host answers
+  uint64_t ans_bytes = 0;
+  uint32_t* partial = nullptr;     // [split][L] GEMV split-K partials
+  uint64_t partial_bytes = 0;
+  uint32_t* tickets = nullptr;     // [row blocks], zeroed once, self-resetting
+  uint64_t tickets_bytes = 0;
   uint8_t* limbs = nullptr;        // Q' or A' limb planes
   uint64_t limbs_bytes = 0;
   uint32_t* big_in = nullptr;      // staging for host Q
@@ -55,6 +57,17 @@ struct qpir_ctx {
   uint64_t big_out_bytes = 0;
   unsigned long long* acc64 = nullptr;  // OUT_MODP accumulator
   uint64_t acc64_bytes = 0;
+};
+
+struct qpir_ctx {
+  Geometry geo;
+  int device = 0;
+  int num_sms = 148;
+  uint8_t* D = nullptr;            // 128-row panels [L/128][G][128][16]
+  uint8_t* rec_stage = nullptr;    // host-record staging for db_write
+  uint64_t rec_stage_bytes = 0;
+  std::mutex mu;                   // guards `arenas`
+  std::map<cudaStream_t, Arena> arenas;
   uint64_t launches = 0;
   // GEMV tuning (env QPIR_GEMV_U / QPIR_GEMV_SPLIT / QPIR_GEMV_CHUNK)
   int gemv_u = 2;
@@ -151,6 +164,11 @@ int ensure(qpir_ctx* ctx, void** buf, uint64_t* have, uint64_t need) {
   return QPIR_OK;
 }
 
+Arena& arena_for(qpir_ctx* ctx, cudaStream_t st) {
+  std::lock_guard<std::mutex> lk(ctx->mu);
+  return ctx->arenas[st];  // std::map references stay valid across inserts
+}
+
 int db_write_device(qpir_ctx* ctx, uint64_t theta0, uint64_t n_rec, const uint8_t* rec,
                     cudaStream_t st) {
   const Geometry& g = ctx->geo;
@@ -219,23 +237,22 @@ int launch_gemv(qpir_ctx* ctx, const uint32_t* qu, uint32_t* ans, cudaStream_t s
   S = (uint32_t)((g.G + gps - 1) / gps);
   uint32_t chunk = (uint32_t)std::max(UNR, ctx->gemv_chunk / UNR * UNR);
   chunk = std::min(chunk, gps);
-  if (S > 1 && (S > ctx->max_split || rb > ctx->max_rb)) {
-    if (ctx->partial) cudaFree(ctx->partial);
-    if (ctx->tickets) cudaFree(ctx->tickets);
-    ctx->partial = nullptr;
-    ctx->tickets = nullptr;
-    ctx->max_split = std::max(S, ctx->max_split);
-    ctx->max_rb = std::max(rb, ctx->max_rb);
-    CUDA_TRY(ctx, cudaMalloc(&ctx->partial, (size_t)ctx->max_split * g.L * 4));
-    CUDA_TRY(ctx, cudaMalloc(&ctx->tickets, (size_t)ctx->max_rb * 4));
-    CUDA_TRY(ctx, cudaMemsetAsync(ctx->tickets, 0, (size_t)ctx->max_rb * 4, st));
+  Arena& ar = arena_for(ctx, st);
+  if (S > 1) {
+    int rc = ensure(ctx, (void**)&ar.partial, &ar.partial_bytes, (uint64_t)S * g.L * 4);
+    if (rc) return rc;
+    if ((uint64_t)rb * 4 > ar.tickets_bytes) {
+      rc = ensure(ctx, (void**)&ar.tickets, &ar.tickets_bytes, (uint64_t)rb * 4);
+      if (rc) return rc;
+      CUDA_TRY(ctx, cudaMemsetAsync(ar.tickets, 0, ar.tickets_bytes, st));
+    }
   }
   GemvArgs a;
   a.D = ctx->D;
   a.qu = qu;
   a.ans = ans;
-  a.partial = ctx->partial;
-  a.tickets = ctx->tickets;
+  a.partial = ar.partial;
+  a.tickets = ar.tickets;
   a.ell_local = (uint32_t)g.ell_local;
   a.L = (uint32_t)g.L;
   a.m = (uint32_t)g.m;
@@ -357,14 +374,7 @@ int qpir_setup(const qpir_params* params, const uint8_t* records, uint64_t recor
     fail(ctx, QPIR_E_OOM, "D: cudaMalloc(%zu) failed", dbytes);
     return bail(QPIR_E_OOM);
   }
-  if (cudaMalloc(&ctx->qu_dev, g.m_pad * 4) != cudaSuccess ||
-      cudaMalloc(&ctx->ans_dev, g.L * 4) != cudaSuccess) {
-    cudaGetLastError();
-    fail(ctx, QPIR_E_OOM, "scratch: cudaMalloc failed");
-    return bail(QPIR_E_OOM);
-  }
-  if (cudaMemsetAsync(ctx->D, 0, dbytes, st) != cudaSuccess ||
-      cudaMemsetAsync(ctx->qu_dev, 0, g.m_pad * 4, st) != cudaSuccess) {
+  if (cudaMemsetAsync(ctx->D, 0, dbytes, st) != cudaSuccess) {
     fail(ctx, QPIR_E_CUDA, "memset failed");
     return bail(QPIR_E_CUDA);
   }
@@ -440,14 +450,23 @@ int qpir_answer(qpir_ctx* ctx, const uint32_t* qu, uint64_t len_qu, uint32_t* an
   cudaStream_t st = (cudaStream_t)stream;
   const int wq = where(qu, ctx->device), wa = where(ans_local, ctx->device);
   if (wq < 0 || wa < 0) return fail(ctx, QPIR_E_PARAM, "qu/ans_local: memory of another device");
+  Arena& ar = arena_for(ctx, st);
+  int rc = QPIR_OK;
   const uint32_t* qd = qu;
   if (wq == 0 || !aligned16(qu)) {
-    CUDA_TRY(ctx, cudaMemcpyAsync(ctx->qu_dev, qu, g.m * 4,
+    rc = ensure(ctx, (void**)&ar.qu_dev, &ar.qu_bytes, g.m_pad * 4);
+    if (rc) return rc;
+    CUDA_TRY(ctx, cudaMemcpyAsync(ar.qu_dev, qu, g.m * 4,
                                   wq ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, st));
-    qd = ctx->qu_dev;
+    qd = ar.qu_dev;
   }
-  uint32_t* ad = wa ? ans_local : ctx->ans_dev;
-  int rc = gemv(ctx, qd, ad, st);
+  uint32_t* ad = ans_local;
+  if (!wa) {
+    rc = ensure(ctx, (void**)&ar.ans_dev, &ar.ans_bytes, g.L * 4);
+    if (rc) return rc;
+    ad = ar.ans_dev;
+  }
+  rc = gemv(ctx, qd, ad, st);
   if (rc) return rc;
   if (!wa) {
     CUDA_TRY(ctx, cudaMemcpyAsync(ans_local, ad, g.ell_local * 4, cudaMemcpyDeviceToHost, st));
@@ -476,36 +495,37 @@ static int answer_batch_impl(qpir_ctx* ctx, const uint32_t* Q, uint64_t B, uint6
   const uint64_t ncols = 4 * B;
   const uint32_t BN = mma_pick_bn(ncols);
   const uint32_t Npad = (uint32_t)round_up(ncols, BN);
-  int rc = ensure(ctx, (void**)&ctx->limbs, &ctx->limbs_bytes, (uint64_t)Npad * g.m_pad);
+  Arena& ar = arena_for(ctx, st);
+  int rc = ensure(ctx, (void**)&ar.limbs, &ar.limbs_bytes, (uint64_t)Npad * g.m_pad);
   if (rc) return rc;
   const uint32_t* Qd = Q;
   if (wq == 0) {
-    rc = ensure(ctx, (void**)&ctx->big_in, &ctx->big_in_bytes, len_Q * 4);
+    rc = ensure(ctx, (void**)&ar.big_in, &ar.big_in_bytes, len_Q * 4);
     if (rc) return rc;
-    CUDA_TRY(ctx, cudaMemcpyAsync(ctx->big_in, Q, len_Q * 4, cudaMemcpyHostToDevice, st));
-    Qd = ctx->big_in;
+    CUDA_TRY(ctx, cudaMemcpyAsync(ar.big_in, Q, len_Q * 4, cudaMemcpyHostToDevice, st));
+    Qd = ar.big_in;
   }
   uint32_t* out = ans_local;
   if (wa == 0) {
-    rc = ensure(ctx, (void**)&ctx->big_out, &ctx->big_out_bytes, len_ans * 4);
+    rc = ensure(ctx, (void**)&ar.big_out, &ar.big_out_bytes, len_ans * 4);
     if (rc) return rc;
-    out = ctx->big_out;
+    out = ar.big_out;
   }
   {
     const uint32_t nq = Npad / 4;  // padded query slots
     dim3 grid((nq + 127) / 128, (uint32_t)g.G);
-    limb_split_kernel<<<grid, 128, 0, st>>>(Qd, ctx->limbs, (uint32_t)B, (uint32_t)g.m,
+    limb_split_kernel<<<grid, 128, 0, st>>>(Qd, ar.limbs, (uint32_t)B, (uint32_t)g.m,
                                             (uint32_t)g.G, Npad, BN);
     LAUNCH_CHECK(ctx);
   }
   if (p == 0) {
-    rc = launch_mma<OUT_QUERY_MAJOR>(ctx, BN, ctx->limbs, Npad, out, (uint32_t)B,
+    rc = launch_mma<OUT_QUERY_MAJOR>(ctx, BN, ar.limbs, Npad, out, (uint32_t)B,
                                      (uint32_t)g.ell_local, len_ans, st);
   } else {
-    rc = ensure(ctx, (void**)&ctx->acc64, &ctx->acc64_bytes, len_ans * 8);
+    rc = ensure(ctx, (void**)&ar.acc64, &ar.acc64_bytes, len_ans * 8);
     if (rc) return rc;
-    rc = launch_mma<OUT_MODP>(ctx, BN, ctx->limbs, Npad, out, (uint32_t)B,
-                              (uint32_t)g.ell_local, len_ans, st, p, ctx->acc64);
+    rc = launch_mma<OUT_MODP>(ctx, BN, ar.limbs, Npad, out, (uint32_t)B,
+                              (uint32_t)g.ell_local, len_ans, st, p, ar.acc64);
   }
   if (rc) return rc;
   if (wa == 0) {
@@ -541,22 +561,23 @@ int qpir_hint(qpir_ctx* ctx, uint32_t* H_local, uint64_t len_H, void* stream) {
   const uint64_t ncols = 4ull * g.lwe_n;
   const uint32_t BN = mma_pick_bn(ncols);
   const uint32_t Npad = (uint32_t)round_up(ncols, BN);
-  int rc = ensure(ctx, (void**)&ctx->limbs, &ctx->limbs_bytes, (uint64_t)Npad * g.m_pad);
+  Arena& ar = arena_for(ctx, st);
+  int rc = ensure(ctx, (void**)&ar.limbs, &ar.limbs_bytes, (uint64_t)Npad * g.m_pad);
   if (rc) return rc;
   uint32_t* out = H_local;
   if (wh == 0 || !aligned16(H_local)) {
-    rc = ensure(ctx, (void**)&ctx->big_out, &ctx->big_out_bytes, len_H * 4);
+    rc = ensure(ctx, (void**)&ar.big_out, &ar.big_out_bytes, len_H * 4);
     if (rc) return rc;
-    out = ctx->big_out;
+    out = ar.big_out;
   }
   {
     const uint32_t nb = Npad / 16;  // Philox blocks (4 outputs x 4 limbs)
     dim3 grid((nb + 127) / 128, (uint32_t)g.G);
-    expand_A_limbs_kernel<<<grid, 128, 0, st>>>(ctx->limbs, g.seed_A, (uint32_t)g.m, g.lwe_n,
+    expand_A_limbs_kernel<<<grid, 128, 0, st>>>(ar.limbs, g.seed_A, (uint32_t)g.m, g.lwe_n,
                                                 (uint32_t)g.G, Npad, BN);
     LAUNCH_CHECK(ctx);
   }
-  rc = launch_mma<OUT_ROW_MAJOR>(ctx, BN, ctx->limbs, Npad, out, g.lwe_n, g.lwe_n, len_H, st);
+  rc = launch_mma<OUT_ROW_MAJOR>(ctx, BN, ar.limbs, Npad, out, g.lwe_n, g.lwe_n, len_H, st);
   if (rc) return rc;
   if (out != H_local) {
     CUDA_TRY(ctx, cudaMemcpyAsync(H_local, out, len_H * 4,
@@ -575,10 +596,15 @@ const char* qpir_last_error(const qpir_ctx* ctx) {
 void qpir_destroy(qpir_ctx* ctx) {
   if (!ctx) return;
   DeviceGuard dg(ctx->device);
-  void* bufs[] = {ctx->D,         ctx->qu_dev, ctx->ans_dev, ctx->partial, ctx->tickets,
-                  ctx->rec_stage, ctx->limbs,  ctx->big_in,  ctx->big_out, ctx->acc64};
+  void* bufs[] = {ctx->D, ctx->rec_stage};
   for (void* b : bufs)
     if (b) cudaFree(b);
+  for (auto& kv : ctx->arenas) {
+    Arena& a = kv.second;
+    void* ab[] = {a.qu_dev, a.ans_dev, a.partial, a.tickets, a.limbs, a.big_in, a.big_out, a.acc64};
+    for (void* b : ab)
+      if (b) cudaFree(b);
+  }
   delete ctx;
 }
 

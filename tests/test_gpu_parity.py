@@ -325,3 +325,33 @@ def test_back_to_back_answers_pdl(cuda_ok, cfg, monkeypatch):
         for i, o in outs:
             assert (_u32(o) == O.answer(D, Qs[i])).all(), i
         assert (_u32(same) == O.answer(D, Qs[23])).all()
+
+
+def test_concurrent_streams_have_private_scratch(cuda_ok, monkeypatch):
+    """Calls on different streams of one context use per-stream arenas (host-query
+    staging, split-K partials, tickets, limb planes): interleaved answers and
+    batches on two streams must all be exact."""
+    monkeypatch.setenv("QPIR_GEMV_SPLIT", "6")
+    P = _srv()
+    n_cells, n_ch, d = 3000, 6, 40
+    rec, D = _db(n_cells, n_ch, d, seed=50)
+    streams = [torch.cuda.Stream(), torch.cuda.Stream()]
+    with P.PirServer(n_cells, n_ch, d, records=rec) as s:
+        jobs = []
+        for i in range(16):
+            st = streams[i % 2]
+            if i % 4 == 3:
+                Q = synth.uniform_u32_np(60 + i, (5, n_cells))
+                pin = torch.from_numpy(Q.view(np.int32)).pin_memory()
+                out = torch.empty((5, s.ell_local), dtype=torch.int32, device="cuda")
+                s.answer_batch(pin, out=out, stream=st)
+                jobs.append((out, O.answer_batch(D, Q), pin))
+            else:
+                q = synth.uniform_u32_np(60 + i, (n_cells,))
+                pin = torch.from_numpy(q.view(np.int32)).pin_memory()
+                out = torch.empty(s.ell_local, dtype=torch.int32, device="cuda")
+                s.answer(pin, out=out, stream=st)  # async H2D into the stream's arena
+                jobs.append((out, O.answer(D, q), pin))
+        torch.cuda.synchronize()
+        for out, want, _ in jobs:
+            assert (_u32(out) == want).all()
