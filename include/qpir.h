@@ -148,7 +148,8 @@ void qpir_destroy(qpir_ctx *ctx);
 /* positions >= r are ignored.  The response to a share is the XOR of the  */
 /* records whose bit is 1 (rho = q . DB over GF(2)); a client XORs the l   */
 /* responses of l servers to rebuild its record.  Same buffer, length,     */
-/* stream and error conventions as above.                                  */
+/* stream and error conventions as above, except that an ENS context has   */
+/* one scratch arena: its calls must be serialised by the caller.          */
 /* ===================================================================== */
 typedef struct qpir_ens_ctx qpir_ens_ctx;
 

@@ -64,32 +64,43 @@ __global__ void pack_records_kernel(PackArgs a) {
 //   byte i of (limb column n, group g) at ((n / BN) * G + g) * BN * 16 + (n % BN) * 16 + i
 //   = limb k of Q[j][16g + i], n = 4j + k (k = 0..3); zero for padding
 // (n >= 4B or 16g + i >= m).  One MMA B tile (BN columns x 8 groups) is then
-// BN * 128 contiguous bytes.  One thread per (query j, group g): 64 B in,
+// BN * 128 contiguous bytes.  One thread per (group g, query j): 64 B in,
 // 4 x 16 B out (64 B contiguous).
 __global__ void limb_split_kernel(const uint32_t* __restrict__ Q, uint8_t* __restrict__ Qp,
                                   uint32_t B, uint32_t m, uint32_t G, uint32_t Npad,
                                   uint32_t BN) {
-  const uint32_t jq = blockIdx.x * blockDim.x + threadIdx.x;  // padded query index
-  const uint32_t g = blockIdx.y;
-  if (jq * 4u >= Npad) return;
+  // threads walk 16-cell groups of one query row (coalesced 64 B per thread);
+  // each thread writes its query's 4 limb rows = 64 contiguous bytes
+  const uint32_t g = blockIdx.x * blockDim.x + threadIdx.x;
+  const uint32_t jq = blockIdx.y;  // padded query index
+  if (g >= G || jq * 4u >= Npad) return;
   uint32_t q[16];
+  const uint32_t c0 = g * 16u;
+  const uint32_t* row = Q + (size_t)jq * m;
+  if (jq < B && c0 + 16u <= m && (m & 3u) == 0 &&
+      (reinterpret_cast<uintptr_t>(Q) & 15u) == 0) {
+    const uint4* p = reinterpret_cast<const uint4*>(row + c0);
 #pragma unroll
-  for (int i = 0; i < 16; ++i) {
-    const uint32_t c = g * 16u + i;
-    q[i] = (jq < B && c < m) ? __ldg(Q + (size_t)jq * m + c) : 0u;
+    for (int i = 0; i < 4; ++i) {
+      const uint4 v = __ldg(p + i);
+      q[4 * i + 0] = v.x;
+      q[4 * i + 1] = v.y;
+      q[4 * i + 2] = v.z;
+      q[4 * i + 3] = v.w;
+    }
+  } else {
+#pragma unroll
+    for (int i = 0; i < 16; ++i) q[i] = (jq < B && c0 + i < m) ? __ldg(row + c0 + i) : 0u;
   }
   uint4* dst = reinterpret_cast<uint4*>(Qp + limb_off(jq * 4u, g, G, BN));
 #pragma unroll
   for (uint32_t k = 0; k < 4; ++k) {
+    const uint32_t sel = k | ((k + 4) << 4);
     uint4 w;
-    w.x = __byte_perm(__byte_perm(q[0], q[1], k | ((k + 4) << 4)),
-                      __byte_perm(q[2], q[3], k | ((k + 4) << 4)), 0x5410);
-    w.y = __byte_perm(__byte_perm(q[4], q[5], k | ((k + 4) << 4)),
-                      __byte_perm(q[6], q[7], k | ((k + 4) << 4)), 0x5410);
-    w.z = __byte_perm(__byte_perm(q[8], q[9], k | ((k + 4) << 4)),
-                      __byte_perm(q[10], q[11], k | ((k + 4) << 4)), 0x5410);
-    w.w = __byte_perm(__byte_perm(q[12], q[13], k | ((k + 4) << 4)),
-                      __byte_perm(q[14], q[15], k | ((k + 4) << 4)), 0x5410);
+    w.x = __byte_perm(__byte_perm(q[0], q[1], sel), __byte_perm(q[2], q[3], sel), 0x5410);
+    w.y = __byte_perm(__byte_perm(q[4], q[5], sel), __byte_perm(q[6], q[7], sel), 0x5410);
+    w.z = __byte_perm(__byte_perm(q[8], q[9], sel), __byte_perm(q[10], q[11], sel), 0x5410);
+    w.w = __byte_perm(__byte_perm(q[12], q[13], sel), __byte_perm(q[14], q[15], sel), 0x5410);
     dst[k] = w;
   }
 }

@@ -513,7 +513,7 @@ static int answer_batch_impl(qpir_ctx* ctx, const uint32_t* Q, uint64_t B, uint6
   }
   {
     const uint32_t nq = Npad / 4;  // padded query slots
-    dim3 grid((nq + 127) / 128, (uint32_t)g.G);
+    dim3 grid((uint32_t)((g.G + 127) / 128), nq);
     limb_split_kernel<<<grid, 128, 0, st>>>(Qd, ar.limbs, (uint32_t)B, (uint32_t)g.m,
                                             (uint32_t)g.G, Npad, BN);
     LAUNCH_CHECK(ctx);
