@@ -683,12 +683,15 @@ def main():
     elif kind == "batch":
         scanned = db_bytes_local * world * B
         value = scanned / (ms_per_step / 1e3) / 1e9
-        ops = 2.0 * ell_local * n_cells * 4 * B
+        limbs = 3 if (wl.get("modp") and wl["modp"] <= (1 << 24)
+                      and os.environ.get("QPIR_MODP3", "1") != "0") else 4
+        ops = 2.0 * ell_local * n_cells * limbs * B  # int8 tensor ops actually executed
         achieved = ops / (k_ms / 1e3) / 1e12
         pk = 2.0 * bf16
         roof = {"bound": "tensor", "achieved": round(achieved, 1), "peak": pk, "unit": "TFLOP/s",
                 "frac": round(achieved / pk, 4), "traffic": None,
                 "kernel": "limb_split_kernel + mma_u8_limb_kernel (step time, upper bound)",
+                "limbs_per_query": limbs,
                 "kernel_ms": round(k_ms, 5),
                 "peak_source": f"{peak_src} bf16_tflops x 2 (nominal int8/bf16 ratio), int8 TOPS",
                 "algorithmic_ops_per_launch": ops}

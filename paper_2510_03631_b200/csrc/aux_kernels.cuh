@@ -66,14 +66,17 @@ __global__ void pack_records_kernel(PackArgs a) {
 // (n >= 4B or 16g + i >= m).  One MMA B tile (BN columns x 8 groups) is then
 // BN * 128 contiguous bytes.  One thread per (group g, query j): 64 B in,
 // 4 x 16 B out (64 B contiguous).
+// LPQ limbs per query (4 for Z_{2^32}; 3 for F_p with p < 2^24 after reducing
+// each entry mod p -- exact, since sum (q mod p) d = sum q d (mod p)).
+template <int LPQ>
 __global__ void limb_split_kernel(const uint32_t* __restrict__ Q, uint8_t* __restrict__ Qp,
                                   uint32_t B, uint32_t m, uint32_t G, uint32_t Npad,
-                                  uint32_t BN) {
+                                  uint32_t BN, uint32_t p) {
   // threads walk 16-cell groups of one query row (coalesced 64 B per thread);
-  // each thread writes its query's 4 limb rows = 64 contiguous bytes
+  // each thread writes its query's LPQ limb rows = 16 * LPQ contiguous bytes
   const uint32_t g = blockIdx.x * blockDim.x + threadIdx.x;
   const uint32_t jq = blockIdx.y;  // padded query index
-  if (g >= G || jq * 4u >= Npad) return;
+  if (g >= G || jq * (uint32_t)LPQ >= Npad) return;
   uint32_t q[16];
   const uint32_t c0 = g * 16u;
   const uint32_t* row = Q + (size_t)jq * m;
@@ -92,9 +95,13 @@ __global__ void limb_split_kernel(const uint32_t* __restrict__ Q, uint8_t* __res
 #pragma unroll
     for (int i = 0; i < 16; ++i) q[i] = (jq < B && c0 + i < m) ? __ldg(row + c0 + i) : 0u;
   }
-  uint4* dst = reinterpret_cast<uint4*>(Qp + limb_off(jq * 4u, g, G, BN));
+  if (p != 0) {
 #pragma unroll
-  for (uint32_t k = 0; k < 4; ++k) {
+    for (int i = 0; i < 16; ++i) q[i] %= p;
+  }
+  uint4* dst = reinterpret_cast<uint4*>(Qp + limb_off(jq * (uint32_t)LPQ, g, G, BN));
+#pragma unroll
+  for (uint32_t k = 0; k < (uint32_t)LPQ; ++k) {
     const uint32_t sel = k | ((k + 4) << 4);
     uint4 w;
     w.x = __byte_perm(__byte_perm(q[0], q[1], sel), __byte_perm(q[2], q[3], sel), 0x5410);

@@ -44,7 +44,9 @@ constexpr uint32_t MMA_THREADS = 192;
 // response bit is the parity of the s32 count, 32 consecutive bit-rows (one
 // warp's TMEM lanes) pack into one u32 of the response with __ballot_sync;
 // K-split partials combine with atomicXor.
-enum : int { OUT_QUERY_MAJOR = 0, OUT_ROW_MAJOR = 1, OUT_MODP = 2, OUT_PARITY = 3 };
+// OUT_MODP3: as OUT_MODP with 3 limbs per query (entries pre-reduced mod
+// p < 2^24 by the limb split), BN a multiple of 48: 25 % fewer MMAs.
+enum : int { OUT_QUERY_MAJOR = 0, OUT_ROW_MAJOR = 1, OUT_MODP = 2, OUT_PARITY = 3, OUT_MODP3 = 4 };
 
 struct MmaArgs {
   const uint8_t* A;   // D shard, 128-row panels [L/128][G][128][16]
@@ -198,7 +200,9 @@ __global__ void __launch_bounds__(MMA_THREADS, 1) mma_u8_limb_kernel(MmaArgs a) 
       for (uint32_t p = 0; p < MT; ++p) {
         const uint32_t row = (mt * MT + p) * MMA_BM + q * 32 + lane;
         const uint32_t taddr = tmem_base + ((q * 32u) << 16) + acc * C::ACC_COLS + p * BN;
-        constexpr uint32_t CH = BN < 64 ? BN : 64;  // columns per TMEM wait
+        // columns per TMEM wait (OUT_MODP3: 48 columns = 16 queries x 3 limbs)
+        constexpr uint32_t CH = OUT_MODE == OUT_MODP3 ? 48 : (BN < 64 ? BN : 64);
+        static_assert(BN % CH == 0, "BN must be a multiple of the epilogue chunk");
 #pragma unroll 1
         for (uint32_t cb = 0; cb < BN; cb += CH) {
           uint32_t v[CH];
@@ -206,6 +210,19 @@ __global__ void __launch_bounds__(MMA_THREADS, 1) mma_u8_limb_kernel(MmaArgs a) 
           for (uint32_t t = 0; t < CH / 16; ++t)
             tmem_ld_32x32b_x16_nowait(taddr + cb + 16 * t, *reinterpret_cast<uint32_t(*)[16]>(v + 16 * t));
           tmem_ld_wait();
+          if constexpr (OUT_MODE == OUT_MODP3) {
+            const uint32_t j0 = (nt * BN + cb) / 3;
+            if (row < a.rows) {
+#pragma unroll
+              for (uint32_t jj = 0; jj < 16; ++jj) {
+                const unsigned long long x = (unsigned long long)v[3 * jj] +
+                                             ((unsigned long long)v[3 * jj + 1] << 8) +
+                                             ((unsigned long long)v[3 * jj + 2] << 16);
+                if (j0 + jj < a.n_out)
+                  atomicAdd(a.out64 + (size_t)(j0 + jj) * a.out_ld + row, x % a.p);
+              }
+            }
+          } else {
 #pragma unroll
           for (uint32_t t = 0; t < CH / 16; ++t) {
             const uint32_t c0 = cb + 16 * t;
@@ -266,6 +283,7 @@ __global__ void __launch_bounds__(MMA_THREADS, 1) mma_u8_limb_kernel(MmaArgs a) 
             }
             }  // OUT_MODE != OUT_MODP
           }
+          }  // OUT_MODE != OUT_MODP3
         }
       }
       tc_fence_before();

@@ -29,6 +29,14 @@ struct MmaJob {
   int gpb = 8;           // column groups per pipeline stage (4 or 8)
 };
 
+// BN for 3 limbs per query (OUT_MODP3): a multiple of 48 so queries never
+// straddle a tile.
+inline uint32_t mma_pick_bn3(uint64_t ncols) {
+  if (ncols <= 48) return 48;
+  if (ncols <= 96) return 96;
+  return 192;
+}
+
 inline uint32_t mma_pick_bn(uint64_t ncols) {
   if (ncols <= 16) return 16;
   if (ncols <= 32) return 32;
@@ -74,8 +82,9 @@ cudaError_t mma_launch_cfg(const MmaJob& j, cudaStream_t st, uint64_t* launches)
   a.m_tiles = j.L / (MMA_BM * MT);
   a.n_tiles = j.Npad / BN;
   const uint32_t kblocks = j.G / GPB;
-  // OUT_MODP: each split's limb sums must stay exact in u32 (<= 66051 cells)
-  const uint32_t max_kps = MODE == OUT_MODP ? 66048u / (16u * GPB) : kblocks;
+  // OUT_MODP(3): each split's limb sums must stay exact in u32 (<= 66051 cells)
+  constexpr bool modp = MODE == OUT_MODP || MODE == OUT_MODP3;
+  const uint32_t max_kps = modp ? 66048u / (16u * GPB) : kblocks;
   const uint32_t min_splits = (kblocks + max_kps - 1) / max_kps;
   a.splits = mma_choose_splits(a.m_tiles * a.n_tiles, kblocks, (uint32_t)j.num_sms,
                                j.forced_split, min_splits);
@@ -84,7 +93,7 @@ cudaError_t mma_launch_cfg(const MmaJob& j, cudaStream_t st, uint64_t* launches)
   a.p = j.p;
   a.out64 = j.out64;
   cudaError_t e = cudaSuccess;
-  if (MODE == OUT_MODP)
+  if (modp)
     e = cudaMemsetAsync(j.out64, 0, j.out_elems * 8, st);
   else if (a.splits > 1)
     e = cudaMemsetAsync(j.out, 0, j.out_elems * 4, st);
@@ -98,7 +107,7 @@ cudaError_t mma_launch_cfg(const MmaJob& j, cudaStream_t st, uint64_t* launches)
   ++*launches;
   e = cudaGetLastError();
   if (e != cudaSuccess) return e;
-  if (MODE == OUT_MODP) {
+  if (modp) {
     const uint32_t blocks = (uint32_t)std::min<uint64_t>((j.out_elems + 255) / 256, 4096);
     modp_fixup_kernel<<<blocks, 256, 0, st>>>(j.out64, j.out, j.out_elems, j.p);
     ++*launches;
@@ -118,13 +127,22 @@ cudaError_t mma_launch(const MmaJob& j, cudaStream_t st, uint64_t* launches) {
                  : mma_launch_cfg<BNV, 1, 4, MODE>(j, st, launches);                 \
     return mt2 ? mma_launch_cfg<BNV, 2, 8, MODE>(j, st, launches)                    \
                : mma_launch_cfg<BNV, 1, 8, MODE>(j, st, launches);
-  switch (j.BN) {
-    QPIR_MMA_CASE(16)
-    QPIR_MMA_CASE(32)
-    QPIR_MMA_CASE(64)
-    QPIR_MMA_CASE(128)
-    default:
-      QPIR_MMA_CASE(256)
+  if constexpr (MODE == OUT_MODP3) {
+    switch (j.BN) {
+      QPIR_MMA_CASE(48)
+      QPIR_MMA_CASE(96)
+      default:
+        QPIR_MMA_CASE(192)
+    }
+  } else {
+    switch (j.BN) {
+      QPIR_MMA_CASE(16)
+      QPIR_MMA_CASE(32)
+      QPIR_MMA_CASE(64)
+      QPIR_MMA_CASE(128)
+      default:
+        QPIR_MMA_CASE(256)
+    }
   }
 #undef QPIR_MMA_CASE
 }

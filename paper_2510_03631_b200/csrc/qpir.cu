@@ -79,6 +79,7 @@ struct qpir_ctx {
   int mma_mt = 2;      // env QPIR_MMA_MT (1 or 2 row panels per CTA tile)
   int mma_split = 0;   // env QPIR_MMA_SPLIT (0 = auto)
   int mma_gpb = 8;     // env QPIR_MMA_GPB (column groups per pipeline stage: 4 or 8)
+  int modp3 = 1;       // env QPIR_MODP3 (3 limbs per query for p < 2^24)
   std::string err;
 };
 
@@ -362,6 +363,7 @@ int qpir_setup(const qpir_params* params, const uint8_t* records, uint64_t recor
   ctx->mma_mt = env_int("QPIR_MMA_MT", 2);
   ctx->mma_split = env_int("QPIR_MMA_SPLIT", 0);
   ctx->mma_gpb = env_int("QPIR_MMA_GPB", 8);
+  ctx->modp3 = env_int("QPIR_MODP3", 1);
   cudaStream_t st = (cudaStream_t)stream;
   auto bail = [&](int code) {
     g_setup_error = ctx->err;
@@ -492,8 +494,11 @@ static int answer_batch_impl(qpir_ctx* ctx, const uint32_t* Q, uint64_t B, uint6
   cudaStream_t st = (cudaStream_t)stream;
   const int wq = where(Q, ctx->device), wa = where(ans_local, ctx->device);
   if (wq < 0 || wa < 0) return fail(ctx, QPIR_E_PARAM, "Q/ans_local: memory of another device");
-  const uint64_t ncols = 4 * B;
-  const uint32_t BN = mma_pick_bn(ncols);
+  // F_p with p < 2^24: 3 limbs per query after reducing entries mod p
+  const bool three = p != 0 && p <= (1u << 24) && ctx->modp3;
+  const uint32_t LPQ = three ? 3u : 4u;
+  const uint64_t ncols = LPQ * B;
+  const uint32_t BN = three ? mma_pick_bn3(ncols) : mma_pick_bn(ncols);
   const uint32_t Npad = (uint32_t)round_up(ncols, BN);
   Arena& ar = arena_for(ctx, st);
   int rc = ensure(ctx, (void**)&ar.limbs, &ar.limbs_bytes, (uint64_t)Npad * g.m_pad);
@@ -512,10 +517,14 @@ static int answer_batch_impl(qpir_ctx* ctx, const uint32_t* Q, uint64_t B, uint6
     out = ar.big_out;
   }
   {
-    const uint32_t nq = Npad / 4;  // padded query slots
+    const uint32_t nq = Npad / LPQ;  // padded query slots
     dim3 grid((uint32_t)((g.G + 127) / 128), nq);
-    limb_split_kernel<<<grid, 128, 0, st>>>(Qd, ar.limbs, (uint32_t)B, (uint32_t)g.m,
-                                            (uint32_t)g.G, Npad, BN);
+    if (three)
+      limb_split_kernel<3><<<grid, 128, 0, st>>>(Qd, ar.limbs, (uint32_t)B, (uint32_t)g.m,
+                                                 (uint32_t)g.G, Npad, BN, p);
+    else
+      limb_split_kernel<4><<<grid, 128, 0, st>>>(Qd, ar.limbs, (uint32_t)B, (uint32_t)g.m,
+                                                 (uint32_t)g.G, Npad, BN, 0u);
     LAUNCH_CHECK(ctx);
   }
   if (p == 0) {
@@ -524,8 +533,12 @@ static int answer_batch_impl(qpir_ctx* ctx, const uint32_t* Q, uint64_t B, uint6
   } else {
     rc = ensure(ctx, (void**)&ar.acc64, &ar.acc64_bytes, len_ans * 8);
     if (rc) return rc;
-    rc = launch_mma<OUT_MODP>(ctx, BN, ar.limbs, Npad, out, (uint32_t)B,
-                              (uint32_t)g.ell_local, len_ans, st, p, ar.acc64);
+    if (three)
+      rc = launch_mma<OUT_MODP3>(ctx, BN, ar.limbs, Npad, out, (uint32_t)B,
+                                 (uint32_t)g.ell_local, len_ans, st, p, ar.acc64);
+    else
+      rc = launch_mma<OUT_MODP>(ctx, BN, ar.limbs, Npad, out, (uint32_t)B,
+                                (uint32_t)g.ell_local, len_ans, st, p, ar.acc64);
   }
   if (rc) return rc;
   if (wa == 0) {
