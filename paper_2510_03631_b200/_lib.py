@@ -104,7 +104,7 @@ for _name in EXPORTS:
 
 
 def _addr(x) -> int | None:
-    """(address, element count) of a buffer without copying."""
+    """Raw address of a buffer (torch tensor, numpy array or int) without copying."""
     if x is None:
         return None
     if isinstance(x, int):

@@ -101,7 +101,7 @@ struct GemvArgs {
   uint32_t* partial;    // [S][L] scratch (S > 1)
   uint32_t* tickets;    // [gridDim.x] zero-initialised, self-resetting
   uint32_t ell_local;   // rows to write
-  uint32_t L;           // padded rows (row stride of a column group)
+  uint32_t L;           // padded rows (stride of one split's partial vector)
   uint32_t m;           // columns (cells)
   uint32_t G;           // column groups (multiple of UNR)
   uint32_t gps;         // groups per split (multiple of UNR)

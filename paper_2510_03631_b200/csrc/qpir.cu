@@ -69,11 +69,11 @@ struct qpir_ctx {
   std::mutex mu;                   // guards `arenas`
   std::map<cudaStream_t, Arena> arenas;
   uint64_t launches = 0;
-  // GEMV tuning (env QPIR_GEMV_U / QPIR_GEMV_SPLIT / QPIR_GEMV_CHUNK)
-  int gemv_u = 2;
-  int gemv_split = 0;  // 0 = auto
-  int gemv_chunk = 512;
-  int gemv_unroll = 4;
+  // Tuning knobs, read once from the environment at setup (sweeps in profiles/):
+  int gemv_u = 2;       // env QPIR_GEMV_U: rows per thread (1, 2, 4)
+  int gemv_split = 0;   // env QPIR_GEMV_SPLIT: K splits (0 = auto)
+  int gemv_chunk = 512; // env QPIR_GEMV_CHUNK: column groups staged in smem at a time
+  int gemv_unroll = 4;  // env QPIR_GEMV_UNROLL: column groups in flight (4 or 8)
   int gemv_order = 0;  // env QPIR_GEMV_ORDER (1 = split-major grid)
   int gemv_pdl = 1;    // env QPIR_GEMV_PDL (programmatic dependent launch of back-to-back GEMVs)
   int mma_mt = 2;      // env QPIR_MMA_MT (1 or 2 row panels per CTA tile)
