@@ -18,6 +18,7 @@
 #include "../../include/qpir.h"
 #include "aux_kernels.cuh"
 #include "gemv.cuh"
+#include "gemv_tma.cuh"
 #include "host_common.h"
 #include "mma_launch.cuh"
 
@@ -76,6 +77,7 @@ struct qpir_ctx {
   int gemv_unroll = 4;  // env QPIR_GEMV_UNROLL: column groups in flight (4 or 8)
   int gemv_order = 0;  // env QPIR_GEMV_ORDER (1 = split-major grid)
   int gemv_pdl = 1;    // env QPIR_GEMV_PDL (programmatic dependent launch of back-to-back GEMVs)
+  int gemv_impl = 0;   // env QPIR_GEMV_IMPL: 0 = SIMT split-K kernel, 1 = persistent TMA-fed
   int mma_mt = 2;      // env QPIR_MMA_MT (1 or 2 row panels per CTA tile)
   int mma_split = 0;   // env QPIR_MMA_SPLIT (0 = auto)
   int mma_gpb = 8;     // env QPIR_MMA_GPB (column groups per pipeline stage: 4 or 8)
@@ -281,7 +283,29 @@ int launch_gemv(qpir_ctx* ctx, const uint32_t* qu, uint32_t* ans, cudaStream_t s
   return QPIR_OK;
 }
 
+// Persistent TMA-fed GEMV (gemv_tma.cuh): stream-K over (panel pair, K-block).
+int launch_gemv_tma(qpir_ctx* ctx, const uint32_t* qu, uint32_t* ans, cudaStream_t st) {
+  const Geometry& g = ctx->geo;
+  GemvTmaArgs a;
+  a.D = ctx->D;
+  a.qu = qu;
+  a.ans = ans;
+  a.ell_local = (uint32_t)g.ell_local;
+  a.m = (uint32_t)g.m;
+  a.G = (uint32_t)g.G;
+  a.pairs = (uint32_t)((g.ell_local + 255) / 256);
+  a.iters = (uint64_t)a.pairs * (g.G / GT_GROUPS);
+  CUDA_TRY(ctx, cudaMemsetAsync(ans, 0, g.ell_local * 4, st));
+  const uint32_t grid = (uint32_t)std::min<uint64_t>(a.iters, (uint64_t)ctx->num_sms);
+  CUDA_TRY(ctx, cudaFuncSetAttribute(gemv_tma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     (int)GT_SMEM));
+  gemv_tma_kernel<<<grid, GT_THREADS, GT_SMEM, st>>>(a);
+  LAUNCH_CHECK(ctx);
+  return QPIR_OK;
+}
+
 int gemv(qpir_ctx* ctx, const uint32_t* qu, uint32_t* ans, cudaStream_t st) {
+  if (ctx->gemv_impl == 1) return launch_gemv_tma(ctx, qu, ans, st);
   const bool u8 = ctx->gemv_unroll == 8;
   switch (ctx->gemv_u) {
     case 1: return u8 ? launch_gemv<1, 8>(ctx, qu, ans, st) : launch_gemv<1, 4>(ctx, qu, ans, st);
@@ -360,6 +384,7 @@ int qpir_setup(const qpir_params* params, const uint8_t* records, uint64_t recor
   ctx->gemv_unroll = env_int("QPIR_GEMV_UNROLL", 4);
   ctx->gemv_order = env_int("QPIR_GEMV_ORDER", 0);
   ctx->gemv_pdl = env_int("QPIR_GEMV_PDL", 1);
+  ctx->gemv_impl = env_int("QPIR_GEMV_IMPL", 0);
   ctx->mma_mt = env_int("QPIR_MMA_MT", 2);
   ctx->mma_split = env_int("QPIR_MMA_SPLIT", 0);
   ctx->mma_gpb = env_int("QPIR_MMA_GPB", 8);

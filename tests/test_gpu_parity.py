@@ -62,7 +62,8 @@ RAGGED = [
 @pytest.mark.parametrize("cfg", [dict(), dict(QPIR_GEMV_U="1", QPIR_GEMV_SPLIT="3", QPIR_GEMV_CHUNK="8"),
                                  dict(QPIR_GEMV_U="4", QPIR_GEMV_SPLIT="1", QPIR_GEMV_CHUNK="4"),
                                  dict(QPIR_GEMV_ORDER="1", QPIR_GEMV_SPLIT="5", QPIR_GEMV_UNROLL="8"),
-                                 dict(QPIR_MMA_MT="1", QPIR_MMA_SPLIT="3")])
+                                 dict(QPIR_MMA_MT="1", QPIR_MMA_SPLIT="3"),
+                                 dict(QPIR_GEMV_IMPL="1")])
 def test_answer_ragged(cuda_ok, geo, cfg, monkeypatch):
     for k, v in cfg.items():
         monkeypatch.setenv(k, v)
@@ -302,7 +303,8 @@ def test_c5_hint_shard_sampled(cuda_ok):
     s.close()
 
 
-@pytest.mark.parametrize("cfg", [dict(), dict(QPIR_GEMV_SPLIT="7"), dict(QPIR_GEMV_PDL="0")])
+@pytest.mark.parametrize("cfg", [dict(), dict(QPIR_GEMV_SPLIT="7"), dict(QPIR_GEMV_PDL="0"),
+                                 dict(QPIR_GEMV_IMPL="1")])
 def test_back_to_back_answers_pdl(cuda_ok, cfg, monkeypatch):
     """Back-to-back GEMVs on one stream overlap under programmatic dependent
     launch; split-K scratch and outputs must not race (every answer exact)."""
