@@ -117,8 +117,9 @@ __global__ void limb_split_kernel(const uint32_t* __restrict__ Q, uint8_t* __res
 // (group g, Philox block jb = j >> 2): 16 Philox calls, 256 contiguous bytes out.
 __global__ void expand_A_limbs_kernel(uint8_t* __restrict__ Ap, uint64_t seed, uint32_t m,
                                       uint32_t n, uint32_t G, uint32_t Npad, uint32_t BN) {
-  const uint32_t jb = blockIdx.x * blockDim.x + threadIdx.x;
-  const uint32_t g = blockIdx.y;
+  // grid.x = column groups (up to 2^31), grid.y = blocks of Philox columns
+  const uint32_t jb = blockIdx.y * blockDim.x + threadIdx.x;
+  const uint32_t g = blockIdx.x;
   if (jb * 16u >= Npad) return;
   const uint2 key = make_uint2((uint32_t)seed, (uint32_t)(seed >> 32));
   uint32_t a[16][4];

@@ -296,9 +296,10 @@ __global__ void ens_bitplane_pack_kernel(const uint8_t* __restrict__ R, uint64_t
 __global__ void ens_share_expand_kernel(const uint8_t* __restrict__ Q, uint32_t B, uint64_t r,
                                         uint64_t nb, uint8_t* __restrict__ Qb, uint32_t G,
                                         uint32_t Npad, uint32_t BN) {
-  const uint32_t q = blockIdx.x * blockDim.x + threadIdx.x;
-  const uint32_t g = blockIdx.y;
-  if (q >= Npad) return;
+  // grid.x = 16-record groups (up to 2^31), grid.y = share slots
+  const uint32_t g = blockIdx.x * blockDim.x + threadIdx.x;
+  const uint32_t q = blockIdx.y;
+  if (q >= Npad || g >= G) return;
   uint32_t bits = 0;
   if (q < B) {
     const uint64_t b0 = (uint64_t)g * 2;

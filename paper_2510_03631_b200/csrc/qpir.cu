@@ -236,6 +236,7 @@ int launch_gemv(qpir_ctx* ctx, const uint32_t* qu, uint32_t* ans, cudaStream_t s
       }
   }
   S = std::max<uint32_t>(1, std::min<uint32_t>(S, (uint32_t)(g.G / UNR)));
+  S = std::min<uint32_t>(S, 65535u);  // grid.y limit
   uint32_t gps = (uint32_t)round_up((g.G + S - 1) / S, UNR);
   S = (uint32_t)((g.G + gps - 1) / gps);
   uint32_t chunk = (uint32_t)std::max(UNR, ctx->gemv_chunk / UNR * UNR);
@@ -477,6 +478,8 @@ int qpir_answer(qpir_ctx* ctx, const uint32_t* qu, uint64_t len_qu, uint32_t* an
   cudaStream_t st = (cudaStream_t)stream;
   const int wq = where(qu, ctx->device), wa = where(ans_local, ctx->device);
   if (wq < 0 || wa < 0) return fail(ctx, QPIR_E_PARAM, "qu/ans_local: memory of another device");
+  if ((reinterpret_cast<uintptr_t>(qu) & 3u) || (reinterpret_cast<uintptr_t>(ans_local) & 3u))
+    return fail(ctx, QPIR_E_PARAM, "qu/ans_local: not 4-byte aligned");
   Arena& ar = arena_for(ctx, st);
   int rc = QPIR_OK;
   const uint32_t* qd = qu;
@@ -506,9 +509,9 @@ static int answer_batch_impl(qpir_ctx* ctx, const uint32_t* Q, uint64_t B, uint6
                              uint32_t* ans_local, uint64_t len_ans, void* stream, uint32_t p) {
   if (!ctx) return fail(nullptr, QPIR_E_STATE, "ctx: NULL");
   const Geometry& g = ctx->geo;
-  if (!Q || !ans_local) return fail(ctx, QPIR_E_PARAM, "Q/ans_local: NULL");
   if (B == 0 || B > 4096) return fail(ctx, QPIR_E_PARAM, "B: %llu not in [1, 4096]",
                                       (unsigned long long)B);
+  if (!Q || !ans_local) return fail(ctx, QPIR_E_PARAM, "Q/ans_local: NULL");
   if (len_Q != B * g.m)
     return fail(ctx, QPIR_E_DIMENSION, "len_Q: %llu != B*m %llu", (unsigned long long)len_Q,
                 (unsigned long long)(B * g.m));
@@ -519,6 +522,8 @@ static int answer_batch_impl(qpir_ctx* ctx, const uint32_t* Q, uint64_t B, uint6
   cudaStream_t st = (cudaStream_t)stream;
   const int wq = where(Q, ctx->device), wa = where(ans_local, ctx->device);
   if (wq < 0 || wa < 0) return fail(ctx, QPIR_E_PARAM, "Q/ans_local: memory of another device");
+  if ((reinterpret_cast<uintptr_t>(Q) & 3u) || (reinterpret_cast<uintptr_t>(ans_local) & 3u))
+    return fail(ctx, QPIR_E_PARAM, "Q/ans_local: not 4-byte aligned");
   // F_p with p < 2^24: 3 limbs per query after reducing entries mod p
   const bool three = p != 0 && p <= (1u << 24) && ctx->modp3;
   const uint32_t LPQ = three ? 3u : 4u;
@@ -596,6 +601,8 @@ int qpir_hint(qpir_ctx* ctx, uint32_t* H_local, uint64_t len_H, void* stream) {
   cudaStream_t st = (cudaStream_t)stream;
   const int wh = where(H_local, ctx->device);
   if (wh < 0) return fail(ctx, QPIR_E_PARAM, "H_local: memory of another device");
+  if (reinterpret_cast<uintptr_t>(H_local) & 3u)
+    return fail(ctx, QPIR_E_PARAM, "H_local: not 4-byte aligned");
   const uint64_t ncols = 4ull * g.lwe_n;
   const uint32_t BN = mma_pick_bn(ncols);
   const uint32_t Npad = (uint32_t)round_up(ncols, BN);
@@ -610,7 +617,7 @@ int qpir_hint(qpir_ctx* ctx, uint32_t* H_local, uint64_t len_H, void* stream) {
   }
   {
     const uint32_t nb = Npad / 16;  // Philox blocks (4 outputs x 4 limbs)
-    dim3 grid((nb + 127) / 128, (uint32_t)g.G);
+    dim3 grid((uint32_t)g.G, (nb + 127) / 128);
     expand_A_limbs_kernel<<<grid, 128, 0, st>>>(ar.limbs, g.seed_A, (uint32_t)g.m, g.lwe_n,
                                                 (uint32_t)g.G, Npad, BN);
     LAUNCH_CHECK(ctx);

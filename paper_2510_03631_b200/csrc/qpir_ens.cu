@@ -303,8 +303,8 @@ int qpir_oop_preprocess(qpir_ens_ctx* ctx, uint32_t n_chunks, uint32_t server,
                     (unsigned long long)ctx->r);
   if (server >= n_chunks) return ENS_FAIL(ctx, QPIR_E_PARAM, "server: %u >= n_chunks", server);
   if (!seeds || !A_out) return ENS_FAIL(ctx, QPIR_E_PARAM, "seeds/A_out: NULL");
-  if (n_seeds == 0 || n_seeds > 65536)
-    return ENS_FAIL(ctx, QPIR_E_PARAM, "n_seeds: %llu not in [1, 65536]", (unsigned long long)n_seeds);
+  if (n_seeds == 0 || n_seeds > 65535)
+    return ENS_FAIL(ctx, QPIR_E_PARAM, "n_seeds: %llu not in [1, 65535]", (unsigned long long)n_seeds);
   if (len_A != n_seeds * ctx->d)
     return ENS_FAIL(ctx, QPIR_E_DIMENSION, "len_A: %llu != n_seeds*d %llu", (unsigned long long)len_A,
                     (unsigned long long)(n_seeds * ctx->d));
@@ -360,7 +360,7 @@ static int ens_batch_tc(qpir_ens_ctx* ctx, const uint8_t* Qd, uint64_t B, cudaSt
   int rc = grow(ctx, (void**)&ctx->Qb, &ctx->Qb_bytes, Npad * m_pad);
   if (rc) return rc;
   {
-    dim3 grid((uint32_t)((Npad + 127) / 128), (uint32_t)G);
+    dim3 grid((uint32_t)((G + 127) / 128), (uint32_t)Npad);
     ens_share_expand_kernel<<<grid, 128, 0, st>>>(Qd, (uint32_t)B, ctx->r, (ctx->r + 7) / 8,
                                                   ctx->Qb, (uint32_t)G, (uint32_t)Npad, BN);
     ENS_LAUNCHED(ctx);
@@ -413,7 +413,7 @@ int qpir_ens_answer_batch(qpir_ens_ctx* ctx, const uint8_t* shares, uint64_t B,
     if (rc) return rc;
   }
   // tensor cores for larger batches when the bit-planes fit in HBM
-  const bool want_tc = ctx->tc == 1 || (ctx->tc < 0 && B >= 32);
+  const bool want_tc = (ctx->tc == 1 || (ctx->tc < 0 && B >= 32)) && B <= 65280;  // grid.y
   if (want_tc) {
     bool used = false;
     rc = ens_batch_tc(ctx, Qd, B, st, &used);

@@ -357,3 +357,29 @@ def test_concurrent_streams_have_private_scratch(cuda_ok, monkeypatch):
         torch.cuda.synchronize()
         for out, want, _ in jobs:
             assert (_u32(out) == want).all()
+
+
+def test_errors_name_the_field(cuda_ok):
+    """Lengths, alignment and foreign pointers are rejected with the field named
+    and nothing written (QPIR_E_DIMENSION / QPIR_E_PARAM)."""
+    P = _srv()
+    from paper_2510_03631_b200 import _lib as L
+    n_cells, n_ch, d = 512, 2, 16
+    rec, D = _db(n_cells, n_ch, d, seed=70)
+    with P.PirServer(n_cells, n_ch, d, records=rec) as s:
+        with pytest.raises(P.QpirError) as ei:
+            s.answer(np.zeros(n_cells - 1, np.uint32))
+        assert ei.value.code == L.QPIR_E_DIMENSION and "m:" in str(ei.value)
+        raw = torch.zeros(4 * n_cells + 4, dtype=torch.uint8, device="cuda")
+        out = torch.empty(s.ell_local, dtype=torch.int32, device="cuda")
+        rc = L._L.qpir_answer(s._ctx, raw.data_ptr() + 1, n_cells, out.data_ptr(), s.ell_local,
+                              None)
+        with pytest.raises(P.QpirError) as ei:
+            L._check(rc, s._ctx)
+        assert ei.value.code == L.QPIR_E_PARAM and "aligned" in str(ei.value)
+        with pytest.raises(P.QpirError) as ei:
+            s.answer_batch(np.zeros((0, n_cells), np.uint32))
+        assert ei.value.code == L.QPIR_E_PARAM and "B:" in str(ei.value)
+        # the context is still usable after errors
+        q = synth.uniform_u32_np(71, (n_cells,))
+        assert (_u32(s.answer(q)) == O.answer(D, q)).all()
