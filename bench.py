@@ -596,11 +596,11 @@ def main():
             h_out = torch.empty((B, srv.ell if world > 1 else ell_local), dtype=torch.int32).pin_memory()
         e2e_steps = max(3, min(args.steps, 200 if kind == "answer" else 10))
         dev_out = out
-        two = kind == "answer" and world == 1
+        two = world == 1  # answers and batches: D2H overlapped on a copy stream
         if two:
-            # every step: pinned-host query -> H2D (inside qpir_answer) -> GEMV on
-            # the compute stream (kernels stay serialised) -> answer D2H to pinned
-            # host on a copy stream, overlapping the next step's kernel
+            # every step: pinned-host query (batch) -> H2D (inside the C call) ->
+            # kernels on the compute stream (kept serialised) -> answer D2H to
+            # pinned host on a copy stream, overlapping the next step's kernels
             copy_stream = torch.cuda.Stream(dev)
             h_ins = [h_in, torch.empty_like(h_in).pin_memory()]
             h_ins[1].copy_(qs[1].cpu())
@@ -615,7 +615,12 @@ def main():
                 b = i % 2
                 if c_used[b]:
                     stream.wait_event(c_ev[b])  # slot's previous D2H has read it
-                srv.answer(h_ins[b], out=d_outs[b], stream=stream)
+                if kind == "answer":
+                    srv.answer(h_ins[b], out=d_outs[b], stream=stream)
+                elif wl.get("modp"):
+                    srv.answer_batch_modp(h_ins[b], wl["modp"], out=d_outs[b], stream=stream)
+                else:
+                    srv.answer_batch(h_ins[b], out=d_outs[b], stream=stream)
                 k_ev[b].record(stream)
                 copy_stream.wait_event(k_ev[b])
                 with torch.cuda.stream(copy_stream):
@@ -657,7 +662,7 @@ def main():
                "d2h_bytes_per_step": int(h_out.numel() * 4), "steps": e2e_steps,
                "ms_per_step": round(te / e2e_steps, 4),
                "path": ("D2H overlapped with the next kernel on a copy stream: "
-                        if (kind == "answer" and world == 1) else "")
+                        if world == 1 else "")
                        + "qpir_answer with pinned host query (H2D inside the C call) "
                        + ("+ NCCL all-gather " if world > 1 else "") + "+ D2H of the answer "
                        "to pinned host, every step"}

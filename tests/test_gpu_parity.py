@@ -383,3 +383,27 @@ def test_errors_name_the_field(cuda_ok):
         # the context is still usable after errors
         q = synth.uniform_u32_np(71, (n_cells,))
         assert (_u32(s.answer(q)) == O.answer(D, q)).all()
+
+
+@pytest.mark.slow
+def test_next_rows_full_size_sampled(cuda_ok):
+    """configs[1]-sized record set (327680 paper-shaped 3 KB records = 1.007 GB):
+    FTR (3-limb tcgen05, mod 65537) and the bit-plane tensor-core ENS batch, every
+    query exact on 24 sampled record-byte columns (the oracle on those columns)."""
+    P = _srv()
+    n_cells, n_ch, d = 8192, 40, 3072
+    r = n_cells * n_ch
+    seed = 81
+    rec_dev = synth.records(seed, 0, r, d, n_ch, device="cuda")
+    rng = np.random.default_rng(3)
+    cols = np.sort(np.concatenate([[0, 13, 596, d - 1], rng.choice(d, 20, replace=False)]))
+    rec_cols = rec_dev[:, torch.from_numpy(cols).cuda()].cpu().numpy()
+    with P.FtrServer(r, d, records=rec_dev) as f:
+        Q = synth.uniform_u32_np(82, (16, r)) % 65537
+        got = P.u32(f.answer_batch(Q))[:, cols]
+        assert (got == O.ftr_respond_batch(rec_cols, Q)).all()
+    with P.EnsServer(r, d, records=rec_dev) as e:
+        nb = (r + 7) // 8
+        Qs = synth.uniform_u8_np(83, (48, nb))
+        got = e.answer_batch(Qs).cpu().numpy()[:, cols]
+        assert (got == O.ens_respond_batch(rec_cols, Qs)).all()
