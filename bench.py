@@ -720,6 +720,17 @@ def main():
             roof["frac_sustained"] = round(achieved / (2.0 * bf16_sus), 4)
         qps = None
         unit = "TOPS (int8)"
+    ctx_peaks = os.path.join(ROOT, "profiles", "r01_context_peaks.json")
+    if os.path.exists(ctx_peaks) and roof.get("bound") in ("hbm", "tensor"):
+        try:
+            cp = json.load(open(ctx_peaks))
+            if roof["bound"] == "hbm":
+                roof["context_read_only_stream_gbs"] = cp.get("hbm_read_only_gbs")
+            else:
+                roof["context_cublaslt_int8_tops"] = {k: v for k, v in cp.items()
+                                                      if k.startswith("int_mm") and k.endswith("tops")}
+        except Exception:
+            pass
     prof = os.path.join(ROOT, "profiles", f"traffic_{args.workload}.json")
     if os.path.exists(prof):
         try:
