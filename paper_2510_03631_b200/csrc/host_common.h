@@ -8,7 +8,16 @@
 #include <cstdlib>
 #include <string>
 
+#include <nvtx3/nvToolsExt.h>
+
 namespace qpir_host {
+
+// NVTX range for the duration of a C-ABI call (visible in Nsight Systems /
+// Compute timelines; header-only nvtx3, no-op without a profiler attached).
+struct NvtxRange {
+  explicit NvtxRange(const char* name) { nvtxRangePushA(name); }
+  ~NvtxRange() { nvtxRangePop(); }
+};
 
 inline uint64_t round_up(uint64_t x, uint64_t a) { return (x + a - 1) / a * a; }
 

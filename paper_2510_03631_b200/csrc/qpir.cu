@@ -351,6 +351,7 @@ extern "C" {
 
 int qpir_setup(const qpir_params* params, const uint8_t* records, uint64_t records_len,
                void* stream, qpir_ctx** out) {
+  NvtxRange nvtx_("qpir_setup");
   g_setup_error.clear();
   if (!out) return fail(nullptr, QPIR_E_PARAM, "out: NULL");
   *out = nullptr;
@@ -420,6 +421,7 @@ int qpir_setup(const qpir_params* params, const uint8_t* records, uint64_t recor
 
 int qpir_db_write(qpir_ctx* ctx, uint64_t theta_begin, uint64_t n_records,
                   const uint8_t* records, uint64_t records_len, void* stream) {
+  NvtxRange nvtx_("qpir_db_write");
   if (!ctx) return fail(nullptr, QPIR_E_STATE, "ctx: NULL");
   const Geometry& g = ctx->geo;
   const uint64_t n_all = g.n_cells * g.n_ch;
@@ -465,6 +467,7 @@ int qpir_geometry(const qpir_ctx* ctx, uint64_t* ell, uint64_t* m, uint64_t* ell
 
 int qpir_answer(qpir_ctx* ctx, const uint32_t* qu, uint64_t len_qu, uint32_t* ans_local,
                 uint64_t len_ans, void* stream) {
+  NvtxRange nvtx_("qpir_answer");
   if (!ctx) return fail(nullptr, QPIR_E_STATE, "ctx: NULL");
   const Geometry& g = ctx->geo;
   if (!qu || !ans_local) return fail(ctx, QPIR_E_PARAM, "qu/ans_local: NULL");
@@ -507,6 +510,7 @@ int qpir_answer(qpir_ctx* ctx, const uint32_t* qu, uint64_t len_qu, uint32_t* an
 
 static int answer_batch_impl(qpir_ctx* ctx, const uint32_t* Q, uint64_t B, uint64_t len_Q,
                              uint32_t* ans_local, uint64_t len_ans, void* stream, uint32_t p) {
+  NvtxRange nvtx_(p ? "qpir_answer_batch_modp" : "qpir_answer_batch");
   if (!ctx) return fail(nullptr, QPIR_E_STATE, "ctx: NULL");
   const Geometry& g = ctx->geo;
   if (B == 0 || B > 4096) return fail(ctx, QPIR_E_PARAM, "B: %llu not in [1, 4096]",
@@ -591,6 +595,7 @@ int qpir_answer_batch_modp(qpir_ctx* ctx, const uint32_t* Q, uint64_t B, uint64_
 }
 
 int qpir_hint(qpir_ctx* ctx, uint32_t* H_local, uint64_t len_H, void* stream) {
+  NvtxRange nvtx_("qpir_hint");
   if (!ctx) return fail(nullptr, QPIR_E_STATE, "ctx: NULL");
   const Geometry& g = ctx->geo;
   if (!H_local) return fail(ctx, QPIR_E_PARAM, "H_local: NULL");

@@ -107,6 +107,7 @@ extern "C" {
 
 int qpir_ens_setup(const qpir_ens_params* p, const uint8_t* records, uint64_t records_len,
                    void* stream, qpir_ens_ctx** out) {
+  NvtxRange nvtx_("qpir_ens_setup");
   g_ens_setup_error.clear();
   if (!out) return set_error(&g_ens_setup_error, QPIR_E_PARAM, "out: NULL");
   *out = nullptr;
@@ -160,6 +161,7 @@ int qpir_ens_setup(const qpir_ens_params* p, const uint8_t* records, uint64_t re
 
 int qpir_ens_db_write(qpir_ens_ctx* ctx, uint64_t theta_begin, uint64_t n_records,
                       const uint8_t* records, uint64_t records_len, void* stream) {
+  NvtxRange nvtx_("qpir_ens_db_write");
   if (!ctx) return QPIR_E_STATE;
   if (theta_begin > ctx->r || n_records > ctx->r - theta_begin)
     return ENS_FAIL(ctx, QPIR_E_DIMENSION, "theta range: [%llu, +%llu) exceeds %llu records",
@@ -238,6 +240,7 @@ static int scan_range(qpir_ens_ctx* ctx, const uint8_t* share_dev, uint64_t row_
 
 int qpir_ens_answer(qpir_ens_ctx* ctx, const uint8_t* share, uint64_t len_share, uint8_t* out,
                     uint64_t len_out, void* stream) {
+  NvtxRange nvtx_("qpir_ens_answer");
   if (!ctx) return QPIR_E_STATE;
   const uint64_t nb = (ctx->r + 7) / 8;
   if (!share || !out) return ENS_FAIL(ctx, QPIR_E_PARAM, "share/out: NULL");
@@ -263,6 +266,7 @@ int qpir_ens_answer(qpir_ens_ctx* ctx, const uint8_t* share, uint64_t len_share,
 int qpir_oop_answer(qpir_ens_ctx* ctx, uint32_t n_chunks, uint32_t server, const uint8_t* q,
                     uint64_t len_q, const uint8_t* A, uint64_t len_A, uint8_t* out,
                     uint64_t len_out, void* stream) {
+  NvtxRange nvtx_("qpir_oop_answer");
   if (!ctx) return QPIR_E_STATE;
   if (n_chunks < 2 || ctx->r % n_chunks != 0)
     return ENS_FAIL(ctx, QPIR_E_PARAM, "n_chunks: %u must be >= 2 and divide r = %llu", n_chunks,
@@ -297,6 +301,7 @@ int qpir_oop_answer(qpir_ens_ctx* ctx, uint32_t n_chunks, uint32_t server, const
 int qpir_oop_preprocess(qpir_ens_ctx* ctx, uint32_t n_chunks, uint32_t server,
                         const uint64_t* seeds, uint64_t n_seeds, uint8_t* A_out, uint64_t len_A,
                         void* stream) {
+  NvtxRange nvtx_("qpir_oop_preprocess");
   if (!ctx) return QPIR_E_STATE;
   if (n_chunks < 2 || ctx->r % n_chunks != 0)
     return ENS_FAIL(ctx, QPIR_E_PARAM, "n_chunks: %u must be >= 2 and divide r = %llu", n_chunks,
@@ -387,6 +392,7 @@ static int ens_batch_tc(qpir_ens_ctx* ctx, const uint8_t* Qd, uint64_t B, cudaSt
 
 int qpir_ens_answer_batch(qpir_ens_ctx* ctx, const uint8_t* shares, uint64_t B,
                           uint64_t len_shares, uint8_t* out, uint64_t len_out, void* stream) {
+  NvtxRange nvtx_("qpir_ens_answer_batch");
   if (!ctx) return QPIR_E_STATE;
   const uint64_t nb = (ctx->r + 7) / 8;
   if (!shares || !out) return ENS_FAIL(ctx, QPIR_E_PARAM, "shares/out: NULL");
