@@ -116,22 +116,25 @@ __global__ void limb_split_kernel(const uint32_t* __restrict__ Q, uint8_t* __res
 // A' (same panel layout as Q') = limb k of A[16g + i][j], n = 4j + k; one thread per
 // (group g, Philox block jb = j >> 2): 16 Philox calls, 256 contiguous bytes out.
 __global__ void expand_A_limbs_kernel(uint8_t* __restrict__ Ap, uint64_t seed, uint32_t m,
-                                      uint32_t n, uint32_t G, uint32_t Npad, uint32_t BN) {
-  // grid.x = column groups (up to 2^31), grid.y = blocks of Philox columns
+                                      uint32_t n, uint32_t G, uint32_t Npad, uint32_t BN,
+                                      uint32_t j_off) {
+  // grid.x = column groups (up to 2^31), grid.y = blocks of Philox columns;
+  // this launch generates hint columns j_off .. j_off + Npad/4 - 1 (j_off % 4 == 0)
   const uint32_t jb = blockIdx.y * blockDim.x + threadIdx.x;
   const uint32_t g = blockIdx.x;
   if (jb * 16u >= Npad) return;
   const uint2 key = make_uint2((uint32_t)seed, (uint32_t)(seed >> 32));
+  const uint32_t jg = j_off + jb * 4u;  // global column of this Philox block
   uint32_t a[16][4];
 #pragma unroll
   for (int i = 0; i < 16; ++i) {
     const uint32_t c = g * 16u + i;
     uint4 v = make_uint4(0, 0, 0, 0);
-    if (c < m && jb * 4u < n) v = philox4x32_10(make_uint4(c, jb, 0u, 0x41u), key);
+    if (c < m && jg < n) v = philox4x32_10(make_uint4(c, jg >> 2, 0u, 0x41u), key);
     a[i][0] = v.x;
-    a[i][1] = (jb * 4u + 1 < n) ? v.y : 0u;
-    a[i][2] = (jb * 4u + 2 < n) ? v.z : 0u;
-    a[i][3] = (jb * 4u + 3 < n) ? v.w : 0u;
+    a[i][1] = (jg + 1 < n) ? v.y : 0u;
+    a[i][2] = (jg + 2 < n) ? v.z : 0u;
+    a[i][3] = (jg + 3 < n) ? v.w : 0u;
   }
   uint4* dst = reinterpret_cast<uint4*>(Ap + limb_off(jb * 16u, g, G, BN));
 #pragma unroll

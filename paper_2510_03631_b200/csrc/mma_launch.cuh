@@ -27,6 +27,7 @@ struct MmaJob {
   int forced_split = 0;  // 0 = auto
   int mt = 2;            // row panels per CTA tile (1 or 2)
   int gpb = 8;           // column groups per pipeline stage (4 or 8)
+  bool out_prezeroed = false;  // caller zeroed `out` (strided chunks): no memset here
 };
 
 // BN for 3 limbs per query (OUT_MODP3): a multiple of 48 so queries never
@@ -95,7 +96,7 @@ cudaError_t mma_launch_cfg(const MmaJob& j, cudaStream_t st, uint64_t* launches)
   cudaError_t e = cudaSuccess;
   if (modp)
     e = cudaMemsetAsync(j.out64, 0, j.out_elems * 8, st);
-  else if (a.splits > 1)
+  else if (a.splits > 1 && !j.out_prezeroed)
     e = cudaMemsetAsync(j.out, 0, j.out_elems * 4, st);
   if (e != cudaSuccess) return e;
   const uint32_t units = a.m_tiles * a.n_tiles * a.splits;

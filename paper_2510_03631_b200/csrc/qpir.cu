@@ -82,6 +82,7 @@ struct qpir_ctx {
   int mma_split = 0;   // env QPIR_MMA_SPLIT (0 = auto)
   int mma_gpb = 8;     // env QPIR_MMA_GPB (column groups per pipeline stage: 4 or 8)
   int modp3 = 1;       // env QPIR_MODP3 (3 limbs per query for p < 2^24)
+  uint64_t limb_budget = 2ull << 30;  // env QPIR_LIMB_BUDGET_MB: max bytes of Q'/A' at once
   std::string err;
 };
 
@@ -318,7 +319,7 @@ int gemv(qpir_ctx* ctx, const uint32_t* qu, uint32_t* ans, cudaStream_t st) {
 template <int MODE>
 int launch_mma(qpir_ctx* ctx, uint32_t BN, const uint8_t* Bl, uint32_t Npad, uint32_t* out,
                uint32_t n_out, uint32_t out_ld, uint64_t out_elems, cudaStream_t st,
-               uint32_t p = 0, unsigned long long* out64 = nullptr) {
+               uint32_t p = 0, unsigned long long* out64 = nullptr, bool prezeroed = false) {
   const Geometry& g = ctx->geo;
   MmaJob j;
   j.A = ctx->D;
@@ -338,6 +339,7 @@ int launch_mma(qpir_ctx* ctx, uint32_t BN, const uint8_t* Bl, uint32_t Npad, uin
   j.forced_split = ctx->mma_split;
   j.mt = ctx->mma_mt;
   j.gpb = ctx->mma_gpb;
+  j.out_prezeroed = prezeroed;
   const cudaError_t e = mma_launch<MODE>(j, st, &ctx->launches);
   if (e != cudaSuccess)
     return fail(ctx, e == cudaErrorMemoryAllocation ? QPIR_E_OOM : QPIR_E_CUDA,
@@ -391,6 +393,8 @@ int qpir_setup(const qpir_params* params, const uint8_t* records, uint64_t recor
   ctx->mma_split = env_int("QPIR_MMA_SPLIT", 0);
   ctx->mma_gpb = env_int("QPIR_MMA_GPB", 8);
   ctx->modp3 = env_int("QPIR_MODP3", 1);
+  if (env_int("QPIR_LIMB_BUDGET_MB", 0) > 0)
+    ctx->limb_budget = (uint64_t)env_int("QPIR_LIMB_BUDGET_MB", 0) << 20;
   cudaStream_t st = (cudaStream_t)stream;
   auto bail = [&](int code) {
     g_setup_error = ctx->err;
@@ -531,7 +535,13 @@ static int answer_batch_impl(qpir_ctx* ctx, const uint32_t* Q, uint64_t B, uint6
   // F_p with p < 2^24: 3 limbs per query after reducing entries mod p
   const bool three = p != 0 && p <= (1u << 24) && ctx->modp3;
   const uint32_t LPQ = three ? 3u : 4u;
-  const uint64_t ncols = LPQ * B;
+  // Q' (LPQ limb columns per query) is materialised per chunk of queries so
+  // that it stays within ~2 GiB whatever B and m are.
+  const uint64_t budget = ctx->limb_budget;
+  uint64_t Bc = B;
+  if (round_up(LPQ * Bc, 256) * g.m_pad > budget)
+    Bc = std::max<uint64_t>(64, (budget / g.m_pad) / LPQ / 64 * 64);
+  const uint64_t ncols = LPQ * std::min<uint64_t>(Bc, B);
   const uint32_t BN = three ? mma_pick_bn3(ncols) : mma_pick_bn(ncols);
   const uint32_t Npad = (uint32_t)round_up(ncols, BN);
   Arena& ar = arena_for(ctx, st);
@@ -550,29 +560,35 @@ static int answer_batch_impl(qpir_ctx* ctx, const uint32_t* Q, uint64_t B, uint6
     if (rc) return rc;
     out = ar.big_out;
   }
-  {
-    const uint32_t nq = Npad / LPQ;  // padded query slots
-    dim3 grid((uint32_t)((g.G + 127) / 128), nq);
-    if (three)
-      limb_split_kernel<3><<<grid, 128, 0, st>>>(Qd, ar.limbs, (uint32_t)B, (uint32_t)g.m,
-                                                 (uint32_t)g.G, Npad, BN, p);
-    else
-      limb_split_kernel<4><<<grid, 128, 0, st>>>(Qd, ar.limbs, (uint32_t)B, (uint32_t)g.m,
-                                                 (uint32_t)g.G, Npad, BN, 0u);
-    LAUNCH_CHECK(ctx);
-  }
-  if (p == 0) {
-    rc = launch_mma<OUT_QUERY_MAJOR>(ctx, BN, ar.limbs, Npad, out, (uint32_t)B,
-                                     (uint32_t)g.ell_local, len_ans, st);
-  } else {
-    rc = ensure(ctx, (void**)&ar.acc64, &ar.acc64_bytes, len_ans * 8);
+  if (p != 0) {
+    rc = ensure(ctx, (void**)&ar.acc64, &ar.acc64_bytes, (uint64_t)std::min(Bc, B) * g.ell_local * 8);
     if (rc) return rc;
-    if (three)
-      rc = launch_mma<OUT_MODP3>(ctx, BN, ar.limbs, Npad, out, (uint32_t)B,
-                                 (uint32_t)g.ell_local, len_ans, st, p, ar.acc64);
+  }
+  for (uint64_t b0 = 0; b0 < B && rc == QPIR_OK; b0 += Bc) {
+    const uint32_t bc = (uint32_t)std::min<uint64_t>(Bc, B - b0);
+    const uint32_t* Qc = Qd + b0 * g.m;
+    uint32_t* oc = out + b0 * g.ell_local;
+    const uint64_t oe = (uint64_t)bc * g.ell_local;
+    {
+      const uint32_t nq = Npad / LPQ;  // padded query slots
+      dim3 grid((uint32_t)((g.G + 127) / 128), nq);
+      if (three)
+        limb_split_kernel<3><<<grid, 128, 0, st>>>(Qc, ar.limbs, bc, (uint32_t)g.m,
+                                                   (uint32_t)g.G, Npad, BN, p);
+      else
+        limb_split_kernel<4><<<grid, 128, 0, st>>>(Qc, ar.limbs, bc, (uint32_t)g.m,
+                                                   (uint32_t)g.G, Npad, BN, 0u);
+      LAUNCH_CHECK(ctx);
+    }
+    if (p == 0)
+      rc = launch_mma<OUT_QUERY_MAJOR>(ctx, BN, ar.limbs, Npad, oc, bc, (uint32_t)g.ell_local, oe,
+                                       st);
+    else if (three)
+      rc = launch_mma<OUT_MODP3>(ctx, BN, ar.limbs, Npad, oc, bc, (uint32_t)g.ell_local, oe, st,
+                                 p, ar.acc64);
     else
-      rc = launch_mma<OUT_MODP>(ctx, BN, ar.limbs, Npad, out, (uint32_t)B,
-                                (uint32_t)g.ell_local, len_ans, st, p, ar.acc64);
+      rc = launch_mma<OUT_MODP>(ctx, BN, ar.limbs, Npad, oc, bc, (uint32_t)g.ell_local, oe, st, p,
+                                ar.acc64);
   }
   if (rc) return rc;
   if (wa == 0) {
@@ -608,7 +624,13 @@ int qpir_hint(qpir_ctx* ctx, uint32_t* H_local, uint64_t len_H, void* stream) {
   if (wh < 0) return fail(ctx, QPIR_E_PARAM, "H_local: memory of another device");
   if (reinterpret_cast<uintptr_t>(H_local) & 3u)
     return fail(ctx, QPIR_E_PARAM, "H_local: not 4-byte aligned");
-  const uint64_t ncols = 4ull * g.lwe_n;
+  // A' (4 limb columns per hint column) is materialised per chunk of hint
+  // columns so that it stays within ~2 GiB whatever n and m are.
+  const uint64_t budget = ctx->limb_budget;
+  uint64_t nc = g.lwe_n;
+  if (round_up(4ull * nc, 256) * g.m_pad > budget)
+    nc = std::max<uint64_t>(64, (budget / g.m_pad) / 4 / 64 * 64);
+  const uint64_t ncols = 4ull * std::min<uint64_t>(nc, g.lwe_n);
   const uint32_t BN = mma_pick_bn(ncols);
   const uint32_t Npad = (uint32_t)round_up(ncols, BN);
   Arena& ar = arena_for(ctx, st);
@@ -620,15 +642,21 @@ int qpir_hint(qpir_ctx* ctx, uint32_t* H_local, uint64_t len_H, void* stream) {
     if (rc) return rc;
     out = ar.big_out;
   }
-  {
-    const uint32_t nb = Npad / 16;  // Philox blocks (4 outputs x 4 limbs)
-    dim3 grid((uint32_t)g.G, (nb + 127) / 128);
-    expand_A_limbs_kernel<<<grid, 128, 0, st>>>(ar.limbs, g.seed_A, (uint32_t)g.m, g.lwe_n,
-                                                (uint32_t)g.G, Npad, BN);
-    LAUNCH_CHECK(ctx);
+  const bool chunked = nc < g.lwe_n;
+  if (chunked) CUDA_TRY(ctx, cudaMemsetAsync(out, 0, len_H * 4, st));  // split tiles add in
+  for (uint64_t j0 = 0; j0 < g.lwe_n; j0 += nc) {
+    const uint32_t w = (uint32_t)std::min<uint64_t>(nc, g.lwe_n - j0);
+    {
+      const uint32_t nb = Npad / 16;  // Philox blocks (4 outputs x 4 limbs)
+      dim3 grid((uint32_t)g.G, (nb + 127) / 128);
+      expand_A_limbs_kernel<<<grid, 128, 0, st>>>(ar.limbs, g.seed_A, (uint32_t)g.m, g.lwe_n,
+                                                  (uint32_t)g.G, Npad, BN, (uint32_t)j0);
+      LAUNCH_CHECK(ctx);
+    }
+    rc = launch_mma<OUT_ROW_MAJOR>(ctx, BN, ar.limbs, Npad, out + j0, w, g.lwe_n, len_H, st, 0,
+                                   nullptr, chunked);
+    if (rc) return rc;
   }
-  rc = launch_mma<OUT_ROW_MAJOR>(ctx, BN, ar.limbs, Npad, out, g.lwe_n, g.lwe_n, len_H, st);
-  if (rc) return rc;
   if (out != H_local) {
     CUDA_TRY(ctx, cudaMemcpyAsync(H_local, out, len_H * 4,
                                   wh ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost, st));

@@ -407,3 +407,21 @@ def test_next_rows_full_size_sampled(cuda_ok):
         Qs = synth.uniform_u8_np(83, (48, nb))
         got = e.answer_batch(Qs).cpu().numpy()[:, cols]
         assert (got == O.ens_respond_batch(rec_cols, Qs)).all()
+
+
+@pytest.mark.parametrize("split", ["0", "3"])
+def test_limb_chunking_batch_and_hint(cuda_ok, split, monkeypatch):
+    """A 1 MB limb budget forces Q' (queries) and A' (hint columns) to be built and
+    multiplied in chunks; results are unchanged (strided hint chunks with K-splits
+    add into a pre-zeroed H)."""
+    monkeypatch.setenv("QPIR_LIMB_BUDGET_MB", "1")
+    monkeypatch.setenv("QPIR_MMA_SPLIT", split)
+    P = _srv()
+    n_cells, n_ch, d, n = 4096, 3, 40, 300
+    rec, D = _db(n_cells, n_ch, d, seed=90)
+    with P.PirServer(n_cells, n_ch, d, lwe_n=n, seed_A=91, records=rec) as s:
+        Q = synth.uniform_u32_np(92, (150, n_cells))   # 600 limb cols x 4096 > 1 MB
+        assert (_u32(s.answer_batch(Q)) == O.answer_batch(D, Q)).all()
+        want = ((Q.astype(object) @ D.T.astype(object)) % 65537).astype(np.uint32)
+        assert (_u32(s.answer_batch_modp(Q, 65537)) == want).all()
+        assert (_u32(s.hint()) == O.hint(D, O.expand_A(91, n_cells, n))).all()
