@@ -168,7 +168,9 @@ int qpir_ens_setup(const qpir_ens_params *params, const uint8_t *records,
 int qpir_ens_db_write(qpir_ens_ctx *ctx, uint64_t theta_begin, uint64_t n_records,
                       const uint8_t *records, uint64_t records_len, void *stream);
 
-/* Response to one share (len_share == ceil(r/8)) -> out: d bytes (len_out == d). */
+/* Response to one share (len_share == ceil(r/8)) -> out: d bytes (len_out == d).
+ * A 4-byte-aligned device share may be read in whole 32-bit words (up to 3
+ * bytes past len_share, within the allocation granularity of cudaMalloc). */
 int qpir_ens_answer(qpir_ens_ctx *ctx, const uint8_t *share, uint64_t len_share,
                     uint8_t *out, uint64_t len_out, void *stream);
 

@@ -126,6 +126,72 @@ __global__ void __launch_bounds__(1024) ens_scan_kernel(EnsArgs a) {
   if (acc.w) atomicXor(o + 3, acc.w);
 }
 
+// Wide-record variant (blockDim == W, one row per CTA step: d > 2 KB, e.g.
+// the paper's 3 KB records).  The row is warp-uniform, so the selector bit is
+// tested once per row from a 32-row word loaded once (CTA ranges start on
+// 32-row boundaries relative to row_lo, the share's bit 0), the row pointer
+// advances by dp, and unselected rows issue no load at all: ~8 instructions
+// per 16-byte chunk instead of ~20 for the general kernel.
+template <int UR>
+__global__ void __launch_bounds__(1024) ens_scan_wide_kernel(EnsArgs a) {
+  const uint32_t w = threadIdx.x;  // 16-byte chunk of the row
+  const uint64_t n_rows = a.row_hi - a.row_lo;
+  const uint64_t t0 = (uint64_t)blockIdx.x * a.rows_per_cta;  // multiple of 32
+  const uint64_t t1 = min(n_rows, t0 + a.rows_per_cta);
+  const uint32_t* q32 = reinterpret_cast<const uint32_t*>(a.q);  // 4-byte aligned
+  uint4 acc = make_uint4(0, 0, 0, 0);
+  for (uint64_t tb = t0; tb < t1; tb += 32) {
+    uint32_t sel = __ldg(q32 + (tb >> 5));
+    const uint32_t nrow = (t1 - tb) < 32 ? (uint32_t)(t1 - tb) : 32u;
+    if (nrow < 32) sel &= (1u << nrow) - 1u;
+    const uint8_t* p = a.R + (size_t)(a.row_lo + tb) * a.dp + (size_t)w * 16;
+#pragma unroll
+    for (int h = 0; h < 32; h += UR) {
+      uint4 v[UR];
+#pragma unroll
+      for (int u = 0; u < UR; ++u)
+        v[u] = ldg_stream_v4_if(p + (size_t)(h + u) * a.dp, (sel >> (h + u)) & 1u);
+#pragma unroll
+      for (int u = 0; u < UR; ++u) {
+        acc.x ^= v[u].x;
+        acc.y ^= v[u].y;
+        acc.z ^= v[u].z;
+        acc.w ^= v[u].w;
+      }
+    }
+  }
+  if (a.partial != nullptr) {
+    __shared__ uint32_t s_last;
+    a.partial[(size_t)blockIdx.x * a.W + w] = acc;
+    __threadfence();
+    __syncthreads();
+    const uint32_t grp = blockIdx.x / a.group;
+    const uint32_t g0 = grp * a.group;
+    const uint32_t g1 = min(gridDim.x, g0 + a.group);
+    if (threadIdx.x == 0) {
+      const uint32_t t = atomicAdd(&a.tickets[grp], 1u);
+      s_last = (t == g1 - g0 - 1) ? 1u : 0u;
+    }
+    __syncthreads();
+    if (!s_last) return;
+    __threadfence();
+    acc = make_uint4(0, 0, 0, 0);
+    for (uint32_t c = g0; c < g1; ++c) {
+      const uint4 v = __ldcg(a.partial + (size_t)c * a.W + w);
+      acc.x ^= v.x;
+      acc.y ^= v.y;
+      acc.z ^= v.z;
+      acc.w ^= v.w;
+    }
+    if (threadIdx.x == 0) a.tickets[grp] = 0u;
+  }
+  uint32_t* o = a.out + (size_t)w * 4;
+  if (acc.x) atomicXor(o + 0, acc.x);
+  if (acc.y) atomicXor(o + 1, acc.y);
+  if (acc.z) atomicXor(o + 2, acc.z);
+  if (acc.w) atomicXor(o + 3, acc.w);
+}
+
 // Selector bits transposed for the batch: Qt[t][k] bit i = share (32k + i) bit t.
 __global__ void ens_transpose_bits_kernel(const uint8_t* __restrict__ Q, uint32_t* __restrict__ Qt,
                                           uint64_t r, uint64_t nb, uint32_t B, uint32_t QW) {

@@ -35,6 +35,7 @@ struct qpir_ens_ctx {
   uint32_t* tickets = nullptr;  // scan group tickets (self-resetting)
   uint64_t tickets_bytes = 0;
   int group = 0;                // env QPIR_ENS_GROUP (0 = auto 32; 1 = atomics only)
+  int wide = 1;                 // env QPIR_ENS_WIDE (uniform-row kernel for d > 2 KB)
   // tensor-core multi-request path (bit-planes, 8x the record bytes)
   uint8_t* bitD = nullptr;
   uint64_t bitD_bytes = 0;
@@ -135,12 +136,13 @@ int qpir_ens_setup(const qpir_ens_params* p, const uint8_t* records, uint64_t re
   ctx->rows_per_cta = env_int("QPIR_ENS_ROWS", 0);
   ctx->ur = env_int("QPIR_ENS_UR", 16);
   ctx->group = env_int("QPIR_ENS_GROUP", 0);
+  ctx->wide = env_int("QPIR_ENS_WIDE", 1);
   ctx->tc = env_int("QPIR_ENS_TC", -1);
   ctx->mma_split = env_int("QPIR_MMA_SPLIT", 0);
   cudaStream_t st = (cudaStream_t)stream;
   const uint64_t nb = (ctx->r + 7) / 8;
   if (cudaMalloc(&ctx->R, ctx->r * ctx->dp) != cudaSuccess ||
-      cudaMalloc(&ctx->q_dev, nb) != cudaSuccess) {
+      cudaMalloc(&ctx->q_dev, round_up(nb, 16)) != cudaSuccess) {
     cudaGetLastError();
     g_ens_setup_error = "records: cudaMalloc failed";
     qpir_ens_destroy(ctx);
@@ -207,6 +209,7 @@ static int scan_range(qpir_ens_ctx* ctx, const uint8_t* share_dev, uint64_t row_
     rows = std::max<uint64_t>(std::min(by_bytes, by_occ), (uint64_t)R * UR);
   }
   rows = round_up(rows, (uint64_t)R * UR);
+  if (R == 1) rows = round_up(rows, 32);  // 32-row selector words (wide kernel)
   a.rows_per_cta = rows;
   const uint64_t grid = (row_hi - row_lo + rows - 1) / rows;
   a.partial = nullptr;
@@ -228,7 +231,14 @@ static int scan_range(qpir_ens_ctx* ctx, const uint8_t* share_dev, uint64_t row_
     a.group = group;
   }
   const size_t smem = R > 1 ? threads * 16 : 0;
-  if (UR == 16)
+  const bool wide = R == 1 && ctx->wide && (rows % 32 == 0) &&
+                    ((reinterpret_cast<uintptr_t>(share_dev) & 3u) == 0);
+  if (wide) {
+    if (UR == 8)
+      ens_scan_wide_kernel<8><<<(uint32_t)grid, threads, 0, st>>>(a);
+    else
+      ens_scan_wide_kernel<16><<<(uint32_t)grid, threads, 0, st>>>(a);
+  } else if (UR == 16)
     ens_scan_kernel<16><<<(uint32_t)grid, threads, smem, st>>>(a);
   else if (UR == 4)
     ens_scan_kernel<4><<<(uint32_t)grid, threads, smem, st>>>(a);

@@ -22,11 +22,15 @@ def _share(seed, r):
     return q
 
 
-@pytest.mark.parametrize("r,d", [(1000, 24), (77, 5), (4099, 100), (513, 3072), (20000, 16)])
-@pytest.mark.parametrize("rows,group", [("0", "0"), ("8", "0"), ("8", "3"), ("8", "1"), ("96", "0")])
-def test_ens_answer_matches_oracle(cuda_ok, r, d, rows, group, monkeypatch):
+@pytest.mark.parametrize("r,d", [(1000, 24), (77, 5), (4099, 100), (513, 3072), (20000, 16),
+                                 (3001, 2500), (100, 16384)])
+@pytest.mark.parametrize("rows,group,wide", [("0", "0", "1"), ("8", "0", "1"), ("8", "3", "1"),
+                                             ("8", "1", "1"), ("96", "0", "1"), ("0", "0", "0"),
+                                             ("64", "5", "0")])
+def test_ens_answer_matches_oracle(cuda_ok, r, d, rows, group, wide, monkeypatch):
     monkeypatch.setenv("QPIR_ENS_ROWS", rows)
     monkeypatch.setenv("QPIR_ENS_GROUP", group)
+    monkeypatch.setenv("QPIR_ENS_WIDE", wide)
     P = _P()
     rec = synth.uniform_u8_np(r + d, (r, d))
     with P.EnsServer(r, d, records=rec) as s:
