@@ -79,6 +79,32 @@ class DistributedPIR:
         a = self.server.answer(qu)
         return gather_answer(a, self.sizes, self.group) if gather else a
 
+    def answer_many(self, queries, stream=None):
+        """Answer a sequence of single queries, overlapping the NCCL gather of
+        query i with the GEMV of query i + 1 (two answer-slice buffers, a side
+        stream for the collective).  Returns the list of full answers."""
+        dev = torch.device("cuda", self.server.device)
+        main = stream or torch.cuda.current_stream(dev)
+        comm = torch.cuda.Stream(dev)
+        bufs = [torch.empty(self.server.ell_local, dtype=torch.int32, device=dev)
+                for _ in range(2)]
+        done = [None, None]
+        outs = []
+        for i, q in enumerate(queries):
+            b = i % 2
+            if done[b] is not None:
+                main.wait_event(done[b])  # the slice's previous gather has read it
+            self.server.answer(q, out=bufs[b], stream=main)
+            ready = torch.cuda.Event()
+            ready.record(main)
+            comm.wait_event(ready)
+            with torch.cuda.stream(comm):
+                outs.append(gather_answer(bufs[b], self.sizes, self.group))
+                done[b] = torch.cuda.Event()
+                done[b].record(comm)
+        main.wait_stream(comm)
+        return outs
+
     def answer_batch(self, Q, gather: bool = True):
         a = self.server.answer_batch(Q)
         return gather_answer(a, self.sizes, self.group) if gather else a

@@ -37,6 +37,12 @@ def test_distributed_pir_ens_ftr_one_rank(nccl1):
     Q = synth.uniform_u32_np(5, (3, n_cells))
     got = pir.answer_batch(torch.from_numpy(Q.view(np.int32)).cuda())
     assert (got.cpu().numpy().view(np.uint32) == O.answer_batch(D, Q)).all()
+    qs = [torch.from_numpy(synth.uniform_u32_np(20 + i, (n_cells,)).view(np.int32)).cuda()
+          for i in range(7)]
+    many = pir.answer_many(qs)
+    torch.cuda.synchronize()
+    for i, a in enumerate(many):
+        assert (a.cpu().numpy().view(np.uint32) == O.answer(D, qs[i].cpu().numpy().view(np.uint32))).all()
 
     r = rec.shape[0]
     ens = DistributedEns(r, d, records=torch.from_numpy(rec).cuda())
