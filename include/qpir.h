@@ -109,7 +109,9 @@ int qpir_answer(qpir_ctx *ctx, const uint32_t *qu, uint64_t len_qu,
 /* Batch of B queries (step a6):
  *   ans_local[b * ell_local + i] = sum_c D[row_begin + i][c] * Q[b * m + c] mod 2^32.
  * Q: B x m u32 query-major (len == B * m); ans_local: B x ell_local (len ==
- * B * ell_local).  1 <= B <= 4096. */
+ * B * ell_local).  1 <= B <= 4096.  u32 device pointers must be 4-byte aligned.
+ * The byte-limb planes of Q are built in chunks of queries under a 2 GiB budget
+ * (env QPIR_LIMB_BUDGET_MB), so B and m only bound the output size. */
 int qpir_answer_batch(qpir_ctx *ctx, const uint32_t *Q, uint64_t B,
                       uint64_t len_Q, uint32_t *ans_local, uint64_t len_ans,
                       void *stream);
@@ -175,7 +177,10 @@ int qpir_ens_answer(qpir_ens_ctx *ctx, const uint8_t *share, uint64_t len_share,
                     uint8_t *out, uint64_t len_out, void *stream);
 
 /* Responses to B shares (B x ceil(r/8), share-major) -> out: B x d bytes.
- * 1 <= B <= 65536. */
+ * 1 <= B <= 65536.  For 32 <= B <= 65280 the GF(2) product runs on tensor
+ * cores over the records' bit-planes, which take 8 * r * d bytes of extra
+ * device memory (built on first use, rebuilt after qpir_ens_db_write); if that
+ * allocation fails, or for smaller B, a CUDA-core XOR kernel is used. */
 int qpir_ens_answer_batch(qpir_ens_ctx *ctx, const uint8_t *shares, uint64_t B,
                           uint64_t len_shares, uint8_t *out, uint64_t len_out,
                           void *stream);
@@ -190,7 +195,7 @@ int qpir_ens_answer_batch(qpir_ens_ctx *ctx, const uint8_t *shares, uint64_t B,
  *   Philox4x32-10(key = S, ctr = (w >> 2, 0, 0, 0x4F))[w & 3], bit p of the
  *   stream = bit (p & 31) of word p >> 5.
  * Online: R_i = A_i XOR q_i . chunk_i, q_i: k bits (ceil(k/8) bytes), touching
- *   only chunk i (1/n of the DB). */
+ *   only chunk i (1/n of the DB).  1 <= n_seeds <= 65535. */
 int qpir_oop_preprocess(qpir_ens_ctx *ctx, uint32_t n_chunks, uint32_t server,
                         const uint64_t *seeds, uint64_t n_seeds, uint8_t *A_out,
                         uint64_t len_A, void *stream);
