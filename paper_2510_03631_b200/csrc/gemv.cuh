@@ -107,6 +107,7 @@ struct GemvArgs {
   uint32_t gps;         // groups per split (multiple of UNR)
   uint32_t chunk;       // groups staged in smem at a time (multiple of UNR)
   uint32_t split_major; // 1: blockIdx.x = split, blockIdx.y = row block (page-local order)
+  uint32_t pf256;       // 1: L2::256B prefetch hint on the D loads
 };
 
 // U rows per thread (rows r, r + 128, ...); UNR column groups per iteration.
@@ -154,8 +155,9 @@ __global__ void __launch_bounds__(GEMV_THREADS) gemv_u8_u32_kernel(GemvArgs a) {
       for (int i = 0; i < UNR; ++i)
 #pragma unroll
         for (int u = 0; u < U; ++u)
-          d[i][u] = live[u] ? ldg_stream_v4(Drow[u] + (size_t)(g + i) * gstride)
-                            : make_uint4(0, 0, 0, 0);
+          d[i][u] = !live[u] ? make_uint4(0, 0, 0, 0)
+                    : a.pf256 ? ldg_stream_v4_pf256(Drow[u] + (size_t)(g + i) * gstride)
+                              : ldg_stream_v4(Drow[u] + (size_t)(g + i) * gstride);
 #pragma unroll
       for (int i = 0; i < UNR; ++i) {
         const uint4* l = sL + (size_t)(g + i - cb) * 4;

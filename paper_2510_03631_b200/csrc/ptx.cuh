@@ -20,6 +20,15 @@ __device__ __forceinline__ uint4 ldg_stream_v4(const void* p) {
   return r;
 }
 
+// Same with an L2 256-byte prefetch hint (fewer, larger DRAM requests).
+__device__ __forceinline__ uint4 ldg_stream_v4_pf256(const void* p) {
+  uint4 r;
+  asm volatile("ld.global.nc.L1::no_allocate.L2::256B.v4.u32 {%0, %1, %2, %3}, [%4];"
+               : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
+               : "l"(p));
+  return r;
+}
+
 // Predicated 128-bit streaming load: returns zeros when !pred, without a branch
 // (keeps many independent loads in flight).
 __device__ __forceinline__ uint4 ldg_stream_v4_if(const void* p, bool pred) {

@@ -78,6 +78,7 @@ struct qpir_ctx {
   int gemv_order = 0;  // env QPIR_GEMV_ORDER (1 = split-major grid)
   int gemv_pdl = 1;    // env QPIR_GEMV_PDL (programmatic dependent launch of back-to-back GEMVs)
   int gemv_impl = 0;   // env QPIR_GEMV_IMPL: 0 = SIMT split-K kernel, 1 = persistent TMA-fed
+  int gemv_pf256 = 0;  // env QPIR_GEMV_PF256: L2 256-byte prefetch hint on D loads
   int mma_mt = 2;      // env QPIR_MMA_MT (1 or 2 row panels per CTA tile)
   int mma_split = 0;   // env QPIR_MMA_SPLIT (0 = auto)
   int mma_gpb = 8;     // env QPIR_MMA_GPB (column groups per pipeline stage: 4 or 8)
@@ -265,6 +266,7 @@ int launch_gemv(qpir_ctx* ctx, const uint32_t* qu, uint32_t* ans, cudaStream_t s
   a.gps = gps;
   a.chunk = chunk;
   a.split_major = (ctx->gemv_order == 1 && rb <= 65535) ? 1u : 0u;
+  a.pf256 = ctx->gemv_pf256 ? 1u : 0u;
   const size_t smem = (size_t)chunk * 64;
   auto kern = gemv_u8_u32_kernel<U, UNR>;
   if (smem > 48 * 1024)
@@ -389,6 +391,7 @@ int qpir_setup(const qpir_params* params, const uint8_t* records, uint64_t recor
   ctx->gemv_order = env_int("QPIR_GEMV_ORDER", 0);
   ctx->gemv_pdl = env_int("QPIR_GEMV_PDL", 1);
   ctx->gemv_impl = env_int("QPIR_GEMV_IMPL", 0);
+  ctx->gemv_pf256 = env_int("QPIR_GEMV_PF256", 0);
   ctx->mma_mt = env_int("QPIR_MMA_MT", 2);
   ctx->mma_split = env_int("QPIR_MMA_SPLIT", 0);
   ctx->mma_gpb = env_int("QPIR_MMA_GPB", 8);
