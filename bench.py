@@ -18,9 +18,16 @@ value = DB bytes scanned by all ranks / max-over-ranks device time.
 """
 from __future__ import annotations
 
+import os
+
+# The CPU oracle (cpu_baseline / --impl reference) uses OpenMP; with torch's
+# own OpenMP threads spin-waiting in the same process its parallel regions
+# slow down by orders of magnitude.  Passive waiting must be set before any
+# OpenMP runtime starts, i.e. before torch is imported.
+os.environ.setdefault("OMP_WAIT_POLICY", "PASSIVE")
+
 import argparse
 import json
-import os
 import statistics
 import subprocess
 import sys
@@ -197,6 +204,45 @@ def cpu_baseline_answer(wl, seed, budget_s=12.0):
             "sample": f"oracle answer over rows of the first {n_ch_s} channels "
                       f"({D.shape[0]} rows x {D.shape[1]} cells = {D.nbytes / 1e6:.1f} MB), "
                       f"{reps} repetitions in {dt:.1f} s"}
+
+
+def cpu_baseline_gemm(wl, seed, kind, budget_s=10.0):
+    """Oracle batch / hint on a bounded sample (a few rows of the same DB, all
+    queries / hint columns), all host cores; the full-size time is reported as an
+    explicit extrapolation from the measured rate."""
+    import synth
+    from oracle import oracle as O
+    O.set_num_threads(os.cpu_count() or 1)
+    n_cells, n_ch, d = wl["n_cells"], wl["n_ch"], wl["d"]
+    rows = 8
+    cells = torch.arange(n_cells, dtype=torch.int64)
+    Dr = np.stack([synth.byte_column(seed, cells * n_ch + (r // d), r % d, d, n_ch).numpy()
+                   for r in range(rows)])
+    if kind == "batch":
+        B = wl["B"]
+        R = synth.uniform_u32_np(seed + 5, (B, n_cells))
+        fn = (lambda: O.ftr_respond_batch(np.ascontiguousarray(Dr.T), R, wl["modp"])) \
+            if wl.get("modp") else (lambda: O.answer_batch(Dr, R))
+        macs = rows * n_cells * B
+        full = wl.get("ell_total", n_ch * d) * n_cells * B
+    else:
+        A = O.expand_A(0x5EED, n_cells, wl["n"])
+        fn = lambda: O.hint(Dr, A)
+        macs = rows * n_cells * wl["n"]
+        full = (n_ch * d // wl.get("shard_of", 1)) * n_cells * wl["n"]
+    fn()
+    t0 = time.perf_counter()
+    reps = 0
+    while time.perf_counter() - t0 < budget_s:
+        fn()
+        reps += 1
+    dt = (time.perf_counter() - t0) / reps
+    rate = macs / dt
+    return {"value": round(rate / 1e9, 3), "unit": "G u32-MAC/s", "cores": O.num_threads(),
+            "kind": "oracle",
+            "sample": f"{rows} rows of the same DB x all {n_cells} cells x all "
+                      f"{'queries' if kind == 'batch' else 'hint columns'}, {reps} repetitions",
+            "extrapolated_full_step_s": round(full / rate, 1)}
 
 
 # ---------------------------------------------------------------- reference arm
@@ -740,6 +786,8 @@ def main():
     cpu_base = None
     if not args.no_cpu_baseline and world == 1 and kind == "answer":
         cpu_base = cpu_baseline_answer(wl, args.seed)
+    elif not args.no_cpu_baseline and world == 1 and kind in ("batch", "hint"):
+        cpu_base = cpu_baseline_gemm(wl, args.seed, kind)
     cfg = {"workload": wl["name"], "n_cells": n_cells, "n_ch": n_ch_total, "rec_bytes": d,
            "ell_local": ell_local, "db_bytes_per_gpu": db_bytes_local,
            "queries_per_step": B if kind != "hint" else 0,

@@ -1,6 +1,9 @@
 import os
 import sys
 
+# oracle OpenMP regions next to torch's spin-waiting OpenMP threads (see bench.py)
+os.environ.setdefault("OMP_WAIT_POLICY", "PASSIVE")
+
 import pytest
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
