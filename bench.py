@@ -734,23 +734,42 @@ def main():
     elif kind == "batch":
         scanned = db_bytes_local * world * B
         value = scanned / (ms_per_step / 1e3) / 1e9
-        limbs = 3 if (wl.get("modp") and wl["modp"] <= (1 << 24)
-                      and os.environ.get("QPIR_MODP3", "1") != "0") else 4
+        mp = wl.get("modp") or 0
+        if mp and mp <= 65537 and os.environ.get("QPIR_MODP2", "1") != "0":
+            limbs = 2
+        elif mp and mp <= (1 << 24) and os.environ.get("QPIR_MODP3", "1") != "0":
+            limbs = 3
+        else:
+            limbs = 4
         ops = 2.0 * ell_local * n_cells * limbs * B  # int8 tensor ops actually executed
-        achieved = ops / (k_ms / 1e3) / 1e12
+        # the step is bound by whichever roof takes longer: streaming D (+ Q in,
+        # ANS out) from HBM once, or the executed int8 MMAs
+        alg_bytes = db_bytes_local + 4 * n_cells * B + 4 * ell_local * B
         pk = 2.0 * bf16
-        roof = {"bound": "tensor", "achieved": round(achieved, 1), "peak": pk, "unit": "TFLOP/s",
-                "frac": round(achieved / pk, 4), "traffic": None,
-                "kernel": "limb_split_kernel + mma_u8_limb_kernel (step time, upper bound)",
-                "limbs_per_query": limbs,
-                "kernel_ms": round(k_ms, 5),
-                "peak_source": f"{peak_src} bf16_tflops x 2 (nominal int8/bf16 ratio), int8 TOPS",
-                "algorithmic_ops_per_launch": ops}
+        t_hbm = alg_bytes / (hbm * 1e9)
+        t_tc = ops / (pk * 1e12)
+        achieved_tc = ops / (k_ms / 1e3) / 1e12
+        achieved_hbm = alg_bytes / (k_ms / 1e3) / 1e9
+        common = {"traffic": None,
+                  "kernel": "limb_split_kernel + mma_u8_limb_kernel (step time, upper bound)",
+                  "limbs_per_query": limbs, "kernel_ms": round(k_ms, 5),
+                  "algorithmic_ops_per_launch": ops, "algorithmic_bytes_per_launch": alg_bytes,
+                  "roof_ms": {"hbm": round(t_hbm * 1e3, 5), "tensor": round(t_tc * 1e3, 5)}}
+        if t_hbm > t_tc:
+            roof = {"bound": "hbm", "achieved": round(achieved_hbm, 1), "peak": hbm,
+                    "unit": "GB/s", "frac": round(achieved_hbm / hbm, 4), **common,
+                    "peak_source": f"{peak_src} hbm_gbs (copy, read+write)",
+                    "tensor_frac": round(achieved_tc / pk, 4)}
+        else:
+            roof = {"bound": "tensor", "achieved": round(achieved_tc, 1), "peak": pk,
+                    "unit": "TFLOP/s", "frac": round(achieved_tc / pk, 4), **common,
+                    "peak_source": f"{peak_src} bf16_tflops x 2 (nominal int8/bf16 ratio), int8 TOPS",
+                    "hbm_frac": round(achieved_hbm / hbm, 4)}
+            if bf16_sus:
+                roof["peak_sustained"] = 2.0 * bf16_sus
+                roof["frac_sustained"] = round(achieved_tc / (2.0 * bf16_sus), 4)
         qps = B * world / (ms_per_step / 1e3)
         unit = "GB/s (query-equivalent)"
-        if bf16_sus:
-            roof["peak_sustained"] = 2.0 * bf16_sus
-            roof["frac_sustained"] = round(achieved / (2.0 * bf16_sus), 4)
     else:
         ops = 2.0 * ell_local * n_cells * 4 * wl["n"]
         value = ops / (ms_per_step / 1e3) / 1e12

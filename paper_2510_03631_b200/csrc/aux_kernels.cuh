@@ -68,10 +68,14 @@ __global__ void pack_records_kernel(PackArgs a) {
 // 4 x 16 B out (64 B contiguous).
 // LPQ limbs per query (4 for Z_{2^32}; 3 for F_p with p < 2^24 after reducing
 // each entry mod p -- exact, since sum (q mod p) d = sum q d (mod p)).
+// LPQ = 2 (p <= 65537): a reduced entry 65536 (only p = 65537) is written as 0
+// and its column appended to the query's exception list (exc_cnt / exc_list,
+// `cap` entries per query) for modp_fixup_kernel.
 template <int LPQ>
 __global__ void limb_split_kernel(const uint32_t* __restrict__ Q, uint8_t* __restrict__ Qp,
                                   uint32_t B, uint32_t m, uint32_t G, uint32_t Npad,
-                                  uint32_t BN, uint32_t p) {
+                                  uint32_t BN, uint32_t p, uint32_t* __restrict__ exc_cnt,
+                                  uint32_t* __restrict__ exc_list, uint32_t cap) {
   // threads walk 16-cell groups of one query row (coalesced 64 B per thread);
   // each thread writes its query's LPQ limb rows = 16 * LPQ contiguous bytes
   const uint32_t g = blockIdx.x * blockDim.x + threadIdx.x;
@@ -98,6 +102,17 @@ __global__ void limb_split_kernel(const uint32_t* __restrict__ Q, uint8_t* __res
   if (p != 0) {
 #pragma unroll
     for (int i = 0; i < 16; ++i) q[i] %= p;
+    if constexpr (LPQ == 2) {
+      if (exc_cnt) {
+#pragma unroll
+        for (int i = 0; i < 16; ++i)
+          if (q[i] == 65536u) {  // jq < B and c0 + i < m: padding entries are 0
+            const uint32_t idx = atomicAdd(exc_cnt + jq, 1u);
+            if (idx < cap) exc_list[(size_t)jq * cap + idx] = c0 + i;
+            q[i] = 0u;
+          }
+      }
+    }
   }
   uint4* dst = reinterpret_cast<uint4*>(Qp + limb_off(jq * (uint32_t)LPQ, g, G, BN));
 #pragma unroll

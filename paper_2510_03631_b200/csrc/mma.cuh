@@ -46,7 +46,11 @@ constexpr uint32_t MMA_THREADS = 192;
 // K-split partials combine with atomicXor.
 // OUT_MODP3: as OUT_MODP with 3 limbs per query (entries pre-reduced mod
 // p < 2^24 by the limb split), BN a multiple of 48: 25 % fewer MMAs.
-enum : int { OUT_QUERY_MAJOR = 0, OUT_ROW_MAJOR = 1, OUT_MODP = 2, OUT_PARITY = 3, OUT_MODP3 = 4 };
+// OUT_MODP2: 2 limbs per query (p <= 65537; entries pre-reduced mod p, the one
+// residue 65536 of p = 65537 added back by modp_fixup_kernel): half the MMAs.
+enum : int {
+  OUT_QUERY_MAJOR = 0, OUT_ROW_MAJOR = 1, OUT_MODP = 2, OUT_PARITY = 3, OUT_MODP3 = 4, OUT_MODP2 = 5
+};
 
 struct MmaArgs {
   const uint8_t* A;   // D shard, 128-row panels [L/128][G][128][16]
@@ -69,8 +73,10 @@ struct MmaCfg {
   static constexpr uint32_t A_BYTES = MT * PANEL_BYTES;
   static constexpr uint32_t B_BYTES = BN * KB_CELLS;
   static constexpr uint32_t STAGE_BYTES = A_BYTES + B_BYTES;
-  static constexpr uint32_t STAGES_RAW = (200u * 1024u) / STAGE_BYTES;
-  static constexpr uint32_t STAGES = STAGES_RAW > 12 ? 12 : STAGES_RAW;
+  // as many stages as fit the 227 KB opt-in smem (minus barriers): deep enough
+  // to cover HBM latency at the per-SM share of bandwidth
+  static constexpr uint32_t STAGES_RAW = (227u * 1024u - 512u) / STAGE_BYTES;
+  static constexpr uint32_t STAGES = STAGES_RAW > 16 ? 16 : STAGES_RAW;
   static constexpr uint32_t ACC_COLS = MT * BN;  // one accumulator buffer
   static constexpr uint32_t ACC_BUFS = (2 * ACC_COLS <= 512) ? 2 : 1;
   static constexpr uint32_t NEED_COLS = ACC_BUFS * ACC_COLS;
@@ -239,6 +245,19 @@ __global__ void __launch_bounds__(MMA_THREADS, 1) mma_u8_limb_kernel(MmaArgs a) 
                   if (split) atomicXor(dst, word); else *dst = word;
                 }
               }
+            } else if constexpr (OUT_MODE == OUT_MODP2) {
+              const uint32_t jq = (nt * BN + c0) / 2;
+              if (row < a.rows) {
+#pragma unroll
+                for (int jj = 0; jj < 8; ++jj) {
+                  const unsigned long long x = (unsigned long long)v[16 * t + 2 * jj] +
+                                               ((unsigned long long)v[16 * t + 2 * jj + 1] << 8);
+                  // x < 2^41: the u64 sum over <= 2^16 K-splits cannot wrap, so
+                  // the one reduction mod p is left to modp_fixup_kernel
+                  if (jq + jj < a.n_out)
+                    atomicAdd(a.out64 + (size_t)(jq + jj) * a.out_ld + row, x);
+                }
+              }
             } else if constexpr (OUT_MODE == OUT_MODP) {
               if (row < a.rows) {
 #pragma unroll
@@ -281,7 +300,7 @@ __global__ void __launch_bounds__(MMA_THREADS, 1) mma_u8_limb_kernel(MmaArgs a) 
                 }
               }
             }
-            }  // OUT_MODE != OUT_MODP
+            }  // OUT_MODE not OUT_MODP / OUT_MODP2
           }
           }  // OUT_MODE != OUT_MODP3
         }
@@ -303,11 +322,51 @@ __global__ void __launch_bounds__(MMA_THREADS, 1) mma_u8_limb_kernel(MmaArgs a) 
 }  // namespace qpir
 
 namespace qpir {
-// out[i] = acc[i] mod p (u64 -> u32), after the OUT_MODP GEMM.
-static __global__ void modp_fixup_kernel(const unsigned long long* __restrict__ acc, uint32_t* __restrict__ out,
-                                  uint64_t n, uint32_t p) {
+// Exception lists of OUT_MODP2 with p = 65537: the residue 65536 does not fit 2
+// byte limbs; the limb split wrote it as 0 and listed its column c per query
+// (up to `cap` entries; cnt[b] > cap means the list overflowed and the fixup
+// rescans that query's row of Q -- adversarial input only).
+struct ModpExceptions {
+  const uint8_t* D = nullptr;  // 128-row panels [L/128][G][128][16]
+  uint32_t G = 0;
+  const uint32_t* Q = nullptr;  // the chunk's queries [B][m]
+  uint32_t m = 0;
+  const uint32_t* cnt = nullptr;   // [B]; nullptr = no exceptions possible
+  const uint32_t* list = nullptr;  // [B][cap]
+  uint32_t cap = 0;
+};
+
+// out[i] = acc[i] mod p (u64 -> u32), after the OUT_MODP* GEMM; with exception
+// lists, the missing terms 65536 * D[r][c] are added first (exact in u64).
+// out / acc are query-major [n][ld]: i = b * ld + r.
+static __global__ void modp_fixup_kernel(const unsigned long long* __restrict__ acc,
+                                         uint32_t* __restrict__ out, uint64_t n, uint32_t p,
+                                         uint32_t ld, ModpExceptions ex) {
   for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
-       i += (uint64_t)gridDim.x * blockDim.x)
-    out[i] = (uint32_t)(acc[i] % p);
+       i += (uint64_t)gridDim.x * blockDim.x) {
+    unsigned long long v = acc[i];
+    if (ex.cnt) {
+      const uint32_t b = (uint32_t)(i / ld), r = (uint32_t)(i % ld);
+      const uint32_t k = ex.cnt[b];
+      if (k) {
+        const uint8_t* Dr = ex.D + (size_t)(r >> 7) * ex.G * 2048 + (r & 127u) * 16u;
+        unsigned long long sum = 0;
+        if (k <= ex.cap) {
+          const uint32_t* lst = ex.list + (size_t)b * ex.cap;
+#pragma unroll 4
+          for (uint32_t e = 0; e < k; ++e) {
+            const uint32_t c = lst[e];
+            sum += Dr[(size_t)(c >> 4) * 2048 + (c & 15u)];
+          }
+        } else {
+          const uint32_t* q = ex.Q + (size_t)b * ex.m;
+          for (uint32_t c = 0; c < ex.m; ++c)
+            if (__ldg(q + c) % p == 65536u) sum += Dr[(size_t)(c >> 4) * 2048 + (c & 15u)];
+        }
+        v += sum << 16;
+      }
+    }
+    out[i] = (uint32_t)(v % p);
+  }
 }
 }  // namespace qpir

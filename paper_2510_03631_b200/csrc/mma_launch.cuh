@@ -28,6 +28,7 @@ struct MmaJob {
   int mt = 2;            // row panels per CTA tile (1 or 2)
   int gpb = 8;           // column groups per pipeline stage (4 or 8)
   bool out_prezeroed = false;  // caller zeroed `out` (strided chunks): no memset here
+  ModpExceptions exc;          // OUT_MODP2, p = 65537: applied by the fixup
 };
 
 // BN for 3 limbs per query (OUT_MODP3): a multiple of 48 so queries never
@@ -51,7 +52,8 @@ inline uint32_t mma_pick_bn(uint64_t ncols) {
 inline uint32_t mma_choose_splits(uint32_t tiles, uint32_t kblocks, uint32_t sms, int forced,
                                   uint32_t min_splits) {
   if (forced > 0)
-    return std::max<uint32_t>(min_splits, std::min<uint32_t>((uint32_t)forced, kblocks));
+    return std::max<uint32_t>(min_splits,
+                              std::min<uint32_t>(std::min<uint32_t>((uint32_t)forced, 65536u), kblocks));
   auto eff = [&](uint32_t units) {
     const uint32_t waves = (units + sms - 1) / sms;
     return (double)units / ((double)waves * sms);
@@ -84,7 +86,7 @@ cudaError_t mma_launch_cfg(const MmaJob& j, cudaStream_t st, uint64_t* launches)
   a.n_tiles = j.Npad / BN;
   const uint32_t kblocks = j.G / GPB;
   // OUT_MODP(3): each split's limb sums must stay exact in u32 (<= 66051 cells)
-  constexpr bool modp = MODE == OUT_MODP || MODE == OUT_MODP3;
+  constexpr bool modp = MODE == OUT_MODP || MODE == OUT_MODP3 || MODE == OUT_MODP2;
   const uint32_t max_kps = modp ? 66048u / (16u * GPB) : kblocks;
   const uint32_t min_splits = (kblocks + max_kps - 1) / max_kps;
   a.splits = mma_choose_splits(a.m_tiles * a.n_tiles, kblocks, (uint32_t)j.num_sms,
@@ -110,7 +112,7 @@ cudaError_t mma_launch_cfg(const MmaJob& j, cudaStream_t st, uint64_t* launches)
   if (e != cudaSuccess) return e;
   if (modp) {
     const uint32_t blocks = (uint32_t)std::min<uint64_t>((j.out_elems + 255) / 256, 4096);
-    modp_fixup_kernel<<<blocks, 256, 0, st>>>(j.out64, j.out, j.out_elems, j.p);
+    modp_fixup_kernel<<<blocks, 256, 0, st>>>(j.out64, j.out, j.out_elems, j.p, j.out_ld, j.exc);
     ++*launches;
     e = cudaGetLastError();
   }

@@ -58,6 +58,8 @@ struct Arena {
   uint64_t big_out_bytes = 0;
   unsigned long long* acc64 = nullptr;  // OUT_MODP accumulator
   uint64_t acc64_bytes = 0;
+  uint32_t* exc = nullptr;         // OUT_MODP2, p = 65537: [Bc] counts + [Bc][cap] columns
+  uint64_t exc_bytes = 0;
 };
 
 struct qpir_ctx {
@@ -83,6 +85,7 @@ struct qpir_ctx {
   int mma_split = 0;   // env QPIR_MMA_SPLIT (0 = auto)
   int mma_gpb = 8;     // env QPIR_MMA_GPB (column groups per pipeline stage: 4 or 8)
   int modp3 = 1;       // env QPIR_MODP3 (3 limbs per query for p < 2^24)
+  int modp2 = 1;       // env QPIR_MODP2 (2 limbs per query for p <= 65537)
   uint64_t limb_budget = 2ull << 30;  // env QPIR_LIMB_BUDGET_MB: max bytes of Q'/A' at once
   std::string err;
 };
@@ -321,7 +324,8 @@ int gemv(qpir_ctx* ctx, const uint32_t* qu, uint32_t* ans, cudaStream_t st) {
 template <int MODE>
 int launch_mma(qpir_ctx* ctx, uint32_t BN, const uint8_t* Bl, uint32_t Npad, uint32_t* out,
                uint32_t n_out, uint32_t out_ld, uint64_t out_elems, cudaStream_t st,
-               uint32_t p = 0, unsigned long long* out64 = nullptr, bool prezeroed = false) {
+               uint32_t p = 0, unsigned long long* out64 = nullptr, bool prezeroed = false,
+               const ModpExceptions& exc = ModpExceptions()) {
   const Geometry& g = ctx->geo;
   MmaJob j;
   j.A = ctx->D;
@@ -342,6 +346,7 @@ int launch_mma(qpir_ctx* ctx, uint32_t BN, const uint8_t* Bl, uint32_t Npad, uin
   j.mt = ctx->mma_mt;
   j.gpb = ctx->mma_gpb;
   j.out_prezeroed = prezeroed;
+  j.exc = exc;
   const cudaError_t e = mma_launch<MODE>(j, st, &ctx->launches);
   if (e != cudaSuccess)
     return fail(ctx, e == cudaErrorMemoryAllocation ? QPIR_E_OOM : QPIR_E_CUDA,
@@ -396,6 +401,7 @@ int qpir_setup(const qpir_params* params, const uint8_t* records, uint64_t recor
   ctx->mma_split = env_int("QPIR_MMA_SPLIT", 0);
   ctx->mma_gpb = env_int("QPIR_MMA_GPB", 8);
   ctx->modp3 = env_int("QPIR_MODP3", 1);
+  ctx->modp2 = env_int("QPIR_MODP2", 1);
   if (env_int("QPIR_LIMB_BUDGET_MB", 0) > 0)
     ctx->limb_budget = (uint64_t)env_int("QPIR_LIMB_BUDGET_MB", 0) << 20;
   cudaStream_t st = (cudaStream_t)stream;
@@ -535,9 +541,11 @@ static int answer_batch_impl(qpir_ctx* ctx, const uint32_t* Q, uint64_t B, uint6
   if (wq < 0 || wa < 0) return fail(ctx, QPIR_E_PARAM, "Q/ans_local: memory of another device");
   if ((reinterpret_cast<uintptr_t>(Q) & 3u) || (reinterpret_cast<uintptr_t>(ans_local) & 3u))
     return fail(ctx, QPIR_E_PARAM, "Q/ans_local: not 4-byte aligned");
-  // F_p with p < 2^24: 3 limbs per query after reducing entries mod p
-  const bool three = p != 0 && p <= (1u << 24) && ctx->modp3;
-  const uint32_t LPQ = three ? 3u : 4u;
+  // F_p: entries reduced mod p, then 2 limbs per query for p <= 65537 (the
+  // residue 65536 of p = 65537 as a listed exception), 3 for p <= 2^24
+  const bool two = p != 0 && p <= 65537u && ctx->modp2;
+  const bool three = !two && p != 0 && p <= (1u << 24) && ctx->modp3;
+  const uint32_t LPQ = two ? 2u : three ? 3u : 4u;
   // Q' (LPQ limb columns per query) is materialised per chunk of queries so
   // that it stays within ~2 GiB whatever B and m are.
   const uint64_t budget = ctx->limb_budget;
@@ -567,6 +575,18 @@ static int answer_batch_impl(qpir_ctx* ctx, const uint32_t* Q, uint64_t B, uint6
     rc = ensure(ctx, (void**)&ar.acc64, &ar.acc64_bytes, (uint64_t)std::min(Bc, B) * g.ell_local * 8);
     if (rc) return rc;
   }
+  // exception lists: Poisson(m / p) entries per uniform query; cap ~ 4x the
+  // mean + 64, an overflowed (adversarial) query falls back to a rescan
+  const bool exc = two && p == 65537u;
+  const uint32_t cap = (uint32_t)std::min<uint64_t>(g.m, 64 + 4 * ((g.m + 65536) / 65537));
+  uint32_t *exc_cnt = nullptr, *exc_list = nullptr;
+  if (exc) {
+    const uint64_t nb = std::min(Bc, B);
+    rc = ensure(ctx, (void**)&ar.exc, &ar.exc_bytes, nb * 4 * (1 + (uint64_t)cap));
+    if (rc) return rc;
+    exc_cnt = ar.exc;
+    exc_list = ar.exc + nb;
+  }
   for (uint64_t b0 = 0; b0 < B && rc == QPIR_OK; b0 += Bc) {
     const uint32_t bc = (uint32_t)std::min<uint64_t>(Bc, B - b0);
     const uint32_t* Qc = Qd + b0 * g.m;
@@ -575,17 +595,38 @@ static int answer_batch_impl(qpir_ctx* ctx, const uint32_t* Q, uint64_t B, uint6
     {
       const uint32_t nq = Npad / LPQ;  // padded query slots
       dim3 grid((uint32_t)((g.G + 127) / 128), nq);
-      if (three)
+      if (exc) CUDA_TRY(ctx, cudaMemsetAsync(exc_cnt, 0, (uint64_t)bc * 4, st));
+      if (two)
+        limb_split_kernel<2><<<grid, 128, 0, st>>>(Qc, ar.limbs, bc, (uint32_t)g.m,
+                                                   (uint32_t)g.G, Npad, BN, p, exc_cnt,
+                                                   exc_list, cap);
+      else if (three)
         limb_split_kernel<3><<<grid, 128, 0, st>>>(Qc, ar.limbs, bc, (uint32_t)g.m,
-                                                   (uint32_t)g.G, Npad, BN, p);
+                                                   (uint32_t)g.G, Npad, BN, p, nullptr,
+                                                   nullptr, 0u);
       else
         limb_split_kernel<4><<<grid, 128, 0, st>>>(Qc, ar.limbs, bc, (uint32_t)g.m,
-                                                   (uint32_t)g.G, Npad, BN, 0u);
+                                                   (uint32_t)g.G, Npad, BN, 0u, nullptr,
+                                                   nullptr, 0u);
       LAUNCH_CHECK(ctx);
     }
     if (p == 0)
       rc = launch_mma<OUT_QUERY_MAJOR>(ctx, BN, ar.limbs, Npad, oc, bc, (uint32_t)g.ell_local, oe,
                                        st);
+    else if (two) {
+      ModpExceptions ex;
+      if (exc) {
+        ex.D = ctx->D;
+        ex.G = (uint32_t)g.G;
+        ex.Q = Qc;
+        ex.m = (uint32_t)g.m;
+        ex.cnt = exc_cnt;
+        ex.list = exc_list;
+        ex.cap = cap;
+      }
+      rc = launch_mma<OUT_MODP2>(ctx, BN, ar.limbs, Npad, oc, bc, (uint32_t)g.ell_local, oe, st,
+                                 p, ar.acc64, false, ex);
+    }
     else if (three)
       rc = launch_mma<OUT_MODP3>(ctx, BN, ar.limbs, Npad, oc, bc, (uint32_t)g.ell_local, oe, st,
                                  p, ar.acc64);
@@ -682,7 +723,8 @@ void qpir_destroy(qpir_ctx* ctx) {
     if (b) cudaFree(b);
   for (auto& kv : ctx->arenas) {
     Arena& a = kv.second;
-    void* ab[] = {a.qu_dev, a.ans_dev, a.partial, a.tickets, a.limbs, a.big_in, a.big_out, a.acc64};
+    void* ab[] = {a.qu_dev, a.ans_dev, a.partial, a.tickets, a.limbs, a.big_in, a.big_out, a.acc64,
+                  a.exc};
     for (void* b : ab)
       if (b) cudaFree(b);
   }

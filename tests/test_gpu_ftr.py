@@ -54,3 +54,25 @@ def test_ftr_end_to_end_reconstruct(cuda_ok):
     for i, th in enumerate(thetas):
         got = O.ftr_reconstruct(resp[i][1:t + 2], [2, 3, 4])  # servers 2..4
         assert (got == rec[th]).all()
+
+
+def test_ftr_two_limb_exceptions(cuda_ok):
+    """p <= 65537 runs on 2 byte limbs; for p = 65537 the residue 65536 is the one
+    value 2 limbs cannot hold and goes through the exception list (cap entries per
+    query) or, past the cap, the rescan path.  Exact in every case."""
+    Pk = _P()
+    r, s = 70001, 8  # 2 K-splits; cap = 64 + 4 * ceil-ish(r / p) = 72
+    rec = synth.uniform_u8_np(21, (r, s))
+    cap = 64 + 4 * ((r + 65536) // 65537)
+    Q = synth.uniform_u32_np(22, (5, r))
+    rng = np.random.default_rng(23)
+    for b, n_exc in enumerate([cap, cap + 1, int(0.3 * r)]):
+        cols = rng.choice(r, n_exc, replace=False)
+        k = rng.integers(0, 65535, n_exc, dtype=np.uint64)  # raw u32 with residue 65536
+        Q[b, cols] = (65536 + k * 65537).astype(np.uint32)
+    Q[3, :] = 65536  # every entry
+    for p in (65537, 65521, 257, 65536):
+        want = ((Q % p).astype(np.int64) @ rec.astype(np.int64)) % p
+        with Pk.FtrServer(r, s, p=p, records=rec) as srv:
+            got = Pk.u32(srv.answer_batch(Q))
+        assert (got == want.astype(np.uint32)).all(), p
