@@ -39,10 +39,46 @@ struct EnsArgs {
   uint4* partial;       // [gridDim.x][W] CTA partials (group reduction), or nullptr
   uint32_t* tickets;    // [ceil(grid / group)] zero-initialised, self-resetting
   uint32_t group;       // CTAs per reduction group
+  // In-kernel finalisation (single-share answer / OOP online): the last CTA to
+  // finish its atomics writes fin_out[i] = out[i] ^ init[i] (i < d bytes) and
+  // re-zeroes `out` and `done`, so a call is one kernel with no memset or
+  // copies around it.  fin_out == nullptr: the result stays in `out`.
+  uint8_t* fin_out;
+  const uint8_t* init;  // XORed into the result (OOP's A_i), or nullptr
+  uint32_t d;           // record bytes
+  uint32_t* done;       // zero-initialised, self-resetting
+  uint32_t leaders;     // CTAs that reach the atomics (grid, or groups)
 };
 
+// Called by every thread of a CTA that has just added its partial into a.out.
+__device__ __forceinline__ void ens_finalize(const EnsArgs& a) {
+  if (a.fin_out == nullptr) return;
+  __shared__ uint32_t s_fin;
+  __threadfence();
+  __syncthreads();
+  if (threadIdx.x == 0) s_fin = (atomicAdd(a.done, 1u) == a.leaders - 1) ? 1u : 0u;
+  __syncthreads();
+  if (!s_fin) return;
+  __threadfence();
+  for (uint32_t i = threadIdx.x; i < a.dp / 4; i += blockDim.x) {
+    const uint32_t v = __ldcg(a.out + i);  // every CTA's atomics, resolved at L2
+    a.out[i] = 0u;
+#pragma unroll
+    for (uint32_t b = 0; b < 4; ++b) {
+      const uint32_t k = 4 * i + b;
+      if (k < a.d) {
+        uint8_t x = (uint8_t)(v >> (8 * b));
+        if (a.init) x ^= a.init[k];
+        a.fin_out[k] = x;
+      }
+    }
+  }
+  if (threadIdx.x == 0) *a.done = 0u;
+}
+
 template <int UR>
-__global__ void __launch_bounds__(1024) ens_scan_kernel(EnsArgs a) {
+__global__ void __launch_bounds__(1024, 1) ens_scan_kernel(EnsArgs a) {
+  asm volatile("griddepcontrol.launch_dependents;");  // PDL: see ens_scan_wide_kernel
   extern __shared__ uint4 s_part[];
   const uint32_t w = threadIdx.x % a.W;
   const uint32_t lr = threadIdx.x / a.W;
@@ -75,6 +111,7 @@ __global__ void __launch_bounds__(1024) ens_scan_kernel(EnsArgs a) {
       acc.w ^= v[u].w;
     }
   }
+  asm volatile("griddepcontrol.wait;" ::: "memory");  // previous grid complete + visible
   const bool owner = lr == 0;  // one thread per 16-byte chunk keeps the CTA result
   if (R > 1) {
     s_part[threadIdx.x] = acc;
@@ -118,28 +155,41 @@ __global__ void __launch_bounds__(1024) ens_scan_kernel(EnsArgs a) {
     }
     if (threadIdx.x == 0) a.tickets[grp] = 0u;
   }
-  if (!owner) return;
-  uint32_t* o = a.out + (size_t)w * 4;
-  if (acc.x) atomicXor(o + 0, acc.x);
-  if (acc.y) atomicXor(o + 1, acc.y);
-  if (acc.z) atomicXor(o + 2, acc.z);
-  if (acc.w) atomicXor(o + 3, acc.w);
+  if (owner) {
+    uint32_t* o = a.out + (size_t)w * 4;
+    if (acc.x) atomicXor(o + 0, acc.x);
+    if (acc.y) atomicXor(o + 1, acc.y);
+    if (acc.z) atomicXor(o + 2, acc.z);
+    if (acc.w) atomicXor(o + 3, acc.w);
+  }
+  ens_finalize(a);
 }
 
-// Wide-record variant (blockDim == W, one row per CTA step: d > 2 KB, e.g.
-// the paper's 3 KB records).  The row is warp-uniform, so the selector bit is
-// tested once per row from a 32-row word loaded once (CTA ranges start on
-// 32-row boundaries relative to row_lo, the share's bit 0), the row pointer
-// advances by dp, and unselected rows issue no load at all: ~8 instructions
-// per 16-byte chunk instead of ~20 for the general kernel.
-template <int UR>
-__global__ void __launch_bounds__(1024) ens_scan_wide_kernel(EnsArgs a) {
-  const uint32_t w = threadIdx.x;  // 16-byte chunk of the row
+// Wide-record variant (one row per CTA step: d > 2 KB, e.g. the paper's 3 KB
+// records).  The row is warp-uniform, so the selector bit is tested once per
+// row from a 32-row word loaded once (CTA ranges start on 32-row boundaries
+// relative to row_lo, the share's bit 0), the row pointer advances by dp, and
+// unselected rows issue no load at all: ~8 instructions per chunk instead of
+// ~20 for the general kernel.  CW = 16-byte chunks per thread (blockDim =
+// W / CW): CW = 2 uses 256-bit loads, doubling the bytes each thread has in
+// flight (measured slower than CW = 1: opt-in, QPIR_ENS_WIDE=2).  The launch
+// bounds (1024, 1) let ptxas spend 64 registers and keep ~11 row loads in
+// flight per thread; under plain (1024) it packed into 32 registers and issued
+// the loads two at a time (SASS), latency-bound at 0.61-0.90 of HBM.
+// Programmatic dependent launch: only the scan (reads of R and q) runs before
+// griddepcontrol.wait, so back-to-back answers overlap one's tail with the
+// next one's first loads; partials, tickets and out are touched after it.
+template <int UR, int CW>
+__global__ void __launch_bounds__(1024, 1) ens_scan_wide_kernel(EnsArgs a) {
+  asm volatile("griddepcontrol.launch_dependents;");
+  const uint32_t w = threadIdx.x * CW;  // first 16-byte chunk of this thread
   const uint64_t n_rows = a.row_hi - a.row_lo;
   const uint64_t t0 = (uint64_t)blockIdx.x * a.rows_per_cta;  // multiple of 32
   const uint64_t t1 = min(n_rows, t0 + a.rows_per_cta);
   const uint32_t* q32 = reinterpret_cast<const uint32_t*>(a.q);  // 4-byte aligned
-  uint4 acc = make_uint4(0, 0, 0, 0);
+  uint4 acc[CW];
+#pragma unroll
+  for (int c = 0; c < CW; ++c) acc[c] = make_uint4(0, 0, 0, 0);
   for (uint64_t tb = t0; tb < t1; tb += 32) {
     uint32_t sel = __ldg(q32 + (tb >> 5));
     const uint32_t nrow = (t1 - tb) < 32 ? (uint32_t)(t1 - tb) : 32u;
@@ -147,22 +197,31 @@ __global__ void __launch_bounds__(1024) ens_scan_wide_kernel(EnsArgs a) {
     const uint8_t* p = a.R + (size_t)(a.row_lo + tb) * a.dp + (size_t)w * 16;
 #pragma unroll
     for (int h = 0; h < 32; h += UR) {
-      uint4 v[UR];
-#pragma unroll
-      for (int u = 0; u < UR; ++u)
-        v[u] = ldg_stream_v4_if(p + (size_t)(h + u) * a.dp, (sel >> (h + u)) & 1u);
+      uint4 v[UR][CW];
 #pragma unroll
       for (int u = 0; u < UR; ++u) {
-        acc.x ^= v[u].x;
-        acc.y ^= v[u].y;
-        acc.z ^= v[u].z;
-        acc.w ^= v[u].w;
+        const bool on = (sel >> (h + u)) & 1u;
+        if constexpr (CW == 2)
+          ldg_stream_v8_if(p + (size_t)(h + u) * a.dp, on, v[u][0], v[u][1]);
+        else
+          v[u][0] = ldg_stream_v4_if(p + (size_t)(h + u) * a.dp, on);
       }
+#pragma unroll
+      for (int u = 0; u < UR; ++u)
+#pragma unroll
+        for (int c = 0; c < CW; ++c) {
+          acc[c].x ^= v[u][c].x;
+          acc[c].y ^= v[u][c].y;
+          acc[c].z ^= v[u][c].z;
+          acc[c].w ^= v[u][c].w;
+        }
     }
   }
+  asm volatile("griddepcontrol.wait;" ::: "memory");  // previous grid complete + visible
   if (a.partial != nullptr) {
     __shared__ uint32_t s_last;
-    a.partial[(size_t)blockIdx.x * a.W + w] = acc;
+#pragma unroll
+    for (int c = 0; c < CW; ++c) a.partial[(size_t)blockIdx.x * a.W + w + c] = acc[c];
     __threadfence();
     __syncthreads();
     const uint32_t grp = blockIdx.x / a.group;
@@ -175,21 +234,29 @@ __global__ void __launch_bounds__(1024) ens_scan_wide_kernel(EnsArgs a) {
     __syncthreads();
     if (!s_last) return;
     __threadfence();
-    acc = make_uint4(0, 0, 0, 0);
-    for (uint32_t c = g0; c < g1; ++c) {
-      const uint4 v = __ldcg(a.partial + (size_t)c * a.W + w);
-      acc.x ^= v.x;
-      acc.y ^= v.y;
-      acc.z ^= v.z;
-      acc.w ^= v.w;
+#pragma unroll
+    for (int c = 0; c < CW; ++c) acc[c] = make_uint4(0, 0, 0, 0);
+    for (uint32_t g = g0; g < g1; ++g) {
+#pragma unroll
+      for (int c = 0; c < CW; ++c) {
+        const uint4 v = __ldcg(a.partial + (size_t)g * a.W + w + c);
+        acc[c].x ^= v.x;
+        acc[c].y ^= v.y;
+        acc[c].z ^= v.z;
+        acc[c].w ^= v.w;
+      }
     }
     if (threadIdx.x == 0) a.tickets[grp] = 0u;
   }
-  uint32_t* o = a.out + (size_t)w * 4;
-  if (acc.x) atomicXor(o + 0, acc.x);
-  if (acc.y) atomicXor(o + 1, acc.y);
-  if (acc.z) atomicXor(o + 2, acc.z);
-  if (acc.w) atomicXor(o + 3, acc.w);
+#pragma unroll
+  for (int c = 0; c < CW; ++c) {
+    uint32_t* o = a.out + (size_t)(w + c) * 4;
+    if (acc[c].x) atomicXor(o + 0, acc[c].x);
+    if (acc[c].y) atomicXor(o + 1, acc[c].y);
+    if (acc[c].z) atomicXor(o + 2, acc[c].z);
+    if (acc[c].w) atomicXor(o + 3, acc[c].w);
+  }
+  ens_finalize(a);
 }
 
 // Selector bits transposed for the batch: Qt[t][k] bit i = share (32k + i) bit t.

@@ -48,6 +48,27 @@ __device__ __forceinline__ uint4 ldg_stream_v4_if(const void* p, bool pred) {
   return r;
 }
 
+// 256-bit predicated streaming load (sm_100: LDG.E.NA.ENL2.256), zero if !pred.
+__device__ __forceinline__ void ldg_stream_v8_if(const void* p, bool pred, uint4& lo, uint4& hi) {
+  asm(
+      "{\n\t"
+      ".reg .pred q;\n\t"
+      "setp.ne.b32 q, %9, 0;\n\t"
+      "mov.u32 %0, 0;\n\t"
+      "mov.u32 %1, 0;\n\t"
+      "mov.u32 %2, 0;\n\t"
+      "mov.u32 %3, 0;\n\t"
+      "mov.u32 %4, 0;\n\t"
+      "mov.u32 %5, 0;\n\t"
+      "mov.u32 %6, 0;\n\t"
+      "mov.u32 %7, 0;\n\t"
+      "@q ld.global.nc.L1::no_allocate.v8.u32 {%0, %1, %2, %3, %4, %5, %6, %7}, [%8];\n\t"
+      "}"
+      : "=r"(lo.x), "=r"(lo.y), "=r"(lo.z), "=r"(lo.w), "=r"(hi.x), "=r"(hi.y), "=r"(hi.z),
+        "=r"(hi.w)
+      : "l"(p), "r"((uint32_t)pred));
+}
+
 // ---------------------------------------------------------------- mbarrier
 __device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
   asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));

@@ -24,6 +24,9 @@ struct qpir_ens_ctx {
   uint8_t* q_dev = nullptr;   // staging for one share (ceil(r/8))
   uint32_t* acc = nullptr;    // [max_B][dp/4] XOR accumulators
   uint64_t acc_B = 0;
+  uint32_t* acc1 = nullptr;   // [dp/4] + 1 done ticket: single-scan accumulator, kept zero
+  uint8_t* io_stage = nullptr;  // [2][d]: host A_i in / host answer out of a single scan
+  uint64_t io_stage_bytes = 0;
   uint8_t* Q_dev = nullptr;   // staging for a batch of shares
   uint64_t Q_bytes = 0;
   uint32_t* Qt = nullptr;     // transposed selector bits
@@ -35,7 +38,9 @@ struct qpir_ens_ctx {
   uint32_t* tickets = nullptr;  // scan group tickets (self-resetting)
   uint64_t tickets_bytes = 0;
   int group = 0;                // env QPIR_ENS_GROUP (0 = auto 32; 1 = atomics only)
-  int wide = 1;                 // env QPIR_ENS_WIDE (uniform-row kernel for d > 2 KB)
+  int wide = 1;                 // env QPIR_ENS_WIDE (uniform-row kernel for d > 2 KB;
+                                //   2 = 32-byte chunks per thread, 256-bit loads)
+  int pdl = 1;                  // env QPIR_ENS_PDL (programmatic dependent launch of scans)
   // tensor-core multi-request path (bit-planes, 8x the record bytes)
   uint8_t* bitD = nullptr;
   uint64_t bitD_bytes = 0;
@@ -137,19 +142,23 @@ int qpir_ens_setup(const qpir_ens_params* p, const uint8_t* records, uint64_t re
   ctx->ur = env_int("QPIR_ENS_UR", 16);
   ctx->group = env_int("QPIR_ENS_GROUP", 0);
   ctx->wide = env_int("QPIR_ENS_WIDE", 1);
+  ctx->pdl = env_int("QPIR_ENS_PDL", 1);
   ctx->tc = env_int("QPIR_ENS_TC", -1);
   ctx->mma_split = env_int("QPIR_MMA_SPLIT", 0);
   cudaStream_t st = (cudaStream_t)stream;
   const uint64_t nb = (ctx->r + 7) / 8;
   if (cudaMalloc(&ctx->R, ctx->r * ctx->dp) != cudaSuccess ||
-      cudaMalloc(&ctx->q_dev, round_up(nb, 16)) != cudaSuccess) {
+      cudaMalloc(&ctx->q_dev, round_up(nb, 16)) != cudaSuccess ||
+      cudaMalloc(&ctx->acc1, ctx->dp + 16) != cudaSuccess) {
     cudaGetLastError();
     g_ens_setup_error = "records: cudaMalloc failed";
     qpir_ens_destroy(ctx);
     return QPIR_E_OOM;
   }
   int rc = QPIR_OK;
-  if (cudaMemsetAsync(ctx->R, 0, ctx->r * ctx->dp, st) != cudaSuccess) rc = QPIR_E_CUDA;
+  if (cudaMemsetAsync(ctx->R, 0, ctx->r * ctx->dp, st) != cudaSuccess ||
+      cudaMemsetAsync(ctx->acc1, 0, ctx->dp + 16, st) != cudaSuccess)
+    rc = QPIR_E_CUDA;
   if (!rc && records) rc = qpir_ens_db_write(ctx, 0, ctx->r, records, records_len, stream);
   if (!rc && cudaStreamSynchronize(st) != cudaSuccess) rc = QPIR_E_CUDA;
   if (rc) {
@@ -185,26 +194,33 @@ int qpir_ens_db_write(qpir_ens_ctx* ctx, uint64_t theta_begin, uint64_t n_record
   return QPIR_OK;
 }
 
+// One scan of rows [row_lo, row_hi) selected by share_dev, finalised in the
+// kernel: out_dev (device, d bytes) = init_dev ^ XOR of the selected rows.
 static int scan_range(qpir_ens_ctx* ctx, const uint8_t* share_dev, uint64_t row_lo,
-                      uint64_t row_hi, cudaStream_t st) {
+                      uint64_t row_hi, const uint8_t* init_dev, uint8_t* out_dev,
+                      cudaStream_t st) {
   EnsArgs a;
   a.R = ctx->R;
   a.q = share_dev;
-  a.out = ctx->acc;
+  a.out = ctx->acc1;
+  a.fin_out = out_dev;
+  a.init = init_dev;
+  a.d = (uint32_t)ctx->d;
+  a.done = ctx->acc1 + ctx->dp / 4;
   a.row_lo = row_lo;
   a.row_hi = row_hi;
   a.dp = (uint32_t)ctx->dp;
   a.W = (uint32_t)(ctx->dp / 16);
   const uint32_t R = std::max<uint32_t>(1, 256 / a.W);
-  const uint32_t threads = a.W * R;
+  uint32_t threads = a.W * R;
   const int UR = ctx->ur == 8 ? 8 : ctx->ur == 4 ? 4 : 16;
   uint64_t rows = ctx->rows_per_cta;
   if (rows == 0) {
-    // ~192 KB of records per CTA (measured best on B200 at d = 3072: 64 rows
-    // with the two-level reduction, profiles/r01_sweep_run10.log), at least
-    // ~4 CTAs per SM for short ranges (OOP flip chunks), and at least one full
-    // unrolled step
-    const uint64_t by_bytes = (192u << 10) / ctx->dp;
+    // ~384 KB of records per CTA (measured best on B200 at d = 3072 with the
+    // 64-register wide kernel: 128 rows, profiles/r01_sweep_run40.log; 64 rows
+    // before, run10), at least ~4 CTAs per SM for short ranges (OOP flip
+    // chunks), and at least one full unrolled step
+    const uint64_t by_bytes = (384u << 10) / ctx->dp;
     const uint64_t by_occ = (row_hi - row_lo + 4ull * ctx->num_sms - 1) / (4ull * ctx->num_sms);
     rows = std::max<uint64_t>(std::min(by_bytes, by_occ), (uint64_t)R * UR);
   }
@@ -230,20 +246,30 @@ static int scan_range(qpir_ens_ctx* ctx, const uint8_t* share_dev, uint64_t row_
     a.tickets = ctx->tickets;
     a.group = group;
   }
+  a.leaders = (uint32_t)(a.partial ? (grid + a.group - 1) / a.group : grid);
   const size_t smem = R > 1 ? threads * 16 : 0;
   const bool wide = R == 1 && ctx->wide && (rows % 32 == 0) &&
                     ((reinterpret_cast<uintptr_t>(share_dev) & 3u) == 0);
-  if (wide) {
-    if (UR == 8)
-      ens_scan_wide_kernel<8><<<(uint32_t)grid, threads, 0, st>>>(a);
-    else
-      ens_scan_wide_kernel<16><<<(uint32_t)grid, threads, 0, st>>>(a);
-  } else if (UR == 16)
-    ens_scan_kernel<16><<<(uint32_t)grid, threads, smem, st>>>(a);
-  else if (UR == 4)
-    ens_scan_kernel<4><<<(uint32_t)grid, threads, smem, st>>>(a);
+  // 32-byte chunks per thread (256-bit loads) when the row stride allows
+  const bool cw2 = wide && ctx->wide == 2 && (a.dp % 32 == 0);
+  if (cw2) threads = a.W / 2;
+  void (*kern)(EnsArgs);
+  if (wide)
+    kern = cw2 ? ens_scan_wide_kernel<16, 2>
+               : UR == 8 ? ens_scan_wide_kernel<8, 1> : ens_scan_wide_kernel<16, 1>;
   else
-    ens_scan_kernel<8><<<(uint32_t)grid, threads, smem, st>>>(a);
+    kern = UR == 16 ? ens_scan_kernel<16> : UR == 4 ? ens_scan_kernel<4> : ens_scan_kernel<8>;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3((uint32_t)grid);
+  cfg.blockDim = dim3(threads);
+  cfg.dynamicSmemBytes = wide ? 0 : smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = ctx->pdl ? 1 : 0;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  ENS_CUDA(ctx, cudaLaunchKernelEx(&cfg, kern, a));
   ENS_LAUNCHED(ctx);
   return QPIR_OK;
 }
@@ -262,15 +288,21 @@ int qpir_ens_answer(qpir_ens_ctx* ctx, const uint8_t* share, uint64_t len_share,
                     (unsigned long long)ctx->d);
   DeviceGuard dg(ctx->device);
   cudaStream_t st = (cudaStream_t)stream;
-  int rc = grow(ctx, (void**)&ctx->acc, &ctx->acc_B, ctx->dp);
+  const int wo = where(out, ctx->device);
+  if (wo < 0) return ENS_FAIL(ctx, QPIR_E_PARAM, "out: memory of another device");
+  int rc = grow(ctx, (void**)&ctx->io_stage, &ctx->io_stage_bytes, 2 * ctx->d);
   if (rc) return rc;
   const uint8_t* qd = nullptr;
   rc = stage_in(ctx, share, nb, ctx->q_dev, &qd, st);
   if (rc) return rc;
-  ENS_CUDA(ctx, cudaMemsetAsync(ctx->acc, 0, ctx->dp, st));
-  rc = scan_range(ctx, qd, 0, ctx->r, st);
+  uint8_t* od = wo ? out : ctx->io_stage + ctx->d;
+  rc = scan_range(ctx, qd, 0, ctx->r, nullptr, od, st);
   if (rc) return rc;
-  return copy_out(ctx, out, 1, st);
+  if (!wo) {
+    ENS_CUDA(ctx, cudaMemcpyAsync(out, od, ctx->d, cudaMemcpyDeviceToHost, st));
+    ENS_CUDA(ctx, cudaStreamSynchronize(st));
+  }
+  return QPIR_OK;
 }
 
 int qpir_oop_answer(qpir_ens_ctx* ctx, uint32_t n_chunks, uint32_t server, const uint8_t* q,
@@ -292,20 +324,25 @@ int qpir_oop_answer(qpir_ens_ctx* ctx, uint32_t n_chunks, uint32_t server, const
                     (unsigned long long)ctx->d);
   DeviceGuard dg(ctx->device);
   cudaStream_t st = (cudaStream_t)stream;
-  int rc = grow(ctx, (void**)&ctx->acc, &ctx->acc_B, ctx->dp);
+  const int wo = where(out, ctx->device);
+  if (wo < 0) return ENS_FAIL(ctx, QPIR_E_PARAM, "out: memory of another device");
+  int rc = grow(ctx, (void**)&ctx->io_stage, &ctx->io_stage_bytes, 2 * ctx->d);
   if (rc) return rc;
   const uint8_t* qd = nullptr;
   rc = stage_in(ctx, q, kb, ctx->q_dev, &qd, st);
   if (rc) return rc;
-  // R_i := A_i XOR q_i . chunk_i (Lemma 2): start the accumulator at A_i
-  const int wA = where(A, ctx->device);
-  if (wA < 0) return ENS_FAIL(ctx, QPIR_E_PARAM, "A: memory of another device");
-  ENS_CUDA(ctx, cudaMemsetAsync(ctx->acc, 0, ctx->dp, st));
-  ENS_CUDA(ctx, cudaMemcpyAsync(ctx->acc, A, ctx->d,
-                                wA ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, st));
-  rc = scan_range(ctx, qd, (uint64_t)server * k, (uint64_t)(server + 1) * k, st);
+  // R_i := A_i XOR q_i . chunk_i (Lemma 2): A_i is XORed in by the finalising CTA
+  const uint8_t* Ad = nullptr;
+  rc = stage_in(ctx, A, ctx->d, ctx->io_stage, &Ad, st);
   if (rc) return rc;
-  return copy_out(ctx, out, 1, st);
+  uint8_t* od = wo ? out : ctx->io_stage + ctx->d;
+  rc = scan_range(ctx, qd, (uint64_t)server * k, (uint64_t)(server + 1) * k, Ad, od, st);
+  if (rc) return rc;
+  if (!wo) {
+    ENS_CUDA(ctx, cudaMemcpyAsync(out, od, ctx->d, cudaMemcpyDeviceToHost, st));
+    ENS_CUDA(ctx, cudaStreamSynchronize(st));
+  }
+  return QPIR_OK;
 }
 
 int qpir_oop_preprocess(qpir_ens_ctx* ctx, uint32_t n_chunks, uint32_t server,
@@ -476,7 +513,8 @@ void qpir_ens_destroy(qpir_ens_ctx* ctx) {
   if (!ctx) return;
   DeviceGuard dg(ctx->device);
   void* bufs[] = {ctx->R,       ctx->q_dev,   ctx->acc,  ctx->Q_dev, ctx->Qt,
-                  ctx->seed_dev, ctx->partial, ctx->tickets, ctx->bitD, ctx->Qb};
+                  ctx->seed_dev, ctx->partial, ctx->tickets, ctx->bitD, ctx->Qb,
+                  ctx->acc1,    ctx->io_stage};
   for (void* b : bufs)
     if (b) cudaFree(b);
   delete ctx;

@@ -26,7 +26,7 @@ def _share(seed, r):
                                  (3001, 2500), (100, 16384)])
 @pytest.mark.parametrize("rows,group,wide", [("0", "0", "1"), ("8", "0", "1"), ("8", "3", "1"),
                                              ("8", "1", "1"), ("96", "0", "1"), ("0", "0", "0"),
-                                             ("64", "5", "0")])
+                                             ("64", "5", "0"), ("0", "0", "2"), ("32", "2", "2")])
 def test_ens_answer_matches_oracle(cuda_ok, r, d, rows, group, wide, monkeypatch):
     monkeypatch.setenv("QPIR_ENS_ROWS", rows)
     monkeypatch.setenv("QPIR_ENS_GROUP", group)
@@ -112,3 +112,37 @@ def test_ens_db_write_and_c2_scale(cuda_ok):
         assert (s.answer(q).cpu().numpy() == O.ens_respond(rec, q)).all()
         Q = np.stack([_share(40 + b, r) for b in range(3)])
         assert (s.answer_batch(Q).cpu().numpy() == O.ens_respond_batch(rec, Q)).all()
+
+
+@pytest.mark.parametrize("r,d", [(20000, 3072), (50000, 64), (4099, 100)])
+@pytest.mark.parametrize("pdl", ["1", "0"])
+def test_ens_oop_back_to_back_no_sync(cuda_ok, r, d, pdl, monkeypatch):
+    """Single-share answers and OOP online answers queued back to back on one
+    stream (programmatic dependent launch lets each scan start while the previous
+    one drains; the in-kernel finaliser re-zeroes the accumulator): every
+    response still equals the oracle's."""
+    monkeypatch.setenv("QPIR_ENS_PDL", pdl)
+    P = _P()
+    rec = synth.uniform_u8_np(r + d + 7, (r, d))
+    n = 4
+    k = r // n
+    rec = rec[: k * n]
+    r = k * n
+    shares = [_share(100 + i, r) for i in range(6)]
+    qs = [_share(200 + i, k) for i in range(6)]
+    As = [synth.uniform_u8_np(300 + i, (d,)) for i in range(6)]
+    with P.EnsServer(r, d, records=rec) as s:
+        st = torch.cuda.Stream()
+        dev = [torch.from_numpy(x).cuda() for x in shares]
+        dq = [torch.from_numpy(x).cuda() for x in qs]
+        dA = [torch.from_numpy(x).cuda() for x in As]
+        torch.cuda.synchronize()
+        outs = []
+        for i in range(6):
+            outs.append(s.answer(dev[i], stream=st))
+            outs.append(s.oop_answer(n, i % n, dq[i], dA[i], stream=st))
+        st.synchronize()
+        for i in range(6):
+            assert (outs[2 * i].cpu().numpy() == O.ens_respond(rec, shares[i])).all(), i
+            want = O.oop_respond(rec, n, i % n, qs[i], As[i])
+            assert (outs[2 * i + 1].cpu().numpy() == want).all(), i
