@@ -71,10 +71,18 @@ __global__ void pack_records_kernel(PackArgs a) {
 // LPQ = 2 (p <= 65537): a reduced entry 65536 (only p = 65537) is written as 0
 // and its column appended to the query's exception list (exc_cnt / exc_list,
 // `cap` entries per query) for modp_fixup_kernel.
+// a mod p for any u32 a and 2 <= p < 2^32 with pM = ceil(2^64 / p) (Lemire,
+// Kaser & Kurz, "Faster remainder by direct computation", 2019): exact, and 3
+// integer instructions instead of the ~20 of a runtime u32 division.
+__device__ __forceinline__ uint32_t fastmod_u32(uint32_t a, uint64_t pM, uint32_t p) {
+  return (uint32_t)__umul64hi(pM * a, p);
+}
+
 template <int LPQ>
 __global__ void limb_split_kernel(const uint32_t* __restrict__ Q, uint8_t* __restrict__ Qp,
                                   uint32_t B, uint32_t m, uint32_t G, uint32_t Npad,
-                                  uint32_t BN, uint32_t p, uint32_t* __restrict__ exc_cnt,
+                                  uint32_t BN, uint32_t p, uint64_t pM,
+                                  uint32_t* __restrict__ exc_cnt,
                                   uint32_t* __restrict__ exc_list, uint32_t cap) {
   // threads walk 16-cell groups of one query row (coalesced 64 B per thread);
   // each thread writes its query's LPQ limb rows = 16 * LPQ contiguous bytes
@@ -101,7 +109,7 @@ __global__ void limb_split_kernel(const uint32_t* __restrict__ Q, uint8_t* __res
   }
   if (p != 0) {
 #pragma unroll
-    for (int i = 0; i < 16; ++i) q[i] %= p;
+    for (int i = 0; i < 16; ++i) q[i] = fastmod_u32(q[i], pM, p);
     if constexpr (LPQ == 2) {
       if (exc_cnt) {
 #pragma unroll

@@ -596,18 +596,19 @@ static int answer_batch_impl(qpir_ctx* ctx, const uint32_t* Q, uint64_t B, uint6
       const uint32_t nq = Npad / LPQ;  // padded query slots
       dim3 grid((uint32_t)((g.G + 127) / 128), nq);
       if (exc) CUDA_TRY(ctx, cudaMemsetAsync(exc_cnt, 0, (uint64_t)bc * 4, st));
+      const uint64_t pM = p >= 2 ? ~0ull / p + 1 : 0;  // fastmod_u32 constant
       if (two)
         limb_split_kernel<2><<<grid, 128, 0, st>>>(Qc, ar.limbs, bc, (uint32_t)g.m,
-                                                   (uint32_t)g.G, Npad, BN, p, exc_cnt,
-                                                   exc_list, cap);
+                                                   (uint32_t)g.G, Npad, BN, p, pM,
+                                                   exc_cnt, exc_list, cap);
       else if (three)
         limb_split_kernel<3><<<grid, 128, 0, st>>>(Qc, ar.limbs, bc, (uint32_t)g.m,
-                                                   (uint32_t)g.G, Npad, BN, p, nullptr,
-                                                   nullptr, 0u);
+                                                   (uint32_t)g.G, Npad, BN, p, pM,
+                                                   nullptr, nullptr, 0u);
       else
         limb_split_kernel<4><<<grid, 128, 0, st>>>(Qc, ar.limbs, bc, (uint32_t)g.m,
-                                                   (uint32_t)g.G, Npad, BN, 0u, nullptr,
-                                                   nullptr, 0u);
+                                                   (uint32_t)g.G, Npad, BN, 0u, 0ull,
+                                                   nullptr, nullptr, 0u);
       LAUNCH_CHECK(ctx);
     }
     if (p == 0)

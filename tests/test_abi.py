@@ -88,3 +88,19 @@ def test_null_ctx_calls_fail_cleanly(L):
     assert L._L.qpir_answer(None, None, 0, None, 0, None) == L.QPIR_E_STATE
     assert L._L.qpir_kernel_launches(None) == 0
     L.qpir_destroy(None)
+
+
+def test_fastmod_constant_is_exact():
+    """limb_split_kernel reduces query entries with Lemire's fastmod
+    (a mod p = hi64((M * a mod 2^64) * p), M = floor((2^64 - 1) / p) + 1): check the
+    identity the kernel relies on for every p the tests use and edge-case a."""
+    import random
+    rng = random.Random(5)
+    for p in (2, 3, 7, 255, 256, 257, 65521, 65536, 65537, 2**24 - 3, 2**31 - 1,
+              4294967291, 2**32 - 1):
+        M = (2**64 - 1) // p + 1
+        xs = [0, 1, p - 1, p, p + 1, 2**32 - 1, 2**32 - 2, (2**32 - 1) // p * p] + \
+             [rng.getrandbits(32) for _ in range(2000)]
+        for a in xs:
+            a &= 2**32 - 1
+            assert (((M * a) % 2**64) * p) >> 64 == a % p, (p, a)
