@@ -371,10 +371,13 @@ def run_ens(args, wl, world, rank, local):
                            "(8 x DB bytes read per batch)"}
     roof = (roof_tc if tc_used else
             {"bound": "hbm", "achieved": round(achieved, 1), "peak": hbm, "unit": "GB/s",
-             "frac": round(achieved / hbm, 4), "traffic": None, "kernel": "ens_scan_kernel",
+             "frac": round(achieved / hbm, 4), "traffic": _traffic(args.workload),
+             "kernel": "ens_scan_wide_kernel",
              "kernel_ms": round(ms, 5), "peak_source": f"{peak_src} hbm_gbs",
              "algorithmic_bytes_per_launch": touched + nb + d,
-             "note": "selected rows only (nnz(q) * d), P:968"} if B == 1 else
+             "note": "selected rows only (nnz(q) * d), P:968; back-to-back answers overlap "
+                     "through programmatic dependent launch (one kernel alone under ncu: "
+                     "profiles/r01_ens_scan_pdl_ncu_full.md)"} if B == 1 else
             {"bound": "alu", "achieved": round(B * r * d / 4 / (ms / 1e3) / 1e12, 3),
              "unit": "T word-XOR/s", "peak": round(148 * 64 * 1.965e9 / 1e12, 2),
              "frac": round(B * r * d / 4 / (ms / 1e3) / (148 * 64 * 1.965e9), 4),
@@ -458,12 +461,25 @@ def run_oop(args, wl, rank, local):
                        "offline_queue": 128, "offline_ms_for_128": round(off_ms, 3)},
             "queries_per_s": round(1e3 / ms, 1),
             "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": hbm, "unit": "GB/s",
-                         "frac": round(achieved / hbm, 4), "traffic": None,
-                         "kernel": "ens_scan_kernel (flip chunk)", "kernel_ms": round(ms, 5),
-                         "peak_source": f"{peak_src} hbm_gbs"},
+                         "frac": round(achieved / hbm, 4), "traffic": _traffic(args.workload),
+                         "kernel": "ens_scan_wide_kernel (flip chunk)", "kernel_ms": round(ms, 5),
+                         "peak_source": f"{peak_src} hbm_gbs",
+                         "note": "back-to-back online answers overlap through programmatic "
+                                 "dependent launch (one kernel alone under ncu: "
+                                 "profiles/r01_oop_scan_ncu_full.md)"},
             "cpu_baseline": None, "e2e": None,
             "gpu_launches": srv.kernel_launches - l0, "clocks": sampler.summary()}
     print(json.dumps(line), flush=True)
+
+
+def _traffic(workload):
+    """DRAM bytes per launch of the dominant kernel from a committed ncu --set full
+    summary (profiles/traffic_<workload>.json), else None."""
+    prof = os.path.join(ROOT, "profiles", f"traffic_{workload}.json")
+    try:
+        return json.load(open(prof)).get("dram_bytes_per_launch")
+    except Exception:
+        return None
 
 
 # ---------------------------------------------------------------- our arm
