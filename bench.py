@@ -493,6 +493,9 @@ def main():
     ap.add_argument("--seed", type=int, default=2025)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--graph", type=int, default=None,
+                    help="1: capture the K timed steps into one CUDA graph and replay it "
+                         "(N = 1; default on for the launch-bound c1 workload only)")
     ap.add_argument("--backend", default="nccl", choices=["nccl", "gloo"],
                     help="gloo + --device-override: functional multi-rank test on one GPU")
     ap.add_argument("--device-override", type=int, default=None,
@@ -616,11 +619,27 @@ def main():
             torch.distributed.barrier()
         torch.cuda.synchronize(dev)
 
+    # CUDA-graph mode (launch-bound configs): the K steps are captured once and
+    # replayed as one graph, so the device time is not the host's call rate
+    use_graph = (args.graph if args.graph is not None else args.workload == "c1") and world == 1
+    if use_graph:
+        stream = torch.cuda.Stream(dev)  # capture needs a non-default stream
     sampler = ClockSampler(physical_gpu(local))
     for i in range(args.warmup):
         step(i)
     drain()
     barrier()
+    graph = None
+    if use_graph:
+        l0 = srv.kernel_launches
+        graph = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(graph, stream=stream, capture_error_mode="relaxed"):
+            for i in range(args.steps):
+                step(i)
+        launches = srv.kernel_launches - l0  # launches recorded into the graph
+        with torch.cuda.stream(stream):
+            graph.replay()  # untimed warm replay
+        barrier()
     time.sleep(0.3)  # let the clock sampler come up
     kev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
            for _ in range(args.steps)]
@@ -630,15 +649,28 @@ def main():
     barrier()
     sampler.start()
     e0.record(stream)
-    for i in range(args.steps):
-        step(i, kev[i])
+    # per-step kernel events only when the step has a side-stream gather (N > 1):
+    # an event record between two launches also cuts the programmatic dependent
+    # launch overlap of back-to-back GEMVs, so at N = 1 the step time is the
+    # kernel time
+    per_step_events = world > 1
+    if use_graph:
+        with torch.cuda.stream(stream):
+            graph.replay()
+    else:
+        for i in range(args.steps):
+            step(i, kev[i] if per_step_events else None)
     drain()
     e1.record(stream)
     barrier()
     sampler.stop()
-    launches = srv.kernel_launches - l0
     t_ms = e0.elapsed_time(e1)
-    k_ms = sum(a.elapsed_time(b) for a, b in kev) / args.steps
+    if use_graph:
+        k_ms = t_ms / args.steps  # the replay holds only the captured steps
+    else:
+        launches = srv.kernel_launches - l0
+        k_ms = (sum(a.elapsed_time(b) for a, b in kev) / args.steps if per_step_events
+                else t_ms / args.steps)  # N = 1: only our kernels are in the step
     if world > 1:
         tt = torch.tensor([t_ms, k_ms], device=dev, dtype=torch.float64)
         torch.distributed.all_reduce(tt, op=torch.distributed.ReduceOp.MAX)
@@ -829,7 +861,9 @@ def main():
            "l2": "inputs larger than L2: D slice per GPU >> 126 MB, no flush needed"
                  if db_bytes_local > 512e6 else "D slice fits in L2 (latency config)",
            "setup_s": round(setup_s, 1), "parallelism": f"row-shard x{world}",
-           "backend": args.backend if world > 1 else None}
+           "backend": args.backend if world > 1 else None,
+           "launch": "K steps replayed from one CUDA graph" if use_graph
+                     else "eager C-ABI calls from Python"}
     line = {"metric": METRIC, "value": round(value, 2), "unit": unit, "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms_per_step, 5),
             "higher_is_better": True, "scaling": scaling, "vs_baseline": None,

@@ -146,3 +146,39 @@ def test_ens_oop_back_to_back_no_sync(cuda_ok, r, d, pdl, monkeypatch):
             assert (outs[2 * i].cpu().numpy() == O.ens_respond(rec, shares[i])).all(), i
             want = O.oop_respond(rec, n, i % n, qs[i], As[i])
             assert (outs[2 * i + 1].cpu().numpy() == want).all(), i
+
+
+def test_ens_oop_cuda_graph(cuda_ok):
+    """Single-share ENS and OOP online answers captured into a CUDA graph (PDL
+    edges, in-kernel finalisation) and replayed with new shares: exact."""
+    P = _P()
+    r, d, n = 8000, 3072, 4
+    k = r // n
+    rec = synth.uniform_u8_np(31, (r, d))
+    st = torch.cuda.Stream()
+    with P.EnsServer(r, d, records=rec) as s:
+        sh = torch.empty((r + 7) // 8, dtype=torch.uint8, device="cuda")
+        q = torch.empty((k + 7) // 8, dtype=torch.uint8, device="cuda")
+        A = torch.empty(d, dtype=torch.uint8, device="cuda")
+        o1 = torch.empty(d, dtype=torch.uint8, device="cuda")
+        o2 = torch.empty(d, dtype=torch.uint8, device="cuda")
+        with torch.cuda.stream(st):
+            s.answer(sh, out=o1, stream=st)
+            s.oop_answer(n, 1, q, A, out=o2, stream=st)
+        st.synchronize()
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g, stream=st, capture_error_mode="relaxed"):
+            s.answer(sh, out=o1, stream=st)
+            s.oop_answer(n, 1, q, A, out=o2, stream=st)
+        for rep in range(2):
+            share, qq = _share(40 + rep, r), _share(50 + rep, k)
+            AA = synth.uniform_u8_np(60 + rep, (d,))
+            sh.copy_(torch.from_numpy(share))
+            q.copy_(torch.from_numpy(qq))
+            A.copy_(torch.from_numpy(AA))
+            torch.cuda.synchronize()
+            with torch.cuda.stream(st):
+                g.replay()
+            st.synchronize()
+            assert (o1.cpu().numpy() == O.ens_respond(rec, share)).all(), rep
+            assert (o2.cpu().numpy() == O.oop_respond(rec, n, 1, qq, AA)).all(), rep

@@ -359,6 +359,44 @@ def test_concurrent_streams_have_private_scratch(cuda_ok, monkeypatch):
             assert (_u32(out) == want).all()
 
 
+def test_cuda_graph_capture_and_replay(cuda_ok):
+    """The C-ABI calls are capturable into a CUDA graph once a first eager call
+    has sized the stream's scratch: answers (split-K GEMV with PDL edges) and a
+    tcgen05 batch captured, replayed twice with the query buffers rewritten in
+    place between replays -- every output exact."""
+    P = _srv()
+    n_cells, n_ch, d = 3000, 6, 40
+    rec, D = _db(n_cells, n_ch, d, seed=71)
+    st = torch.cuda.Stream()
+    with P.PirServer(n_cells, n_ch, d, records=rec) as s:
+        qd = [torch.empty(n_cells, dtype=torch.int32, device="cuda") for _ in range(6)]
+        Qd = torch.empty((5, n_cells), dtype=torch.int32, device="cuda")
+        outs = [torch.empty(s.ell_local, dtype=torch.int32, device="cuda") for _ in range(6)]
+        outB = torch.empty((5, s.ell_local), dtype=torch.int32, device="cuda")
+        with torch.cuda.stream(st):  # eager first: sizes the stream's arena
+            s.answer(qd[0], out=outs[0], stream=st)
+            s.answer_batch(Qd, out=outB, stream=st)
+        st.synchronize()
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g, stream=st, capture_error_mode="relaxed"):
+            for i in range(6):
+                s.answer(qd[i], out=outs[i], stream=st)
+            s.answer_batch(Qd, out=outB, stream=st)
+        for rep in range(2):
+            qs = [synth.uniform_u32_np(700 + 10 * rep + i, (n_cells,)) for i in range(6)]
+            Q = synth.uniform_u32_np(800 + rep, (5, n_cells))
+            for i in range(6):
+                qd[i].copy_(torch.from_numpy(qs[i].view(np.int32)))
+            Qd.copy_(torch.from_numpy(Q.view(np.int32)))
+            torch.cuda.synchronize()
+            with torch.cuda.stream(st):
+                g.replay()
+            st.synchronize()
+            for i in range(6):
+                assert (_u32(outs[i]) == O.answer(D, qs[i])).all(), (rep, i)
+            assert (_u32(outB) == O.answer_batch(D, Q)).all(), rep
+
+
 def test_errors_name_the_field(cuda_ok):
     """Lengths, alignment and foreign pointers are rejected with the field named
     and nothing written (QPIR_E_DIMENSION / QPIR_E_PARAM)."""
