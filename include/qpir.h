@@ -36,6 +36,13 @@
  *     arena: staging buffers, split-K partials, tickets); calls on one stream
  *     are ordered by that stream.  qpir_db_write must not overlap any other
  *     call on the context.  The D shard is never modified by answer/hint calls.
+ *   - CUDA graphs: answer / batch / hint calls with device buffers may be
+ *     captured into a CUDA graph (relaxed or thread-local capture mode) once a
+ *     first eager call on that stream has sized its scratch; the graph reads
+ *     the caller's buffers at replay time.  Back-to-back GEMV answers (and ENS
+ *     scans) are launched with programmatic dependent launch: the next one
+ *     starts streaming D while the previous one drains, and waits for it
+ *     before touching any buffer the previous one writes.
  *   - Errors: functions return QPIR_OK (0) or a QPIR_E_* code; no partial
  *     outputs on error.  qpir_last_error(ctx) (or qpir_last_error(NULL) for a
  *     failed qpir_setup) names the offending field, e.g. "m: 8191 != 8192".
