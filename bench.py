@@ -688,7 +688,9 @@ def main():
             h_in = torch.empty((B, n_cells), dtype=torch.int32).pin_memory()
             h_in.copy_(qs[0].cpu())
             h_out = torch.empty((B, srv.ell if world > 1 else ell_local), dtype=torch.int32).pin_memory()
-        e2e_steps = max(3, min(args.steps, 200 if kind == "answer" else 10))
+        # as many steps as the device-timed loop (up to 200), so both run in the
+        # same power / clock state (batches are power-capped in steady state)
+        e2e_steps = max(3, min(args.steps, 200))
         dev_out = out
         two = world == 1  # answers and batches: D2H overlapped on a copy stream
         if two:

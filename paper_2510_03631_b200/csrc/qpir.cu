@@ -38,11 +38,25 @@ struct Geometry {
 
 }  // namespace
 
+// Host-input staging ring: the H2D copy of call i + 1's query runs on the
+// arena's own copy stream while call i's kernels run; the compute stream waits
+// only on that copy's event (two slots, each reused once the kernels that read
+// it have finished).
+struct InRing {
+  void* buf[2] = {nullptr, nullptr};
+  uint64_t bytes[2] = {0, 0};
+  cudaEvent_t ready[2] = {nullptr, nullptr};  // H2D into slot k done (copy stream)
+  cudaEvent_t done[2] = {nullptr, nullptr};   // kernels reading slot k done (compute stream)
+  unsigned slot = 0;
+};
+
 // Per-stream scratch: calls on different streams of one context may run
 // concurrently (each stream owns its staging buffers, split-K partials and
 // tickets); calls on one stream are ordered by the stream.
 struct Arena {
-  uint32_t* qu_dev = nullptr;      // staging for host / unaligned qu
+  cudaStream_t h2d = nullptr;      // copy stream for host inputs (lazily created)
+  InRing in_small, in_big;         // host qu / host Q staging rings
+  uint32_t* qu_dev = nullptr;      // staging for an unaligned device qu
   uint64_t qu_bytes = 0;
   uint32_t* ans_dev = nullptr;     // staging for host answers
   uint64_t ans_bytes = 0;
@@ -52,8 +66,6 @@ struct Arena {
   uint64_t tickets_bytes = 0;
   uint8_t* limbs = nullptr;        // Q' or A' limb planes
   uint64_t limbs_bytes = 0;
-  uint32_t* big_in = nullptr;      // staging for host Q
-  uint64_t big_in_bytes = 0;
   uint32_t* big_out = nullptr;     // staging for host ANS / H
   uint64_t big_out_bytes = 0;
   unsigned long long* acc64 = nullptr;  // OUT_MODP accumulator
@@ -86,6 +98,7 @@ struct qpir_ctx {
   int mma_gpb = 8;     // env QPIR_MMA_GPB (column groups per pipeline stage: 4 or 8)
   int modp3 = 1;       // env QPIR_MODP3 (3 limbs per query for p < 2^24)
   int modp2 = 1;       // env QPIR_MODP2 (2 limbs per query for p <= 65537)
+  int h2d_stream = 1;  // env QPIR_H2D_STREAM (host inputs copied on a side stream)
   uint64_t limb_budget = 2ull << 30;  // env QPIR_LIMB_BUDGET_MB: max bytes of Q'/A' at once
   std::string err;
 };
@@ -175,6 +188,45 @@ int ensure(qpir_ctx* ctx, void** buf, uint64_t* have, uint64_t need) {
 Arena& arena_for(qpir_ctx* ctx, cudaStream_t st) {
   std::lock_guard<std::mutex> lk(ctx->mu);
   return ctx->arenas[st];  // std::map references stay valid across inserts
+}
+
+// Stage `bytes` of host memory for kernels on `st`: H2D on the arena's copy
+// stream into the next ring slot, `st` waits on it.  Returns the slot (the
+// caller records ring.done[slot] on `st` after the kernels that read it), or
+// -1 after a same-stream copy (while `st` is being captured into a CUDA graph,
+// or with QPIR_H2D_STREAM=0).
+int stage_host(qpir_ctx* ctx, Arena& ar, InRing& ring, const void* src, uint64_t bytes,
+               uint64_t alloc, cudaStream_t st, const void** dev, int* slot_out) {
+  *slot_out = -1;
+  cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+  CUDA_TRY(ctx, cudaStreamIsCapturing(st, &cs));
+  if (cs != cudaStreamCaptureStatusNone || !ctx->h2d_stream) {
+    int rc = ensure(ctx, &ring.buf[0], &ring.bytes[0], alloc);
+    if (rc) return rc;
+    CUDA_TRY(ctx, cudaMemcpyAsync(ring.buf[0], src, bytes, cudaMemcpyHostToDevice, st));
+    *dev = ring.buf[0];
+    return QPIR_OK;
+  }
+  if (!ar.h2d) CUDA_TRY(ctx, cudaStreamCreateWithFlags(&ar.h2d, cudaStreamNonBlocking));
+  const unsigned k = ring.slot;
+  ring.slot ^= 1u;
+  if (!ring.ready[k]) {
+    CUDA_TRY(ctx, cudaEventCreateWithFlags(&ring.ready[k], cudaEventDisableTiming));
+    CUDA_TRY(ctx, cudaEventCreateWithFlags(&ring.done[k], cudaEventDisableTiming));
+  }
+  if (ring.bytes[k] < alloc) {
+    // the slot may still be read by earlier kernels: wait before freeing it
+    CUDA_TRY(ctx, cudaEventSynchronize(ring.done[k]));
+    int rc = ensure(ctx, &ring.buf[k], &ring.bytes[k], alloc);
+    if (rc) return rc;
+  }
+  CUDA_TRY(ctx, cudaStreamWaitEvent(ar.h2d, ring.done[k], 0));
+  CUDA_TRY(ctx, cudaMemcpyAsync(ring.buf[k], src, bytes, cudaMemcpyHostToDevice, ar.h2d));
+  CUDA_TRY(ctx, cudaEventRecord(ring.ready[k], ar.h2d));
+  CUDA_TRY(ctx, cudaStreamWaitEvent(st, ring.ready[k], 0));
+  *dev = ring.buf[k];
+  *slot_out = (int)k;
+  return QPIR_OK;
 }
 
 int db_write_device(qpir_ctx* ctx, uint64_t theta0, uint64_t n_rec, const uint8_t* rec,
@@ -402,6 +454,7 @@ int qpir_setup(const qpir_params* params, const uint8_t* records, uint64_t recor
   ctx->mma_gpb = env_int("QPIR_MMA_GPB", 8);
   ctx->modp3 = env_int("QPIR_MODP3", 1);
   ctx->modp2 = env_int("QPIR_MODP2", 1);
+  ctx->h2d_stream = env_int("QPIR_H2D_STREAM", 1);
   if (env_int("QPIR_LIMB_BUDGET_MB", 0) > 0)
     ctx->limb_budget = (uint64_t)env_int("QPIR_LIMB_BUDGET_MB", 0) << 20;
   cudaStream_t st = (cudaStream_t)stream;
@@ -499,11 +552,16 @@ int qpir_answer(qpir_ctx* ctx, const uint32_t* qu, uint64_t len_qu, uint32_t* an
   Arena& ar = arena_for(ctx, st);
   int rc = QPIR_OK;
   const uint32_t* qd = qu;
-  if (wq == 0 || !aligned16(qu)) {
+  int slot = -1;
+  if (wq == 0) {
+    const void* dv = nullptr;
+    rc = stage_host(ctx, ar, ar.in_small, qu, g.m * 4, g.m_pad * 4, st, &dv, &slot);
+    if (rc) return rc;
+    qd = static_cast<const uint32_t*>(dv);
+  } else if (!aligned16(qu)) {
     rc = ensure(ctx, (void**)&ar.qu_dev, &ar.qu_bytes, g.m_pad * 4);
     if (rc) return rc;
-    CUDA_TRY(ctx, cudaMemcpyAsync(ar.qu_dev, qu, g.m * 4,
-                                  wq ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, st));
+    CUDA_TRY(ctx, cudaMemcpyAsync(ar.qu_dev, qu, g.m * 4, cudaMemcpyDeviceToDevice, st));
     qd = ar.qu_dev;
   }
   uint32_t* ad = ans_local;
@@ -514,6 +572,7 @@ int qpir_answer(qpir_ctx* ctx, const uint32_t* qu, uint64_t len_qu, uint32_t* an
   }
   rc = gemv(ctx, qd, ad, st);
   if (rc) return rc;
+  if (slot >= 0) CUDA_TRY(ctx, cudaEventRecord(ar.in_small.done[slot], st));
   if (!wa) {
     CUDA_TRY(ctx, cudaMemcpyAsync(ans_local, ad, g.ell_local * 4, cudaMemcpyDeviceToHost, st));
     CUDA_TRY(ctx, cudaStreamSynchronize(st));
@@ -559,11 +618,12 @@ static int answer_batch_impl(qpir_ctx* ctx, const uint32_t* Q, uint64_t B, uint6
   int rc = ensure(ctx, (void**)&ar.limbs, &ar.limbs_bytes, (uint64_t)Npad * g.m_pad);
   if (rc) return rc;
   const uint32_t* Qd = Q;
+  int slot = -1;
   if (wq == 0) {
-    rc = ensure(ctx, (void**)&ar.big_in, &ar.big_in_bytes, len_Q * 4);
+    const void* dv = nullptr;
+    rc = stage_host(ctx, ar, ar.in_big, Q, len_Q * 4, len_Q * 4, st, &dv, &slot);
     if (rc) return rc;
-    CUDA_TRY(ctx, cudaMemcpyAsync(ar.big_in, Q, len_Q * 4, cudaMemcpyHostToDevice, st));
-    Qd = ar.big_in;
+    Qd = static_cast<const uint32_t*>(dv);
   }
   uint32_t* out = ans_local;
   if (wa == 0) {
@@ -636,6 +696,7 @@ static int answer_batch_impl(qpir_ctx* ctx, const uint32_t* Q, uint64_t B, uint6
                                 ar.acc64);
   }
   if (rc) return rc;
+  if (slot >= 0) CUDA_TRY(ctx, cudaEventRecord(ar.in_big.done[slot], st));
   if (wa == 0) {
     CUDA_TRY(ctx, cudaMemcpyAsync(ans_local, out, len_ans * 4, cudaMemcpyDeviceToHost, st));
     CUDA_TRY(ctx, cudaStreamSynchronize(st));
@@ -724,10 +785,17 @@ void qpir_destroy(qpir_ctx* ctx) {
     if (b) cudaFree(b);
   for (auto& kv : ctx->arenas) {
     Arena& a = kv.second;
-    void* ab[] = {a.qu_dev, a.ans_dev, a.partial, a.tickets, a.limbs, a.big_in, a.big_out, a.acc64,
-                  a.exc};
+    void* ab[] = {a.qu_dev, a.ans_dev, a.partial, a.tickets, a.limbs, a.big_out, a.acc64,
+                  a.exc, a.in_small.buf[0], a.in_small.buf[1], a.in_big.buf[0], a.in_big.buf[1]};
+    if (a.h2d) cudaStreamSynchronize(a.h2d);
     for (void* b : ab)
       if (b) cudaFree(b);
+    for (InRing* r : {&a.in_small, &a.in_big})
+      for (int k = 0; k < 2; ++k) {
+        if (r->ready[k]) cudaEventDestroy(r->ready[k]);
+        if (r->done[k]) cudaEventDestroy(r->done[k]);
+      }
+    if (a.h2d) cudaStreamDestroy(a.h2d);
   }
   delete ctx;
 }
