@@ -359,6 +359,35 @@ def test_concurrent_streams_have_private_scratch(cuda_ok, monkeypatch):
             assert (_u32(out) == want).all()
 
 
+def test_host_input_ring_grows_and_reuses(cuda_ok):
+    """Host (pinned and pageable) queries go through the arena's copy stream and
+    two-slot staging ring: batches of growing B (forcing slot reallocation while
+    earlier kernels may still read the other slot) and answers interleaved on
+    one stream without syncs -- all exact."""
+    P = _srv()
+    n_cells, n_ch, d = 2000, 5, 24
+    rec, D = _db(n_cells, n_ch, d, seed=81)
+    st = torch.cuda.Stream()
+    with P.PirServer(n_cells, n_ch, d, records=rec) as s:
+        jobs = []
+        for i, B in enumerate([1, 3, 2, 9, 4, 17, 17, 5]):
+            Q = synth.uniform_u32_np(900 + i, (B, n_cells))
+            src = torch.from_numpy(Q.view(np.int32))
+            src = src.pin_memory() if i % 2 == 0 else src  # pinned / pageable
+            out = torch.empty((B, s.ell_local), dtype=torch.int32, device="cuda")
+            s.answer_batch(src, out=out, stream=st)
+            jobs.append((out, O.answer_batch(D, Q), src))
+            q = synth.uniform_u32_np(950 + i, (n_cells,))
+            qs = torch.from_numpy(q.view(np.int32))
+            qs = qs.pin_memory() if i % 3 else qs
+            o1 = torch.empty(s.ell_local, dtype=torch.int32, device="cuda")
+            s.answer(qs, out=o1, stream=st)
+            jobs.append((o1, O.answer(D, q), qs))
+        st.synchronize()
+        for out, want, _ in jobs:
+            assert (_u32(out) == want).all()
+
+
 def test_cuda_graph_capture_and_replay(cuda_ok):
     """The C-ABI calls are capturable into a CUDA graph once a first eager call
     has sized the stream's scratch: answers (split-K GEMV with PDL edges) and a
