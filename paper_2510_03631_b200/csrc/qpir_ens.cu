@@ -17,8 +17,22 @@ namespace {
 thread_local std::string g_ens_setup_error;
 }
 
+// Host-input staging ring for single answers (share, OOP q and A_i): the H2D
+// copy runs on the context's copy stream, the compute stream waits only on its
+// event, so the next answer's input lands while the previous scan runs.
+struct EnsRing {
+  uint8_t* buf[2] = {nullptr, nullptr};
+  uint64_t bytes[2] = {0, 0};
+  cudaEvent_t ready[2] = {nullptr, nullptr};
+  cudaEvent_t done[2] = {nullptr, nullptr};
+  unsigned slot = 0;
+};
+
 struct qpir_ens_ctx {
   uint64_t r = 0, d = 0, dp = 0;
+  cudaStream_t h2d = nullptr;   // copy stream for host inputs (lazily created)
+  EnsRing r_share, r_q, r_A;
+  int h2d_stream = 1;           // env QPIR_H2D_STREAM
   int device = 0, num_sms = 148;
   uint8_t* R = nullptr;       // [r][dp]
   uint8_t* q_dev = nullptr;   // staging for one share (ceil(r/8))
@@ -97,6 +111,49 @@ int stage_in(qpir_ens_ctx* ctx, const uint8_t* src, uint64_t bytes, uint8_t* sta
   return QPIR_OK;
 }
 
+// Stage a possibly-host input through `ring` for work on `st`: device inputs
+// pass through (slot -1); host inputs are copied on the copy stream (or on `st`
+// while it is being captured into a CUDA graph).  The caller records
+// ring.done[slot] on `st` after the kernels that read the slot.
+int stage_ring(qpir_ens_ctx* ctx, EnsRing& ring, const uint8_t* src, uint64_t bytes,
+               cudaStream_t st, const uint8_t** dev, int* slot) {
+  *slot = -1;
+  const int w = where(src, ctx->device);
+  if (w < 0) return ENS_FAIL(ctx, QPIR_E_PARAM, "input: memory of another device");
+  if (w == 1) {
+    *dev = src;
+    return QPIR_OK;
+  }
+  cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+  ENS_CUDA(ctx, cudaStreamIsCapturing(st, &cs));
+  const bool side = cs == cudaStreamCaptureStatusNone && ctx->h2d_stream;
+  const unsigned k = side ? ring.slot : 0u;
+  if (side) {
+    ring.slot ^= 1u;
+    if (!ctx->h2d) ENS_CUDA(ctx, cudaStreamCreateWithFlags(&ctx->h2d, cudaStreamNonBlocking));
+    if (!ring.ready[k]) {
+      ENS_CUDA(ctx, cudaEventCreateWithFlags(&ring.ready[k], cudaEventDisableTiming));
+      ENS_CUDA(ctx, cudaEventCreateWithFlags(&ring.done[k], cudaEventDisableTiming));
+    }
+  }
+  if (ring.bytes[k] < bytes) {
+    if (ring.done[k]) ENS_CUDA(ctx, cudaEventSynchronize(ring.done[k]));
+    int rc = grow(ctx, (void**)&ring.buf[k], &ring.bytes[k], round_up(bytes, 16));
+    if (rc) return rc;
+  }
+  if (side) {
+    ENS_CUDA(ctx, cudaStreamWaitEvent(ctx->h2d, ring.done[k], 0));
+    ENS_CUDA(ctx, cudaMemcpyAsync(ring.buf[k], src, bytes, cudaMemcpyHostToDevice, ctx->h2d));
+    ENS_CUDA(ctx, cudaEventRecord(ring.ready[k], ctx->h2d));
+    ENS_CUDA(ctx, cudaStreamWaitEvent(st, ring.ready[k], 0));
+    *slot = (int)k;
+  } else {
+    ENS_CUDA(ctx, cudaMemcpyAsync(ring.buf[k], src, bytes, cudaMemcpyHostToDevice, st));
+  }
+  *dev = ring.buf[k];
+  return QPIR_OK;
+}
+
 // Copy B rows of d bytes out of the dp-strided accumulator into `out`.
 int copy_out(qpir_ens_ctx* ctx, uint8_t* out, uint64_t B, cudaStream_t st) {
   const int w = where(out, ctx->device);
@@ -143,6 +200,7 @@ int qpir_ens_setup(const qpir_ens_params* p, const uint8_t* records, uint64_t re
   ctx->group = env_int("QPIR_ENS_GROUP", 0);
   ctx->wide = env_int("QPIR_ENS_WIDE", 1);
   ctx->pdl = env_int("QPIR_ENS_PDL", 1);
+  ctx->h2d_stream = env_int("QPIR_H2D_STREAM", 1);
   ctx->tc = env_int("QPIR_ENS_TC", -1);
   ctx->mma_split = env_int("QPIR_MMA_SPLIT", 0);
   cudaStream_t st = (cudaStream_t)stream;
@@ -293,11 +351,13 @@ int qpir_ens_answer(qpir_ens_ctx* ctx, const uint8_t* share, uint64_t len_share,
   int rc = grow(ctx, (void**)&ctx->io_stage, &ctx->io_stage_bytes, 2 * ctx->d);
   if (rc) return rc;
   const uint8_t* qd = nullptr;
-  rc = stage_in(ctx, share, nb, ctx->q_dev, &qd, st);
+  int slot = -1;
+  rc = stage_ring(ctx, ctx->r_share, share, nb, st, &qd, &slot);
   if (rc) return rc;
   uint8_t* od = wo ? out : ctx->io_stage + ctx->d;
   rc = scan_range(ctx, qd, 0, ctx->r, nullptr, od, st);
   if (rc) return rc;
+  if (slot >= 0) ENS_CUDA(ctx, cudaEventRecord(ctx->r_share.done[slot], st));
   if (!wo) {
     ENS_CUDA(ctx, cudaMemcpyAsync(out, od, ctx->d, cudaMemcpyDeviceToHost, st));
     ENS_CUDA(ctx, cudaStreamSynchronize(st));
@@ -329,15 +389,18 @@ int qpir_oop_answer(qpir_ens_ctx* ctx, uint32_t n_chunks, uint32_t server, const
   int rc = grow(ctx, (void**)&ctx->io_stage, &ctx->io_stage_bytes, 2 * ctx->d);
   if (rc) return rc;
   const uint8_t* qd = nullptr;
-  rc = stage_in(ctx, q, kb, ctx->q_dev, &qd, st);
+  int sq = -1, sA = -1;
+  rc = stage_ring(ctx, ctx->r_q, q, kb, st, &qd, &sq);
   if (rc) return rc;
   // R_i := A_i XOR q_i . chunk_i (Lemma 2): A_i is XORed in by the finalising CTA
   const uint8_t* Ad = nullptr;
-  rc = stage_in(ctx, A, ctx->d, ctx->io_stage, &Ad, st);
+  rc = stage_ring(ctx, ctx->r_A, A, ctx->d, st, &Ad, &sA);
   if (rc) return rc;
   uint8_t* od = wo ? out : ctx->io_stage + ctx->d;
   rc = scan_range(ctx, qd, (uint64_t)server * k, (uint64_t)(server + 1) * k, Ad, od, st);
   if (rc) return rc;
+  if (sq >= 0) ENS_CUDA(ctx, cudaEventRecord(ctx->r_q.done[sq], st));
+  if (sA >= 0) ENS_CUDA(ctx, cudaEventRecord(ctx->r_A.done[sA], st));
   if (!wo) {
     ENS_CUDA(ctx, cudaMemcpyAsync(out, od, ctx->d, cudaMemcpyDeviceToHost, st));
     ENS_CUDA(ctx, cudaStreamSynchronize(st));
@@ -515,8 +578,16 @@ void qpir_ens_destroy(qpir_ens_ctx* ctx) {
   void* bufs[] = {ctx->R,       ctx->q_dev,   ctx->acc,  ctx->Q_dev, ctx->Qt,
                   ctx->seed_dev, ctx->partial, ctx->tickets, ctx->bitD, ctx->Qb,
                   ctx->acc1,    ctx->io_stage};
+  if (ctx->h2d) cudaStreamSynchronize(ctx->h2d);
   for (void* b : bufs)
     if (b) cudaFree(b);
+  for (EnsRing* g : {&ctx->r_share, &ctx->r_q, &ctx->r_A})
+    for (int k = 0; k < 2; ++k) {
+      if (g->buf[k]) cudaFree(g->buf[k]);
+      if (g->ready[k]) cudaEventDestroy(g->ready[k]);
+      if (g->done[k]) cudaEventDestroy(g->done[k]);
+    }
+  if (ctx->h2d) cudaStreamDestroy(ctx->h2d);
   delete ctx;
 }
 
