@@ -63,7 +63,21 @@ struct MmaArgs {
   uint32_t m_tiles, n_tiles, splits, kps;  // work units = m_tiles * n_tiles * splits
   uint32_t p;         // OUT_MODP modulus
   unsigned long long* out64;  // OUT_MODP accumulator [n_out][out_ld]
+  // K-lockstep (L2 reuse): the CTAs of one wave of units issue their loads
+  // chunk by chunk (ls_chunk K-blocks), at most ls_drift chunks ahead of the
+  // slowest CTA of the wave, so the D panels and B tiles they share stay in L2
+  // instead of being re-read from HBM by CTAs that drifted apart.
+  // Only CTAs that have started a wave count (kprog[2w + 1]), so a CTA never
+  // waits for one that is not resident (e.g. SMs held by a concurrent launch).
+  uint32_t* kprog;    // [waves][2]: chunks issued, CTAs arrived (zeroed per launch), or nullptr
+  uint32_t ls_chunk, ls_drift;
 };
+
+__device__ __forceinline__ uint32_t ld_acquire_u32(const uint32_t* p) {
+  uint32_t v;
+  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
 
 // GPB = 16-cell column groups per pipeline stage (K-block = 16 * GPB cells).
 template <uint32_t BN, uint32_t MT, uint32_t GPB>
@@ -136,11 +150,21 @@ __global__ void __launch_bounds__(MMA_THREADS, 1) mma_u8_limb_kernel(MmaArgs a) 
   if (warp == 0) {
     // ------------------------------------------------------------ producer
     if (lane == 0) {
-      uint32_t stage = 0, phase = 0;
-      for (uint32_t u = blockIdx.x; u < num_units; u += gridDim.x) {
+      uint32_t stage = 0, phase = 0, wave = 0;
+      const uint32_t LS = a.kprog ? a.ls_chunk : 0u;
+      for (uint32_t u = blockIdx.x; u < num_units; u += gridDim.x, ++wave) {
         uint32_t mt, nt, kb0, kb1;
         decode(u, mt, nt, kb0, kb1);
+        uint32_t* issued = LS ? a.kprog + 2 * wave : nullptr;
+        if (LS) atomicAdd(issued + 1, 1u);  // arrived
         for (uint32_t kb = kb0; kb < kb1; ++kb) {
+          if (LS && (kb - kb0) % LS == 0) {
+            const uint32_t j = (kb - kb0) / LS;
+            if (j >= a.ls_drift) {
+              const uint32_t need = j - a.ls_drift + 1;  // chunks every arrived CTA issued
+              while (ld_acquire_u32(issued) < ld_acquire_u32(issued + 1) * need) __nanosleep(128);
+            }
+          }
           mbar_wait(&empty[stage], phase ^ 1);
           mbar_arrive_expect_tx(&full[stage], C::STAGE_BYTES);
           uint8_t* dst = smem + stage * C::STAGE_BYTES;
@@ -155,6 +179,13 @@ __global__ void __launch_bounds__(MMA_THREADS, 1) mma_u8_limb_kernel(MmaArgs a) 
                    a.B + ((size_t)nt * a.G + (size_t)kb * GPB) * (BN * 16), C::B_BYTES,
                    &full[stage]);
           if (++stage == STAGES) { stage = 0; phase ^= 1; }
+          if (LS && ((kb - kb0) % LS == LS - 1 || kb + 1 == kb1))
+            atomicAdd(issued, 1u);  // chunk issued
+        }
+        if (LS) {
+          // a shorter unit (last K-split) still counts as having issued every chunk
+          const uint32_t mine = (kb1 - kb0 + LS - 1) / LS, all = (a.kps + LS - 1) / LS;
+          if (mine < all) atomicAdd(issued, all - mine);
         }
       }
     }

@@ -29,6 +29,9 @@ struct MmaJob {
   int gpb = 8;           // column groups per pipeline stage (4 or 8)
   bool out_prezeroed = false;  // caller zeroed `out` (strided chunks): no memset here
   ModpExceptions exc;          // OUT_MODP2, p = 65537: applied by the fixup
+  uint32_t* kprog = nullptr;   // K-lockstep scratch (kprog_cap u32), nullptr = off
+  uint32_t kprog_cap = 0;
+  uint32_t ls_chunk = 0, ls_drift = 1;  // K-blocks per lockstep chunk (0 = off)
 };
 
 // BN for 3 limbs per query (OUT_MODP3): a multiple of 48 so queries never
@@ -95,14 +98,25 @@ cudaError_t mma_launch_cfg(const MmaJob& j, cudaStream_t st, uint64_t* launches)
   a.splits = (kblocks + a.kps - 1) / a.kps;  // no empty split
   a.p = j.p;
   a.out64 = j.out64;
+  const uint32_t units = a.m_tiles * a.n_tiles * a.splits;
+  const uint32_t grid = std::min<uint32_t>(units, (uint32_t)j.num_sms);
+  const uint32_t waves = (units + grid - 1) / grid;
+  // lockstep only pays when CTAs share D panels (several N tiles) over long K
+  // ranges (C5 hint: 42.5 -> 18.8 GB of DRAM reads per launch; FTR and C4 B = 64
+  // have one N tile)
+  const bool ls = j.kprog && j.ls_chunk && a.n_tiles >= 2 && 2 * waves <= j.kprog_cap &&
+                  a.kps >= 4 * j.ls_chunk;
+  a.kprog = ls ? j.kprog : nullptr;
+  a.ls_chunk = j.ls_chunk;
+  a.ls_drift = std::max<uint32_t>(1, j.ls_drift);
   cudaError_t e = cudaSuccess;
+  if (ls) e = cudaMemsetAsync(j.kprog, 0, waves * 8, st);
+  if (e != cudaSuccess) return e;
   if (modp)
     e = cudaMemsetAsync(j.out64, 0, j.out_elems * 8, st);
   else if (a.splits > 1 && !j.out_prezeroed)
     e = cudaMemsetAsync(j.out, 0, j.out_elems * 4, st);
   if (e != cudaSuccess) return e;
-  const uint32_t units = a.m_tiles * a.n_tiles * a.splits;
-  const uint32_t grid = std::min<uint32_t>(units, (uint32_t)j.num_sms);
   auto kern = mma_u8_limb_kernel<BN, MT, GPB, MODE>;
   e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::TOTAL);
   if (e != cudaSuccess) return e;

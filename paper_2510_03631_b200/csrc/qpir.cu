@@ -70,6 +70,7 @@ struct Arena {
   uint64_t big_out_bytes = 0;
   unsigned long long* acc64 = nullptr;  // OUT_MODP accumulator
   uint64_t acc64_bytes = 0;
+  uint32_t* kprog = nullptr;       // tcgen05 engine K-lockstep counters [kKprogCap]
   uint32_t* exc = nullptr;         // OUT_MODP2, p = 65537: [Bc] counts + [Bc][cap] columns
   uint64_t exc_bytes = 0;
 };
@@ -99,6 +100,8 @@ struct qpir_ctx {
   int modp3 = 1;       // env QPIR_MODP3 (3 limbs per query for p < 2^24)
   int modp2 = 1;       // env QPIR_MODP2 (2 limbs per query for p <= 65537)
   int h2d_stream = 1;  // env QPIR_H2D_STREAM (host inputs copied on a side stream)
+  int mma_ls = 16;     // env QPIR_MMA_LOCKSTEP: K-blocks per lockstep chunk (0 = off)
+  int mma_drift = 1;   // env QPIR_MMA_DRIFT: chunks a CTA may run ahead of its wave
   uint64_t limb_budget = 2ull << 30;  // env QPIR_LIMB_BUDGET_MB: max bytes of Q'/A' at once
   std::string err;
 };
@@ -399,6 +402,19 @@ int launch_mma(qpir_ctx* ctx, uint32_t BN, const uint8_t* Bl, uint32_t Npad, uin
   j.gpb = ctx->mma_gpb;
   j.out_prezeroed = prezeroed;
   j.exc = exc;
+  if (ctx->mma_ls > 0) {
+    constexpr uint32_t kKprogCap = 4096;
+    Arena& ar = arena_for(ctx, st);
+    if (!ar.kprog) {
+      uint64_t have = 0;
+      int rc = ensure(ctx, (void**)&ar.kprog, &have, kKprogCap * 4);
+      if (rc) return rc;
+    }
+    j.kprog = ar.kprog;
+    j.kprog_cap = kKprogCap;
+    j.ls_chunk = (uint32_t)ctx->mma_ls;
+    j.ls_drift = (uint32_t)std::max(1, ctx->mma_drift);
+  }
   const cudaError_t e = mma_launch<MODE>(j, st, &ctx->launches);
   if (e != cudaSuccess)
     return fail(ctx, e == cudaErrorMemoryAllocation ? QPIR_E_OOM : QPIR_E_CUDA,
@@ -455,6 +471,8 @@ int qpir_setup(const qpir_params* params, const uint8_t* records, uint64_t recor
   ctx->modp3 = env_int("QPIR_MODP3", 1);
   ctx->modp2 = env_int("QPIR_MODP2", 1);
   ctx->h2d_stream = env_int("QPIR_H2D_STREAM", 1);
+  ctx->mma_ls = env_int("QPIR_MMA_LOCKSTEP", 16);
+  ctx->mma_drift = env_int("QPIR_MMA_DRIFT", 1);
   if (env_int("QPIR_LIMB_BUDGET_MB", 0) > 0)
     ctx->limb_budget = (uint64_t)env_int("QPIR_LIMB_BUDGET_MB", 0) << 20;
   cudaStream_t st = (cudaStream_t)stream;
@@ -786,7 +804,8 @@ void qpir_destroy(qpir_ctx* ctx) {
   for (auto& kv : ctx->arenas) {
     Arena& a = kv.second;
     void* ab[] = {a.qu_dev, a.ans_dev, a.partial, a.tickets, a.limbs, a.big_out, a.acc64,
-                  a.exc, a.in_small.buf[0], a.in_small.buf[1], a.in_big.buf[0], a.in_big.buf[1]};
+                  a.exc, a.in_small.buf[0], a.in_small.buf[1], a.in_big.buf[0], a.in_big.buf[1],
+                  a.kprog};
     if (a.h2d) cudaStreamSynchronize(a.h2d);
     for (void* b : ab)
       if (b) cudaFree(b);

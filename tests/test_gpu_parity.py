@@ -359,6 +359,36 @@ def test_concurrent_streams_have_private_scratch(cuda_ok, monkeypatch):
             assert (_u32(out) == want).all()
 
 
+@pytest.mark.timeout(300)
+def test_lockstep_gemms_on_concurrent_streams(cuda_ok, monkeypatch):
+    """The tcgen05 engine's K-lockstep (CTAs of a wave wait for the slowest
+    arrived CTA) with two hints and a batch running at once on three streams, so
+    that some CTAs of each grid are not resident while others spin: no deadlock,
+    every result exact; chunk sizes 1 and 16 K-blocks."""
+    P = _srv()
+    n_cells, n_ch, d, n = 16384, 2, 24, 256  # G = 1024 groups: 128 K-blocks, N = 1024
+    rec, D = _db(n_cells, n_ch, d, seed=91)
+    A = O.expand_A(5, n_cells, n)
+    Hw = O.hint(D, A)
+    Q = synth.uniform_u32_np(92, (128, n_cells))
+    want = O.answer_batch(D, Q)
+    for ls in ("1", "16"):
+        monkeypatch.setenv("QPIR_MMA_LOCKSTEP", ls)
+        with P.PirServer(n_cells, n_ch, d, lwe_n=n, seed_A=5, records=rec) as s:
+            sts = [torch.cuda.Stream() for _ in range(3)]
+            Qd = torch.from_numpy(Q.view(np.int32)).cuda()
+            outs = []
+            for rep in range(3):
+                h1 = s.hint(stream=sts[0])
+                h2 = s.hint(stream=sts[1])
+                b = s.answer_batch(Qd, stream=sts[2])
+                outs.append((h1, h2, b))
+            torch.cuda.synchronize()
+            for h1, h2, b in outs:
+                assert (_u32(h1) == Hw).all() and (_u32(h2) == Hw).all()
+                assert (_u32(b) == want).all()
+
+
 def test_host_input_ring_grows_and_reuses(cuda_ok):
     """Host (pinned and pageable) queries go through the arena's copy stream and
     two-slot staging ring: batches of growing B (forcing slot reallocation while
