@@ -135,14 +135,17 @@ __global__ void __launch_bounds__(MMA_THREADS, 1) mma_u8_limb_kernel(MmaArgs a) 
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
 
-  // unit -> (m tile, n tile, split); n and split fastest so that CTAs running
-  // at the same time share the D panels of one m tile through L2.
+  // unit -> (split, m tile, n tile); the K-split slowest, n fastest: the CTAs
+  // running at the same time cover the same K range of ~148 / n_tiles m tiles x
+  // all n tiles, so each D panel is shared by n_tiles CTAs and each B tile by
+  // the wave's m tiles through L2 (with split fastest, a wave mixed K ranges and
+  // re-read every B tile once per split: hint 18.8 GB of DRAM reads -> see DESIGN).
   auto decode = [&](uint32_t u, uint32_t& mt, uint32_t& nt, uint32_t& kb0, uint32_t& kb1) {
-    const uint32_t per_m = a.n_tiles * a.splits;
-    mt = u / per_m;
-    const uint32_t r = u % per_m;
-    nt = r / a.splits;
-    const uint32_t s = r % a.splits;
+    const uint32_t per_s = a.m_tiles * a.n_tiles;
+    const uint32_t s = u / per_s;
+    const uint32_t r = u % per_s;
+    mt = r / a.n_tiles;
+    nt = r % a.n_tiles;
     kb0 = s * a.kps;
     kb1 = min(kblocks, kb0 + a.kps);
   };
