@@ -129,7 +129,11 @@ int qpir_answer_batch(qpir_ctx *ctx, const uint32_t *Q, uint64_t B,
  * exact for any u32 Q entries and any 2 <= p < 2^32 (results < p).  With
  * n_ch = 1 and n_cells = r records, row b of D is byte b of every record, so
  * row i of the answer is word i of the FTR response rho . DB (one word = one
- * record byte, DESIGN R17).  Same buffers and B range as qpir_answer_batch. */
+ * record byte, DESIGN R17).  Same buffers and B range as qpir_answer_batch.
+ * Internally the entries are reduced mod p first and split into 2 byte limbs
+ * for p <= 65537 (the residue 65536 of p = 65537 is listed per query and added
+ * back by the mod-p fixup), 3 for p <= 2^24, 4 otherwise: the cost falls with
+ * p, the result does not depend on the path. */
 int qpir_answer_batch_modp(qpir_ctx *ctx, const uint32_t *Q, uint64_t B,
                            uint64_t len_Q, uint32_t p, uint32_t *ans_local,
                            uint64_t len_ans, void *stream);
