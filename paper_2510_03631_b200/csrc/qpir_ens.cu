@@ -31,17 +31,16 @@ struct EnsRing {
 struct qpir_ens_ctx {
   uint64_t r = 0, d = 0, dp = 0;
   cudaStream_t h2d = nullptr;   // copy stream for host inputs (lazily created)
-  EnsRing r_share, r_q, r_A;
+  EnsRing r_share, r_q, r_A, r_batch;
   int h2d_stream = 1;           // env QPIR_H2D_STREAM
   int device = 0, num_sms = 148;
   uint8_t* R = nullptr;       // [r][dp]
-  uint8_t* q_dev = nullptr;   // staging for one share (ceil(r/8))
   uint32_t* acc = nullptr;    // [max_B][dp/4] XOR accumulators
   uint64_t acc_B = 0;
   uint32_t* acc1 = nullptr;   // [dp/4] + 1 done ticket: single-scan accumulator, kept zero
   uint8_t* io_stage = nullptr;  // [2][d]: host A_i in / host answer out of a single scan
   uint64_t io_stage_bytes = 0;
-  uint8_t* Q_dev = nullptr;   // staging for a batch of shares
+  uint8_t* Q_dev = nullptr;   // OOP offline: the expanded selectors of a seed batch
   uint64_t Q_bytes = 0;
   uint32_t* Qt = nullptr;     // transposed selector bits
   uint64_t Qt_bytes = 0;
@@ -94,20 +93,6 @@ int grow(qpir_ens_ctx* ctx, void** buf, uint64_t* have, uint64_t need) {
   *have = 0;
   ENS_CUDA(ctx, cudaMalloc(buf, need));
   *have = need;
-  return QPIR_OK;
-}
-
-// Stage a possibly-host input of `bytes` into a device buffer; returns the device pointer.
-int stage_in(qpir_ens_ctx* ctx, const uint8_t* src, uint64_t bytes, uint8_t* staging,
-             const uint8_t** dev, cudaStream_t st) {
-  const int w = where(src, ctx->device);
-  if (w < 0) return ENS_FAIL(ctx, QPIR_E_PARAM, "input: memory of another device");
-  if (w == 1) {
-    *dev = src;
-    return QPIR_OK;
-  }
-  ENS_CUDA(ctx, cudaMemcpyAsync(staging, src, bytes, cudaMemcpyHostToDevice, st));
-  *dev = staging;
   return QPIR_OK;
 }
 
@@ -204,9 +189,7 @@ int qpir_ens_setup(const qpir_ens_params* p, const uint8_t* records, uint64_t re
   ctx->tc = env_int("QPIR_ENS_TC", -1);
   ctx->mma_split = env_int("QPIR_MMA_SPLIT", 0);
   cudaStream_t st = (cudaStream_t)stream;
-  const uint64_t nb = (ctx->r + 7) / 8;
   if (cudaMalloc(&ctx->R, ctx->r * ctx->dp) != cudaSuccess ||
-      cudaMalloc(&ctx->q_dev, round_up(nb, 16)) != cudaSuccess ||
       cudaMalloc(&ctx->acc1, ctx->dp + 16) != cudaSuccess) {
     cudaGetLastError();
     g_ens_setup_error = "records: cudaMalloc failed";
@@ -521,20 +504,20 @@ int qpir_ens_answer_batch(qpir_ens_ctx* ctx, const uint8_t* shares, uint64_t B,
   const uint32_t QW = (uint32_t)((B + 31) / 32);
   rc = grow(ctx, (void**)&ctx->Qt, &ctx->Qt_bytes, ctx->r * QW * 4);
   if (rc) return rc;
-  const uint8_t* Qd = shares;
-  if (where(shares, ctx->device) != 1) {
-    rc = grow(ctx, (void**)&ctx->Q_dev, &ctx->Q_bytes, B * nb);
-    if (rc) return rc;
-    rc = stage_in(ctx, shares, B * nb, ctx->Q_dev, &Qd, st);
-    if (rc) return rc;
-  }
+  const uint8_t* Qd = nullptr;
+  int slot = -1;
+  rc = stage_ring(ctx, ctx->r_batch, shares, B * nb, st, &Qd, &slot);
+  if (rc) return rc;
   // tensor cores for larger batches when the bit-planes fit in HBM
   const bool want_tc = (ctx->tc == 1 || (ctx->tc < 0 && B >= 32)) && B <= 65280;  // grid.y
   if (want_tc) {
     bool used = false;
     rc = ens_batch_tc(ctx, Qd, B, st, &used);
     if (rc) return rc;
-    if (used) return copy_out(ctx, out, B, st);
+    if (used) {
+      if (slot >= 0) ENS_CUDA(ctx, cudaEventRecord(ctx->r_batch.done[slot], st));
+      return copy_out(ctx, out, B, st);
+    }
   }
   ENS_CUDA(ctx, cudaMemsetAsync(ctx->acc, 0, B * ctx->dp, st));
   {
@@ -563,6 +546,7 @@ int qpir_ens_answer_batch(qpir_ens_ctx* ctx, const uint8_t* shares, uint64_t B,
   dim3 grid((uint32_t)((ctx->r + rows - 1) / rows), slices, qblocks);
   ens_batch_kernel<<<grid, ENS_CW * ENS_QB, 0, st>>>(a);
   ENS_LAUNCHED(ctx);
+  if (slot >= 0) ENS_CUDA(ctx, cudaEventRecord(ctx->r_batch.done[slot], st));
   return copy_out(ctx, out, B, st);
 }
 
@@ -575,13 +559,13 @@ const char* qpir_ens_last_error(const qpir_ens_ctx* ctx) {
 void qpir_ens_destroy(qpir_ens_ctx* ctx) {
   if (!ctx) return;
   DeviceGuard dg(ctx->device);
-  void* bufs[] = {ctx->R,       ctx->q_dev,   ctx->acc,  ctx->Q_dev, ctx->Qt,
+  void* bufs[] = {ctx->R,       ctx->acc,  ctx->Q_dev, ctx->Qt,
                   ctx->seed_dev, ctx->partial, ctx->tickets, ctx->bitD, ctx->Qb,
                   ctx->acc1,    ctx->io_stage};
   if (ctx->h2d) cudaStreamSynchronize(ctx->h2d);
   for (void* b : bufs)
     if (b) cudaFree(b);
-  for (EnsRing* g : {&ctx->r_share, &ctx->r_q, &ctx->r_A})
+  for (EnsRing* g : {&ctx->r_share, &ctx->r_q, &ctx->r_A, &ctx->r_batch})
     for (int k = 0; k < 2; ++k) {
       if (g->buf[k]) cudaFree(g->buf[k]);
       if (g->ready[k]) cudaEventDestroy(g->ready[k]);
