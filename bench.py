@@ -176,6 +176,17 @@ def build_db(P, wl, n_ch_total, row_begin, row_end, seed, device, lwe_n=1024):
     return s
 
 
+def _host_cpu():
+    """The host CPU the oracle runs on (record the model)."""
+    try:
+        for ln in open("/proc/cpuinfo"):
+            if ln.startswith("model name"):
+                return f"{ln.split(':', 1)[1].strip()}, {os.cpu_count()} logical CPUs"
+    except OSError:
+        pass
+    return f"{os.cpu_count()} logical CPUs"
+
+
 def _warm_oracle(fn, seconds):
     """Untimed oracle calls for `seconds`: on the GPU box's host the oracle's
     speed rises over the first seconds of a process (13 -> 18+ GB/s,
@@ -211,6 +222,7 @@ def cpu_baseline_answer(wl, seed, budget_s=12.0):
     dt = time.perf_counter() - t0
     gbs = reps * D.nbytes / dt / 1e9
     return {"value": round(gbs, 3), "unit": "GB/s", "cores": O.num_threads(), "kind": "oracle",
+            "host": _host_cpu(),
             "sample": f"oracle answer over rows of the first {n_ch_s} channels "
                       f"({D.shape[0]} rows x {D.shape[1]} cells = {D.nbytes / 1e6:.1f} MB), "
                       f"{reps} repetitions in {dt:.1f} s"}
@@ -249,7 +261,7 @@ def cpu_baseline_gemm(wl, seed, kind, budget_s=10.0):
     dt = (time.perf_counter() - t0) / reps
     rate = macs / dt
     return {"value": round(rate / 1e9, 3), "unit": "G u32-MAC/s", "cores": O.num_threads(),
-            "kind": "oracle",
+            "kind": "oracle", "host": _host_cpu(),
             "sample": f"{rows} rows of the same DB x all {n_cells} cells x all "
                       f"{'queries' if kind == 'batch' else 'hint columns'}, {reps} repetitions",
             "extrapolated_full_step_s": round(full / rate, 1)}
@@ -283,6 +295,7 @@ def run_reference(args, wl, world, rank):
     sample = (f"oracle answer over rows of the first {n_ch_s} channels ({D.shape[0]} rows x "
               f"{D.shape[1]} cells = {D.nbytes / 1e6:.1f} MB) per step")
     cb = {"value": round(gbs, 3), "unit": "GB/s", "cores": O.num_threads(), "kind": "oracle",
+          "host": _host_cpu(),
           "sample": sample}
     line = {"impl": "reference", "metric": METRIC, "value": round(gbs, 3), "unit": "GB/s",
             "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
