@@ -50,25 +50,41 @@ inline uint32_t mma_pick_bn(uint64_t ncols) {
   return 256;
 }
 
-// Split K so that work units fill the SMs evenly (a few % tail at most); split
-// partials are combined with commutative atomics (exact for u32 add / XOR).
+// Split K so that work units fill the SMs evenly without making units so
+// short that their fixed cost dominates.  Cost in "wave K-blocks" (one K-block
+// of every CTA): waves(s) * (K-blocks per unit + c0) for the main loop, c0 ~ 6
+// K-blocks of per-unit cost (pipeline ramp, epilogue), plus the output traffic a
+// split adds -- a memset and one atomic pass per split instead of plain stores
+// -- converted at `wave_bytes` (the D bytes all CTAs stream per K-block).  Fitted
+// to tools/batch_size_probe.py (C2, B = 4: 1-2 splits 160-165 us vs 4 splits
+// 172 us; B = 64: 1 split 220 us vs 2 splits 236 us).  Split partials are
+// combined with commutative atomics (exact for u32 add / XOR).
+// HBM-bound tiles (hbm_bound: MT * BN <= 256, a few MMA clocks per streamed
+// K-block) with enough tiles to occupy every SM take no extra split at all: a
+// partial last wave costs little when the remaining CTAs share the whole HBM
+// bandwidth, while every split adds per-unit cost (A/B in one process,
+// tools/split_ab_probe.py: C2 B = 4..32, 1 split 159-171 us vs 2 splits 167-181).
 inline uint32_t mma_choose_splits(uint32_t tiles, uint32_t kblocks, uint32_t sms, int forced,
-                                  uint32_t min_splits) {
+                                  uint32_t min_splits, double out_bytes = 0.0,
+                                  double wave_bytes = 1.0, bool hbm_bound = false) {
   if (forced > 0)
     return std::max<uint32_t>(min_splits,
                               std::min<uint32_t>(std::min<uint32_t>((uint32_t)forced, 65536u), kblocks));
-  auto eff = [&](uint32_t units) {
-    const uint32_t waves = (units + sms - 1) / sms;
-    return (double)units / ((double)waves * sms);
+  if (hbm_bound && tiles >= sms) return min_splits;
+  constexpr double c0 = 6.0;
+  auto cost = [&](uint32_t s) {
+    const double waves = (double)((tiles * s + sms - 1) / sms);
+    const double out_passes = s > 1 ? (double)s + 1.0 : 1.0;
+    return waves * ((double)((kblocks + s - 1) / s) + c0) + out_passes * out_bytes / wave_bytes;
   };
   uint32_t best = min_splits;
-  double best_eff = eff(tiles * min_splits);
-  for (uint32_t s = min_splits + 1; s <= min_splits + 8; ++s) {
-    if (kblocks / s < 16) break;
-    const double e = eff(tiles * s);
-    if (e > best_eff + 0.02) {
+  double best_cost = cost(min_splits);
+  for (uint32_t s = min_splits + 1; s <= min_splits + 64; ++s) {
+    if (kblocks / s < 8) break;
+    const double c = cost(s);
+    if (c < best_cost * 0.99) {
       best = s;
-      best_eff = e;
+      best_cost = c;
     }
   }
   return best;
@@ -93,7 +109,9 @@ cudaError_t mma_launch_cfg(const MmaJob& j, cudaStream_t st, uint64_t* launches)
   const uint32_t max_kps = modp ? 66048u / (16u * GPB) : kblocks;
   const uint32_t min_splits = (kblocks + max_kps - 1) / max_kps;
   a.splits = mma_choose_splits(a.m_tiles * a.n_tiles, kblocks, (uint32_t)j.num_sms,
-                               j.forced_split, min_splits);
+                               j.forced_split, min_splits,
+                               (double)j.out_elems * (modp ? 8.0 : 4.0),
+                               (double)C::A_BYTES * (double)j.num_sms, MT * BN <= 256);
   a.kps = std::min((kblocks + a.splits - 1) / a.splits, max_kps);
   a.splits = (kblocks + a.kps - 1) / a.kps;  // no empty split
   a.p = j.p;
