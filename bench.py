@@ -125,7 +125,7 @@ class ClockSampler:
         t0, t1 = self.marks
         rows = [s for (t, s) in self.samples if t0 - 0.06 <= t <= t1 + 0.06] or \
                [s for (_, s) in self.samples[-3:]]
-        sm, mx, reasons = [], [], set()
+        sm, mx, pw, reasons = [], [], [], set()
         for r in rows:
             f = [x.strip() for x in r.split(",")]
             try:
@@ -133,12 +133,17 @@ class ClockSampler:
                 mx.append(float(f[1]))
             except (ValueError, IndexError):
                 continue
+            try:
+                pw.append(float(f[2]))
+            except (ValueError, IndexError):
+                pass
             for name, v in zip(self.NAMES, f[4:8]):
                 if v.lower().startswith("active"):
                     reasons.add(name)
         return {"sm_mhz": statistics.median(sm) if sm else None,
                 "sm_max_mhz": max(mx) if mx else None,
-                "reasons": sorted(reasons), "samples": len(sm)}
+                "reasons": sorted(reasons), "samples": len(sm),
+                "power_w_median": statistics.median(pw) if pw else None}
 
 
 # ---------------------------------------------------------------- helpers
