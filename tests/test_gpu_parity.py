@@ -360,13 +360,15 @@ def test_concurrent_streams_have_private_scratch(cuda_ok, monkeypatch):
 
 
 @pytest.mark.timeout(300)
-def test_lockstep_gemms_on_concurrent_streams(cuda_ok, monkeypatch):
+@pytest.mark.parametrize("n_cells", [16384, 16768])
+def test_lockstep_gemms_on_concurrent_streams(cuda_ok, monkeypatch, n_cells):
     """The tcgen05 engine's K-lockstep (CTAs of a wave wait for the slowest
     arrived CTA) with two hints and a batch running at once on three streams, so
     that some CTAs of each grid are not resident while others spin: no deadlock,
-    every result exact; chunk sizes 1 and 16 K-blocks."""
+    every result exact; chunk sizes 1 and 16 K-blocks; 16768 cells = 131 K-blocks,
+    so the last K-split is shorter and credits its missing chunks."""
     P = _srv()
-    n_cells, n_ch, d, n = 16384, 2, 24, 256  # G = 1024 groups: 128 K-blocks, N = 1024
+    n_ch, d, n = 2, 24, 256  # 16384 cells: G = 1024 groups, 128 K-blocks; N = 1024
     rec, D = _db(n_cells, n_ch, d, seed=91)
     A = O.expand_A(5, n_cells, n)
     Hw = O.hint(D, A)
