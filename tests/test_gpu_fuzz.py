@@ -70,3 +70,83 @@ def test_fuzz_ens_oop(cuda_ok, case):
             A = s.oop_preprocess(n, i, seeds[i:i + 1].view(np.int64).copy())[0]
             out ^= s.oop_answer(n, i, qq[i], A).cpu().numpy()
         assert (out == rec[theta]).all()
+
+
+@pytest.mark.parametrize("case", range(10))
+def test_fuzz_engine_knobs(cuda_ok, case, monkeypatch):
+    """The tcgen05 engine under random tuning knobs (lockstep chunk, forced
+    K-splits, row panels per tile, K-block size, limb count of the F_p path) on
+    shapes long enough in K for lockstep and several column tiles: bit-exact."""
+    P = _P()
+    rng = np.random.default_rng(3000 + case)
+    knobs = {"QPIR_MMA_LOCKSTEP": str(int(rng.choice([0, 1, 2, 16]))),
+             "QPIR_MMA_DRIFT": str(int(rng.choice([1, 2]))),
+             "QPIR_MMA_SPLIT": str(int(rng.choice([0, 0, 1, 3, 7]))),
+             "QPIR_MMA_MT": str(int(rng.choice([1, 2]))),
+             "QPIR_MMA_GPB": str(int(rng.choice([4, 8]))),
+             "QPIR_MODP2": str(int(rng.choice([0, 1]))),
+             "QPIR_MODP3": str(int(rng.choice([0, 1])))}
+    for k, v in knobs.items():
+        monkeypatch.setenv(k, v)
+    n_cells = int(rng.integers(4000, 12000))
+    n_ch = int(rng.integers(1, 5))
+    d = int(rng.integers(8, 100))
+    n = int(rng.choice([65, 128, 200]))
+    B = int(rng.choice([3, 40, 100]))
+    rec = synth.uniform_u8_np(case + 70, (n_cells * n_ch, d))
+    D = O.pack(rec, n_cells, n_ch, d, n_cells)
+    with P.PirServer(n_cells, n_ch, d, lwe_n=n, seed_A=case + 1, records=rec) as s:
+        Q = synth.uniform_u32_np(case + 80, (B, n_cells))
+        assert (P.u32(s.answer_batch(Q)) == O.answer_batch(D, Q)).all(), knobs
+        assert (P.u32(s.hint()) == O.hint(D, O.expand_A(case + 1, n_cells, n))).all(), knobs
+        p = int(rng.choice([257, 65521, 65537, 16777213, 2147483647]))
+        Qp = Q.copy()
+        Qp[0, : min(50, n_cells)] = 65536  # residue 65536 entries (p = 65537 exceptions)
+        want = ((Qp.astype(np.uint64) % p).astype(object) @ D.T.astype(object)) % p
+        assert (P.u32(s.answer_batch_modp(Qp, p)) == want.astype(np.uint32)).all(), knobs
+
+
+@pytest.mark.parametrize("case", range(10))
+def test_fuzz_scan_knobs(cuda_ok, case, monkeypatch):
+    """GEMV and ENS scan under random tuning knobs (rows per thread, groups in
+    flight, forced splits, smem chunk, TMA variant, PDL; ENS rows per CTA, rows
+    in flight, reduction group, wide / 256-bit kernels, PDL), several answers
+    back to back on one stream: bit-exact."""
+    P = _P()
+    rng = np.random.default_rng(4000 + case)
+    knobs = {"QPIR_GEMV_U": str(int(rng.choice([1, 2, 4]))),
+             "QPIR_GEMV_UNROLL": str(int(rng.choice([4, 8]))),
+             "QPIR_GEMV_SPLIT": str(int(rng.choice([0, 1, 3, 9]))),
+             "QPIR_GEMV_CHUNK": str(int(rng.choice([64, 512]))),
+             "QPIR_GEMV_IMPL": str(int(rng.choice([0, 0, 1]))),
+             "QPIR_GEMV_PDL": str(int(rng.choice([0, 1]))),
+             "QPIR_ENS_ROWS": str(int(rng.choice([0, 32, 96]))),
+             "QPIR_ENS_UR": str(int(rng.choice([4, 8, 16]))),
+             "QPIR_ENS_GROUP": str(int(rng.choice([0, 1, 5]))),
+             "QPIR_ENS_WIDE": str(int(rng.choice([0, 1, 2]))),
+             "QPIR_ENS_PDL": str(int(rng.choice([0, 1])))}
+    for k, v in knobs.items():
+        monkeypatch.setenv(k, v)
+    n_cells = int(rng.integers(100, 9000))
+    n_ch = int(rng.integers(1, 5))
+    d = int(rng.integers(1, 64))
+    rec = synth.uniform_u8_np(case + 90, (n_cells * n_ch, d))
+    D = O.pack(rec, n_cells, n_ch, d, n_cells)
+    with P.PirServer(n_cells, n_ch, d, records=rec) as s:
+        qs = [synth.uniform_u32_np(case * 10 + i, (n_cells,)) for i in range(4)]
+        outs = [s.answer(torch.from_numpy(q.view(np.int32)).cuda()) for q in qs]
+        for q, o in zip(qs, outs):
+            assert (P.u32(o) == O.answer(D, q)).all(), knobs
+    r = int(rng.integers(33, 5000))
+    de = int(rng.choice([16, 48, 3072, int(rng.integers(1, 4000))]))
+    rec2 = synth.uniform_u8_np(case + 95, (r, de))
+    with P.EnsServer(r, de, records=rec2) as s:
+        shs = []
+        for i in range(4):
+            q = synth.uniform_u8_np(case * 10 + 5 + i, ((r + 7) // 8,))
+            if r % 8:
+                q[-1] &= (1 << (r % 8)) - 1
+            shs.append(q)
+        outs = [s.answer(torch.from_numpy(q).cuda()) for q in shs]
+        for q, o in zip(shs, outs):
+            assert (o.cpu().numpy() == O.ens_respond(rec2, q)).all(), knobs
