@@ -2,9 +2,11 @@
 """Benchmark of the LWE-PIR answer path (BASELINE.json metric:
 "PIR answer DB-scan GB/s and queries/sec per GPU at 1/2/4/8 B200 vs HBM roof").
 
-    python bench.py [--gpus N] [--steps K] [--warmup W] [--workload c2|c3|c4-64|c4-256|c5|c1]
-                    [--impl ours|reference] [--no-cpu-baseline]
-    torchrun --nproc-per-node N bench.py --gpus N ...
+    python bench.py [--gpus N] [--steps K] [--warmup W]
+                    [--workload c1|c2|c3|c4-64|c4-256|c5|ens-c2|ens-c2-b128|ftr-c2-b128|oop-c2]
+                    [--impl ours|reference] [--no-cpu-baseline] [--no-e2e] [--graph 0|1]
+    torchrun --nproc-per-node N bench.py --gpus N ...   (plain `--gpus N` re-runs itself
+                                                        under torchrun on 127.0.0.1)
 
 A step = one pass of the whole hot path over one batch of synthetic input:
   c2 (default)  single query on the regional 1.007 GB DB (BASELINE.json configs[1]):
@@ -591,6 +593,17 @@ def main():
     ap.add_argument("--device-override", type=int, default=None,
                     help="put every rank on this CUDA device (functional tests only)")
     args = ap.parse_args()
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        # `python bench.py --gpus N` without a launcher: re-run under torchrun,
+        # one rank per GPU, rendezvous on 127.0.0.1
+        import socket
+        with socket.socket() as sk:
+            sk.bind(("127.0.0.1", 0))
+            port = sk.getsockname()[1]
+        os.execv(sys.executable, [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+                                  f"--nproc-per-node={args.gpus}", "--master-addr", "127.0.0.1",
+                                  "--master-port", str(port), os.path.abspath(__file__)]
+                 + sys.argv[1:])
     wl = dict(WORKLOADS[args.workload])
     world, rank, local = dist_env()
     if args.impl == "reference":
