@@ -8,18 +8,24 @@
 // accumulation (no saturation: the idesc saturate bit is 0, sums wrap mod 2^32)
 // and the epilogue recombines  ANS[:, j] = sum_k 2^{8k} C[:, 4j + k]  mod 2^32.
 //
-// Structure (one CTA per SM, persistent over work units = tile x K-split):
+// Structure (one CTA per SM, persistent over work units = tile x K-split,
+// ordered K-split slowest so the CTAs of a wave share one K range):
 //   warp 0     : producer -- per K-block of 128 cells, one 1-D bulk async copy
 //                (TMA engine, SASS UBLKCP) per 128-row D panel (16 KB each) and
-//                one for the B tile (BN x 128 B), into a STAGES-deep smem ring;
-//                mbarrier complete_tx.
+//                one for the B tile (BN x 128 B), into a STAGES-deep smem ring
+//                (as deep as 227 KB allows); mbarrier complete_tx.  With several
+//                column tiles it keeps K-lockstep with its wave (at most ls_drift
+//                chunks ahead of the slowest arrived CTA) so shared D panels and
+//                B tiles are read from L2, not HBM.
 //   warp 1     : TMEM allocator + MMA issuer -- one thread issues
 //                tcgen05.mma.cta_group::1.kind::i8 (M = 128, N = BN, K = 32),
 //                MT x 4 per K-block (MT row panels share each B tile), into a
 //                TMEM accumulator (double-buffered when 2 * MT * BN <= 512 cols);
 //                tcgen05.commit frees smem stages and signals the epilogue.
 //   warps 2..5 : epilogue -- tcgen05.ld 32 lanes x 16 columns, limb recombine,
-//                coalesced u32 stores (red.add when K is split), release TMEM.
+//                coalesced u32 stores (red.add when K is split), release TMEM;
+//                other modes: mod-p partials into a u64 scratch (FTR), GF(2)
+//                parity packed with __ballot_sync (ENS), row-major H (hint).
 // The smem operand layout equals the global layout (16-cell interleave):
 // [8 groups][rows][16 B] = the canonical no-swizzle K-major layout, core
 // matrices of 8 rows x 16 B contiguous (SBO = 128 B between 8-row core
