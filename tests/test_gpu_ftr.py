@@ -76,3 +76,32 @@ def test_ftr_two_limb_exceptions(cuda_ok):
         with Pk.FtrServer(r, s, p=p, records=rec) as srv:
             got = Pk.u32(srv.answer_batch(Q))
         assert (got == want.astype(np.uint32)).all(), p
+
+
+def test_ftr_and_batches_back_to_back(cuda_ok):
+    """FTR (2-limb, exception lists, growing and shrinking batch sizes) and LWE
+    batches queued back to back on one stream with no syncs and a hint in
+    between: every result exact."""
+    Pk = _P()
+    r, s = 70001, 12
+    rec = synth.uniform_u8_np(41, (r, s))
+    st = torch.cuda.Stream()
+    with Pk.FtrServer(r, s, records=rec) as srv:
+        jobs = []
+        for i, B in enumerate([5, 64, 3, 128, 7, 64]):
+            Q = synth.uniform_u32_np(600 + i, (B, r))
+            Q[0, i * 10:i * 10 + 40] = 65536 + 65537 * i  # residue 65536 entries
+            Qd = torch.from_numpy(Q.view(np.int32)).cuda()
+            if i % 2:
+                out = srv.answer_batch(Qd, stream=st)
+                want = ((Q % P).astype(np.int64) @ rec.astype(np.int64)) % P
+            else:
+                out = srv.server.answer_batch(Qd, stream=st)  # plain LWE batch, mod 2^32
+                want = (Q.astype(np.uint64) @ rec.astype(np.uint64)) & 0xFFFFFFFF
+            jobs.append((out, want.astype(np.uint32), Qd))
+            if i == 2:
+                jobs.append((srv.server.hint(stream=st), None, None))
+        st.synchronize()
+        for out, want, _ in jobs:
+            if want is not None:
+                assert (Pk.u32(out) == want).all()
