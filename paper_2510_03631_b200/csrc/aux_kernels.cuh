@@ -136,22 +136,27 @@ __global__ void limb_split_kernel(const uint32_t* __restrict__ Q, uint8_t* __res
 }
 
 // ---------------------------------------------------------------- a7 A'
-// A' (same panel layout as Q') = limb k of A[16g + i][j], n = 4j + k; one thread per
-// (group g, Philox block jb = j >> 2): 16 Philox calls, 256 contiguous bytes out.
-__global__ void expand_A_limbs_kernel(uint8_t* __restrict__ Ap, uint64_t seed, uint32_t m,
-                                      uint32_t n, uint32_t G, uint32_t Npad, uint32_t BN,
-                                      uint32_t j_off) {
-  // grid.x = column groups (up to 2^31), grid.y = blocks of Philox columns;
+// A' (same panel layout as Q') = limb k of A[16g + i][j], n = 4j + k.  Four
+// lanes share one (group g, Philox block jb = j >> 2): lane `sub` runs the 4
+// Philox calls of cells 16g + 4sub .. + 3 and writes, for each of the 16 limb
+// columns of the block, its 4-byte quarter of the 16-byte chunk (the 4 lanes
+// together write whole chunks).  16 registers of A per lane instead of 64 keeps
+// occupancy high enough to hide the Philox latency chains.
+__global__ void __launch_bounds__(256) expand_A_limbs_kernel(
+    uint8_t* __restrict__ Ap, uint64_t seed, uint32_t m, uint32_t n, uint32_t G, uint32_t Npad,
+    uint32_t BN, uint32_t j_off) {
+  // grid.x = column groups (up to 2^31), grid.y = blocks of 64 Philox blocks;
   // this launch generates hint columns j_off .. j_off + Npad/4 - 1 (j_off % 4 == 0)
-  const uint32_t jb = blockIdx.y * blockDim.x + threadIdx.x;
+  const uint32_t sub = threadIdx.x & 3u;
+  const uint32_t jb = blockIdx.y * (blockDim.x / 4) + threadIdx.x / 4;
   const uint32_t g = blockIdx.x;
   if (jb * 16u >= Npad) return;
   const uint2 key = make_uint2((uint32_t)seed, (uint32_t)(seed >> 32));
   const uint32_t jg = j_off + jb * 4u;  // global column of this Philox block
-  uint32_t a[16][4];
+  uint32_t a[4][4];
 #pragma unroll
-  for (int i = 0; i < 16; ++i) {
-    const uint32_t c = g * 16u + i;
+  for (int i = 0; i < 4; ++i) {
+    const uint32_t c = g * 16u + sub * 4u + i;
     uint4 v = make_uint4(0, 0, 0, 0);
     if (c < m && jg < n) v = philox4x32_10(make_uint4(c, jg >> 2, 0u, 0x41u), key);
     a[i][0] = v.x;
@@ -159,19 +164,14 @@ __global__ void expand_A_limbs_kernel(uint8_t* __restrict__ Ap, uint64_t seed, u
     a[i][2] = (jg + 2 < n) ? v.z : 0u;
     a[i][3] = (jg + 3 < n) ? v.w : 0u;
   }
-  uint4* dst = reinterpret_cast<uint4*>(Ap + limb_off(jb * 16u, g, G, BN));
+  uint32_t* dst = reinterpret_cast<uint32_t*>(Ap + limb_off(jb * 16u, g, G, BN)) + sub;
 #pragma unroll
   for (int jj = 0; jj < 4; ++jj) {
 #pragma unroll
     for (uint32_t k = 0; k < 4; ++k) {
-      uint32_t w[4];
-#pragma unroll
-      for (int t = 0; t < 4; ++t) {
-        const uint32_t sel = k | ((k + 4) << 4);
-        w[t] = __byte_perm(__byte_perm(a[4 * t + 0][jj], a[4 * t + 1][jj], sel),
-                           __byte_perm(a[4 * t + 2][jj], a[4 * t + 3][jj], sel), 0x5410);
-      }
-      dst[jj * 4 + k] = make_uint4(w[0], w[1], w[2], w[3]);
+      const uint32_t sel = k | ((k + 4) << 4);
+      dst[(jj * 4 + k) * 4] = __byte_perm(__byte_perm(a[0][jj], a[1][jj], sel),
+                                          __byte_perm(a[2][jj], a[3][jj], sel), 0x5410);
     }
   }
 }

@@ -771,9 +771,9 @@ int qpir_hint(qpir_ctx* ctx, uint32_t* H_local, uint64_t len_H, void* stream) {
   for (uint64_t j0 = 0; j0 < g.lwe_n; j0 += nc) {
     const uint32_t w = (uint32_t)std::min<uint64_t>(nc, g.lwe_n - j0);
     {
-      const uint32_t nb = Npad / 16;  // Philox blocks (4 outputs x 4 limbs)
-      dim3 grid((uint32_t)g.G, (nb + 127) / 128);
-      expand_A_limbs_kernel<<<grid, 128, 0, st>>>(ar.limbs, g.seed_A, (uint32_t)g.m, g.lwe_n,
+      const uint32_t nb = Npad / 16;  // Philox blocks (4 outputs x 4 limbs), 4 lanes each
+      dim3 grid((uint32_t)g.G, (nb + 63) / 64);
+      expand_A_limbs_kernel<<<grid, 256, 0, st>>>(ar.limbs, g.seed_A, (uint32_t)g.m, g.lwe_n,
                                                   (uint32_t)g.G, Npad, BN, (uint32_t)j0);
       LAUNCH_CHECK(ctx);
     }
