@@ -438,7 +438,7 @@ def run_ens(args, wl, world, rank, local):
     if tc_used:
         ach = bitplane_bytes / (ms / 1e3) / 1e9
         roof_tc = {"bound": "hbm", "achieved": round(ach, 1), "peak": hbm, "unit": "GB/s",
-                   "frac": round(ach / hbm, 4), "traffic": None,
+                   "frac": round(ach / hbm, 4), "traffic": _traffic(args.workload),
                    "kernel": "ens_share_expand_kernel + mma_u8_limb_kernel<OUT_PARITY>",
                    "kernel_ms": round(ms, 5), "peak_source": f"{peak_src} hbm_gbs",
                    "algorithmic_bytes_per_launch": bitplane_bytes,
