@@ -31,6 +31,10 @@
  *   - Streams: `stream` is a cudaStream_t (NULL = legacy default stream).  Work
  *     is enqueued on it.  If any output is host memory the call synchronises
  *     the stream before returning; with device outputs it returns immediately.
+ *     Host inputs are copied on a copy stream the library owns (per context
+ *     and stream), which `stream` then waits on: pageable inputs may be reused
+ *     as soon as the call returns; pinned inputs must stay unchanged until
+ *     `stream` has passed the call (as with cudaMemcpyAsync on `stream`).
  *   - Concurrency: answer / batch / hint calls on one context may run
  *     concurrently on different streams (each stream gets its own scratch
  *     arena: staging buffers, split-K partials, tickets); calls on one stream
