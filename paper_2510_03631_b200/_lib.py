@@ -67,7 +67,7 @@ class QpirError(RuntimeError):
 
 if not os.path.exists(LIB_PATH):
     raise ImportError(
-        f"{LIB_PATH} is missing: build it with `python -m paper_2510_03631_b200.build` "
+        f"{LIB_PATH} is missing: build it with `python paper_2510_03631_b200/build.py` "
         "(there is no CPU fallback)"
     )
 
