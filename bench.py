@@ -274,6 +274,47 @@ def cpu_baseline_gemm(wl, seed, kind, budget_s=10.0):
             "extrapolated_full_step_s": round(full / rate, 1)}
 
 
+def cpu_baseline_ens(wl, seed, kind, B=1, n_chunks=4, budget_s=8.0):
+    """Oracle ENS answer / batch or OOP online answer on a bounded sample: the first
+    32768 records (100.7 MB) of the same DB, all host cores, in the line's unit."""
+    import synth
+    from oracle import oracle as O
+    O.set_num_threads(os.cpu_count() or 1)
+    d, n_ch = wl["d"], wl["n_ch"]
+    rs = 32768
+    dev = "cuda" if torch.cuda.is_available() else "cpu"
+    rec = synth.records(seed, 0, rs, d, n_ch, device=dev).cpu().numpy()
+    nbs = rs // 8
+    if kind == "oop":
+        k = rs // n_chunks
+        q = synth.uniform_u8_np(seed + 3, (k // 8,))
+        A = O.oop_preprocess(rec, n_chunks, 0, 7919)
+        fn = lambda: O.oop_respond(rec, n_chunks, 0, q, A)  # noqa: E731
+        per_call = rs * d  # whole-DB equivalent, as the line
+    elif B == 1:
+        q = synth.uniform_u8_np(seed + 7, (nbs,))
+        fn = lambda: O.ens_respond(rec, q)  # noqa: E731
+        per_call = rs * d
+    else:
+        Q = synth.uniform_u8_np(seed + 7, (B, nbs))
+        fn = lambda: O.ens_respond_batch(rec, Q)  # noqa: E731
+        per_call = B * rs * d  # query-equivalent, as the line
+    _warm_oracle(fn, 2.0)
+    t0 = time.perf_counter()
+    reps = 0
+    while time.perf_counter() - t0 < budget_s:
+        fn()
+        reps += 1
+    dt = time.perf_counter() - t0
+    what = ("OOP online answer (n = 4)" if kind == "oop" else
+            "ENS answer" if B == 1 else f"ENS batch of {B} shares")
+    return {"value": round(reps * per_call / dt / 1e9, 3),
+            "unit": "GB/s" + ("" if B == 1 else " (query-equivalent)"),
+            "cores": O.num_threads(), "kind": "oracle", "host": _host_cpu(),
+            "sample": f"oracle {what} over the first {rs} records ({rs * d / 1e6:.1f} MB) of "
+                      f"the same DB, {reps} repetitions in {dt:.1f} s"}
+
+
 # ---------------------------------------------------------------- reference arm
 def run_reference(args, wl, world, rank):
     if rank != 0:
@@ -469,7 +510,8 @@ def run_ens(args, wl, world, rank, local):
                        "setup_s": round(setup_s, 1),
                        "l2": "inputs larger than L2 (1.007 GB records)"},
             "queries_per_s": round(world * B / (ms / 1e3), 1), "roofline": roof,
-            "cpu_baseline": None,
+            "cpu_baseline": (cpu_baseline_ens(wl, args.seed, "ens", B)
+                             if world == 1 and not args.no_cpu_baseline else None),
             "e2e": {"value": round(world * db * B / (te / 1e3) / 1e9, 2), "unit": "GB/s",
                     "h2d_bytes_per_step": B * nb, "d2h_bytes_per_step": B * d,
                     "ms_per_step": round(te, 4), "timing": e2e_timing},
@@ -554,7 +596,8 @@ def run_oop(args, wl, rank, local):
                          "note": "back-to-back online answers overlap through programmatic "
                                  "dependent launch (one kernel alone under ncu: "
                                  "profiles/r01_oop_scan_ncu_full.md)"},
-            "cpu_baseline": None,
+            "cpu_baseline": (cpu_baseline_ens(wl, args.seed, "oop", n_chunks=n)
+                             if not args.no_cpu_baseline else None),
             "e2e": {"value": round(r * d / (te / 1e3) / 1e9, 2), "unit": "GB/s",
                     "h2d_bytes_per_step": kb + d, "d2h_bytes_per_step": d,
                     "ms_per_step": round(te, 4),
