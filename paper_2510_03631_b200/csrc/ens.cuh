@@ -429,9 +429,12 @@ __global__ void ens_bitplane_pack_kernel(const uint8_t* __restrict__ R, uint64_t
 __global__ void ens_share_expand_kernel(const uint8_t* __restrict__ Q, uint32_t B, uint64_t r,
                                         uint64_t nb, uint8_t* __restrict__ Qb, uint32_t G,
                                         uint32_t Npad, uint32_t BN) {
-  // grid.x = 16-record groups (up to 2^31), grid.y = share slots
-  const uint32_t g = blockIdx.x * blockDim.x + threadIdx.x;
-  const uint32_t q = blockIdx.y;
+  // Share slot fastest: consecutive threads write consecutive 16-byte columns of
+  // one group (coalesced runs of BN * 16 bytes -- the 8x-expanded output is the
+  // traffic that matters); their 2-byte share reads hit the L2-resident shares.
+  // grid.x = blocks of share slots, grid.y / grid.z = 16-record groups
+  const uint32_t q = blockIdx.x * blockDim.x + threadIdx.x;
+  const uint32_t g = blockIdx.y + blockIdx.z * gridDim.y;
   if (q >= Npad || g >= G) return;
   uint32_t bits = 0;
   if (q < B) {

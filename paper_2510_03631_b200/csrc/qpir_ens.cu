@@ -458,8 +458,11 @@ static int ens_batch_tc(qpir_ens_ctx* ctx, const uint8_t* Qd, uint64_t B, cudaSt
   int rc = grow(ctx, (void**)&ctx->Qb, &ctx->Qb_bytes, Npad * m_pad);
   if (rc) return rc;
   {
-    dim3 grid((uint32_t)((G + 127) / 128), (uint32_t)Npad);
-    ens_share_expand_kernel<<<grid, 128, 0, st>>>(Qd, (uint32_t)B, ctx->r, (ctx->r + 7) / 8,
+    const uint32_t gy = (uint32_t)std::min<uint64_t>(G, 65535);
+    const uint32_t gz = (uint32_t)((G + gy - 1) / gy);
+    const uint32_t tpb = (uint32_t)std::min<uint64_t>(Npad, 128);
+    dim3 grid((uint32_t)((Npad + tpb - 1) / tpb), gy, gz);
+    ens_share_expand_kernel<<<grid, tpb, 0, st>>>(Qd, (uint32_t)B, ctx->r, (ctx->r + 7) / 8,
                                                   ctx->Qb, (uint32_t)G, (uint32_t)Npad, BN);
     ENS_LAUNCHED(ctx);
   }
