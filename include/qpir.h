@@ -165,8 +165,8 @@ void qpir_destroy(qpir_ctx *ctx);
 /* positions >= r are ignored.  The response to a share is the XOR of the  */
 /* records whose bit is 1 (rho = q . DB over GF(2)); a client XORs the l   */
 /* responses of l servers to rebuild its record.  Same buffer, length,     */
-/* stream and error conventions as above, except that an ENS context has   */
-/* one scratch arena: its calls must be serialised by the caller.          */
+/* stream, error and concurrency conventions as above (per-stream scratch: */
+/* calls on different streams may run concurrently).                       */
 /* ===================================================================== */
 typedef struct qpir_ens_ctx qpir_ens_ctx;
 
@@ -192,10 +192,10 @@ int qpir_ens_answer(qpir_ens_ctx *ctx, const uint8_t *share, uint64_t len_share,
                     uint8_t *out, uint64_t len_out, void *stream);
 
 /* Responses to B shares (B x ceil(r/8), share-major) -> out: B x d bytes.
- * 1 <= B <= 65536.  For 32 <= B <= 65280 the GF(2) product runs on tensor
- * cores over the records' bit-planes, which take 8 * r * d bytes of extra
- * device memory (built on first use, rebuilt after qpir_ens_db_write); if that
- * allocation fails, or for smaller B, a CUDA-core XOR kernel is used. */
+ * 1 <= B <= 65536 (Alg. 3 multi-request form).  For B >= 32
+ * the GF(2) product runs on tensor cores (records read once in place and
+ * expanded on chip; the shares take B * r bytes of scratch as 0/1 bytes);
+ * smaller B use a CUDA-core XOR kernel.  qpir_ens_last_path reports which. */
 int qpir_ens_answer_batch(qpir_ens_ctx *ctx, const uint8_t *shares, uint64_t B,
                           uint64_t len_shares, uint8_t *out, uint64_t len_out,
                           void *stream);
@@ -219,8 +219,34 @@ int qpir_oop_answer(qpir_ens_ctx *ctx, uint32_t n_chunks, uint32_t server,
                     uint8_t *out, uint64_t len_out, void *stream);
 
 uint64_t qpir_ens_kernel_launches(const qpir_ens_ctx *ctx);
+
+/* Which kernel path the last ENS/OOP call of this context took (for reports). */
+#define QPIR_ENS_PATH_NONE 0       /* no call yet                              */
+#define QPIR_ENS_PATH_SCAN 1       /* single-share scan (answer / OOP online)  */
+#define QPIR_ENS_PATH_CUDA_CORES 2 /* multi-request XOR kernel on CUDA cores   */
+#define QPIR_ENS_PATH_TENSOR 3     /* multi-request GF(2) product on tcgen05   */
+int qpir_ens_last_path(const qpir_ens_ctx *ctx);
 const char *qpir_ens_last_error(const qpir_ens_ctx *ctx);
 void qpir_ens_destroy(qpir_ens_ctx *ctx);
+
+/* ===================================================================== */
+/* Cross-rank combine of record-sharded NEXT rows (dist.py, one process per */
+/* GPU): after an all-gather of the n_parts per-rank partial responses     */
+/* (rank-major, n_parts x len), fold them on the device.  parts and out    */
+/* must be device memory of one device (QPIR_E_PARAM otherwise: there is   */
+/* no host fallback); the kernel is queued on `stream`, no sync.           */
+/* ===================================================================== */
+/* ENS / OOP (GF(2); Lemma 1 proof PAPER.md:1227, Alg. 3):
+ * out[i] = XOR over r of parts[r * len + i]  (len bytes). */
+int qpir_xor_fold(const uint8_t *parts, uint64_t n_parts, uint64_t len, uint8_t *out,
+                  void *stream);
+/* FTR (F_p; Lemma 1 proof "R_j := rho_j . DB", Alg. 4):
+ * out[i] = (sum over r of parts[r * len + i]) mod p, summed exactly in 64 bits;
+ * 1 <= n_parts <= 2^32, p >= 2. */
+int qpir_sum_mod_p(const uint32_t *parts, uint64_t n_parts, uint64_t len, uint32_t p,
+                   uint32_t *out, void *stream);
+/* Message of the last failed combine call of this thread ("" if none). */
+const char *qpir_combine_last_error(void);
 
 #ifdef __cplusplus
 }

@@ -69,6 +69,8 @@ def lib():
         L.qo_ftr_respond_batch.argtypes = [_u8p, _u64, _u64, _u32p, _u64, _u32, _u32p]
         L.qo_ftr_reconstruct.argtypes = [_u32p, _u32p, _u32, _u64, _u32, _u32p]
         L.qo_ftr_reconstruct.restype = ctypes.c_int
+        L.qo_ftr_decode_bw.argtypes = [_u32p, _u32p, _u32, _u64, _u32, _u32, _u32p, _u32p]
+        L.qo_ftr_decode_bw.restype = ctypes.c_int
         L.qo_oop_preprocess.argtypes = [_u8p, _u64, _u64, _u32, _u32, _u64, _u8p]
         L.qo_oop_query.argtypes = [_u64, _u64, _u32, _u64p, _u8p]
         L.qo_oop_respond.argtypes = [_u8p, _u64, _u64, _u32, _u32, _u8p, _u8p, _u8p]
@@ -277,6 +279,32 @@ def ftr_reconstruct(resp: np.ndarray, alpha, p: int = FTR_P) -> np.ndarray:
     if rc != 0:
         raise ValueError("evaluation points must be distinct")
     return out
+
+
+class FtrDecodeError(ValueError):
+    """Robust reconstruction failed: too few responses or more than
+    floor((k - t - 1) / 2) of them wrong."""
+
+
+def ftr_decode(resp: np.ndarray, alpha, t: int, p: int = FTR_P):
+    """Berlekamp-Welch unique decoding (qo_ftr_decode_bw): returns (block, bad)
+    where bad[i] = 1 marks server i's response as inconsistent with the decoded
+    polynomial.  Raises FtrDecodeError beyond the unique-decoding radius."""
+    resp = _c(resp, np.uint32)
+    k, s_ = resp.shape
+    al = _c(alpha, np.uint32)
+    assert al.shape == (k,)
+    out = np.empty(s_, np.uint32)
+    bad = np.empty(k, np.uint32)
+    rc = lib().qo_ftr_decode_bw(_p(resp, _u32p), _p(al, _u32p), k, s_, t, p, _p(out, _u32p),
+                                _p(bad, _u32p))
+    if rc == -1:
+        raise ValueError("evaluation points must be distinct")
+    if rc == 1:
+        raise FtrDecodeError(f"k = {k} responses <= t = {t}: incomplete")
+    if rc == 2:
+        raise FtrDecodeError(f"more than {(k - t - 1) // 2} corrupted responses")
+    return out, bad.astype(bool)
 
 
 # ---------------------------------------------------------------- OOP (CIP-PIR, NEXT-3)

@@ -433,6 +433,108 @@ int qo_ftr_reconstruct(const uint32_t *resp, const uint32_t *alpha, uint32_t k, 
   return 0;
 }
 
+/* Robust BlockReconst ("nu-Byzantine fault tolerance"; Lemma 1 proof,
+ * P:1227): Berlekamp-Welch unique decoding of the k
+ * responses, which are evaluations y_i = F(alpha_i) of a polynomial F of
+ * degree <= t (sum_j f_j(x) DB[j][b], each f_j of degree t) with up to
+ * e = floor((k - t - 1) / 2) of them wrong.  Per word b, the textbook steps:
+ *   1. unknowns: E(x) = x^e + E_{e-1} x^{e-1} + ... + E_0 (error locator, monic)
+ *      and Q(x) = Q_0 + ... + Q_{e+t} x^{e+t};
+ *   2. the k linear equations Q(alpha_i) = y_i E(alpha_i), i.e.
+ *      sum_c Q_c alpha_i^c - y_i sum_{a<e} E_a alpha_i^a = y_i alpha_i^e,
+ *      solved by Gaussian elimination over F_p (free unknowns set to 0: any
+ *      solution gives Q = F E when at most e responses are wrong);
+ *   3. F = Q / E by polynomial long division; the remainder must be 0 and
+ *      deg F <= t;
+ *   4. F must agree with at least k - e responses (else: more than e errors);
+ *   5. the word is F(0) (= the record byte, since f_j(0) = e_theta[j]).
+ * The paper's Guruswami-Sudan list decoder reaches nu < k - floor(sqrt(k t))
+ * (P:1227); unique decoding stops at e (DESIGN R21).  bad[i] (if not NULL) is
+ * set to 1 for every server whose response disagrees with F in some word.
+ * Returns 0 on success, 1 if k <= t (too few responses), 2 if decoding fails
+ * (more errors than e), -1 if two alphas coincide.  p prime, k <= 64. */
+int qo_ftr_decode_bw(const uint32_t *resp, const uint32_t *alpha, uint32_t k, uint64_t s,
+                     uint32_t t, uint32_t p, uint32_t *out, uint32_t *bad) {
+  if (k <= t) return 1;
+  if (k > 64) return 1;
+  for (uint32_t i = 0; i < k; ++i)
+    for (uint32_t m = i + 1; m < k; ++m)
+      if (alpha[i] % p == alpha[m] % p) return -1;
+  const uint32_t e = (k - t - 1) / 2;
+  const uint32_t nq = e + t + 1, nu = nq + e; /* unknowns: Q_0..Q_{e+t}, E_0..E_{e-1} */
+  uint64_t M[64][130];                        /* k x (nu + 1) augmented matrix */
+  if (bad)
+    for (uint32_t i = 0; i < k; ++i) bad[i] = 0;
+  for (uint64_t b = 0; b < s; ++b) {
+    /* step 2: the linear system */
+    for (uint32_t i = 0; i < k; ++i) {
+      const uint64_t a = alpha[i] % p, y = resp[(uint64_t)i * s + b] % p;
+      uint64_t apow = 1;
+      for (uint32_t c = 0; c < nq; ++c) {
+        M[i][c] = apow;
+        if (c < e) M[i][nq + c] = (p - mulmod(y, apow, p)) % p;
+        apow = mulmod(apow, a, p);
+      }
+      M[i][nu] = mulmod(y, powmod(a, e, p), p);
+    }
+    /* Gaussian elimination to reduced row echelon form */
+    uint32_t pivcol[64];
+    uint32_t rank = 0;
+    for (uint32_t c = 0; c < nu && rank < k; ++c) {
+      uint32_t piv = rank;
+      while (piv < k && M[piv][c] == 0) ++piv;
+      if (piv == k) continue;
+      for (uint32_t x = 0; x <= nu; ++x) {
+        uint64_t tmp = M[rank][x];
+        M[rank][x] = M[piv][x];
+        M[piv][x] = tmp;
+      }
+      const uint64_t inv = powmod(M[rank][c], p - 2, p);
+      for (uint32_t x = 0; x <= nu; ++x) M[rank][x] = mulmod(M[rank][x], inv, p);
+      for (uint32_t i = 0; i < k; ++i) {
+        if (i == rank || M[i][c] == 0) continue;
+        const uint64_t f = M[i][c];
+        for (uint32_t x = 0; x <= nu; ++x) M[i][x] = (M[i][x] + p - mulmod(f, M[rank][x], p)) % p;
+      }
+      pivcol[rank++] = c;
+    }
+    for (uint32_t i = rank; i < k; ++i)
+      if (M[i][nu] != 0) return 2; /* inconsistent: more than e errors */
+    uint64_t sol[129];
+    for (uint32_t c = 0; c < nu; ++c) sol[c] = 0;
+    for (uint32_t i = 0; i < rank; ++i) sol[pivcol[i]] = M[i][nu];
+    /* step 3: F = Q / E, E monic of degree e */
+    uint64_t Q[129], E[65], F[129];
+    for (uint32_t c = 0; c < nq; ++c) Q[c] = sol[c];
+    for (uint32_t a = 0; a < e; ++a) E[a] = sol[nq + a];
+    E[e] = 1;
+    for (uint32_t c = 0; c < nq; ++c) F[c] = 0;
+    for (int32_t c = (int32_t)nq - 1; c >= (int32_t)e; --c) {
+      const uint64_t q = Q[c]; /* leading coefficient / 1 */
+      F[c - e] = q;
+      for (uint32_t a = 0; a <= e; ++a)
+        Q[c - e + a] = (Q[c - e + a] + p - mulmod(q, E[a], p)) % p;
+    }
+    for (uint32_t c = 0; c < e; ++c)
+      if (Q[c] != 0) return 2; /* E does not divide Q */
+    /* deg F <= t holds by construction (deg Q - e <= t) */
+    /* step 4: agreement */
+    uint32_t agree = 0;
+    for (uint32_t i = 0; i < k; ++i) {
+      const uint64_t a = alpha[i] % p;
+      uint64_t v = 0;
+      for (int32_t c = (int32_t)t; c >= 0; --c) v = (mulmod(v, a, p) + F[c]) % p;
+      if (v == resp[(uint64_t)i * s + b] % p)
+        ++agree;
+      else if (bad)
+        bad[i] = 1;
+    }
+    if (agree + e < k) return 2;
+    out[b] = (uint32_t)F[0]; /* step 5 */
+  }
+  return 0;
+}
+
 /* ------------------------------------------------------------------ */
 /* NEXT-3: QPADL-OOP = CIP-PIR offline-online (P:930-942;       */
 /* Lemma 2 proof).  B blocks (records of d bytes) in n chunks  */

@@ -24,6 +24,12 @@ from ._lib import QpirError, qpir_params  # noqa: F401
 __all__ = ["PirServer", "EnsServer", "FtrServer", "QpirError", "u32", "qpir_params"]
 
 
+def _st(device: int, stream):
+    """Default stream of a call: torch's current stream on the context's device
+    (calls then order with torch work, including inside torch.cuda.stream(...))."""
+    return torch.cuda.current_stream(device) if stream is None else stream
+
+
 def u32(t) -> np.ndarray:
     """torch int32 (u32 bit pattern) tensor -> numpy uint32 array (copies to host)."""
     if isinstance(t, np.ndarray):
@@ -42,14 +48,14 @@ class PirServer:
                         row_end=row_end, device=device, reserved1=0)
         self.device = device
         self.lwe_n = lwe_n
-        self._ctx = _lib.qpir_setup(p, records, stream)
+        self._ctx = _lib.qpir_setup(p, records, _st(device, stream))
         self.ell, self.m, self.ell_local, self.row_begin = _lib.qpir_geometry(self._ctx)
         self.n_cells, self.n_ch, self.rec_bytes = n_cells, n_ch, rec_bytes
 
     # ------------------------------------------------------------------ DB
     def db_write(self, theta_begin: int, records, stream=None) -> None:
         n = int(records.shape[0]) if records.ndim == 2 else records.numel() // self.rec_bytes
-        _lib.qpir_db_write(self._ctx, theta_begin, records, n, stream)
+        _lib.qpir_db_write(self._ctx, theta_begin, records, n, _st(self.device, stream))
 
     # ------------------------------------------------------------------ answers
     def _dev(self):
@@ -58,27 +64,27 @@ class PirServer:
     def answer(self, qu, out=None, stream=None):
         if out is None:
             out = torch.empty(self.ell_local, dtype=torch.int32, device=self._dev())
-        _lib.qpir_answer(self._ctx, qu, out, stream)
+        _lib.qpir_answer(self._ctx, qu, out, _st(self.device, stream))
         return out
 
     def answer_batch(self, Q, out=None, stream=None):
         B = int(Q.shape[0])
         if out is None:
             out = torch.empty((B, self.ell_local), dtype=torch.int32, device=self._dev())
-        _lib.qpir_answer_batch(self._ctx, Q, B, out, stream)
+        _lib.qpir_answer_batch(self._ctx, Q, B, out, _st(self.device, stream))
         return out
 
     def answer_batch_modp(self, Q, p: int, out=None, stream=None):
         B = int(Q.shape[0])
         if out is None:
             out = torch.empty((B, self.ell_local), dtype=torch.int32, device=self._dev())
-        _lib.qpir_answer_batch_modp(self._ctx, Q, B, p, out, stream)
+        _lib.qpir_answer_batch_modp(self._ctx, Q, B, p, out, _st(self.device, stream))
         return out
 
     def hint(self, out=None, stream=None):
         if out is None:
             out = torch.empty((self.ell_local, self.lwe_n), dtype=torch.int32, device=self._dev())
-        _lib.qpir_hint(self._ctx, out, stream)
+        _lib.qpir_hint(self._ctx, out, _st(self.device, stream))
         return out
 
     @property
@@ -113,16 +119,16 @@ class EnsServer:
         self.device = device
         self.r, self.d = n_records, rec_bytes
         self.share_bytes = (n_records + 7) // 8
-        self._ctx = _lib.qpir_ens_setup(p, records, stream)
+        self._ctx = _lib.qpir_ens_setup(p, records, _st(device, stream))
 
     def db_write(self, theta_begin: int, records, stream=None) -> None:
         n = int(records.shape[0]) if records.ndim == 2 else records.numel() // self.d
-        _lib.qpir_ens_db_write(self._ctx, theta_begin, records, n, stream)
+        _lib.qpir_ens_db_write(self._ctx, theta_begin, records, n, _st(self.device, stream))
 
     def answer(self, share, out=None, stream=None):
         if out is None:
             out = torch.empty(self.d, dtype=torch.uint8, device=torch.device("cuda", self.device))
-        _lib.qpir_ens_answer(self._ctx, share, out, stream)
+        _lib.qpir_ens_answer(self._ctx, share, out, _st(self.device, stream))
         return out
 
     def answer_batch(self, shares, out=None, stream=None):
@@ -130,7 +136,7 @@ class EnsServer:
         if out is None:
             out = torch.empty((B, self.d), dtype=torch.uint8,
                               device=torch.device("cuda", self.device))
-        _lib.qpir_ens_answer_batch(self._ctx, shares, B, out, stream)
+        _lib.qpir_ens_answer_batch(self._ctx, shares, B, out, _st(self.device, stream))
         return out
 
     # ---- NEXT-3: OOP / CIP-PIR offline-online on the same records
@@ -139,15 +145,20 @@ class EnsServer:
         n = int(seeds.shape[0])
         if out is None:
             out = torch.empty((n, self.d), dtype=torch.uint8, device=torch.device("cuda", self.device))
-        _lib.qpir_oop_preprocess(self._ctx, n_chunks, server, seeds, out, stream)
+        _lib.qpir_oop_preprocess(self._ctx, n_chunks, server, seeds, out, _st(self.device, stream))
         return out
 
     def oop_answer(self, n_chunks: int, server: int, q, A, out=None, stream=None):
         """Online: R_i = A_i XOR q_i . chunk_i (touches 1/n of the DB)."""
         if out is None:
             out = torch.empty(self.d, dtype=torch.uint8, device=torch.device("cuda", self.device))
-        _lib.qpir_oop_answer(self._ctx, n_chunks, server, q, A, out, stream)
+        _lib.qpir_oop_answer(self._ctx, n_chunks, server, q, A, out, _st(self.device, stream))
         return out
+
+    @property
+    def last_path(self) -> str:
+        """Kernel path of the last call: "scan", "cuda_cores", "tensor" (or "none")."""
+        return ("none", "scan", "cuda_cores", "tensor")[_lib.qpir_ens_last_path(self._ctx)]
 
     @property
     def kernel_launches(self) -> int:

@@ -28,8 +28,12 @@ EXPORTS = (
     "qpir_hint", "qpir_kernel_launches", "qpir_last_error", "qpir_destroy",
     "qpir_answer_batch_modp", "qpir_ens_setup", "qpir_ens_db_write", "qpir_ens_answer", "qpir_ens_answer_batch",
     "qpir_ens_kernel_launches", "qpir_ens_last_error", "qpir_ens_destroy",
-    "qpir_oop_preprocess", "qpir_oop_answer",
+    "qpir_oop_preprocess", "qpir_oop_answer", "qpir_ens_last_path",
+    "qpir_xor_fold", "qpir_sum_mod_p", "qpir_combine_last_error",
 )
+
+# qpir_ens_last_path values (include/qpir.h)
+QPIR_ENS_PATH_NONE, QPIR_ENS_PATH_SCAN, QPIR_ENS_PATH_CUDA_CORES, QPIR_ENS_PATH_TENSOR = 0, 1, 2, 3
 
 
 class qpir_params(ctypes.Structure):
@@ -93,12 +97,18 @@ _L.qpir_ens_answer.argtypes = [_vp, _vp, _u64, _vp, _u64, _vp]
 _L.qpir_ens_answer_batch.argtypes = [_vp, _vp, _u64, _u64, _vp, _u64, _vp]
 _L.qpir_ens_kernel_launches.argtypes = [_vp]
 _L.qpir_ens_kernel_launches.restype = _u64
+_L.qpir_ens_last_path.argtypes = [_vp]
+_L.qpir_ens_last_path.restype = ctypes.c_int
 _L.qpir_ens_last_error.argtypes = [_vp]
 _L.qpir_ens_last_error.restype = ctypes.c_char_p
 _L.qpir_ens_destroy.argtypes = [_vp]
 _L.qpir_oop_preprocess.argtypes = [_vp, ctypes.c_uint32, ctypes.c_uint32, _vp, _u64, _vp, _u64, _vp]
 _L.qpir_oop_answer.argtypes = [_vp, ctypes.c_uint32, ctypes.c_uint32, _vp, _u64, _vp, _u64, _vp,
                                _u64, _vp]
+_L.qpir_xor_fold.argtypes = [_vp, _u64, _u64, _vp, _vp]
+_L.qpir_sum_mod_p.argtypes = [_vp, _u64, _u64, ctypes.c_uint32, _vp, _vp]
+_L.qpir_combine_last_error.argtypes = []
+_L.qpir_combine_last_error.restype = ctypes.c_char_p
 for _name in EXPORTS:
     getattr(_L, _name)
 
@@ -125,8 +135,14 @@ def _numel(x) -> int:
 
 
 def _stream(stream) -> int | None:
+    """cudaStream_t handle.  None -> torch's current stream on the current
+    device (so calls order with torch work inside `with torch.cuda.stream(s)`);
+    an int is passed through (0 = the legacy default stream)."""
     if stream is None:
-        return None
+        import torch
+        if not torch.cuda.is_available():
+            return None
+        return torch.cuda.current_stream().cuda_stream
     if isinstance(stream, int):
         return stream
     return stream.cuda_stream  # torch.cuda.Stream
@@ -225,6 +241,10 @@ def qpir_ens_kernel_launches(ctx: int) -> int:
     return int(_L.qpir_ens_kernel_launches(ctx))
 
 
+def qpir_ens_last_path(ctx: int) -> int:
+    return int(_L.qpir_ens_last_path(ctx))
+
+
 def qpir_ens_last_error(ctx: int | None = None) -> str:
     return _L.qpir_ens_last_error(ctx).decode()
 
@@ -242,3 +262,18 @@ def qpir_oop_preprocess(ctx: int, n_chunks: int, server: int, seeds, A_out, stre
 def qpir_oop_answer(ctx: int, n_chunks: int, server: int, q, A, out, stream=None):
     _check_ens(_L.qpir_oop_answer(ctx, n_chunks, server, _addr(q), _numel(q), _addr(A), _numel(A),
                                   _addr(out), _numel(out), _stream(stream)), ctx)
+
+
+# ------------------------------------------------------------ cross-rank combine
+def _check_combine(rc: int):
+    if rc != QPIR_OK:
+        raise QpirError(rc, _L.qpir_combine_last_error().decode())
+
+
+def qpir_xor_fold(parts, n_parts: int, length: int, out, stream=None):
+    _check_combine(_L.qpir_xor_fold(_addr(parts), n_parts, length, _addr(out), _stream(stream)))
+
+
+def qpir_sum_mod_p(parts, n_parts: int, length: int, p: int, out, stream=None):
+    _check_combine(_L.qpir_sum_mod_p(_addr(parts), n_parts, length, p, _addr(out),
+                                     _stream(stream)))

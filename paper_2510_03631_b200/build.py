@@ -13,7 +13,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(HERE)
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libqpir.so")
-SOURCES = [os.path.join(CSRC, "qpir.cu"), os.path.join(CSRC, "qpir_ens.cu")]
+SOURCES = [os.path.join(CSRC, f) for f in ("qpir.cu", "qpir_ens.cu", "qpir_combine.cu")]
 HEADERS = [os.path.join(CSRC, f) for f in os.listdir(CSRC) if f.endswith((".cuh", ".h"))] + [
     os.path.join(ROOT, "include", "qpir.h")
 ]

@@ -79,6 +79,8 @@ __device__ __forceinline__ void ens_finalize(const EnsArgs& a) {
 template <int UR>
 __global__ void __launch_bounds__(1024, 1) ens_scan_kernel(EnsArgs a) {
   asm volatile("griddepcontrol.launch_dependents;");  // PDL: see ens_scan_wide_kernel
+  // the share selects which rows are read: nothing can be touched before the wait
+  asm volatile("griddepcontrol.wait;" ::: "memory");
   extern __shared__ uint4 s_part[];
   const uint32_t w = threadIdx.x % a.W;
   const uint32_t lr = threadIdx.x / a.W;
@@ -111,7 +113,6 @@ __global__ void __launch_bounds__(1024, 1) ens_scan_kernel(EnsArgs a) {
       acc.w ^= v[u].w;
     }
   }
-  asm volatile("griddepcontrol.wait;" ::: "memory");  // previous grid complete + visible
   const bool owner = lr == 0;  // one thread per 16-byte chunk keeps the CTA result
   if (R > 1) {
     s_part[threadIdx.x] = acc;
@@ -176,12 +177,15 @@ __global__ void __launch_bounds__(1024, 1) ens_scan_kernel(EnsArgs a) {
 // bounds (1024, 1) let ptxas spend 64 registers and keep ~11 row loads in
 // flight per thread; under plain (1024) it packed into 32 registers and issued
 // the loads two at a time (SASS), latency-bound at 0.61-0.90 of HBM.
-// Programmatic dependent launch: only the scan (reads of R and q) runs before
-// griddepcontrol.wait, so back-to-back answers overlap one's tail with the
-// next one's first loads; partials, tickets and out are touched after it.
+// Programmatic dependent launch: the next scan's CTAs become resident while this
+// grid drains, but every read waits at griddepcontrol.wait -- the share (which
+// the previous kernel on the stream may have written) decides which rows of R
+// are read, so there is nothing to prefetch before it; back-to-back answers
+// still save the launch and CTA ramp.
 template <int UR, int CW>
 __global__ void __launch_bounds__(1024, 1) ens_scan_wide_kernel(EnsArgs a) {
   asm volatile("griddepcontrol.launch_dependents;");
+  asm volatile("griddepcontrol.wait;" ::: "memory");  // previous grid complete + visible
   const uint32_t w = threadIdx.x * CW;  // first 16-byte chunk of this thread
   const uint64_t n_rows = a.row_hi - a.row_lo;
   const uint64_t t0 = (uint64_t)blockIdx.x * a.rows_per_cta;  // multiple of 32
@@ -217,7 +221,6 @@ __global__ void __launch_bounds__(1024, 1) ens_scan_wide_kernel(EnsArgs a) {
         }
     }
   }
-  asm volatile("griddepcontrol.wait;" ::: "memory");  // previous grid complete + visible
   if (a.partial != nullptr) {
     __shared__ uint32_t s_last;
 #pragma unroll
@@ -380,52 +383,9 @@ __global__ void oop_expand_kernel(const unsigned long long* __restrict__ seeds, 
 
 namespace qpir {
 // ---------------------------------------------------------------- ENS on tensor cores
-// Bit-plane operand for the GF(2) multi-request product (NEXT-1, DESIGN 6):
-// Dbits[8j + k][theta] = bit k of byte j of record theta, in the engine's
-// 128-row panel layout ((row >> 7) * G + (theta >> 4)) * 2048 + (row & 127) * 16
-// + (theta & 15).  One thread per (panel, 16-record group): 16 x 16-byte record
-// loads in, one contiguous 2 KB panel block out.
-__device__ __forceinline__ uint32_t gather_byte(uint32_t a, uint32_t b, uint32_t c, uint32_t e,
-                                                uint32_t k) {
-  const uint32_t sel = k | ((k + 4u) << 4);
-  return __byte_perm(__byte_perm(a, b, sel), __byte_perm(c, e, sel), 0x5410);
-}
-
-__device__ __forceinline__ uint32_t u4_word(const uint4& v, uint32_t i) {
-  return i == 0 ? v.x : i == 1 ? v.y : i == 2 ? v.z : v.w;
-}
-
-__global__ void ens_bitplane_pack_kernel(const uint8_t* __restrict__ R, uint64_t r, uint32_t dp,
-                                         uint8_t* __restrict__ Dbits, uint32_t G) {
-  const uint32_t g = blockIdx.x * blockDim.x + threadIdx.x;
-  const uint32_t pnl = blockIdx.y;  // record bytes 16 * pnl .. 16 * pnl + 15
-  if (g >= G) return;
-  uint4 rec[16];
-#pragma unroll
-  for (int i = 0; i < 16; ++i) {
-    const uint64_t th = (uint64_t)g * 16 + i;
-    rec[i] = (th < r && pnl * 16u < dp)
-                 ? __ldg(reinterpret_cast<const uint4*>(R + th * dp + (size_t)pnl * 16))
-                 : make_uint4(0, 0, 0, 0);
-  }
-  uint4* dst = reinterpret_cast<uint4*>(Dbits + ((size_t)pnl * G + g) * 2048);
-#pragma unroll 1
-  for (uint32_t jj = 0; jj < 16; ++jj) {
-    const uint32_t wsel = jj >> 2, bsel = jj & 3;
-    uint32_t X[4];  // byte jj of records 4t .. 4t+3
-#pragma unroll
-    for (int t = 0; t < 4; ++t)
-      X[t] = gather_byte(u4_word(rec[4 * t + 0], wsel), u4_word(rec[4 * t + 1], wsel),
-                         u4_word(rec[4 * t + 2], wsel), u4_word(rec[4 * t + 3], wsel), bsel);
-#pragma unroll
-    for (uint32_t k = 0; k < 8; ++k)
-      dst[jj * 8 + k] = make_uint4((X[0] >> k) & 0x01010101u, (X[1] >> k) & 0x01010101u,
-                                   (X[2] >> k) & 0x01010101u, (X[3] >> k) & 0x01010101u);
-  }
-}
-
-// Shares as the B operand: byte (share q, record theta) = bit theta of share q
-// (0/1), BN-column panels like the LWE limbs.  One thread per (q, 16-record group).
+// Shares as a tensor-core operand (ens_mma.cuh): byte (share q, record theta) =
+// bit theta of share q (0/1), in BN-row panels [Npad/BN][G16][BN][16] (K-major,
+// 16 records per 16-byte row).  One thread per (q, 16-record group).
 __global__ void ens_share_expand_kernel(const uint8_t* __restrict__ Q, uint32_t B, uint64_t r,
                                         uint64_t nb, uint8_t* __restrict__ Qb, uint32_t G,
                                         uint32_t Npad, uint32_t BN) {

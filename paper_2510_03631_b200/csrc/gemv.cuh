@@ -108,16 +108,20 @@ struct GemvArgs {
   uint32_t chunk;       // groups staged in smem at a time (multiple of UNR)
   uint32_t split_major; // 1: blockIdx.x = split, blockIdx.y = row block (page-local order)
   uint32_t pf256;       // 1: L2::256B prefetch hint on the D loads
+  uint32_t l2pf;        // 1: bulk L2 prefetch of the CTA's D slice before griddepcontrol.wait
 };
 
 // U rows per thread (rows r, r + 128, ...); UNR column groups per iteration.
 template <int U, int UNR>
-__global__ void __launch_bounds__(GEMV_THREADS) gemv_u8_u32_kernel(GemvArgs a) {
+__global__ void __launch_bounds__(GEMV_THREADS) qpir_gemv_u8_u32_kernel(GemvArgs a) {
   extern __shared__ uint4 sL[];
-  // Programmatic dependent launch: let the next query's GEMV start streaming D
-  // while this grid drains.  Only reads (D, qu) happen before griddepcontrol.wait;
-  // every global write (partials, tickets, ans) comes after it, so back-to-back
-  // answers never race on the shared scratch or output buffers.
+  // Programmatic dependent launch: let the next query's GEMV start while this
+  // grid drains.  Before griddepcontrol.wait this CTA touches ONLY the D shard
+  // (library-owned; a device-side db_write launches the next GEMV without PDL,
+  // qpir.cu): its first UNR column groups go to registers and, with l2pf, its
+  // whole D slice is prefetched into L2 by the TMA engine.  qu (which the
+  // previous kernel on the stream may have written) is staged after the wait,
+  // and every global write (partials, tickets, ans) comes after it too.
   asm volatile("griddepcontrol.launch_dependents;");
   const uint32_t tid = threadIdx.x;
   // Grid order: with split_major the CTAs that run at the same time walk
@@ -142,6 +146,27 @@ __global__ void __launch_bounds__(GEMV_THREADS) gemv_u8_u32_kernel(GemvArgs a) {
     Drow[u] = a.D + (size_t)(r >> 7) * a.G * 2048 + (r & 127u) * 16;
   }
   constexpr size_t gstride = 2048;
+  auto load = [&](uint32_t g, uint4 (&d)[UNR][U]) {
+#pragma unroll
+    for (int i = 0; i < UNR; ++i)
+#pragma unroll
+      for (int u = 0; u < U; ++u)
+        d[i][u] = !live[u] ? make_uint4(0, 0, 0, 0)
+                  : a.pf256 ? ldg_stream_v4_pf256(Drow[u] + (size_t)(g + i) * gstride)
+                            : ldg_stream_v4(Drow[u] + (size_t)(g + i) * gstride);
+  };
+
+  // ---- before the wait: D only
+  if (a.l2pf && tid < U) {
+    // one bulk L2 prefetch per 128-row panel of this CTA: groups [gb, ge)
+    const uint32_t r = rblk * (GEMV_THREADS * U) + tid * GEMV_THREADS;
+    if (r < a.ell_local)
+      l2_prefetch_bulk(a.D + (size_t)(r >> 7) * a.G * 2048 + (size_t)gb * gstride,
+                       (ge - gb) * (uint32_t)gstride);
+  }
+  uint4 d[UNR][U];
+  load(gb, d);
+  asm volatile("griddepcontrol.wait;" ::: "memory");  // previous grid complete + visible
 
   for (uint32_t cb = gb; cb < ge; cb += a.chunk) {
     const uint32_t ce = min(ge, cb + a.chunk);
@@ -150,14 +175,7 @@ __global__ void __launch_bounds__(GEMV_THREADS) gemv_u8_u32_kernel(GemvArgs a) {
     __syncthreads();
 #pragma unroll 1
     for (uint32_t g = cb; g < ce; g += UNR) {
-      uint4 d[UNR][U];
-#pragma unroll
-      for (int i = 0; i < UNR; ++i)
-#pragma unroll
-        for (int u = 0; u < U; ++u)
-          d[i][u] = !live[u] ? make_uint4(0, 0, 0, 0)
-                    : a.pf256 ? ldg_stream_v4_pf256(Drow[u] + (size_t)(g + i) * gstride)
-                              : ldg_stream_v4(Drow[u] + (size_t)(g + i) * gstride);
+      if (g != gb) load(g, d);
 #pragma unroll
       for (int i = 0; i < UNR; ++i) {
         const uint4* l = sL + (size_t)(g + i - cb) * 4;
@@ -172,7 +190,6 @@ __global__ void __launch_bounds__(GEMV_THREADS) gemv_u8_u32_kernel(GemvArgs a) {
 #pragma unroll
   for (int u = 0; u < U; ++u)
     out[u] = acc[u][0] + (acc[u][1] << 8) + (acc[u][2] << 16) + (acc[u][3] << 24);
-  asm volatile("griddepcontrol.wait;" ::: "memory");  // previous grid complete + visible
 
   if (nsplit == 1) {
 #pragma unroll

@@ -7,6 +7,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <atomic>
 #include <cstdarg>
 #include <map>
 #include <mutex>
@@ -18,7 +19,6 @@
 #include "../../include/qpir.h"
 #include "aux_kernels.cuh"
 #include "gemv.cuh"
-#include "gemv_tma.cuh"
 #include "host_common.h"
 #include "mma_launch.cuh"
 
@@ -92,8 +92,9 @@ struct qpir_ctx {
   int gemv_unroll = 4;  // env QPIR_GEMV_UNROLL: column groups in flight (4 or 8)
   int gemv_order = 0;  // env QPIR_GEMV_ORDER (1 = split-major grid)
   int gemv_pdl = 1;    // env QPIR_GEMV_PDL (programmatic dependent launch of back-to-back GEMVs)
-  int gemv_impl = 0;   // env QPIR_GEMV_IMPL: 0 = SIMT split-K kernel, 1 = persistent TMA-fed
   int gemv_pf256 = 0;  // env QPIR_GEMV_PF256: L2 256-byte prefetch hint on D loads
+  int gemv_l2pf = 0;   // env QPIR_GEMV_L2PF: bulk L2 prefetch of a CTA's D slice before the PDL wait
+  std::atomic<bool> d_written{false};  // a device db_write is queued: next GEMV without PDL
   int mma_mt = 2;      // env QPIR_MMA_MT (1 or 2 row panels per CTA tile)
   int mma_split = 0;   // env QPIR_MMA_SPLIT (0 = auto)
   int mma_gpb = 8;     // env QPIR_MMA_GPB (column groups per pipeline stage: 4 or 8)
@@ -269,6 +270,7 @@ int db_write_device(qpir_ctx* ctx, uint64_t theta0, uint64_t n_rec, const uint8_
     pack_records_kernel<<<grid, 128, 0, st>>>(b);
     LAUNCH_CHECK(ctx);
   }
+  ctx->d_written.store(true);
   return QPIR_OK;
 }
 
@@ -325,8 +327,9 @@ int launch_gemv(qpir_ctx* ctx, const uint32_t* qu, uint32_t* ans, cudaStream_t s
   a.chunk = chunk;
   a.split_major = (ctx->gemv_order == 1 && rb <= 65535) ? 1u : 0u;
   a.pf256 = ctx->gemv_pf256 ? 1u : 0u;
+  a.l2pf = ctx->gemv_l2pf ? 1u : 0u;
   const size_t smem = (size_t)chunk * 64;
-  auto kern = gemv_u8_u32_kernel<U, UNR>;
+  auto kern = qpir_gemv_u8_u32_kernel<U, UNR>;
   if (smem > 48 * 1024)
     CUDA_TRY(ctx, cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   const dim3 grid = a.split_major ? dim3(S, rb) : dim3(rb, S);
@@ -337,7 +340,10 @@ int launch_gemv(qpir_ctx* ctx, const uint32_t* qu, uint32_t* ans, cudaStream_t s
   cfg.stream = st;
   cudaLaunchAttribute attr[1];
   attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-  attr[0].val.programmaticStreamSerializationAllowed = ctx->gemv_pdl ? 1 : 0;
+  // The GEMV reads D before griddepcontrol.wait: right after a device-side
+  // db_write (pack_records_kernel writes D) it is launched without PDL.
+  const bool after_write = ctx->d_written.exchange(false);
+  attr[0].val.programmaticStreamSerializationAllowed = (ctx->gemv_pdl && !after_write) ? 1 : 0;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
   CUDA_TRY(ctx, cudaLaunchKernelEx(&cfg, kern, a));
@@ -345,29 +351,7 @@ int launch_gemv(qpir_ctx* ctx, const uint32_t* qu, uint32_t* ans, cudaStream_t s
   return QPIR_OK;
 }
 
-// Persistent TMA-fed GEMV (gemv_tma.cuh): stream-K over (panel pair, K-block).
-int launch_gemv_tma(qpir_ctx* ctx, const uint32_t* qu, uint32_t* ans, cudaStream_t st) {
-  const Geometry& g = ctx->geo;
-  GemvTmaArgs a;
-  a.D = ctx->D;
-  a.qu = qu;
-  a.ans = ans;
-  a.ell_local = (uint32_t)g.ell_local;
-  a.m = (uint32_t)g.m;
-  a.G = (uint32_t)g.G;
-  a.pairs = (uint32_t)((g.ell_local + 255) / 256);
-  a.iters = (uint64_t)a.pairs * (g.G / GT_GROUPS);
-  CUDA_TRY(ctx, cudaMemsetAsync(ans, 0, g.ell_local * 4, st));
-  const uint32_t grid = (uint32_t)std::min<uint64_t>(a.iters, (uint64_t)ctx->num_sms);
-  CUDA_TRY(ctx, cudaFuncSetAttribute(gemv_tma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                     (int)GT_SMEM));
-  gemv_tma_kernel<<<grid, GT_THREADS, GT_SMEM, st>>>(a);
-  LAUNCH_CHECK(ctx);
-  return QPIR_OK;
-}
-
 int gemv(qpir_ctx* ctx, const uint32_t* qu, uint32_t* ans, cudaStream_t st) {
-  if (ctx->gemv_impl == 1) return launch_gemv_tma(ctx, qu, ans, st);
   const bool u8 = ctx->gemv_unroll == 8;
   switch (ctx->gemv_u) {
     case 1: return u8 ? launch_gemv<1, 8>(ctx, qu, ans, st) : launch_gemv<1, 4>(ctx, qu, ans, st);
@@ -463,8 +447,8 @@ int qpir_setup(const qpir_params* params, const uint8_t* records, uint64_t recor
   ctx->gemv_unroll = env_int("QPIR_GEMV_UNROLL", 4);
   ctx->gemv_order = env_int("QPIR_GEMV_ORDER", 0);
   ctx->gemv_pdl = env_int("QPIR_GEMV_PDL", 1);
-  ctx->gemv_impl = env_int("QPIR_GEMV_IMPL", 0);
   ctx->gemv_pf256 = env_int("QPIR_GEMV_PF256", 0);
+  ctx->gemv_l2pf = env_int("QPIR_GEMV_L2PF", 0);
   ctx->mma_mt = env_int("QPIR_MMA_MT", 2);
   ctx->mma_split = env_int("QPIR_MMA_SPLIT", 0);
   ctx->mma_gpb = env_int("QPIR_MMA_GPB", 8);

@@ -1,12 +1,17 @@
 // qpir_ens.cu -- C ABI for QPADL-ENS (Chor XOR PIR; NEXT-1), include/qpir.h.
-// Host side only: validation, device memory, dispatch to ens.cuh kernels.
+// Host side only: validation, per-stream device scratch, dispatch to the
+// ens.cuh scan / CUDA-core batch kernels and the ens_mma.cuh tensor-core batch.
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <atomic>
+#include <map>
+#include <mutex>
 #include <string>
 
 #include "../../include/qpir.h"
 #include "ens.cuh"
+#include "ens_mma.cuh"
 #include "host_common.h"
 #include "mma_launch.cuh"
 
@@ -18,7 +23,7 @@ thread_local std::string g_ens_setup_error;
 }
 
 // Host-input staging ring for single answers (share, OOP q and A_i): the H2D
-// copy runs on the context's copy stream, the compute stream waits only on its
+// copy runs on the arena's copy stream, the compute stream waits only on its
 // event, so the next answer's input lands while the previous scan runs.
 struct EnsRing {
   uint8_t* buf[2] = {nullptr, nullptr};
@@ -28,21 +33,21 @@ struct EnsRing {
   unsigned slot = 0;
 };
 
-struct qpir_ens_ctx {
-  uint64_t r = 0, d = 0, dp = 0;
+// Per-stream scratch: calls on different streams of one context may run
+// concurrently (each stream owns its staging rings, accumulators, scan
+// partials / tickets and tensor-core operands); calls on one stream are
+// ordered by the stream.
+struct EnsArena {
   cudaStream_t h2d = nullptr;   // copy stream for host inputs (lazily created)
   EnsRing r_share, r_q, r_A, r_batch;
-  int h2d_stream = 1;           // env QPIR_H2D_STREAM
-  int device = 0, num_sms = 148;
-  uint8_t* R = nullptr;       // [r][dp]
-  uint32_t* acc = nullptr;    // [max_B][dp/4] XOR accumulators
+  uint32_t* acc = nullptr;      // [max_B][dp/4] response words of a batch
   uint64_t acc_B = 0;
-  uint32_t* acc1 = nullptr;   // [dp/4] + 1 done ticket: single-scan accumulator, kept zero
-  uint8_t* io_stage = nullptr;  // [2][d]: host A_i in / host answer out of a single scan
+  uint32_t* acc1 = nullptr;     // [dp/4] + 1 done ticket: single-scan accumulator, kept zero
+  uint8_t* io_stage = nullptr;  // [2][d]: host answer out of a single scan
   uint64_t io_stage_bytes = 0;
-  uint8_t* Q_dev = nullptr;   // OOP offline: the expanded selectors of a seed batch
+  uint8_t* Q_dev = nullptr;     // OOP offline: the expanded selectors of a seed batch
   uint64_t Q_bytes = 0;
-  uint32_t* Qt = nullptr;     // transposed selector bits
+  uint32_t* Qt = nullptr;       // transposed selector bits (CUDA-core batch)
   uint64_t Qt_bytes = 0;
   uint8_t* seed_dev = nullptr;  // OOP seeds
   uint64_t seed_bytes = 0;
@@ -50,19 +55,25 @@ struct qpir_ens_ctx {
   uint64_t partial_bytes = 0;
   uint32_t* tickets = nullptr;  // scan group tickets (self-resetting)
   uint64_t tickets_bytes = 0;
+  uint8_t* Qb = nullptr;        // shares as 0/1 bytes (tensor-core A operand)
+  uint64_t Qb_bytes = 0;
+};
+
+struct qpir_ens_ctx {
+  uint64_t r = 0, d = 0, dp = 0;
+  int h2d_stream = 1;           // env QPIR_H2D_STREAM
+  int device = 0, num_sms = 148;
+  uint8_t* R = nullptr;         // [r][dp]
+  std::mutex mu;                // guards `arenas`
+  std::map<cudaStream_t, EnsArena> arenas;
   int group = 0;                // env QPIR_ENS_GROUP (0 = auto 32; 1 = atomics only)
   int wide = 1;                 // env QPIR_ENS_WIDE (uniform-row kernel for d > 2 KB;
                                 //   2 = 32-byte chunks per thread, 256-bit loads)
   int pdl = 1;                  // env QPIR_ENS_PDL (programmatic dependent launch of scans)
-  // tensor-core multi-request path (bit-planes, 8x the record bytes)
-  uint8_t* bitD = nullptr;
-  uint64_t bitD_bytes = 0;
-  bool bitD_valid = false;
-  uint8_t* Qb = nullptr;        // shares as 0/1 bytes (B operand)
-  uint64_t Qb_bytes = 0;
   int tc = -1;                  // env QPIR_ENS_TC: -1 auto, 0 CUDA cores, 1 tensor cores
-  int mma_split = 0;
-  uint64_t launches = 0;
+  int mma_split = 0;            // env QPIR_MMA_SPLIT (0 = auto)
+  std::atomic<uint64_t> launches{0};
+  std::atomic<int> last_path{QPIR_ENS_PATH_NONE};
   int rows_per_cta = 0;       // env QPIR_ENS_ROWS (0 = auto)
   int ur = 16;                // env QPIR_ENS_UR (rows in flight per thread: 4, 8, 16)
   std::string err;
@@ -96,12 +107,28 @@ int grow(qpir_ens_ctx* ctx, void** buf, uint64_t* have, uint64_t need) {
   return QPIR_OK;
 }
 
+// The arena of stream `st`, created on first use; its single-scan accumulator
+// (acc1, self-resetting in the kernel) is zeroed on `st` once.
+int arena_for(qpir_ens_ctx* ctx, cudaStream_t st, EnsArena** out) {
+  EnsArena* ar;
+  {
+    std::lock_guard<std::mutex> lk(ctx->mu);
+    ar = &ctx->arenas[st];  // std::map references stay valid across inserts
+  }
+  if (!ar->acc1) {
+    ENS_CUDA(ctx, cudaMalloc(&ar->acc1, ctx->dp + 16));
+    ENS_CUDA(ctx, cudaMemsetAsync(ar->acc1, 0, ctx->dp + 16, st));
+  }
+  *out = ar;
+  return QPIR_OK;
+}
+
 // Stage a possibly-host input through `ring` for work on `st`: device inputs
-// pass through (slot -1); host inputs are copied on the copy stream (or on `st`
-// while it is being captured into a CUDA graph).  The caller records
+// pass through (slot -1); host inputs are copied on the arena's copy stream (or
+// on `st` while it is being captured into a CUDA graph).  The caller records
 // ring.done[slot] on `st` after the kernels that read the slot.
-int stage_ring(qpir_ens_ctx* ctx, EnsRing& ring, const uint8_t* src, uint64_t bytes,
-               cudaStream_t st, const uint8_t** dev, int* slot) {
+int stage_ring(qpir_ens_ctx* ctx, EnsArena& ar, EnsRing& ring, const uint8_t* src,
+               uint64_t bytes, cudaStream_t st, const uint8_t** dev, int* slot) {
   *slot = -1;
   const int w = where(src, ctx->device);
   if (w < 0) return ENS_FAIL(ctx, QPIR_E_PARAM, "input: memory of another device");
@@ -115,7 +142,7 @@ int stage_ring(qpir_ens_ctx* ctx, EnsRing& ring, const uint8_t* src, uint64_t by
   const unsigned k = side ? ring.slot : 0u;
   if (side) {
     ring.slot ^= 1u;
-    if (!ctx->h2d) ENS_CUDA(ctx, cudaStreamCreateWithFlags(&ctx->h2d, cudaStreamNonBlocking));
+    if (!ar.h2d) ENS_CUDA(ctx, cudaStreamCreateWithFlags(&ar.h2d, cudaStreamNonBlocking));
     if (!ring.ready[k]) {
       ENS_CUDA(ctx, cudaEventCreateWithFlags(&ring.ready[k], cudaEventDisableTiming));
       ENS_CUDA(ctx, cudaEventCreateWithFlags(&ring.done[k], cudaEventDisableTiming));
@@ -127,9 +154,9 @@ int stage_ring(qpir_ens_ctx* ctx, EnsRing& ring, const uint8_t* src, uint64_t by
     if (rc) return rc;
   }
   if (side) {
-    ENS_CUDA(ctx, cudaStreamWaitEvent(ctx->h2d, ring.done[k], 0));
-    ENS_CUDA(ctx, cudaMemcpyAsync(ring.buf[k], src, bytes, cudaMemcpyHostToDevice, ctx->h2d));
-    ENS_CUDA(ctx, cudaEventRecord(ring.ready[k], ctx->h2d));
+    ENS_CUDA(ctx, cudaStreamWaitEvent(ar.h2d, ring.done[k], 0));
+    ENS_CUDA(ctx, cudaMemcpyAsync(ring.buf[k], src, bytes, cudaMemcpyHostToDevice, ar.h2d));
+    ENS_CUDA(ctx, cudaEventRecord(ring.ready[k], ar.h2d));
     ENS_CUDA(ctx, cudaStreamWaitEvent(st, ring.ready[k], 0));
     *slot = (int)k;
   } else {
@@ -140,10 +167,10 @@ int stage_ring(qpir_ens_ctx* ctx, EnsRing& ring, const uint8_t* src, uint64_t by
 }
 
 // Copy B rows of d bytes out of the dp-strided accumulator into `out`.
-int copy_out(qpir_ens_ctx* ctx, uint8_t* out, uint64_t B, cudaStream_t st) {
+int copy_out(qpir_ens_ctx* ctx, EnsArena& ar, uint8_t* out, uint64_t B, cudaStream_t st) {
   const int w = where(out, ctx->device);
   if (w < 0) return ENS_FAIL(ctx, QPIR_E_PARAM, "out: memory of another device");
-  ENS_CUDA(ctx, cudaMemcpy2DAsync(out, ctx->d, ctx->acc, ctx->dp, ctx->d, B,
+  ENS_CUDA(ctx, cudaMemcpy2DAsync(out, ctx->d, ar.acc, ctx->dp, ctx->d, B,
                                   w ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost, st));
   if (!w) ENS_CUDA(ctx, cudaStreamSynchronize(st));
   return QPIR_OK;
@@ -189,17 +216,14 @@ int qpir_ens_setup(const qpir_ens_params* p, const uint8_t* records, uint64_t re
   ctx->tc = env_int("QPIR_ENS_TC", -1);
   ctx->mma_split = env_int("QPIR_MMA_SPLIT", 0);
   cudaStream_t st = (cudaStream_t)stream;
-  if (cudaMalloc(&ctx->R, ctx->r * ctx->dp) != cudaSuccess ||
-      cudaMalloc(&ctx->acc1, ctx->dp + 16) != cudaSuccess) {
+  if (cudaMalloc(&ctx->R, ctx->r * ctx->dp) != cudaSuccess) {
     cudaGetLastError();
     g_ens_setup_error = "records: cudaMalloc failed";
     qpir_ens_destroy(ctx);
     return QPIR_E_OOM;
   }
   int rc = QPIR_OK;
-  if (cudaMemsetAsync(ctx->R, 0, ctx->r * ctx->dp, st) != cudaSuccess ||
-      cudaMemsetAsync(ctx->acc1, 0, ctx->dp + 16, st) != cudaSuccess)
-    rc = QPIR_E_CUDA;
+  if (cudaMemsetAsync(ctx->R, 0, ctx->r * ctx->dp, st) != cudaSuccess) rc = QPIR_E_CUDA;
   if (!rc && records) rc = qpir_ens_db_write(ctx, 0, ctx->r, records, records_len, stream);
   if (!rc && cudaStreamSynchronize(st) != cudaSuccess) rc = QPIR_E_CUDA;
   if (rc) {
@@ -223,11 +247,13 @@ int qpir_ens_db_write(qpir_ens_ctx* ctx, uint64_t theta_begin, uint64_t n_record
     return ENS_FAIL(ctx, QPIR_E_DIMENSION, "records_len: %llu != %llu",
                     (unsigned long long)records_len, (unsigned long long)(n_records * ctx->d));
   if (n_records == 0) return QPIR_OK;
+  if (!records) return ENS_FAIL(ctx, QPIR_E_PARAM, "records: NULL");
   DeviceGuard dg(ctx->device);
   const int w = where(records, ctx->device);
   if (w < 0) return ENS_FAIL(ctx, QPIR_E_PARAM, "records: memory of another device");
-  ctx->bitD_valid = false;  // the tensor-core bit-planes are rebuilt on next use
   cudaStream_t st = (cudaStream_t)stream;
+  // a copy (not a kernel): stream-ordered before any later scan, which reads R
+  // only after griddepcontrol.wait
   ENS_CUDA(ctx, cudaMemcpy2DAsync(ctx->R + theta_begin * ctx->dp, ctx->dp, records, ctx->d,
                                   ctx->d, n_records,
                                   w ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, st));
@@ -237,17 +263,17 @@ int qpir_ens_db_write(qpir_ens_ctx* ctx, uint64_t theta_begin, uint64_t n_record
 
 // One scan of rows [row_lo, row_hi) selected by share_dev, finalised in the
 // kernel: out_dev (device, d bytes) = init_dev ^ XOR of the selected rows.
-static int scan_range(qpir_ens_ctx* ctx, const uint8_t* share_dev, uint64_t row_lo,
-                      uint64_t row_hi, const uint8_t* init_dev, uint8_t* out_dev,
-                      cudaStream_t st) {
+static int scan_range(qpir_ens_ctx* ctx, EnsArena& ar, const uint8_t* share_dev,
+                      uint64_t row_lo, uint64_t row_hi, const uint8_t* init_dev,
+                      uint8_t* out_dev, cudaStream_t st) {
   EnsArgs a;
   a.R = ctx->R;
   a.q = share_dev;
-  a.out = ctx->acc1;
+  a.out = ar.acc1;
   a.fin_out = out_dev;
   a.init = init_dev;
   a.d = (uint32_t)ctx->d;
-  a.done = ctx->acc1 + ctx->dp / 4;
+  a.done = ar.acc1 + ctx->dp / 4;
   a.row_lo = row_lo;
   a.row_hi = row_hi;
   a.dp = (uint32_t)ctx->dp;
@@ -276,15 +302,15 @@ static int scan_range(qpir_ens_ctx* ctx, const uint8_t* share_dev, uint64_t row_
   if (grid > 4ull * ctx->num_sms && group > 1) {
     // many small CTAs: two-level XOR reduction instead of grid x W atomics
     const uint64_t ngroups = (grid + group - 1) / group;
-    int rc = grow(ctx, (void**)&ctx->partial, &ctx->partial_bytes, grid * a.W * 16);
+    int rc = grow(ctx, (void**)&ar.partial, &ar.partial_bytes, grid * a.W * 16);
     if (rc) return rc;
-    if (ngroups * 4 > ctx->tickets_bytes) {
-      rc = grow(ctx, (void**)&ctx->tickets, &ctx->tickets_bytes, ngroups * 4);
+    if (ngroups * 4 > ar.tickets_bytes) {
+      rc = grow(ctx, (void**)&ar.tickets, &ar.tickets_bytes, ngroups * 4);
       if (rc) return rc;
-      ENS_CUDA(ctx, cudaMemsetAsync(ctx->tickets, 0, ctx->tickets_bytes, st));
+      ENS_CUDA(ctx, cudaMemsetAsync(ar.tickets, 0, ar.tickets_bytes, st));
     }
-    a.partial = reinterpret_cast<uint4*>(ctx->partial);
-    a.tickets = ctx->tickets;
+    a.partial = reinterpret_cast<uint4*>(ar.partial);
+    a.tickets = ar.tickets;
     a.group = group;
   }
   a.leaders = (uint32_t)(a.partial ? (grid + a.group - 1) / a.group : grid);
@@ -312,6 +338,7 @@ static int scan_range(qpir_ens_ctx* ctx, const uint8_t* share_dev, uint64_t row_
   cfg.numAttrs = 1;
   ENS_CUDA(ctx, cudaLaunchKernelEx(&cfg, kern, a));
   ENS_LAUNCHED(ctx);
+  ctx->last_path = QPIR_ENS_PATH_SCAN;
   return QPIR_OK;
 }
 
@@ -331,16 +358,19 @@ int qpir_ens_answer(qpir_ens_ctx* ctx, const uint8_t* share, uint64_t len_share,
   cudaStream_t st = (cudaStream_t)stream;
   const int wo = where(out, ctx->device);
   if (wo < 0) return ENS_FAIL(ctx, QPIR_E_PARAM, "out: memory of another device");
-  int rc = grow(ctx, (void**)&ctx->io_stage, &ctx->io_stage_bytes, 2 * ctx->d);
+  EnsArena* ar = nullptr;
+  int rc = arena_for(ctx, st, &ar);
+  if (rc) return rc;
+  rc = grow(ctx, (void**)&ar->io_stage, &ar->io_stage_bytes, 2 * ctx->d);
   if (rc) return rc;
   const uint8_t* qd = nullptr;
   int slot = -1;
-  rc = stage_ring(ctx, ctx->r_share, share, nb, st, &qd, &slot);
+  rc = stage_ring(ctx, *ar, ar->r_share, share, nb, st, &qd, &slot);
   if (rc) return rc;
-  uint8_t* od = wo ? out : ctx->io_stage + ctx->d;
-  rc = scan_range(ctx, qd, 0, ctx->r, nullptr, od, st);
+  uint8_t* od = wo ? out : ar->io_stage + ctx->d;
+  rc = scan_range(ctx, *ar, qd, 0, ctx->r, nullptr, od, st);
   if (rc) return rc;
-  if (slot >= 0) ENS_CUDA(ctx, cudaEventRecord(ctx->r_share.done[slot], st));
+  if (slot >= 0) ENS_CUDA(ctx, cudaEventRecord(ar->r_share.done[slot], st));
   if (!wo) {
     ENS_CUDA(ctx, cudaMemcpyAsync(out, od, ctx->d, cudaMemcpyDeviceToHost, st));
     ENS_CUDA(ctx, cudaStreamSynchronize(st));
@@ -369,21 +399,24 @@ int qpir_oop_answer(qpir_ens_ctx* ctx, uint32_t n_chunks, uint32_t server, const
   cudaStream_t st = (cudaStream_t)stream;
   const int wo = where(out, ctx->device);
   if (wo < 0) return ENS_FAIL(ctx, QPIR_E_PARAM, "out: memory of another device");
-  int rc = grow(ctx, (void**)&ctx->io_stage, &ctx->io_stage_bytes, 2 * ctx->d);
+  EnsArena* ar = nullptr;
+  int rc = arena_for(ctx, st, &ar);
+  if (rc) return rc;
+  rc = grow(ctx, (void**)&ar->io_stage, &ar->io_stage_bytes, 2 * ctx->d);
   if (rc) return rc;
   const uint8_t* qd = nullptr;
   int sq = -1, sA = -1;
-  rc = stage_ring(ctx, ctx->r_q, q, kb, st, &qd, &sq);
+  rc = stage_ring(ctx, *ar, ar->r_q, q, kb, st, &qd, &sq);
   if (rc) return rc;
   // R_i := A_i XOR q_i . chunk_i (Lemma 2): A_i is XORed in by the finalising CTA
   const uint8_t* Ad = nullptr;
-  rc = stage_ring(ctx, ctx->r_A, A, ctx->d, st, &Ad, &sA);
+  rc = stage_ring(ctx, *ar, ar->r_A, A, ctx->d, st, &Ad, &sA);
   if (rc) return rc;
-  uint8_t* od = wo ? out : ctx->io_stage + ctx->d;
-  rc = scan_range(ctx, qd, (uint64_t)server * k, (uint64_t)(server + 1) * k, Ad, od, st);
+  uint8_t* od = wo ? out : ar->io_stage + ctx->d;
+  rc = scan_range(ctx, *ar, qd, (uint64_t)server * k, (uint64_t)(server + 1) * k, Ad, od, st);
   if (rc) return rc;
-  if (sq >= 0) ENS_CUDA(ctx, cudaEventRecord(ctx->r_q.done[sq], st));
-  if (sA >= 0) ENS_CUDA(ctx, cudaEventRecord(ctx->r_A.done[sA], st));
+  if (sq >= 0) ENS_CUDA(ctx, cudaEventRecord(ar->r_q.done[sq], st));
+  if (sA >= 0) ENS_CUDA(ctx, cudaEventRecord(ar->r_A.done[sA], st));
   if (!wo) {
     ENS_CUDA(ctx, cudaMemcpyAsync(out, od, ctx->d, cudaMemcpyDeviceToHost, st));
     ENS_CUDA(ctx, cudaStreamSynchronize(st));
@@ -408,83 +441,92 @@ int qpir_oop_preprocess(qpir_ens_ctx* ctx, uint32_t n_chunks, uint32_t server,
                     (unsigned long long)(n_seeds * ctx->d));
   DeviceGuard dg(ctx->device);
   cudaStream_t st = (cudaStream_t)stream;
-  const uint64_t nb = (ctx->r + 7) / 8;
-  int rc = grow(ctx, (void**)&ctx->Q_dev, &ctx->Q_bytes, n_seeds * nb);
+  EnsArena* ar = nullptr;
+  int rc = arena_for(ctx, st, &ar);
   if (rc) return rc;
-  rc = grow(ctx, (void**)&ctx->seed_dev, &ctx->seed_bytes, n_seeds * 8);
+  const uint64_t nb = (ctx->r + 7) / 8;
+  rc = grow(ctx, (void**)&ar->Q_dev, &ar->Q_bytes, n_seeds * nb);
+  if (rc) return rc;
+  rc = grow(ctx, (void**)&ar->seed_dev, &ar->seed_bytes, n_seeds * 8);
   if (rc) return rc;
   const int ws = where(seeds, ctx->device);
   if (ws < 0) return ENS_FAIL(ctx, QPIR_E_PARAM, "seeds: memory of another device");
-  ENS_CUDA(ctx, cudaMemcpyAsync(ctx->seed_dev, seeds, n_seeds * 8,
+  ENS_CUDA(ctx, cudaMemcpyAsync(ar->seed_dev, seeds, n_seeds * 8,
                                 ws ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, st));
   {
     dim3 grid((uint32_t)((nb + 255) / 256), (uint32_t)n_seeds);
-    oop_expand_kernel<<<grid, 256, 0, st>>>((const unsigned long long*)ctx->seed_dev, ctx->Q_dev,
+    oop_expand_kernel<<<grid, 256, 0, st>>>((const unsigned long long*)ar->seed_dev, ar->Q_dev,
                                             ctx->r, ctx->r / n_chunks, n_chunks, server, nb);
     ENS_LAUNCHED(ctx);
   }
   // A = q . DB for every seed: the ENS multi-request kernel on the expanded shares
-  return qpir_ens_answer_batch(ctx, ctx->Q_dev, n_seeds, n_seeds * nb, A_out, len_A, stream);
+  return qpir_ens_answer_batch(ctx, ar->Q_dev, n_seeds, n_seeds * nb, A_out, len_A, stream);
 }
 
-// Multi-request GF(2) product on tensor cores (DESIGN 6): the records'
-// bit-planes (8 x r x d bytes of 0/1, built once per DB version) times the
-// shares as 0/1 bytes, s32 counts, parity packed by the OUT_PARITY epilogue.
-static int ens_batch_tc(qpir_ens_ctx* ctx, const uint8_t* Qd, uint64_t B, cudaStream_t st,
-                        bool* used) {
-  *used = false;
-  const uint64_t Lbits = round_up(8 * ctx->dp, 256);
+}  // extern "C"
+
+// Multi-request GF(2) product on tensor cores (ens_mma.cuh): the records are
+// read once, in place, and expanded to weighted bit-rows in shared memory;
+// the shares are 0/1 bytes (B x r bytes, expanded once per call).
+template <uint32_t MS, uint32_t NT, uint32_t S, uint32_t RS>
+static cudaError_t ens_mma_launch(qpir_ens_ctx* ctx, EnsMmaArgs a, cudaStream_t st) {
+  using C = EmCfg<MS, NT, S, RS>;
+  auto kern = qpir_ens_mma_kernel<MS, NT, S, RS>;
+  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::TOTAL);
+  if (e != cudaSuccess) return e;
+  const uint32_t units = a.s_tiles * a.w_tiles * a.splits;
+  kern<<<std::min<uint32_t>(units, (uint32_t)ctx->num_sms), EM_THREADS, C::TOTAL, st>>>(a);
+  return cudaGetLastError();
+}
+
+static int ens_batch_tc(qpir_ens_ctx* ctx, EnsArena& ar, const uint8_t* Qd, uint64_t B,
+                        cudaStream_t st) {
+  // MS share tiles of 128 x NT width tiles of 256 bit-rows (32 record bytes)
+  // share the 512 TMEM columns: B <= 128 -> 1 x 2 (64 record bytes per unit),
+  // larger B -> 2 x 1 (the expanded record slice feeds 256 shares).
+  const uint32_t MS = B <= 128 ? 1 : 2, NT = B <= 128 ? 2 : 1;
   const uint64_t m_pad = round_up(ctx->r, 128);
-  const uint64_t G = m_pad / 16;
-  if (G > 0xFFFFFFFFull || Lbits > 0x7FFFFFFFull) return QPIR_OK;
-  if (!ctx->bitD) {
-    if (cudaMalloc(&ctx->bitD, Lbits * m_pad) != cudaSuccess) {
-      cudaGetLastError();
-      ctx->bitD = nullptr;
-      return QPIR_OK;  // not enough HBM for the bit-planes: CUDA-core path
-    }
-    ctx->bitD_bytes = Lbits * m_pad;
-    ctx->bitD_valid = false;
-  }
-  if (!ctx->bitD_valid) {
-    dim3 grid((uint32_t)((G + 127) / 128), (uint32_t)(Lbits / 128));
-    ens_bitplane_pack_kernel<<<grid, 128, 0, st>>>(ctx->R, ctx->r, (uint32_t)ctx->dp, ctx->bitD,
-                                                   (uint32_t)G);
-    ENS_LAUNCHED(ctx);
-    ctx->bitD_valid = true;
-  }
-  const uint32_t BN = mma_pick_bn(B);
-  const uint64_t Npad = round_up(B, BN);
-  int rc = grow(ctx, (void**)&ctx->Qb, &ctx->Qb_bytes, Npad * m_pad);
+  const uint32_t G16 = (uint32_t)(m_pad / 16);
+  const uint64_t Npad = round_up(B, 128ull * MS);
+  int rc = grow(ctx, (void**)&ar.Qb, &ar.Qb_bytes, Npad * m_pad);
   if (rc) return rc;
   {
-    const uint32_t gy = (uint32_t)std::min<uint64_t>(G, 65535);
-    const uint32_t gz = (uint32_t)((G + gy - 1) / gy);
-    const uint32_t tpb = (uint32_t)std::min<uint64_t>(Npad, 128);
-    dim3 grid((uint32_t)((Npad + tpb - 1) / tpb), gy, gz);
-    ens_share_expand_kernel<<<grid, tpb, 0, st>>>(Qd, (uint32_t)B, ctx->r, (ctx->r + 7) / 8,
-                                                  ctx->Qb, (uint32_t)G, (uint32_t)Npad, BN);
+    const uint32_t gy = std::min<uint32_t>(G16, 65535);
+    const uint32_t gz = (G16 + gy - 1) / gy;
+    dim3 grid((uint32_t)(Npad / 128), gy, gz);
+    ens_share_expand_kernel<<<grid, 128, 0, st>>>(Qd, (uint32_t)B, ctx->r, (ctx->r + 7) / 8, ar.Qb,
+                                                  G16, (uint32_t)Npad, 128);
     ENS_LAUNCHED(ctx);
   }
-  MmaJob j;
-  j.A = ctx->bitD;
-  j.L = (uint32_t)Lbits;
-  j.G = (uint32_t)G;
-  j.rows = (uint32_t)(8 * ctx->dp);
-  j.B = ctx->Qb;
-  j.Npad = (uint32_t)Npad;
-  j.BN = BN;
-  j.out = ctx->acc;
-  j.n_out = (uint32_t)B;
-  j.out_ld = (uint32_t)(ctx->dp / 4);
-  j.out_elems = B * (ctx->dp / 4);
-  j.num_sms = ctx->num_sms;
-  j.forced_split = ctx->mma_split;
-  const cudaError_t e = mma_launch<OUT_PARITY>(j, st, &ctx->launches);
+  EnsMmaArgs a;
+  a.R = ctx->R;
+  a.Qb = ar.Qb;
+  a.out = ar.acc;
+  a.r = ctx->r;
+  a.dp = (uint32_t)ctx->dp;
+  a.out_ld = (uint32_t)(ctx->dp / 4);
+  a.B = (uint32_t)B;
+  a.G16 = G16;
+  a.s_tiles = (uint32_t)(Npad / (128ull * MS));
+  a.w_tiles = (uint32_t)((ctx->dp + 32 * NT - 1) / (32 * NT));
+  a.kblocks = (uint32_t)((ctx->r + EM_KB - 1) / EM_KB);
+  const uint32_t tiles = a.s_tiles * a.w_tiles;
+  // wave_bytes: the record bytes all CTAs expand per K-block (cost model of
+  // mma_choose_splits: the split adds a memset and XOR atomics on the output)
+  a.splits = mma_choose_splits(tiles, a.kblocks, (uint32_t)ctx->num_sms, ctx->mma_split, 1,
+                               (double)B * ctx->dp, (double)EM_KB * 32 * NT * ctx->num_sms, false);
+  a.kbps = (a.kblocks + a.splits - 1) / a.splits;
+  a.splits = (a.kblocks + a.kbps - 1) / a.kbps;
+  if (a.splits > 1) ENS_CUDA(ctx, cudaMemsetAsync(ar.acc, 0, B * ctx->dp, st));
+  const cudaError_t e = MS == 1 ? ens_mma_launch<1, 2, 4, 8>(ctx, a, st)
+                                : ens_mma_launch<2, 1, 5, 12>(ctx, a, st);
   if (e != cudaSuccess) return ENS_FAIL(ctx, QPIR_E_CUDA, "tcgen05 GF(2) GEMM: %s", cudaGetErrorString(e));
-  *used = true;
+  ctx->launches++;
+  ctx->last_path = QPIR_ENS_PATH_TENSOR;
   return QPIR_OK;
 }
+
+extern "C" {
 
 int qpir_ens_answer_batch(qpir_ens_ctx* ctx, const uint8_t* shares, uint64_t B,
                           uint64_t len_shares, uint8_t* out, uint64_t len_out, void* stream) {
@@ -502,58 +544,62 @@ int qpir_ens_answer_batch(qpir_ens_ctx* ctx, const uint8_t* shares, uint64_t B,
                     (unsigned long long)(B * ctx->d));
   DeviceGuard dg(ctx->device);
   cudaStream_t st = (cudaStream_t)stream;
-  int rc = grow(ctx, (void**)&ctx->acc, &ctx->acc_B, B * ctx->dp);
+  EnsArena* ar = nullptr;
+  int rc = arena_for(ctx, st, &ar);
   if (rc) return rc;
-  const uint32_t QW = (uint32_t)((B + 31) / 32);
-  rc = grow(ctx, (void**)&ctx->Qt, &ctx->Qt_bytes, ctx->r * QW * 4);
+  rc = grow(ctx, (void**)&ar->acc, &ar->acc_B, B * ctx->dp);
   if (rc) return rc;
   const uint8_t* Qd = nullptr;
   int slot = -1;
-  rc = stage_ring(ctx, ctx->r_batch, shares, B * nb, st, &Qd, &slot);
+  rc = stage_ring(ctx, *ar, ar->r_batch, shares, B * nb, st, &Qd, &slot);
   if (rc) return rc;
-  // tensor cores for larger batches when the bit-planes fit in HBM
-  const bool want_tc = (ctx->tc == 1 || (ctx->tc < 0 && B >= 32)) && B <= 65280;  // grid.y
+  // tensor cores for larger batches (the shares operand, B x r bytes, must fit)
+  const bool want_tc = ctx->tc == 1 || (ctx->tc < 0 && B >= 32);
   if (want_tc) {
-    bool used = false;
-    rc = ens_batch_tc(ctx, Qd, B, st, &used);
+    rc = ens_batch_tc(ctx, *ar, Qd, B, st);
     if (rc) return rc;
-    if (used) {
-      if (slot >= 0) ENS_CUDA(ctx, cudaEventRecord(ctx->r_batch.done[slot], st));
-      return copy_out(ctx, out, B, st);
+  } else {
+    const uint32_t QW = (uint32_t)((B + 31) / 32);
+    rc = grow(ctx, (void**)&ar->Qt, &ar->Qt_bytes, ctx->r * QW * 4);
+    if (rc) return rc;
+    ENS_CUDA(ctx, cudaMemsetAsync(ar->acc, 0, B * ctx->dp, st));
+    {
+      dim3 grid((uint32_t)((ctx->r + 255) / 256), QW);
+      ens_transpose_bits_kernel<<<grid, 256, 0, st>>>(Qd, ar->Qt, ctx->r, nb, (uint32_t)B, QW);
+      ENS_LAUNCHED(ctx);
     }
-  }
-  ENS_CUDA(ctx, cudaMemsetAsync(ctx->acc, 0, B * ctx->dp, st));
-  {
-    dim3 grid((uint32_t)((ctx->r + 255) / 256), QW);
-    ens_transpose_bits_kernel<<<grid, 256, 0, st>>>(Qd, ctx->Qt, ctx->r, nb, (uint32_t)B, QW);
+    EnsBatchArgs a;
+    a.R = ctx->R;
+    a.Qt = ar->Qt;
+    a.out = ar->acc;
+    a.r = ctx->r;
+    a.dp = (uint32_t)ctx->dp;
+    a.W = (uint32_t)(ctx->dp / 16);
+    a.QW = QW;
+    a.B = (uint32_t)B;
+    const uint32_t slices = (a.W + ENS_CW - 1) / ENS_CW;
+    const uint32_t qblocks = (uint32_t)((B + ENS_QG * ENS_QB - 1) / (ENS_QG * ENS_QB));
+    // enough CTAs for ~8 per SM, rows split evenly
+    const uint64_t want = 8ull * ctx->num_sms;
+    uint64_t splits = std::max<uint64_t>(1, (want + slices * qblocks - 1) / (slices * qblocks));
+    uint64_t rows = ctx->rows_per_cta ? (uint64_t)ctx->rows_per_cta
+                                      : std::min<uint64_t>(256, (ctx->r + splits - 1) / splits);
+    rows = round_up(std::max<uint64_t>(rows, 4), 4);
+    a.rows_per_cta = rows;
+    dim3 grid((uint32_t)((ctx->r + rows - 1) / rows), slices, qblocks);
+    ens_batch_kernel<<<grid, ENS_CW * ENS_QB, 0, st>>>(a);
     ENS_LAUNCHED(ctx);
+    ctx->last_path = QPIR_ENS_PATH_CUDA_CORES;
   }
-  EnsBatchArgs a;
-  a.R = ctx->R;
-  a.Qt = ctx->Qt;
-  a.out = ctx->acc;
-  a.r = ctx->r;
-  a.dp = (uint32_t)ctx->dp;
-  a.W = (uint32_t)(ctx->dp / 16);
-  a.QW = QW;
-  a.B = (uint32_t)B;
-  const uint32_t slices = (a.W + ENS_CW - 1) / ENS_CW;
-  const uint32_t qblocks = (uint32_t)((B + ENS_QG * ENS_QB - 1) / (ENS_QG * ENS_QB));
-  // enough CTAs for ~8 per SM, rows split evenly
-  const uint64_t want = 8ull * ctx->num_sms;
-  uint64_t splits = std::max<uint64_t>(1, (want + slices * qblocks - 1) / (slices * qblocks));
-  uint64_t rows = ctx->rows_per_cta ? (uint64_t)ctx->rows_per_cta
-                                    : std::min<uint64_t>(256, (ctx->r + splits - 1) / splits);
-  rows = round_up(std::max<uint64_t>(rows, 4), 4);
-  a.rows_per_cta = rows;
-  dim3 grid((uint32_t)((ctx->r + rows - 1) / rows), slices, qblocks);
-  ens_batch_kernel<<<grid, ENS_CW * ENS_QB, 0, st>>>(a);
-  ENS_LAUNCHED(ctx);
-  if (slot >= 0) ENS_CUDA(ctx, cudaEventRecord(ctx->r_batch.done[slot], st));
-  return copy_out(ctx, out, B, st);
+  if (slot >= 0) ENS_CUDA(ctx, cudaEventRecord(ar->r_batch.done[slot], st));
+  return copy_out(ctx, *ar, out, B, st);
 }
 
-uint64_t qpir_ens_kernel_launches(const qpir_ens_ctx* ctx) { return ctx ? ctx->launches : 0; }
+uint64_t qpir_ens_kernel_launches(const qpir_ens_ctx* ctx) { return ctx ? ctx->launches.load() : 0; }
+
+int qpir_ens_last_path(const qpir_ens_ctx* ctx) {
+  return ctx ? ctx->last_path.load() : QPIR_ENS_PATH_NONE;
+}
 
 const char* qpir_ens_last_error(const qpir_ens_ctx* ctx) {
   return ctx ? ctx->err.c_str() : g_ens_setup_error.c_str();
@@ -562,19 +608,21 @@ const char* qpir_ens_last_error(const qpir_ens_ctx* ctx) {
 void qpir_ens_destroy(qpir_ens_ctx* ctx) {
   if (!ctx) return;
   DeviceGuard dg(ctx->device);
-  void* bufs[] = {ctx->R,       ctx->acc,  ctx->Q_dev, ctx->Qt,
-                  ctx->seed_dev, ctx->partial, ctx->tickets, ctx->bitD, ctx->Qb,
-                  ctx->acc1,    ctx->io_stage};
-  if (ctx->h2d) cudaStreamSynchronize(ctx->h2d);
-  for (void* b : bufs)
-    if (b) cudaFree(b);
-  for (EnsRing* g : {&ctx->r_share, &ctx->r_q, &ctx->r_A, &ctx->r_batch})
-    for (int k = 0; k < 2; ++k) {
-      if (g->buf[k]) cudaFree(g->buf[k]);
-      if (g->ready[k]) cudaEventDestroy(g->ready[k]);
-      if (g->done[k]) cudaEventDestroy(g->done[k]);
-    }
-  if (ctx->h2d) cudaStreamDestroy(ctx->h2d);
+  if (ctx->R) cudaFree(ctx->R);
+  for (auto& kv : ctx->arenas) {
+    EnsArena& a = kv.second;
+    if (a.h2d) cudaStreamSynchronize(a.h2d);
+    void* bufs[] = {a.acc, a.acc1, a.io_stage, a.Q_dev, a.Qt, a.seed_dev, a.partial, a.tickets, a.Qb};
+    for (void* b : bufs)
+      if (b) cudaFree(b);
+    for (EnsRing* g : {&a.r_share, &a.r_q, &a.r_A, &a.r_batch})
+      for (int k = 0; k < 2; ++k) {
+        if (g->buf[k]) cudaFree(g->buf[k]);
+        if (g->ready[k]) cudaEventDestroy(g->ready[k]);
+        if (g->done[k]) cudaEventDestroy(g->done[k]);
+      }
+    if (a.h2d) cudaStreamDestroy(a.h2d);
+  }
   delete ctx;
 }
 

@@ -126,30 +126,42 @@ def shard_records(r: int, world: int, rank: int, align: int = 1):
     return min(r, u0 * align), min(r, u1 * align)
 
 
-def xor_combine(part: torch.Tensor, group=None) -> torch.Tensor:
-    """XOR of every rank's uint8 partial response (NCCL has no XOR reduction:
-    all-gather the d-byte partials and fold them; the payload is a few KB)."""
+def gather_parts(part: torch.Tensor, group=None) -> torch.Tensor:
+    """[world, *part.shape] stack of every rank's partial response (rank-major),
+    on part's device -- communication only (NCCL all-gather over NVLink; gloo
+    list all-gather through host memory in CPU tests)."""
     world = dist.get_world_size(group)
+    part = part.contiguous()
     if dist.get_backend(group) == "nccl":
         buf = torch.empty((world, *part.shape), dtype=part.dtype, device=part.device)
-        dist.all_gather_into_tensor(buf, part.contiguous().unsqueeze(0), group=group)
-        parts = list(buf)
-    else:
-        host = part.contiguous().cpu()
-        parts = [torch.empty_like(host) for _ in range(world)]
-        dist.all_gather(parts, host, group=group)
-    out = parts[0].clone()
-    for t in parts[1:]:
-        out ^= t.to(out.device)
-    return out.to(part.device)
+        dist.all_gather_into_tensor(buf, part.unsqueeze(0), group=group)
+        return buf
+    host = part.cpu()
+    parts = [torch.empty_like(host) for _ in range(world)]
+    dist.all_gather(parts, host, group=group)
+    return torch.stack(parts).to(part.device)
+
+
+def xor_combine(part: torch.Tensor, group=None) -> torch.Tensor:
+    """XOR of every rank's uint8 partial response (NCCL has no XOR reduction):
+    all-gather the d-byte partials, then fold them with the library's device
+    kernel (qpir_xor_fold)."""
+    from . import _lib
+    parts = gather_parts(part, group)
+    out = torch.empty_like(part)
+    _lib.qpir_xor_fold(parts, parts.shape[0], part.numel(), out)
+    return out
 
 
 def sum_mod_p(part_u32: torch.Tensor, p: int, group=None) -> torch.Tensor:
     """Sum of every rank's partial F_p response (values < p) mod p, exactly:
-    all-reduce in int64 (world * p < 2^63), then reduce."""
-    acc = part_u32.to(torch.int64) & 0xFFFFFFFF
-    dist.all_reduce(acc, op=dist.ReduceOp.SUM, group=group)
-    return (acc % p).to(torch.int64)
+    all-gather the u32 partials, then fold them with the library's device
+    kernel (qpir_sum_mod_p, 64-bit sums)."""
+    from . import _lib
+    parts = gather_parts(part_u32, group)
+    out = torch.empty_like(part_u32)
+    _lib.qpir_sum_mod_p(parts, parts.shape[0], part_u32.numel(), p, out)
+    return out
 
 
 class DistributedEns:

@@ -80,7 +80,9 @@ def test_shard_rows_whole_channels():
 def _worker_next(rank, world, port, q):
     import synth
     from oracle import oracle as O
-    from paper_2510_03631_b200.dist import shard_records, sum_mod_p, xor_combine
+    # communication only (the device fold kernels are covered by test_gpu_dist.py);
+    # the fold itself is written out here, from the definitions (XOR / sum mod p)
+    from paper_2510_03631_b200.dist import gather_parts, shard_records
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
     dist.init_process_group("gloo", rank=rank, world_size=world)
@@ -93,12 +95,15 @@ def _worker_next(rank, world, port, q):
         share[-1] &= (1 << (r % 8)) - 1
         local = share[t0 // 8:(t1 + 7) // 8]
         part = torch.from_numpy(O.ens_respond(rec[t0:t1], local))
-        ok_ens = bool((xor_combine(part).numpy() == O.ens_respond(rec, share)).all())
+        parts = gather_parts(part).numpy()
+        folded = np.bitwise_xor.reduce(parts, axis=0)
+        ok_ens = bool((folded == O.ens_respond(rec, share)).all())
         # FTR: contiguous shards, partial sums mod p combined exactly
         f0, f1 = shard_records(r, world, rank)
         Q = synth.uniform_u32_np(11, (3, r)) % p
         partf = torch.from_numpy(O.ftr_respond_batch(rec[f0:f1], Q[:, f0:f1]).view(np.int32))
-        ok_ftr = bool((sum_mod_p(partf, p).numpy() == O.ftr_respond_batch(rec, Q)).all())
+        pf = gather_parts(partf).numpy().view(np.uint32).astype(np.int64)
+        ok_ftr = bool(((pf.sum(0) % p) == O.ftr_respond_batch(rec, Q)).all())
         q.put((rank, ok_ens, ok_ftr))
     finally:
         dist.destroy_process_group()

@@ -53,3 +53,23 @@ def test_distributed_pir_ens_ftr_one_rank(nccl1):
     Qf = synth.uniform_u32_np(7, (2, r)) % 65537
     got = ftr.answer_batch(torch.from_numpy(Qf.view(np.int32)).cuda())
     assert (got.cpu().numpy() == O.ftr_respond_batch(rec, Qf)).all()
+
+
+@pytest.mark.parametrize("n,length", [(1, 3072), (2, 3072), (5, 17), (8, 100000)])
+def test_combine_kernels_match_definitions(cuda_ok, n, length):
+    """qpir_xor_fold / qpir_sum_mod_p (the cross-rank fold after the all-gather)
+    against their definitions written out in numpy: XOR over parts, and the
+    exact integer sum reduced mod p; host pointers are refused (no fallback)."""
+    from paper_2510_03631_b200 import _lib
+    parts8 = synth.uniform_u8_np(60 + n, (n, length))
+    out8 = torch.empty(length, dtype=torch.uint8, device="cuda")
+    _lib.qpir_xor_fold(torch.from_numpy(parts8).cuda(), n, length, out8)
+    assert (out8.cpu().numpy() == np.bitwise_xor.reduce(parts8, axis=0)).all()
+    for p in (65537, 2, 4294967291):
+        parts32 = synth.uniform_u32_np(70 + n, (n, length)) % p
+        out32 = torch.empty(length, dtype=torch.int32, device="cuda")
+        _lib.qpir_sum_mod_p(torch.from_numpy(parts32.view(np.int32)).cuda(), n, length, p, out32)
+        want = (parts32.astype(object).sum(0) % p).astype(np.uint32)
+        assert (out32.cpu().numpy().view(np.uint32) == want).all(), p
+    with pytest.raises(_lib.QpirError):
+        _lib.qpir_xor_fold(parts8, n, length, out8)  # host parts

@@ -50,10 +50,12 @@ def test_ens_answer_matches_oracle(cuda_ok, r, d, rows, group, wide, monkeypatch
             assert (got.cpu().numpy() == want).all()
 
 
-@pytest.mark.parametrize("B", [1, 7, 64, 130])
+@pytest.mark.parametrize("B", [1, 7, 64, 128, 130, 256, 300])
 @pytest.mark.parametrize("tc", ["0", "1"])
 def test_ens_batch_matches_oracle(cuda_ok, B, tc, monkeypatch):
-    """tc = 1: GF(2) product on tcgen05 over bit-planes (OUT_PARITY epilogue);
+    """tc = 1: GF(2) product on tcgen05 (records expanded on chip into weighted
+    bit-rows, ens_mma.cuh; B <= 128: one share tile x 64 record bytes per unit,
+    B > 128: two share tiles x 32 bytes, B > 256: several share-tile groups);
     tc = 0: CUDA-core predicated-XOR kernel."""
     monkeypatch.setenv("QPIR_ENS_TC", tc)
     P = _P()
@@ -63,8 +65,35 @@ def test_ens_batch_matches_oracle(cuda_ok, B, tc, monkeypatch):
     want = O.ens_respond_batch(rec, Q)
     with P.EnsServer(r, d, records=torch.from_numpy(rec).cuda()) as s:
         got = s.answer_batch(Q).cpu().numpy()
+        assert s.last_path == ("tensor" if tc == "1" else "cuda_cores")
         assert (got == want).all()
         assert (s.answer(Q[B // 2]).cpu().numpy() == want[B // 2]).all()
+        assert s.last_path == "scan"
+
+
+def test_ens_tc_extreme_bits(cuda_ok, monkeypatch):
+    """Tensor-core path on all-0xFF records and all-ones shares: every bit-row
+    count is r (accumulated as r * 2^i for bit i, up to r * 128), so the
+    response is all-ones iff r is odd -- each weight 2^0..2^7 must land on its
+    own bit; then unit shares return single records exactly."""
+    monkeypatch.setenv("QPIR_ENS_TC", "1")
+    P = _P()
+    for r in (4097, 4096):
+        d = 77
+        rec = np.full((r, d), 0xFF, np.uint8)
+        nb = (r + 7) // 8
+        ones = np.full((40, nb), 0xFF, np.uint8)
+        if r % 8:
+            ones[:, -1] = (1 << (r % 8)) - 1
+        with P.EnsServer(r, d, records=rec) as s:
+            got = s.answer_batch(ones).cpu().numpy()
+            assert (got == (0xFF if r % 2 else 0)).all()
+        rec = synth.uniform_u8_np(r, (r, d))
+        units = np.zeros((40, nb), np.uint8)
+        idx = np.linspace(0, r - 1, 40).astype(int)
+        units[np.arange(40), idx >> 3] = (1 << (idx & 7)).astype(np.uint8)
+        with P.EnsServer(r, d, records=rec) as s:
+            assert (s.answer_batch(units).cpu().numpy() == rec[idx]).all()
 
 
 def test_ens_bruteforce_reconstruct(cuda_ok):
@@ -96,6 +125,32 @@ def test_ens_tc_ragged_and_split(cuda_ok, split, monkeypatch):
             rec2[5] ^= 0xFF
             s.db_write(5, rec2[5:6])
             assert (s.answer_batch(Q).cpu().numpy() == O.ens_respond_batch(rec2, Q)).all()
+
+
+@pytest.mark.parametrize("tc", ["0", "1"])
+def test_ens_mutation_one_byte_is_detected(cuda_ok, tc, monkeypatch):
+    """SURVEY 5 mutation test for ENS: flip bits of one byte of record t via
+    db_write; a response whose share selects t changes in exactly that byte (by
+    exactly the flipped bits), one that does not select t is unchanged."""
+    monkeypatch.setenv("QPIR_ENS_TC", tc)
+    P = _P()
+    r, d, t, b, flip = 4099, 100, 1234, 57, 0x21
+    rec = synth.uniform_u8_np(61, (r, d))
+    Q = np.stack([_share(62 + i, r) for i in range(40)])
+    sel = (Q[:, t >> 3] >> (t & 7)) & 1
+    assert sel.any() and not sel.all()
+    with P.EnsServer(r, d, records=rec) as s:
+        before = s.answer_batch(Q).cpu().numpy()
+        assert (before == O.ens_respond_batch(rec, Q)).all()
+        bad = rec[t].copy()
+        bad[b] ^= flip
+        s.db_write(t, bad[None, :])
+        after = s.answer_batch(Q).cpu().numpy()
+    delta = before ^ after
+    assert (delta[sel == 0] == 0).all()
+    assert (delta[sel == 1][:, b] == flip).all()
+    delta[:, b] = 0
+    assert (delta == 0).all()
 
 
 def test_ens_db_write_and_c2_scale(cuda_ok):

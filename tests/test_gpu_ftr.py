@@ -105,3 +105,35 @@ def test_ftr_and_batches_back_to_back(cuda_ok):
         for out, want, _ in jobs:
             if want is not None:
                 assert (Pk.u32(out) == want).all()
+
+
+@pytest.mark.parametrize("l,t", [(5, 1), (7, 2), (9, 2)])
+def test_ftr_byzantine_responses_decoded(cuda_ok, l, t):
+    """nu-Byzantine robustness (Lemma 1 proof P:1227):
+    nu = floor((l - t - 1) / 2) of the l GPU responses are corrupted (a faulty
+    or malicious server adds garbage); Berlekamp-Welch decoding (oracle client)
+    of the GPU responses still returns record theta exactly and names exactly the
+    corrupted servers.  The paper's Guruswami-Sudan list decoder would tolerate
+    nu < l - floor(sqrt(l t)) (e.g. l = 9, t = 2: 5 vs 3 here; DESIGN R21)."""
+    Pk = _P()
+    r, s = 3001, 96
+    nu = (l - t - 1) // 2
+    rec = synth.uniform_u8_np(31 + l, (r, s))
+    thetas = [0, 1500, r - 1]
+    Q = np.concatenate([O.ftr_query(th, r, l, t, seed=70 + th) for th in thetas])
+    with Pk.FtrServer(r, s, records=rec) as srv:
+        resp = Pk.u32(srv.answer_batch(Q)).reshape(len(thetas), l, s)
+    assert (resp.reshape(-1, s) == O.ftr_respond_batch(rec, Q)).all()
+    rng = np.random.default_rng(l * 10 + t)
+    al = np.arange(1, l + 1)
+    for i, th in enumerate(thetas):
+        bad_srv = rng.choice(l, nu, replace=False)
+        corrupted = resp[i].copy()
+        for j in bad_srv:
+            corrupted[j] = (corrupted[j] + rng.integers(1, P, s)) % P
+        got, flagged = O.ftr_decode(corrupted, al, t)
+        assert (got == rec[th]).all()
+        assert set(np.nonzero(flagged)[0]) == set(bad_srv)
+        # plain Lagrange on the same corrupted set is wrong (the decoder is needed)
+        if nu:
+            assert (O.ftr_reconstruct(corrupted, al) != rec[th]).any()

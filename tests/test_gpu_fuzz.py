@@ -118,7 +118,7 @@ def test_fuzz_scan_knobs(cuda_ok, case, monkeypatch):
              "QPIR_GEMV_UNROLL": str(int(rng.choice([4, 8]))),
              "QPIR_GEMV_SPLIT": str(int(rng.choice([0, 1, 3, 9]))),
              "QPIR_GEMV_CHUNK": str(int(rng.choice([64, 512]))),
-             "QPIR_GEMV_IMPL": str(int(rng.choice([0, 0, 1]))),
+             "QPIR_GEMV_L2PF": str(int(rng.choice([0, 1]))),
              "QPIR_GEMV_PDL": str(int(rng.choice([0, 1]))),
              "QPIR_ENS_ROWS": str(int(rng.choice([0, 32, 96]))),
              "QPIR_ENS_UR": str(int(rng.choice([4, 8, 16]))),

@@ -62,8 +62,7 @@ RAGGED = [
 @pytest.mark.parametrize("cfg", [dict(), dict(QPIR_GEMV_U="1", QPIR_GEMV_SPLIT="3", QPIR_GEMV_CHUNK="8"),
                                  dict(QPIR_GEMV_U="4", QPIR_GEMV_SPLIT="1", QPIR_GEMV_CHUNK="4"),
                                  dict(QPIR_GEMV_ORDER="1", QPIR_GEMV_SPLIT="5", QPIR_GEMV_UNROLL="8"),
-                                 dict(QPIR_MMA_MT="1", QPIR_MMA_SPLIT="3"),
-                                 dict(QPIR_GEMV_IMPL="1")])
+                                 dict(QPIR_MMA_MT="1", QPIR_MMA_SPLIT="3")])
 def test_answer_ragged(cuda_ok, geo, cfg, monkeypatch):
     for k, v in cfg.items():
         monkeypatch.setenv(k, v)
@@ -121,13 +120,56 @@ def test_db_write_streaming(cuda_ok):
         assert (_u32(s.answer(qu)) == O.answer(D, qu)).all()
 
 
-def test_wraparound_kat_gemv_and_tc(cuda_ok):
-    """P9: all-0xFF D times all-0xFFFFFFFF queries, K = 65536: every byte-limb sum
-    is 255*255*65536 = 4,261,478,400 > 2^31, so the GEMV's dp4a accumulators and
-    the tensor-core s32 accumulators must wrap (not saturate).  Expected value in
-    closed form: sum_c 255 * (2^32 - 1) = -255 * m mod 2^32."""
+def test_mutation_one_db_byte_is_detected(cuda_ok):
+    """SURVEY 5 mutation test: the parity checks have teeth.  Flip one byte of
+    one record through qpir_db_write: the GEMV, the batch and the hint must then
+    differ from the unmutated oracle in exactly that byte's row, by exactly
+    delta * (query or A entry of its column) mod 2^32 (linearity of D -> D.x),
+    and agree with the oracle on the mutated DB."""
     P = _srv()
-    n_cells, n_ch, d = 65536, 1, 128
+    n_cells, n_ch, d, n = 1024, 16, 8, 64
+    rec, D = _db(n_cells, n_ch, d, seed=90)
+    theta, b = 5 * n_ch + 11, 6
+    row, col = O.position(n_ch, d, n_cells, theta, b)
+    qu = synth.uniform_u32_np(91, (n_cells,))
+    Q = synth.uniform_u32_np(92, (5, n_cells))
+    A = O.expand_A(93, n_cells, n)
+    with P.PirServer(n_cells, n_ch, d, lwe_n=n, seed_A=93, records=rec) as s:
+        assert (_u32(s.answer(qu)) == O.answer(D, qu)).all()
+        assert (_u32(s.hint()) == O.hint(D, A)).all()
+        bad = rec[theta].copy()
+        delta = 0x5A
+        bad[b] ^= delta
+        s.db_write(theta, bad[None, :])
+        D2 = D.copy()
+        D2[row, col] = bad[b]
+        diff = (int(bad[b]) - int(rec[theta][b])) & M32
+        got, want = _u32(s.answer(qu)), O.answer(D, qu)
+        assert (got != want).sum() == 1 and got[row] == (int(want[row]) + diff * int(qu[col])) & M32
+        assert (got == O.answer(D2, qu)).all()
+        gotB, wantB = _u32(s.answer_batch(Q)), O.answer_batch(D, Q)
+        assert ((gotB != wantB).sum(0) > 0).sum() == 1 and (gotB[:, row] != wantB[:, row]).all()
+        assert (gotB == O.answer_batch(D2, Q)).all()
+        gotH, wantH = _u32(s.hint()), O.hint(D, A)
+        assert ((gotH != wantH).sum(1) > 0).sum() == 1
+        assert (gotH[row] == ((wantH[row].astype(np.int64) + diff * A[col].astype(np.int64)) & M32)).all()
+        assert (gotH == O.hint(D2, A)).all()
+
+
+@pytest.mark.parametrize("n_cells", [65536, 131072])
+def test_wraparound_kat_gemv_and_tc(cuda_ok, n_cells, monkeypatch):
+    """P9: all-0xFF D times all-0xFFFFFFFF queries with ONE K-split, so a single
+    accumulator sums the whole row: every byte-limb sum is 255*255*m
+    (4.26e9 > 2^31 at m = 65536; 8.52e9 > 2^32 at m = 131072), so the GEMV's
+    dp4a accumulators and the tensor-core s32 TMEM accumulators must wrap mod
+    2^32 (idesc saturate bit 0), never saturate.  QPIR_GEMV_SPLIT=1 /
+    QPIR_MMA_SPLIT=1 force one unit per row tile (the auto split would cut K
+    into pieces whose sums stay below 2^31).  Expected value in closed form:
+    sum_c 255 * (2^32 - 1) = -255 * m mod 2^32."""
+    monkeypatch.setenv("QPIR_GEMV_SPLIT", "1")
+    monkeypatch.setenv("QPIR_MMA_SPLIT", "1")
+    P = _srv()
+    n_ch, d = 1, 128
     rec = np.full((n_cells * n_ch, d), 255, np.uint8)
     want = (-255 * n_cells) & M32
     with P.PirServer(n_cells, n_ch, d, records=rec) as s:
@@ -136,6 +178,10 @@ def test_wraparound_kat_gemv_and_tc(cuda_ok):
         Q = np.full((4, n_cells), M32, np.uint32)
         ans = _u32(s.answer_batch(Q))
         assert (ans == want).all()
+        # mixed extreme limbs: 0xFF00FF00 has limbs (0, 255, 0, 255)
+        Q2 = np.full((3, n_cells), 0xFF00FF00, np.uint32)
+        assert (_u32(s.answer_batch(Q2)) == (255 * 0xFF00FF00 * n_cells) & M32).all()
+        assert (_u32(s.answer(Q2[0])) == (255 * 0xFF00FF00 * n_cells) & M32).all()
 
 
 # ------------------------------------------------------------------ batch (a6)
@@ -264,11 +310,24 @@ def test_c3_nationwide_sampled(cuda_ok):
     s.close()
 
 
+def _channel_slab(seed, ch, n_cells, n_ch, d):
+    """Rows [ch*d, (ch+1)*d) of D for m = n_cells (one row block, DESIGN R10):
+    the channel's records (synth, generated on the GPU only for speed) packed
+    by the oracle as a one-channel DB."""
+    theta = torch.arange(n_cells, device="cuda", dtype=torch.int64) * n_ch + ch
+    rec = synth.records_at(seed, theta, d, n_ch, 512).cpu().numpy()
+    return O.pack(rec, n_cells, 1, d, n_cells)
+
+
 @pytest.mark.slow
 @pytest.mark.parametrize("B", [64, 256])
 def test_c4_batch_sampled(cuda_ok, B):
     """configs[3]: 65536 cells x 40 x 3072 = 8.05 GB, B concurrent queries;
-    24 sampled rows exact for all B queries, + 2 columns == single answers."""
+    24 sampled rows exact for all B queries, + 2 columns == single answers,
+    + Freivalds (40 rounds over Z_{2^32}, P8 of SURVEY 8(c)) on the FULL ANS:
+    ANS^T X == D (Q^T X) with the right side from the oracle, channel by
+    channel.  For a wrong product E != 0 (mod 2^32) a uniform column of X gives
+    E x == 0 with probability <= 1/2, so 40 columns miss with <= 2^-40."""
     P = _srv()
     n_cells, n_ch, d = 65536, 40, 3072
     seed = 25
@@ -282,29 +341,43 @@ def test_c4_batch_sampled(cuda_ok, B):
     for j in (0, B - 1):
         assert (_u32(s.answer(Q[j])) == ANS[j]).all()
     s.close()
+    X = synth.uniform_u32_np(27, (B, 40))             # 40 Freivalds rounds
+    left = np.matmul(ANS.T, X)                         # uint32 matmul wraps mod 2^32
+    V = np.ascontiguousarray(np.matmul(Q.T, X).T)      # (Q^T X)^T: 40 queries
+    for ch in range(n_ch):
+        right = O.answer_batch(_channel_slab(seed, ch, n_cells, n_ch, d), V)
+        assert (left[ch * d:(ch + 1) * d].T == right).all(), f"Freivalds fails in channel {ch}"
 
 
 @pytest.mark.slow
 def test_c5_hint_shard_sampled(cuda_ok):
     """configs[4], one rank's shard at G = 8: rows [0, 15360) of the 32 GB DB,
-    n = 1024; 12 sampled rows of H exact against the oracle's D.A."""
+    n = 1024; 64 sampled rows of H exact against the oracle's D.A, and
+    Freivalds (40 rounds over Z_{2^32}) on the FULL shard: H X == D (A X)."""
     P = _srv()
     n_cells, n_ch, d, n = 262144, 40, 3072, 1024
     seed, seed_A = 27, 0x5EED
     from paper_2510_03631_b200.dist import shard_rows
     r0, r1 = shard_rows(n_cells, n_ch, d, n_cells, 8, 0)
+    assert r0 == 0 and (r1 - r0) % d == 0
     s = _setup_synth_db(P, n_cells, n_ch, d, seed, lwe_n=n, seed_A=seed_A, row_begin=r0, row_end=r1)
     H = _u32(s.hint())
+    s.close()
     rng = np.random.default_rng(2)
-    rows = np.concatenate([[0, r1 - r0 - 1], rng.choice(r1 - r0, 10, replace=False)])
+    rows = np.concatenate([[0, r1 - r0 - 1], rng.choice(r1 - r0, 62, replace=False)])
     Dr = _sampled_rows(seed, rows + r0, n_cells, n_ch, d)
     A = O.expand_A(seed_A, n_cells, n)
     assert (H[rows] == O.hint(Dr, A)).all()
-    s.close()
+    X = synth.uniform_u32_np(28, (n, 40))
+    left = np.matmul(H, X)
+    V = np.ascontiguousarray(np.matmul(A, X).T)        # (A X)^T
+    del A
+    for ch in range((r1 - r0) // d):
+        right = O.answer_batch(_channel_slab(seed, ch, n_cells, n_ch, d), V)
+        assert (left[ch * d:(ch + 1) * d].T == right).all(), f"Freivalds fails in channel {ch}"
 
 
-@pytest.mark.parametrize("cfg", [dict(), dict(QPIR_GEMV_SPLIT="7"), dict(QPIR_GEMV_PDL="0"),
-                                 dict(QPIR_GEMV_IMPL="1")])
+@pytest.mark.parametrize("cfg", [dict(), dict(QPIR_GEMV_SPLIT="7"), dict(QPIR_GEMV_PDL="0")])
 def test_back_to_back_answers_pdl(cuda_ok, cfg, monkeypatch):
     """Back-to-back GEMVs on one stream overlap under programmatic dependent
     launch; split-K scratch and outputs must not race (every answer exact)."""
@@ -327,6 +400,55 @@ def test_back_to_back_answers_pdl(cuda_ok, cfg, monkeypatch):
         for i, o in outs:
             assert (_u32(o) == O.answer(D, Qs[i])).all(), i
         assert (_u32(same) == O.answer(D, Qs[23])).all()
+
+
+@pytest.mark.parametrize("cfg", [dict(), dict(QPIR_GEMV_SPLIT="1"), dict(QPIR_GEMV_L2PF="1")])
+def test_pdl_inputs_written_by_previous_kernel(cuda_ok, cfg, monkeypatch):
+    """Programmatic dependent launch hazard (PDL: the next kernel may start
+    before the previous one ends, and only its writes are visible after
+    griddepcontrol.wait).  No syncs anywhere between the producers and the
+    answers: (1) a torch kernel writes qu on the stream right before each of
+    1000 answers; (2) each answer's query is the previous GEMV's output
+    (GEMV -> GEMV on one stream, the case where the producer triggers its
+    dependents early); (3) a device-side db_write (pack kernel writes D) is
+    followed at once by an answer.  Every result must be exact."""
+    for k, v in cfg.items():
+        monkeypatch.setenv(k, v)
+    P = _srv()
+    n_cells, n_ch, d = 2048, 1, 2048  # ell = m = 2048: an answer can be the next query
+    rec, D = _db(n_cells, n_ch, d, seed=95)
+    base = synth.uniform_u32_np(96, (n_cells,))
+    keys = torch.arange(1000, dtype=torch.int32, device="cuda") * 0x9E3779B1
+    with P.PirServer(n_cells, n_ch, d, records=torch.from_numpy(rec).cuda()) as s:
+        assert s.ell_local == n_cells
+        qb = torch.from_numpy(base.view(np.int32)).cuda()
+        qd = torch.empty_like(qb)
+        outs = torch.empty((1000, s.ell_local), dtype=torch.int32, device="cuda")
+        for i in range(1000):
+            torch.bitwise_xor(qb, keys[i], out=qd)  # kernel writes qu, then the answer
+            s.answer(qd, out=outs[i])
+        # chain: query i+1 = answer i
+        chain = torch.empty((8, s.ell_local), dtype=torch.int32, device="cuda")
+        s.answer(qb, out=chain[0])
+        for i in range(1, 8):
+            s.answer(chain[i - 1], out=chain[i])
+        # device db_write immediately followed by an answer (no sync)
+        rec2 = rec.copy()
+        rec2[::7] ^= 0x3C
+        s.db_write(0, torch.from_numpy(rec2).cuda())
+        after = s.answer(qb)
+        torch.cuda.synchronize()
+        o = _u32(outs)
+        kk = keys.cpu().numpy().view(np.uint32)
+        want = O.answer_batch(D, base[None, :] ^ kk[:, None])
+        bad = np.nonzero((o != want).any(1))[0]
+        assert bad.size == 0, f"answers {bad[:10]} wrong"
+        c = _u32(chain)
+        q = base
+        for i in range(8):
+            q = O.answer(D, q)
+            assert (c[i] == q).all(), i
+        assert (_u32(after) == O.answer(O.pack(rec2, n_cells, n_ch, d, n_cells), base)).all()
 
 
 def test_concurrent_streams_have_private_scratch(cuda_ok, monkeypatch):

@@ -44,6 +44,25 @@ def test_expand_A_indexing():
     assert len(set(A[0].tolist())) == 12
 
 
+def test_keygen_indexing():
+    """s[j] = Philox(key=seed_s, ctr=(j>>2, 0, 0, 0x53))[j&3] (DESIGN R6), each
+    element re-derived from the KAT-pinned Philox.  Catches s = 0, a wrong
+    domain tag, A's stream reused for s, and a wrong j -> (block, lane) map."""
+    seed = 0xFEDCBA9876543210
+    n = 19
+    s = O.keygen(seed, n)
+    key = [seed & M32, seed >> 32]
+    assert s.dtype == np.uint32 and s.shape == (n,)
+    for j in range(n):
+        assert s[j] == O.philox4x32_10([j >> 2, 0, 0, 0x53], key)[j & 3]
+    assert (s != 0).all() and len(set(s.tolist())) == n
+    # not A's stream: A[c=0..n) is drawn with domain 0x41 and ctr[0] = cell
+    A = O.expand_A(seed, 1, n)
+    assert (A[0] != s).all()
+    # distinct seeds give distinct secrets; the key uses both seed halves
+    assert (O.keygen(seed ^ 1, n) != s).any() and (O.keygen(seed ^ (1 << 40), n) != s).any()
+
+
 # ------------------------------------------------------------------ layout
 @pytest.mark.parametrize("n_cells,n_ch,d,m", [(16, 3, 5, 16), (20, 3, 4, 8), (7, 2, 3, 3)])
 def test_layout_is_a_bijection(n_cells, n_ch, d, m):

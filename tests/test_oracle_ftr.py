@@ -79,3 +79,74 @@ def test_t1_single_server_view_uniform():
             counts[sh[0, 0], sh[0, 1]] += 1
         chi2 = ((counts - 100.0) ** 2 / 100.0).sum()
         assert chi2 < 90.0  # 48 dof
+
+
+# ---------------------------------------------------------------- robust decoding
+def test_bw_without_errors_equals_lagrange():
+    """No corruption: Berlekamp-Welch decodes to the same words as Lagrange
+    interpolation at 0 ("when zero corruption, plain Lagrange")."""
+    rng = np.random.default_rng(11)
+    for k, t in [(2, 1), (3, 1), (5, 2), (7, 3), (7, 1)]:
+        resp = rng.integers(0, P, (k, 9)).astype(np.uint32)
+        # make the rows a degree-t code word: evaluate random polynomials
+        coef = rng.integers(0, P, (t + 1, 9))
+        al = np.arange(1, k + 1)
+        resp = np.stack([sum(coef[c] * pow(int(a), c, P) for c in range(t + 1)) % P
+                         for a in al]).astype(np.uint32)
+        got, bad = O.ftr_decode(resp, al, t)
+        assert (got == O.ftr_reconstruct(resp[: t + 1], al[: t + 1])).all()
+        assert (got == coef[0] % P).all() and not bad.any()
+
+
+def test_bw_robustness_exhaustive_small():
+    """SPEC invariant (FTR robustness): for all (k, t, nu) with
+    nu <= floor((k - t - 1) / 2) and k <= 7, corrupting any nu responses (every
+    choice of positions, random wrong values) never changes the reconstructed
+    block, and the corrupted servers are exactly the ones flagged."""
+    r, s = 12, 5
+    rec = synth.uniform_u8_np(21, (r, s))
+    rng = np.random.default_rng(22)
+    checked = 0
+    for k in range(2, 8):
+        for t in range(0, k):
+            e = (k - t - 1) // 2
+            theta = int(rng.integers(r))
+            sh = O.ftr_query(theta, r, k, t, seed=1000 + 10 * k + t)
+            resp = np.stack([O.ftr_respond(rec, sh[i]) for i in range(k)])
+            al = np.arange(1, k + 1)
+            for nu in range(0, e + 1):
+                for pos in itertools.combinations(range(k), nu):
+                    bad_resp = resp.copy()
+                    for i in pos:
+                        bad_resp[i] = (bad_resp[i] + rng.integers(1, P, s)) % P
+                    got, bad = O.ftr_decode(bad_resp, al, t)
+                    assert (got == rec[theta]).all(), (k, t, pos)
+                    assert set(np.nonzero(bad)[0]) == set(pos), (k, t, pos)
+                    checked += 1
+    assert checked > 100
+
+
+def test_bw_beyond_radius_and_incomplete():
+    """k <= t responses: incompleteness error; e + 1 corrupted responses: the
+    unique decoder reports failure (it cannot be right in general: with
+    k = 5, t = 2 two bad rows of a 3-of-5 code are undecodable)."""
+    r, s, k, t = 10, 6, 5, 2
+    rec = synth.uniform_u8_np(23, (r, s))
+    sh = O.ftr_query(4, r, k, t, seed=24)
+    resp = np.stack([O.ftr_respond(rec, sh[i]) for i in range(k)])
+    al = np.arange(1, k + 1)
+    with pytest.raises(O.FtrDecodeError):
+        O.ftr_decode(resp[:t], al[:t], t)
+    rng = np.random.default_rng(25)
+    fails = 0
+    for trial in range(20):
+        bad_resp = resp.copy()
+        pos = rng.choice(k, (k - t - 1) // 2 + 1, replace=False)
+        for i in pos:
+            bad_resp[i] = (bad_resp[i] + rng.integers(1, P, s)) % P
+        try:
+            got, _ = O.ftr_decode(bad_resp, al, t)
+            fails += int(not (got == rec[4]).all())
+        except O.FtrDecodeError:
+            fails += 1
+    assert fails == 20  # never silently "right" beyond the radius on random errors
