@@ -86,8 +86,18 @@ typedef struct {
   uint64_t row_begin; /* this context's shard [row_begin, row_end) of [0, ell);   */
   uint64_t row_end;   /* row_end = 0 means ell (the whole matrix)                 */
   int32_t device;     /* CUDA device ordinal                                      */
-  int32_t reserved1;  /* must be 0                                                */
+  int32_t flags;      /* 0 or QPIR_FLAG_STABLE_INPUTS                             */
 } qpir_params;
+
+/* Caller's promise: a device query / share buffer passed to an answer call is
+ * never written by the kernel that immediately precedes that call on its
+ * stream.  The answer kernels are launched with programmatic dependent launch
+ * (they may start while the previous kernel on the stream drains, and that
+ * kernel's writes are visible only after griddepcontrol.wait); with the flag
+ * they read their inputs before the wait, overlapping the previous grid's
+ * tail.  Without it only the DB is read before the wait (host inputs are staged
+ * by the library and are always read early). */
+#define QPIR_FLAG_STABLE_INPUTS 1
 
 /* Create a context on params->device holding the D shard.  `records` is the
  * full theta-ordered record array (n_cells * n_ch * rec_bytes bytes, host or
@@ -174,7 +184,7 @@ typedef struct {
   uint64_t n_records; /* r                                       */
   uint64_t rec_bytes; /* d, 1..16384                             */
   int32_t device;     /* CUDA device ordinal                     */
-  int32_t reserved;   /* must be 0                               */
+  int32_t flags;      /* 0 or QPIR_FLAG_STABLE_INPUTS (shares)   */
 } qpir_ens_params;
 
 /* Create an ENS context holding all r records (records may be NULL: zero DB). */

@@ -42,10 +42,13 @@ class PirServer:
 
     def __init__(self, n_cells: int, n_ch: int, rec_bytes: int, *, m: int = 0,
                  lwe_n: int = 1024, seed_A: int = 0, row_begin: int = 0, row_end: int = 0,
-                 device: int = 0, records=None, stream=None):
+                 device: int = 0, records=None, stream=None, stable_inputs: bool = False):
+        # stable_inputs: QPIR_FLAG_STABLE_INPUTS (include/qpir.h) -- device query
+        # buffers are never written by the kernel right before an answer call
         p = qpir_params(n_cells=n_cells, n_ch=n_ch, rec_bytes=rec_bytes, m=m, lwe_n=lwe_n,
                         log_q=32, log_p=8, reserved0=0, seed_A=seed_A, row_begin=row_begin,
-                        row_end=row_end, device=device, reserved1=0)
+                        row_end=row_end, device=device,
+                        flags=_lib.QPIR_FLAG_STABLE_INPUTS if stable_inputs else 0)
         self.device = device
         self.lwe_n = lwe_n
         self._ctx = _lib.qpir_setup(p, records, _st(device, stream))
@@ -113,9 +116,9 @@ class EnsServer:
     """QPADL-ENS server (Chor XOR PIR): r records of d bytes on one GPU."""
 
     def __init__(self, n_records: int, rec_bytes: int, *, device: int = 0, records=None,
-                 stream=None):
+                 stream=None, stable_inputs: bool = False):
         p = _lib.qpir_ens_params(n_records=n_records, rec_bytes=rec_bytes, device=device,
-                                 reserved=0)
+                                 flags=_lib.QPIR_FLAG_STABLE_INPUTS if stable_inputs else 0)
         self.device = device
         self.r, self.d = n_records, rec_bytes
         self.share_bytes = (n_records + 7) // 8

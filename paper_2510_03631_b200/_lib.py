@@ -14,7 +14,9 @@ import os
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libqpir.so")
+# QPIR_LIB: load another build of the same ABI (A/B measurements against an
+# earlier build of this library; there is no other implementation behind it)
+LIB_PATH = os.environ.get("QPIR_LIB") or os.path.join(_HERE, "libqpir.so")
 
 QPIR_OK = 0
 QPIR_E_PARAM = 1
@@ -50,7 +52,7 @@ class qpir_params(ctypes.Structure):
         ("row_begin", ctypes.c_uint64),
         ("row_end", ctypes.c_uint64),
         ("device", ctypes.c_int32),
-        ("reserved1", ctypes.c_int32),
+        ("flags", ctypes.c_int32),
     ]
 
 
@@ -59,8 +61,11 @@ class qpir_ens_params(ctypes.Structure):
         ("n_records", ctypes.c_uint64),
         ("rec_bytes", ctypes.c_uint64),
         ("device", ctypes.c_int32),
-        ("reserved", ctypes.c_int32),
+        ("flags", ctypes.c_int32),
     ]
+
+
+QPIR_FLAG_STABLE_INPUTS = 1  # include/qpir.h
 
 
 class QpirError(RuntimeError):
@@ -75,7 +80,26 @@ if not os.path.exists(LIB_PATH):
         "(there is no CPU fallback)"
     )
 
+class _OlderBuild:
+    """QPIR_LIB pointing at an earlier build (A/B timing): symbols it lacks
+    become stubs that raise when called, so the rest still binds."""
+
+    def __init__(self, lib):
+        self._lib = lib
+
+    def __getattr__(self, name):
+        try:
+            return getattr(self._lib, name)
+        except AttributeError:
+            def stub(*_a):
+                raise QpirError(QPIR_E_STATE, f"{name}: not exported by {LIB_PATH}")
+            setattr(self, name, stub)
+            return stub
+
+
 _L = ctypes.CDLL(LIB_PATH)
+if os.environ.get("QPIR_LIB"):
+    _L = _OlderBuild(_L)
 _vp = ctypes.c_void_p
 _u64 = ctypes.c_uint64
 _L.qpir_setup.argtypes = [ctypes.POINTER(qpir_params), _vp, _u64, _vp, ctypes.POINTER(_vp)]

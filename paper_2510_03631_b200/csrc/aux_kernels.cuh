@@ -4,6 +4,7 @@
 #include <cstdint>
 
 #include "layout.cuh"
+#include "mma.cuh"
 #include "philox.cuh"
 
 namespace qpir {
@@ -71,13 +72,7 @@ __global__ void pack_records_kernel(PackArgs a) {
 // LPQ = 2 (p <= 65537): a reduced entry 65536 (only p = 65537) is written as 0
 // and its column appended to the query's exception list (exc_cnt / exc_list,
 // `cap` entries per query) for modp_fixup_kernel.
-// a mod p for any u32 a and 2 <= p < 2^32 with pM = ceil(2^64 / p) (Lemire,
-// Kaser & Kurz, "Faster remainder by direct computation", 2019): exact, and 3
-// integer instructions instead of the ~20 of a runtime u32 division.
-__device__ __forceinline__ uint32_t fastmod_u32(uint32_t a, uint64_t pM, uint32_t p) {
-  return (uint32_t)__umul64hi(pM * a, p);
-}
-
+// fastmod_u32: mma.cuh (shared with the fused split of the tcgen05 engine).
 template <int LPQ>
 __global__ void limb_split_kernel(const uint32_t* __restrict__ Q, uint8_t* __restrict__ Qp,
                                   uint32_t B, uint32_t m, uint32_t G, uint32_t Npad,

@@ -48,6 +48,7 @@ struct EnsArgs {
   uint32_t d;           // record bytes
   uint32_t* done;       // zero-initialised, self-resetting
   uint32_t leaders;     // CTAs that reach the atomics (grid, or groups)
+  uint32_t early;       // 1: the share is not the previous kernel's output: scan before the PDL wait
 };
 
 // Called by every thread of a CTA that has just added its partial into a.out.
@@ -79,8 +80,7 @@ __device__ __forceinline__ void ens_finalize(const EnsArgs& a) {
 template <int UR>
 __global__ void __launch_bounds__(1024, 1) ens_scan_kernel(EnsArgs a) {
   asm volatile("griddepcontrol.launch_dependents;");  // PDL: see ens_scan_wide_kernel
-  // the share selects which rows are read: nothing can be touched before the wait
-  asm volatile("griddepcontrol.wait;" ::: "memory");
+  if (!a.early) asm volatile("griddepcontrol.wait;" ::: "memory");
   extern __shared__ uint4 s_part[];
   const uint32_t w = threadIdx.x % a.W;
   const uint32_t lr = threadIdx.x / a.W;
@@ -113,6 +113,7 @@ __global__ void __launch_bounds__(1024, 1) ens_scan_kernel(EnsArgs a) {
       acc.w ^= v[u].w;
     }
   }
+  if (a.early) asm volatile("griddepcontrol.wait;" ::: "memory");  // before any global write
   const bool owner = lr == 0;  // one thread per 16-byte chunk keeps the CTA result
   if (R > 1) {
     s_part[threadIdx.x] = acc;
@@ -178,14 +179,15 @@ __global__ void __launch_bounds__(1024, 1) ens_scan_kernel(EnsArgs a) {
 // flight per thread; under plain (1024) it packed into 32 registers and issued
 // the loads two at a time (SASS), latency-bound at 0.61-0.90 of HBM.
 // Programmatic dependent launch: the next scan's CTAs become resident while this
-// grid drains, but every read waits at griddepcontrol.wait -- the share (which
-// the previous kernel on the stream may have written) decides which rows of R
-// are read, so there is nothing to prefetch before it; back-to-back answers
-// still save the launch and CTA ramp.
+// grid drains.  The share decides which rows of R are read, so unless it is
+// known not to be the previous kernel's output (a.early: staged by the library
+// from host memory, or QPIR_FLAG_STABLE_INPUTS) every read waits at
+// griddepcontrol.wait; with a.early the scan overlaps the previous grid's tail
+// and only the partials / tickets / out writes wait.
 template <int UR, int CW>
 __global__ void __launch_bounds__(1024, 1) ens_scan_wide_kernel(EnsArgs a) {
   asm volatile("griddepcontrol.launch_dependents;");
-  asm volatile("griddepcontrol.wait;" ::: "memory");  // previous grid complete + visible
+  if (!a.early) asm volatile("griddepcontrol.wait;" ::: "memory");  // previous grid complete + visible
   const uint32_t w = threadIdx.x * CW;  // first 16-byte chunk of this thread
   const uint64_t n_rows = a.row_hi - a.row_lo;
   const uint64_t t0 = (uint64_t)blockIdx.x * a.rows_per_cta;  // multiple of 32
@@ -221,6 +223,7 @@ __global__ void __launch_bounds__(1024, 1) ens_scan_wide_kernel(EnsArgs a) {
         }
     }
   }
+  if (a.early) asm volatile("griddepcontrol.wait;" ::: "memory");  // before any global write
   if (a.partial != nullptr) {
     __shared__ uint32_t s_last;
 #pragma unroll

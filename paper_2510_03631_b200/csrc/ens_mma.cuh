@@ -57,6 +57,7 @@ struct EnsMmaArgs {
   uint32_t s_tiles;   // groups of MS share tiles
   uint32_t w_tiles;   // width tiles of 32 * NT record bytes
   uint32_t splits, kbps, kblocks;
+  uint64_t s_tstride;  // bytes per share tile of Qb (G16 * 2048), 64-bit: see MmaArgs::a_pstride
 };
 
 template <uint32_t MS, uint32_t NT, uint32_t S, uint32_t RS>
@@ -78,20 +79,6 @@ struct EmCfg {
   static_assert(ACC_COLS <= 512, "accumulator exceeds TMEM");
   static_assert(TOTAL <= 227 * 1024, "smem");
 };
-
-__device__ __forceinline__ void cp_async_16_zfill(void* smem_dst, const void* src, bool valid) {
-  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(smem_u32(smem_dst)), "l"(src),
-               "r"(valid ? 16u : 0u)
-               : "memory");
-}
-__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
-template <int N>
-__device__ __forceinline__ void cp_async_wait() {
-  asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
-}
-__device__ __forceinline__ void fence_proxy_async_smem() {
-  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-}
 
 template <uint32_t MS, uint32_t NT, uint32_t S, uint32_t RS>
 __global__ void __launch_bounds__(EM_THREADS, 1) qpir_ens_mma_kernel(EnsMmaArgs a) {
@@ -148,7 +135,7 @@ __global__ void __launch_bounds__(EM_THREADS, 1) qpir_ens_mma_kernel(EnsMmaArgs 
 #pragma unroll
           for (uint32_t s = 0; s < MS; ++s)
             bulk_g2s(dst + s * C::A_TILE,
-                     a.Qb + ((size_t)(sg * MS + s) * a.G16 + (size_t)kb * 4) * 2048, C::A_TILE,
+                     a.Qb + (uint64_t)(sg * MS + s) * a.s_tstride + (uint64_t)kb * (4 * 2048), C::A_TILE,
                      &full[stage]);
           if (++stage == S) { stage = 0; phase ^= 1; }
         }
@@ -260,7 +247,7 @@ __global__ void __launch_bounds__(EM_THREADS, 1) qpir_ens_mma_kernel(EnsMmaArgs 
             const uint64_t th = (uint64_t)kb * EM_KB + rr;
             const uint32_t off = byte0 + c * 16;
             const bool ok = th < a.r && off < a.dp;
-            cp_async_16_zfill(slot + x * 16, ok ? a.R + th * a.dp + off : a.R, ok);
+            cp_async_16(slot + x * 16, ok ? a.R + th * a.dp + off : a.R, ok);
           }
         }
         cp_async_commit();  // one group per K-block (empty past the unit's end)

@@ -109,19 +109,21 @@ struct GemvArgs {
   uint32_t split_major; // 1: blockIdx.x = split, blockIdx.y = row block (page-local order)
   uint32_t pf256;       // 1: L2::256B prefetch hint on the D loads
   uint32_t l2pf;        // 1: bulk L2 prefetch of the CTA's D slice before griddepcontrol.wait
+  uint32_t early;       // 1: qu is not the previous kernel's output: scan before the wait
 };
 
 // U rows per thread (rows r, r + 128, ...); UNR column groups per iteration.
 template <int U, int UNR>
 __global__ void __launch_bounds__(GEMV_THREADS) qpir_gemv_u8_u32_kernel(GemvArgs a) {
   extern __shared__ uint4 sL[];
-  // Programmatic dependent launch: let the next query's GEMV start while this
-  // grid drains.  Before griddepcontrol.wait this CTA touches ONLY the D shard
-  // (library-owned; a device-side db_write launches the next GEMV without PDL,
-  // qpir.cu): its first UNR column groups go to registers and, with l2pf, its
-  // whole D slice is prefetched into L2 by the TMA engine.  qu (which the
-  // previous kernel on the stream may have written) is staged after the wait,
-  // and every global write (partials, tickets, ans) comes after it too.
+  // Programmatic dependent launch: the next query's GEMV may start while this
+  // grid drains; only the previous kernel's writes are visible after
+  // griddepcontrol.wait.  Before the wait a CTA touches only the D shard
+  // (library-owned; right after a device-side db_write the GEMV is launched
+  // without PDL, qpir.cu) -- unless a.early: then qu is known not to come from
+  // the previous kernel (staged by the library from host memory, or the caller
+  // set QPIR_FLAG_STABLE_INPUTS) and the whole scan runs before the wait.
+  // Every global write (partials, tickets, ans) comes after the wait.
   asm volatile("griddepcontrol.launch_dependents;");
   const uint32_t tid = threadIdx.x;
   // Grid order: with split_major the CTAs that run at the same time walk
@@ -156,9 +158,9 @@ __global__ void __launch_bounds__(GEMV_THREADS) qpir_gemv_u8_u32_kernel(GemvArgs
                             : ldg_stream_v4(Drow[u] + (size_t)(g + i) * gstride);
   };
 
-  // ---- before the wait: D only
+  // ---- before the wait: D only (first UNR groups in flight; optional bulk L2
+  // prefetch of the whole slice)
   if (a.l2pf && tid < U) {
-    // one bulk L2 prefetch per 128-row panel of this CTA: groups [gb, ge)
     const uint32_t r = rblk * (GEMV_THREADS * U) + tid * GEMV_THREADS;
     if (r < a.ell_local)
       l2_prefetch_bulk(a.D + (size_t)(r >> 7) * a.G * 2048 + (size_t)gb * gstride,
@@ -166,7 +168,7 @@ __global__ void __launch_bounds__(GEMV_THREADS) qpir_gemv_u8_u32_kernel(GemvArgs
   }
   uint4 d[UNR][U];
   load(gb, d);
-  asm volatile("griddepcontrol.wait;" ::: "memory");  // previous grid complete + visible
+  if (!a.early) asm volatile("griddepcontrol.wait;" ::: "memory");  // qu may be the previous grid's output
 
   for (uint32_t cb = gb; cb < ge; cb += a.chunk) {
     const uint32_t ce = min(ge, cb + a.chunk);
@@ -185,6 +187,7 @@ __global__ void __launch_bounds__(GEMV_THREADS) qpir_gemv_u8_u32_kernel(GemvArgs
       }
     }
   }
+  if (a.early) asm volatile("griddepcontrol.wait;" ::: "memory");  // before any global write
 
   uint32_t out[U];
 #pragma unroll

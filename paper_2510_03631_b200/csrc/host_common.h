@@ -21,6 +21,18 @@ struct NvtxRange {
 
 inline uint64_t round_up(uint64_t x, uint64_t a) { return (x + a - 1) / a * a; }
 
+// QPIR_DEBUG_SYNC=1: synchronise after every launch so that an execution error
+// is reported by the launch that caused it (debugging aid; off by default).
+inline bool debug_sync_enabled() {
+  static const bool on = getenv("QPIR_DEBUG_SYNC") && atoi(getenv("QPIR_DEBUG_SYNC")) != 0;
+  return on;
+}
+inline cudaError_t launch_status() {
+  cudaError_t e = cudaGetLastError();
+  if (e == cudaSuccess && debug_sync_enabled()) e = cudaDeviceSynchronize();
+  return e;
+}
+
 inline int env_int(const char* name, int dflt) {
   const char* v = getenv(name);
   return v ? atoi(v) : dflt;

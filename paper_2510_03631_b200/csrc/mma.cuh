@@ -77,7 +77,40 @@ struct MmaArgs {
   // waits for one that is not resident (e.g. SMs held by a concurrent launch).
   uint32_t* kprog;    // [waves][2]: chunks issued, CTAs arrived (zeroed per launch), or nullptr
   uint32_t ls_chunk, ls_drift;
+  // Byte strides of one 128-row panel of A (G * 2048) and one BN-column tile of
+  // B (G * BN * 16), passed as 64-bit values: computed in-kernel from the
+  // 32-bit G, ptxas (CUDA 12.9) folded "base + (u64)G << 11" into a 32-bit
+  // uniform LEA with the high half zeroed (SASS "UMOV URn+1, URZ; ULEA URn"
+  // feeding UBLKCP: an illegal address for the second D panel; see
+  // tools/sass_counts.py, which checks every build for that pattern).
+  uint64_t a_pstride, b_tstride;
+  // Fused limb split (OUT_MODP2, CONV kernels): converter warps build the B
+  // operand (reduced 2-limb planes) from the u32 queries while the GEMM runs.
+  // Conversion chunks = K-blocks, taken from a global work counter (so every
+  // chunk is converted as long as any CTA runs: no CTA waits on a non-resident
+  // one) in the order the units consume them; a chunk publishes
+  // kb_done[kb] = epoch (release), the producer acquires it before its bulk copy.
+  const uint32_t* Q = nullptr;   // u32 queries [qB][qm]
+  uint32_t qB = 0, qm = 0;
+  uint64_t pM = 0;               // fastmod constant ceil(2^64 / p)
+  uint8_t* Bw = nullptr;         // the B operand, written by the converters
+  uint32_t* exc_cnt = nullptr;   // p = 65537: per-query exception counts / lists
+  uint32_t* exc_list = nullptr;
+  uint32_t exc_cap = 0;
+  uint32_t* kb_done = nullptr;   // [kblocks] epoch flags
+  uint32_t epoch = 0;
+  unsigned long long* conv_ctr = nullptr;  // monotonic work counter
+  unsigned long long conv_base = 0;        // its value at this launch
 };
+
+constexpr uint32_t MMA_CONV_THREADS = 128;  // 4 converter warps (CONV kernels)
+
+__device__ __forceinline__ void st_release_u32(uint32_t* p, uint32_t v) {
+  asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+__device__ __forceinline__ void fence_proxy_async_global() {
+  asm volatile("fence.proxy.async.global;" ::: "memory");
+}
 
 __device__ __forceinline__ uint32_t ld_acquire_u32(const uint32_t* p) {
   uint32_t v;
@@ -108,8 +141,15 @@ struct MmaCfg {
   static_assert(ACC_COLS <= 512, "accumulator exceeds TMEM");
 };
 
-template <uint32_t BN, uint32_t MT, uint32_t GPB, int OUT_MODE>
-__global__ void __launch_bounds__(MMA_THREADS, 1) mma_u8_limb_kernel(MmaArgs a) {
+// a mod p for any u32 a and 2 <= p < 2^32 with pM = ceil(2^64 / p) (Lemire,
+// Kaser & Kurz, "Faster remainder by direct computation", 2019): exact.
+__device__ __forceinline__ uint32_t fastmod_u32(uint32_t a, uint64_t pM, uint32_t p) {
+  return (uint32_t)__umul64hi(pM * a, p);
+}
+
+template <uint32_t BN, uint32_t MT, uint32_t GPB, int OUT_MODE, bool CONV = false>
+__global__ void __launch_bounds__(CONV ? MMA_THREADS + MMA_CONV_THREADS : MMA_THREADS, 1)
+    mma_u8_limb_kernel(MmaArgs a) {
   using C = MmaCfg<BN, MT, GPB>;
   constexpr uint32_t STAGES = C::STAGES;
   extern __shared__ __align__(1024) uint8_t smem[];
@@ -174,18 +214,24 @@ __global__ void __launch_bounds__(MMA_THREADS, 1) mma_u8_limb_kernel(MmaArgs a) 
               while (ld_acquire_u32(issued) < ld_acquire_u32(issued + 1) * need) __nanosleep(128);
             }
           }
+          if constexpr (CONV) {
+            // the converters' generic-proxy stores of this K-block's limb planes
+            // are visible (acquire) before the async-proxy bulk copy reads them
+            while (ld_acquire_u32(a.kb_done + kb) != a.epoch) __nanosleep(64);
+            fence_proxy_async_global();
+          }
           mbar_wait(&empty[stage], phase ^ 1);
           mbar_arrive_expect_tx(&full[stage], C::STAGE_BYTES);
           uint8_t* dst = smem + stage * C::STAGE_BYTES;
 #pragma unroll
           for (uint32_t p = 0; p < MT; ++p) {
-            const size_t panel = (size_t)mt * MT + p;
+            const uint64_t panel = (uint64_t)mt * MT + p;
             bulk_g2s(dst + p * C::PANEL_BYTES,
-                     a.A + (panel * a.G + (size_t)kb * GPB) * 2048, C::PANEL_BYTES,
+                     a.A + panel * a.a_pstride + (uint64_t)kb * (GPB * 2048), C::PANEL_BYTES,
                      &full[stage]);
           }
           bulk_g2s(dst + C::A_BYTES,
-                   a.B + ((size_t)nt * a.G + (size_t)kb * GPB) * (BN * 16), C::B_BYTES,
+                   a.B + (uint64_t)nt * a.b_tstride + (uint64_t)kb * (GPB * BN * 16), C::B_BYTES,
                    &full[stage]);
           if (++stage == STAGES) { stage = 0; phase ^= 1; }
           if (LS && ((kb - kb0) % LS == LS - 1 || kb + 1 == kb1))
@@ -232,7 +278,7 @@ __global__ void __launch_bounds__(MMA_THREADS, 1) mma_u8_limb_kernel(MmaArgs a) 
       }
       if (++acc == C::ACC_BUFS) { acc = 0; acc_phase ^= 1; }
     }
-  } else {
+  } else if (!CONV || warp < 6) {
     // ------------------------------------------------------------ epilogue
     const uint32_t q = warp & 3;  // TMEM lane quarter this warp may access
     const bool split = a.splits > 1;
@@ -348,6 +394,65 @@ __global__ void __launch_bounds__(MMA_THREADS, 1) mma_u8_limb_kernel(MmaArgs a) 
       tc_fence_before();
       mbar_arrive(&tempty[acc]);
       if (++acc == C::ACC_BUFS) { acc = 0; acc_phase ^= 1; }
+    }
+  } else {
+    // ------------------------------------------------------------ converters
+    // (CONV only) K-block kb of the B operand: limb k of (Q[j][c] mod p), c in
+    // the block's 16 * GPB cells, for every padded query slot j; the residue
+    // 65536 of p = 65537 (17 bits) is written as 0 and listed for the fixup.
+    // Warp cw takes queries cw, cw + 4, ...; lane l the 4 cells 4l .. 4l + 3.
+    static_assert(!CONV || (OUT_MODE == OUT_MODP2 && GPB == 8), "fused split: 2 limbs, K-block 128");
+    if constexpr (CONV) {
+      __shared__ uint32_t s_job[2];
+      const uint32_t ct = threadIdx.x - MMA_THREADS, cw = ct / 32, cl = ct % 32;
+      const uint32_t total = a.splits * a.kps;
+      const uint32_t nq = a.n_tiles * BN / 2;  // padded query slots
+      const bool vec = (a.qm & 3u) == 0 && ((reinterpret_cast<uintptr_t>(a.Q) & 15u) == 0);
+      for (uint32_t it = 0;; ++it) {
+        if (ct == 0)
+          s_job[it & 1] = (uint32_t)(atomicAdd(a.conv_ctr, 1ull) - a.conv_base);
+        asm volatile("bar.sync 1, %0;" ::"n"(MMA_CONV_THREADS) : "memory");
+        const uint32_t jb = s_job[it & 1];
+        if (jb >= total) break;
+        const uint32_t sp = jb % a.splits, ii = jb / a.splits;  // consumption order
+        const uint32_t kb = sp * a.kps + ii;
+        const bool live = kb < kblocks && ii < a.kps;
+        if (live) {
+          const uint32_t c0 = kb * (16 * GPB) + 4 * cl;
+          const uint32_t g = c0 >> 4;
+          for (uint32_t j = cw; j < nq; j += 4) {
+            uint32_t v[4] = {0u, 0u, 0u, 0u};
+            if (j < a.qB) {
+              const uint32_t* row = a.Q + (size_t)j * a.qm;
+              if (vec && c0 + 4 <= a.qm) {
+                const uint4 x = __ldg(reinterpret_cast<const uint4*>(row + c0));
+                v[0] = x.x; v[1] = x.y; v[2] = x.z; v[3] = x.w;
+              } else {
+#pragma unroll
+                for (int e = 0; e < 4; ++e) v[e] = (c0 + e < a.qm) ? __ldg(row + c0 + e) : 0u;
+              }
+#pragma unroll
+              for (int e = 0; e < 4; ++e) {
+                v[e] = fastmod_u32(v[e], a.pM, a.p);
+                if (v[e] == 65536u && a.exc_cnt) {  // p = 65537 only; padding cells are 0
+                  const uint32_t idx = atomicAdd(a.exc_cnt + j, 1u);
+                  if (idx < a.exc_cap) a.exc_list[(size_t)j * a.exc_cap + idx] = c0 + e;
+                  v[e] = 0u;
+                }
+              }
+            }
+            const uint32_t w0 = __byte_perm(__byte_perm(v[0], v[1], 0x0040), __byte_perm(v[2], v[3], 0x0040), 0x5410);
+            const uint32_t w1 = __byte_perm(__byte_perm(v[0], v[1], 0x0051), __byte_perm(v[2], v[3], 0x0051), 0x5410);
+            const uint32_t n0 = 2 * j;  // limb columns 2j, 2j + 1 (same BN panel: BN even)
+            uint8_t* dst = a.Bw + (((size_t)(n0 / BN) * a.G + g) * BN + (n0 % BN)) * 16 + (cl & 3) * 4;
+            *reinterpret_cast<uint32_t*>(dst) = w0;
+            *reinterpret_cast<uint32_t*>(dst + 16) = w1;
+          }
+          __threadfence();
+        }
+        asm volatile("bar.sync 1, %0;" ::"n"(MMA_CONV_THREADS) : "memory");
+        if (ct == 0 && live) st_release_u32(a.kb_done + kb, a.epoch);
+      }
     }
   }
 

@@ -7,6 +7,7 @@
 #include <algorithm>
 #include <cstdint>
 
+#include "host_common.h"
 #include "mma.cuh"
 
 namespace qpir {
@@ -32,6 +33,16 @@ struct MmaJob {
   uint32_t* kprog = nullptr;   // K-lockstep scratch (kprog_cap u32), nullptr = off
   uint32_t kprog_cap = 0;
   uint32_t ls_chunk = 0, ls_drift = 1;  // K-blocks per lockstep chunk (0 = off)
+  // fused limb split (OUT_MODP2, gpb 8): converter warps build B from the u32
+  // queries inside the GEMM (mma.cuh CONV); B is then the writable Q' buffer
+  bool conv = false;
+  const uint32_t* Q = nullptr;
+  uint32_t qB = 0, qm = 0;
+  uint64_t pM = 0;
+  uint32_t* kb_done = nullptr;           // >= G / 8 flags
+  uint32_t epoch = 0;
+  unsigned long long* conv_ctr = nullptr;
+  unsigned long long* conv_base = nullptr;  // host-side running base (advanced here)
 };
 
 // BN for 3 limbs per query (OUT_MODP3): a multiple of 48 so queries never
@@ -90,7 +101,7 @@ inline uint32_t mma_choose_splits(uint32_t tiles, uint32_t kblocks, uint32_t sms
   return best;
 }
 
-template <uint32_t BN, uint32_t MT, uint32_t GPB, int MODE>
+template <uint32_t BN, uint32_t MT, uint32_t GPB, int MODE, bool CONV = false>
 cudaError_t mma_launch_cfg(const MmaJob& j, cudaStream_t st, uint64_t* launches) {
   using C = MmaCfg<BN, MT, GPB>;
   MmaArgs a;
@@ -135,24 +146,59 @@ cudaError_t mma_launch_cfg(const MmaJob& j, cudaStream_t st, uint64_t* launches)
   else if (a.splits > 1 && !j.out_prezeroed)
     e = cudaMemsetAsync(j.out, 0, j.out_elems * 4, st);
   if (e != cudaSuccess) return e;
-  auto kern = mma_u8_limb_kernel<BN, MT, GPB, MODE>;
+  if constexpr (CONV) {
+    a.Q = j.Q;
+    a.qB = j.qB;
+    a.qm = j.qm;
+    a.pM = j.pM;
+    a.Bw = const_cast<uint8_t*>(j.B);
+    a.exc_cnt = const_cast<uint32_t*>(j.exc.cnt);
+    a.exc_list = const_cast<uint32_t*>(j.exc.list);
+    a.exc_cap = j.exc.cap;
+    a.kb_done = j.kb_done;
+    a.epoch = j.epoch;
+    a.conv_ctr = j.conv_ctr;
+    a.conv_base = *j.conv_base;
+    // every converter group takes one index past the end before it stops
+    *j.conv_base += (unsigned long long)a.splits * a.kps + grid;
+  }
+  a.a_pstride = (uint64_t)j.G * 2048;
+  a.b_tstride = (uint64_t)j.G * BN * 16;
+  auto kern = mma_u8_limb_kernel<BN, MT, GPB, MODE, CONV>;
   e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::TOTAL);
   if (e != cudaSuccess) return e;
-  kern<<<grid, MMA_THREADS, C::TOTAL, st>>>(a);
+  kern<<<grid, CONV ? MMA_THREADS + MMA_CONV_THREADS : MMA_THREADS, C::TOTAL, st>>>(a);
   ++*launches;
-  e = cudaGetLastError();
+  e = qpir_host::launch_status();
   if (e != cudaSuccess) return e;
   if (modp) {
     const uint32_t blocks = (uint32_t)std::min<uint64_t>((j.out_elems + 255) / 256, 4096);
     modp_fixup_kernel<<<blocks, 256, 0, st>>>(j.out64, j.out, j.out_elems, j.p, j.out_ld, j.exc);
     ++*launches;
-    e = cudaGetLastError();
+    e = qpir_host::launch_status();
   }
   return e;
 }
 
 template <int MODE>
 cudaError_t mma_launch(const MmaJob& j, cudaStream_t st, uint64_t* launches) {
+  if constexpr (MODE == OUT_MODP2) {
+    if (j.conv) {  // fused limb split: K-block of 128 cells, BN = 2 x queries per tile
+      const bool m2 = j.mt != 1;
+      switch (j.BN) {
+        case 16: return m2 ? mma_launch_cfg<16, 2, 8, MODE, true>(j, st, launches)
+                           : mma_launch_cfg<16, 1, 8, MODE, true>(j, st, launches);
+        case 32: return m2 ? mma_launch_cfg<32, 2, 8, MODE, true>(j, st, launches)
+                           : mma_launch_cfg<32, 1, 8, MODE, true>(j, st, launches);
+        case 64: return m2 ? mma_launch_cfg<64, 2, 8, MODE, true>(j, st, launches)
+                           : mma_launch_cfg<64, 1, 8, MODE, true>(j, st, launches);
+        case 128: return m2 ? mma_launch_cfg<128, 2, 8, MODE, true>(j, st, launches)
+                            : mma_launch_cfg<128, 1, 8, MODE, true>(j, st, launches);
+        default: return m2 ? mma_launch_cfg<256, 2, 8, MODE, true>(j, st, launches)
+                           : mma_launch_cfg<256, 1, 8, MODE, true>(j, st, launches);
+      }
+    }
+  }
   const bool mt2 = j.mt != 1;
   const bool g4 = j.gpb == 4;
 #define QPIR_MMA_CASE(BNV)                                                           \

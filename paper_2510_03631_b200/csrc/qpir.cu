@@ -73,6 +73,11 @@ struct Arena {
   uint32_t* kprog = nullptr;       // tcgen05 engine K-lockstep counters [kKprogCap]
   uint32_t* exc = nullptr;         // OUT_MODP2, p = 65537: [Bc] counts + [Bc][cap] columns
   uint64_t exc_bytes = 0;
+  uint32_t* kb_done = nullptr;     // fused FTR limb split: per-K-block epoch flags (zeroed once)
+  uint64_t kb_done_bytes = 0;
+  unsigned long long* conv_ctr = nullptr;  // fused split work counter (monotonic, zeroed once)
+  unsigned long long conv_base = 0;        // its value at the next launch
+  uint32_t epoch = 0;                      // last epoch published into kb_done
 };
 
 struct qpir_ctx {
@@ -94,12 +99,14 @@ struct qpir_ctx {
   int gemv_pdl = 1;    // env QPIR_GEMV_PDL (programmatic dependent launch of back-to-back GEMVs)
   int gemv_pf256 = 0;  // env QPIR_GEMV_PF256: L2 256-byte prefetch hint on D loads
   int gemv_l2pf = 0;   // env QPIR_GEMV_L2PF: bulk L2 prefetch of a CTA's D slice before the PDL wait
+  int flags = 0;       // qpir_params.flags (QPIR_FLAG_STABLE_INPUTS)
   std::atomic<bool> d_written{false};  // a device db_write is queued: next GEMV without PDL
   int mma_mt = 2;      // env QPIR_MMA_MT (1 or 2 row panels per CTA tile)
   int mma_split = 0;   // env QPIR_MMA_SPLIT (0 = auto)
   int mma_gpb = 8;     // env QPIR_MMA_GPB (column groups per pipeline stage: 4 or 8)
   int modp3 = 1;       // env QPIR_MODP3 (3 limbs per query for p < 2^24)
   int modp2 = 1;       // env QPIR_MODP2 (2 limbs per query for p <= 65537)
+  int ftr_fuse = 1;    // env QPIR_FTR_FUSE (2-limb split inside the GEMM: converter warps)
   int h2d_stream = 1;  // env QPIR_H2D_STREAM (host inputs copied on a side stream)
   int mma_ls = 16;     // env QPIR_MMA_LOCKSTEP: K-blocks per lockstep chunk (0 = off)
   int mma_drift = 1;   // env QPIR_MMA_DRIFT: chunks a CTA may run ahead of its wave
@@ -133,7 +140,7 @@ int fail(qpir_ctx* ctx, int code, const char* fmt, ...) {
 #define LAUNCH_CHECK(ctx)                                                                 \
   do {                                                                                    \
     (ctx)->launches++;                                                                    \
-    cudaError_t e_ = cudaGetLastError();                                                  \
+    cudaError_t e_ = qpir_host::launch_status();                                          \
     if (e_ != cudaSuccess)                                                                \
       return fail((ctx), QPIR_E_CUDA, "kernel launch: %s (%s:%d)", cudaGetErrorString(e_), \
                   __FILE__, __LINE__);                                                    \
@@ -143,8 +150,9 @@ int validate(const qpir_params* p, Geometry* g) {
   if (!p) return fail(nullptr, QPIR_E_PARAM, "params: NULL");
   if (p->log_q != 32) return fail(nullptr, QPIR_E_PARAM, "log_q: %u != 32", p->log_q);
   if (p->log_p != 8) return fail(nullptr, QPIR_E_PARAM, "log_p: %u != 8", p->log_p);
-  if (p->reserved0 != 0 || p->reserved1 != 0)
-    return fail(nullptr, QPIR_E_PARAM, "reserved: must be 0");
+  if (p->reserved0 != 0) return fail(nullptr, QPIR_E_PARAM, "reserved0: must be 0");
+  if (p->flags & ~QPIR_FLAG_STABLE_INPUTS)
+    return fail(nullptr, QPIR_E_PARAM, "flags: unknown bits 0x%x", (unsigned)p->flags);
   if (p->lwe_n == 0 || p->lwe_n > 65536)
     return fail(nullptr, QPIR_E_PARAM, "lwe_n: %u not in [1, 65536]", p->lwe_n);
   if (p->n_cells == 0) return fail(nullptr, QPIR_E_DIMENSION, "n_cells: 0");
@@ -274,8 +282,11 @@ int db_write_device(qpir_ctx* ctx, uint64_t theta0, uint64_t n_rec, const uint8_
   return QPIR_OK;
 }
 
+// early: qu was not written by the kernel preceding this launch on `st` (the
+// library staged it from host memory with a copy, or the caller set
+// QPIR_FLAG_STABLE_INPUTS), so the scan may run before griddepcontrol.wait.
 template <int U, int UNR>
-int launch_gemv(qpir_ctx* ctx, const uint32_t* qu, uint32_t* ans, cudaStream_t st) {
+int launch_gemv(qpir_ctx* ctx, const uint32_t* qu, uint32_t* ans, cudaStream_t st, bool early) {
   const Geometry& g = ctx->geo;
   const uint32_t rows_per_cta = GEMV_THREADS * U;
   const uint32_t rb = (uint32_t)((g.ell_local + rows_per_cta - 1) / rows_per_cta);
@@ -328,6 +339,7 @@ int launch_gemv(qpir_ctx* ctx, const uint32_t* qu, uint32_t* ans, cudaStream_t s
   a.split_major = (ctx->gemv_order == 1 && rb <= 65535) ? 1u : 0u;
   a.pf256 = ctx->gemv_pf256 ? 1u : 0u;
   a.l2pf = ctx->gemv_l2pf ? 1u : 0u;
+  a.early = early ? 1u : 0u;
   const size_t smem = (size_t)chunk * 64;
   auto kern = qpir_gemv_u8_u32_kernel<U, UNR>;
   if (smem > 48 * 1024)
@@ -351,12 +363,12 @@ int launch_gemv(qpir_ctx* ctx, const uint32_t* qu, uint32_t* ans, cudaStream_t s
   return QPIR_OK;
 }
 
-int gemv(qpir_ctx* ctx, const uint32_t* qu, uint32_t* ans, cudaStream_t st) {
+int gemv(qpir_ctx* ctx, const uint32_t* qu, uint32_t* ans, cudaStream_t st, bool early) {
   const bool u8 = ctx->gemv_unroll == 8;
   switch (ctx->gemv_u) {
-    case 1: return u8 ? launch_gemv<1, 8>(ctx, qu, ans, st) : launch_gemv<1, 4>(ctx, qu, ans, st);
-    case 4: return u8 ? launch_gemv<4, 8>(ctx, qu, ans, st) : launch_gemv<4, 4>(ctx, qu, ans, st);
-    default: return u8 ? launch_gemv<2, 8>(ctx, qu, ans, st) : launch_gemv<2, 4>(ctx, qu, ans, st);
+    case 1: return u8 ? launch_gemv<1, 8>(ctx, qu, ans, st, early) : launch_gemv<1, 4>(ctx, qu, ans, st, early);
+    case 4: return u8 ? launch_gemv<4, 8>(ctx, qu, ans, st, early) : launch_gemv<4, 4>(ctx, qu, ans, st, early);
+    default: return u8 ? launch_gemv<2, 8>(ctx, qu, ans, st, early) : launch_gemv<2, 4>(ctx, qu, ans, st, early);
   }
 }
 
@@ -364,7 +376,7 @@ template <int MODE>
 int launch_mma(qpir_ctx* ctx, uint32_t BN, const uint8_t* Bl, uint32_t Npad, uint32_t* out,
                uint32_t n_out, uint32_t out_ld, uint64_t out_elems, cudaStream_t st,
                uint32_t p = 0, unsigned long long* out64 = nullptr, bool prezeroed = false,
-               const ModpExceptions& exc = ModpExceptions()) {
+               const ModpExceptions& exc = ModpExceptions(), const MmaJob* conv = nullptr) {
   const Geometry& g = ctx->geo;
   MmaJob j;
   j.A = ctx->D;
@@ -386,6 +398,17 @@ int launch_mma(qpir_ctx* ctx, uint32_t BN, const uint8_t* Bl, uint32_t Npad, uin
   j.gpb = ctx->mma_gpb;
   j.out_prezeroed = prezeroed;
   j.exc = exc;
+  if (conv) {  // fused limb split (OUT_MODP2): the converter fields of the caller's job
+    j.conv = true;
+    j.Q = conv->Q;
+    j.qB = conv->qB;
+    j.qm = conv->qm;
+    j.pM = conv->pM;
+    j.kb_done = conv->kb_done;
+    j.epoch = conv->epoch;
+    j.conv_ctr = conv->conv_ctr;
+    j.conv_base = conv->conv_base;
+  }
   if (ctx->mma_ls > 0) {
     constexpr uint32_t kKprogCap = 4096;
     Arena& ar = arena_for(ctx, st);
@@ -449,11 +472,13 @@ int qpir_setup(const qpir_params* params, const uint8_t* records, uint64_t recor
   ctx->gemv_pdl = env_int("QPIR_GEMV_PDL", 1);
   ctx->gemv_pf256 = env_int("QPIR_GEMV_PF256", 0);
   ctx->gemv_l2pf = env_int("QPIR_GEMV_L2PF", 0);
+  ctx->flags = params->flags;
   ctx->mma_mt = env_int("QPIR_MMA_MT", 2);
   ctx->mma_split = env_int("QPIR_MMA_SPLIT", 0);
   ctx->mma_gpb = env_int("QPIR_MMA_GPB", 8);
   ctx->modp3 = env_int("QPIR_MODP3", 1);
   ctx->modp2 = env_int("QPIR_MODP2", 1);
+  ctx->ftr_fuse = env_int("QPIR_FTR_FUSE", 1);
   ctx->h2d_stream = env_int("QPIR_H2D_STREAM", 1);
   ctx->mma_ls = env_int("QPIR_MMA_LOCKSTEP", 16);
   ctx->mma_drift = env_int("QPIR_MMA_DRIFT", 1);
@@ -572,7 +597,9 @@ int qpir_answer(qpir_ctx* ctx, const uint32_t* qu, uint64_t len_qu, uint32_t* an
     if (rc) return rc;
     ad = ar.ans_dev;
   }
-  rc = gemv(ctx, qd, ad, st);
+  // qu staged by the library (host copy / realignment copy) cannot be the
+  // previous kernel's output; a caller's device buffer only with the flag
+  rc = gemv(ctx, qd, ad, st, qd != qu || (ctx->flags & QPIR_FLAG_STABLE_INPUTS));
   if (rc) return rc;
   if (slot >= 0) CUDA_TRY(ctx, cudaEventRecord(ar.in_small.done[slot], st));
   if (!wa) {
@@ -654,11 +681,42 @@ static int answer_batch_impl(qpir_ctx* ctx, const uint32_t* Q, uint64_t B, uint6
     const uint32_t* Qc = Qd + b0 * g.m;
     uint32_t* oc = out + b0 * g.ell_local;
     const uint64_t oe = (uint64_t)bc * g.ell_local;
-    {
+    // 2 limbs: the split runs inside the GEMM (converter warps, mma.cuh) unless
+    // QPIR_FTR_FUSE=0 or the K-block is not 128 cells
+    const bool fuse = two && ctx->ftr_fuse && ctx->mma_gpb != 4;
+    const uint64_t pM = p >= 2 ? ~0ull / p + 1 : 0;  // fastmod_u32 constant
+    if (exc) CUDA_TRY(ctx, cudaMemsetAsync(exc_cnt, 0, (uint64_t)bc * 4, st));
+    MmaJob cj;
+    if (fuse) {
+      const uint64_t flags = (g.G / 8) * 4;
+      if (ar.kb_done_bytes < flags) {
+        rc = ensure(ctx, (void**)&ar.kb_done, &ar.kb_done_bytes, flags);
+        if (rc) return rc;
+        CUDA_TRY(ctx, cudaMemsetAsync(ar.kb_done, 0, flags, st));
+        ar.epoch = 0;
+      }
+      if (!ar.conv_ctr) {
+        uint64_t have = 0;
+        rc = ensure(ctx, (void**)&ar.conv_ctr, &have, 8);
+        if (rc) return rc;
+        CUDA_TRY(ctx, cudaMemsetAsync(ar.conv_ctr, 0, 8, st));
+        ar.conv_base = 0;
+      }
+      if (++ar.epoch == 0) {  // 2^32 launches: restart the flags
+        CUDA_TRY(ctx, cudaMemsetAsync(ar.kb_done, 0, ar.kb_done_bytes, st));
+        ar.epoch = 1;
+      }
+      cj.Q = Qc;
+      cj.qB = bc;
+      cj.qm = (uint32_t)g.m;
+      cj.pM = pM;
+      cj.kb_done = ar.kb_done;
+      cj.epoch = ar.epoch;
+      cj.conv_ctr = ar.conv_ctr;
+      cj.conv_base = &ar.conv_base;
+    } else {
       const uint32_t nq = Npad / LPQ;  // padded query slots
       dim3 grid((uint32_t)((g.G + 127) / 128), nq);
-      if (exc) CUDA_TRY(ctx, cudaMemsetAsync(exc_cnt, 0, (uint64_t)bc * 4, st));
-      const uint64_t pM = p >= 2 ? ~0ull / p + 1 : 0;  // fastmod_u32 constant
       if (two)
         limb_split_kernel<2><<<grid, 128, 0, st>>>(Qc, ar.limbs, bc, (uint32_t)g.m,
                                                    (uint32_t)g.G, Npad, BN, p, pM,
@@ -688,7 +746,7 @@ static int answer_batch_impl(qpir_ctx* ctx, const uint32_t* Q, uint64_t B, uint6
         ex.cap = cap;
       }
       rc = launch_mma<OUT_MODP2>(ctx, BN, ar.limbs, Npad, oc, bc, (uint32_t)g.ell_local, oe, st,
-                                 p, ar.acc64, false, ex);
+                                 p, ar.acc64, false, ex, fuse ? &cj : nullptr);
     }
     else if (three)
       rc = launch_mma<OUT_MODP3>(ctx, BN, ar.limbs, Npad, oc, bc, (uint32_t)g.ell_local, oe, st,
@@ -789,7 +847,7 @@ void qpir_destroy(qpir_ctx* ctx) {
     Arena& a = kv.second;
     void* ab[] = {a.qu_dev, a.ans_dev, a.partial, a.tickets, a.limbs, a.big_out, a.acc64,
                   a.exc, a.in_small.buf[0], a.in_small.buf[1], a.in_big.buf[0], a.in_big.buf[1],
-                  a.kprog};
+                  a.kprog, a.kb_done, a.conv_ctr};
     if (a.h2d) cudaStreamSynchronize(a.h2d);
     for (void* b : ab)
       if (b) cudaFree(b);

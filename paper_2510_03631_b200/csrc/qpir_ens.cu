@@ -71,6 +71,7 @@ struct qpir_ens_ctx {
                                 //   2 = 32-byte chunks per thread, 256-bit loads)
   int pdl = 1;                  // env QPIR_ENS_PDL (programmatic dependent launch of scans)
   int tc = -1;                  // env QPIR_ENS_TC: -1 auto, 0 CUDA cores, 1 tensor cores
+  int flags = 0;                // qpir_ens_params.flags (QPIR_FLAG_STABLE_INPUTS)
   int mma_split = 0;            // env QPIR_MMA_SPLIT (0 = auto)
   std::atomic<uint64_t> launches{0};
   std::atomic<int> last_path{QPIR_ENS_PATH_NONE};
@@ -187,7 +188,8 @@ int qpir_ens_setup(const qpir_ens_params* p, const uint8_t* records, uint64_t re
   if (!out) return set_error(&g_ens_setup_error, QPIR_E_PARAM, "out: NULL");
   *out = nullptr;
   if (!p) return set_error(&g_ens_setup_error, QPIR_E_PARAM, "params: NULL");
-  if (p->reserved != 0) return set_error(&g_ens_setup_error, QPIR_E_PARAM, "reserved: must be 0");
+  if (p->flags & ~QPIR_FLAG_STABLE_INPUTS)
+    return set_error(&g_ens_setup_error, QPIR_E_PARAM, "flags: unknown bits 0x%x", (unsigned)p->flags);
   if (p->n_records == 0) return set_error(&g_ens_setup_error, QPIR_E_DIMENSION, "n_records: 0");
   if (p->rec_bytes == 0 || p->rec_bytes > 16384)
     return set_error(&g_ens_setup_error, QPIR_E_DIMENSION, "rec_bytes: %llu not in [1, 16384]",
@@ -214,6 +216,7 @@ int qpir_ens_setup(const qpir_ens_params* p, const uint8_t* records, uint64_t re
   ctx->pdl = env_int("QPIR_ENS_PDL", 1);
   ctx->h2d_stream = env_int("QPIR_H2D_STREAM", 1);
   ctx->tc = env_int("QPIR_ENS_TC", -1);
+  ctx->flags = p->flags;
   ctx->mma_split = env_int("QPIR_MMA_SPLIT", 0);
   cudaStream_t st = (cudaStream_t)stream;
   if (cudaMalloc(&ctx->R, ctx->r * ctx->dp) != cudaSuccess) {
@@ -263,10 +266,14 @@ int qpir_ens_db_write(qpir_ens_ctx* ctx, uint64_t theta_begin, uint64_t n_record
 
 // One scan of rows [row_lo, row_hi) selected by share_dev, finalised in the
 // kernel: out_dev (device, d bytes) = init_dev ^ XOR of the selected rows.
+// early: the share was not written by the kernel preceding this launch (staged
+// by the library from host memory, or QPIR_FLAG_STABLE_INPUTS): the scan may
+// run before griddepcontrol.wait.
 static int scan_range(qpir_ens_ctx* ctx, EnsArena& ar, const uint8_t* share_dev,
                       uint64_t row_lo, uint64_t row_hi, const uint8_t* init_dev,
-                      uint8_t* out_dev, cudaStream_t st) {
+                      uint8_t* out_dev, cudaStream_t st, bool early) {
   EnsArgs a;
+  a.early = early ? 1u : 0u;
   a.R = ctx->R;
   a.q = share_dev;
   a.out = ar.acc1;
@@ -368,7 +375,8 @@ int qpir_ens_answer(qpir_ens_ctx* ctx, const uint8_t* share, uint64_t len_share,
   rc = stage_ring(ctx, *ar, ar->r_share, share, nb, st, &qd, &slot);
   if (rc) return rc;
   uint8_t* od = wo ? out : ar->io_stage + ctx->d;
-  rc = scan_range(ctx, *ar, qd, 0, ctx->r, nullptr, od, st);
+  rc = scan_range(ctx, *ar, qd, 0, ctx->r, nullptr, od, st,
+                  qd != share || (ctx->flags & QPIR_FLAG_STABLE_INPUTS));
   if (rc) return rc;
   if (slot >= 0) ENS_CUDA(ctx, cudaEventRecord(ar->r_share.done[slot], st));
   if (!wo) {
@@ -413,7 +421,8 @@ int qpir_oop_answer(qpir_ens_ctx* ctx, uint32_t n_chunks, uint32_t server, const
   rc = stage_ring(ctx, *ar, ar->r_A, A, ctx->d, st, &Ad, &sA);
   if (rc) return rc;
   uint8_t* od = wo ? out : ar->io_stage + ctx->d;
-  rc = scan_range(ctx, *ar, qd, (uint64_t)server * k, (uint64_t)(server + 1) * k, Ad, od, st);
+  rc = scan_range(ctx, *ar, qd, (uint64_t)server * k, (uint64_t)(server + 1) * k, Ad, od, st,
+                  qd != q || (ctx->flags & QPIR_FLAG_STABLE_INPUTS));
   if (rc) return rc;
   if (sq >= 0) ENS_CUDA(ctx, cudaEventRecord(ar->r_q.done[sq], st));
   if (sA >= 0) ENS_CUDA(ctx, cudaEventRecord(ar->r_A.done[sA], st));
@@ -507,6 +516,7 @@ static int ens_batch_tc(qpir_ens_ctx* ctx, EnsArena& ar, const uint8_t* Qd, uint
   a.out_ld = (uint32_t)(ctx->dp / 4);
   a.B = (uint32_t)B;
   a.G16 = G16;
+  a.s_tstride = (uint64_t)G16 * 2048;
   a.s_tiles = (uint32_t)(Npad / (128ull * MS));
   a.w_tiles = (uint32_t)((ctx->dp + 32 * NT - 1) / (32 * NT));
   a.kblocks = (uint32_t)((ctx->r + EM_KB - 1) / EM_KB);

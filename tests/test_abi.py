@@ -55,7 +55,7 @@ def test_params_struct_layout_matches_header(L, tmp_path):
 
 def _params(L, **kw):
     p = dict(n_cells=1024, n_ch=16, rec_bytes=8, m=0, lwe_n=1024, log_q=32, log_p=8,
-             reserved0=0, seed_A=1, row_begin=0, row_end=0, device=0, reserved1=0)
+             reserved0=0, seed_A=1, row_begin=0, row_end=0, device=0, flags=0)
     p.update(kw)
     return L.qpir_params(**p)
 
@@ -67,7 +67,8 @@ def _params(L, **kw):
     (dict(n_cells=0), 2, "n_cells"),
     (dict(row_end=129), 2, "row_end"),
     (dict(row_begin=64, row_end=64), 2, "row_begin"),
-    (dict(reserved0=3), 1, "reserved"),
+    (dict(reserved0=3), 1, "reserved0"),
+    (dict(flags=6), 1, "flags"),
 ])
 def test_setup_validates_before_cuda(L, kw, code, field):
     with pytest.raises(L.QpirError) as ei:

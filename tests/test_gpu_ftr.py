@@ -16,8 +16,15 @@ def _P():
     return Pk
 
 
-@pytest.mark.parametrize("r,s,B", [(700, 33, 1), (1000, 24, 5), (3001, 200, 64), (70000, 16, 9)])
-def test_ftr_batch_matches_oracle(cuda_ok, r, s, B):
+@pytest.mark.parametrize("r,s,B", [(700, 33, 1), (1000, 24, 5), (3001, 200, 64), (70000, 16, 9),
+                                   (5000, 300, 128), (2000, 40, 129), (9000, 20, 300)])
+@pytest.mark.parametrize("fuse,split", [("1", "0"), ("0", "0"), ("1", "5")])
+def test_ftr_batch_matches_oracle(cuda_ok, r, s, B, fuse, split, monkeypatch):
+    """FTR batch vs the oracle; fuse = 1: the 2-limb split runs in the GEMM's
+    converter warps (any CTA converts any K-block, flags per K-block), with auto
+    or forced K-splits; B > 128 spans several N tiles of the limb operand."""
+    monkeypatch.setenv("QPIR_FTR_FUSE", fuse)
+    monkeypatch.setenv("QPIR_MMA_SPLIT", split)
     Pk = _P()
     rec = synth.uniform_u8_np(r + s, (r, s))
     Q = synth.uniform_u32_np(B + 3, (B, r)) % P
@@ -56,10 +63,14 @@ def test_ftr_end_to_end_reconstruct(cuda_ok):
         assert (got == rec[th]).all()
 
 
-def test_ftr_two_limb_exceptions(cuda_ok):
+@pytest.mark.parametrize("fuse", ["1", "0"])
+def test_ftr_two_limb_exceptions(cuda_ok, fuse, monkeypatch):
     """p <= 65537 runs on 2 byte limbs; for p = 65537 the residue 65536 is the one
     value 2 limbs cannot hold and goes through the exception list (cap entries per
-    query) or, past the cap, the rescan path.  Exact in every case."""
+    query) or, past the cap, the rescan path.  Exact in every case, with the
+    limb split fused into the GEMM (converter warps, fuse = 1) or as its own
+    kernel (fuse = 0)."""
+    monkeypatch.setenv("QPIR_FTR_FUSE", fuse)
     Pk = _P()
     r, s = 70001, 8  # 2 K-splits; cap = 64 + 4 * ceil-ish(r / p) = 72
     rec = synth.uniform_u8_np(21, (r, s))

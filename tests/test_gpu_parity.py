@@ -341,12 +341,17 @@ def test_c4_batch_sampled(cuda_ok, B):
     for j in (0, B - 1):
         assert (_u32(s.answer(Q[j])) == ANS[j]).all()
     s.close()
+    import time
+    t0 = time.time()
     X = synth.uniform_u32_np(27, (B, 40))             # 40 Freivalds rounds
     left = np.matmul(ANS.T, X)                         # uint32 matmul wraps mod 2^32
     V = np.ascontiguousarray(np.matmul(Q.T, X).T)      # (Q^T X)^T: 40 queries
+    print(f"[c4 B={B}] Freivalds left side {time.time() - t0:.1f} s", flush=True)
     for ch in range(n_ch):
         right = O.answer_batch(_channel_slab(seed, ch, n_cells, n_ch, d), V)
         assert (left[ch * d:(ch + 1) * d].T == right).all(), f"Freivalds fails in channel {ch}"
+        if ch % 10 == 0:
+            print(f"[c4 B={B}] channel {ch} done at {time.time() - t0:.1f} s", flush=True)
 
 
 @pytest.mark.slow
