@@ -10,6 +10,7 @@ import torch
 
 import synth
 from oracle import oracle as O
+from _exact import matmul_mod32  # exact float64-limb products (pinned in test_exact_helper.py)
 
 pytestmark = pytest.mark.gpu
 M32 = (1 << 32) - 1
@@ -325,9 +326,9 @@ def test_c4_batch_sampled(cuda_ok, B):
     """configs[3]: 65536 cells x 40 x 3072 = 8.05 GB, B concurrent queries;
     24 sampled rows exact for all B queries, + 2 columns == single answers,
     + Freivalds (40 rounds over Z_{2^32}, P8 of SURVEY 8(c)) on the FULL ANS:
-    ANS^T X == D (Q^T X) with the right side from the oracle, channel by
-    channel.  For a wrong product E != 0 (mod 2^32) a uniform column of X gives
-    E x == 0 with probability <= 1/2, so 40 columns miss with <= 2^-40."""
+    ANS^T X == D (Q^T X), channel by channel, both sides exact float64-limb
+    products (tests/_exact.py) of the oracle-packed D and the inputs.  For a
+    wrong product E != 0 (mod 2^32) a uniform column of X gives E x == 0 with probability <= 1/2, so 40 columns miss with <= 2^-40."""
     P = _srv()
     n_cells, n_ch, d = 65536, 40, 3072
     seed = 25
@@ -341,17 +342,12 @@ def test_c4_batch_sampled(cuda_ok, B):
     for j in (0, B - 1):
         assert (_u32(s.answer(Q[j])) == ANS[j]).all()
     s.close()
-    import time
-    t0 = time.time()
     X = synth.uniform_u32_np(27, (B, 40))             # 40 Freivalds rounds
-    left = np.matmul(ANS.T, X)                         # uint32 matmul wraps mod 2^32
-    V = np.ascontiguousarray(np.matmul(Q.T, X).T)      # (Q^T X)^T: 40 queries
-    print(f"[c4 B={B}] Freivalds left side {time.time() - t0:.1f} s", flush=True)
+    left = matmul_mod32(np.ascontiguousarray(ANS.T), X)          # ANS^T X (ell, 40)
+    V = np.ascontiguousarray(matmul_mod32(np.ascontiguousarray(Q.T), X).T)  # (Q^T X)^T
     for ch in range(n_ch):
-        right = O.answer_batch(_channel_slab(seed, ch, n_cells, n_ch, d), V)
-        assert (left[ch * d:(ch + 1) * d].T == right).all(), f"Freivalds fails in channel {ch}"
-        if ch % 10 == 0:
-            print(f"[c4 B={B}] channel {ch} done at {time.time() - t0:.1f} s", flush=True)
+        right = matmul_mod32(_channel_slab(seed, ch, n_cells, n_ch, d), np.ascontiguousarray(V.T))
+        assert (left[ch * d:(ch + 1) * d] == right).all(), f"Freivalds fails in channel {ch}"
 
 
 @pytest.mark.slow
@@ -374,12 +370,12 @@ def test_c5_hint_shard_sampled(cuda_ok):
     A = O.expand_A(seed_A, n_cells, n)
     assert (H[rows] == O.hint(Dr, A)).all()
     X = synth.uniform_u32_np(28, (n, 40))
-    left = np.matmul(H, X)
-    V = np.ascontiguousarray(np.matmul(A, X).T)        # (A X)^T
+    left = matmul_mod32(H, X)                          # H X (rows, 40)
+    AX = matmul_mod32(A, X)                            # A X (m, 40)
     del A
     for ch in range((r1 - r0) // d):
-        right = O.answer_batch(_channel_slab(seed, ch, n_cells, n_ch, d), V)
-        assert (left[ch * d:(ch + 1) * d].T == right).all(), f"Freivalds fails in channel {ch}"
+        right = matmul_mod32(_channel_slab(seed, ch, n_cells, n_ch, d), AX)
+        assert (left[ch * d:(ch + 1) * d] == right).all(), f"Freivalds fails in channel {ch}"
 
 
 @pytest.mark.parametrize("cfg", [dict(), dict(QPIR_GEMV_SPLIT="7"), dict(QPIR_GEMV_PDL="0")])
