@@ -172,7 +172,10 @@ def build_db(P, wl, n_ch_total, row_begin, row_end, seed, device, lwe_n=1024):
     import synth
     n_cells, d = wl["n_cells"], wl["d"]
     s = P.PirServer(n_cells, n_ch_total, d, lwe_n=lwe_n, seed_A=0x5EED, row_begin=row_begin,
-                    row_end=row_end, device=device)
+                    row_end=row_end, device=device, stable_inputs=True)
+    # stable_inputs: the timed loops answer device queries written (and
+    # synchronised) before the loop, never by the kernel right before an answer
+    # call, so the scan may start before griddepcontrol.wait (include/qpir.h)
     n_rec = n_cells * n_ch_total
     chunk = max(1, (256 << 20) // d)
     for t0 in range(0, n_rec, chunk):
@@ -405,7 +408,7 @@ def run_ens(args, wl, world, rank, local):
     n_cells, n_ch, d = wl["n_cells"], wl["n_ch"], wl["d"]
     r = n_cells * n_ch
     t0 = time.time()
-    srv = P.EnsServer(r, d, device=local)
+    srv = P.EnsServer(r, d, device=local, stable_inputs=True)
     chunk = max(1, (256 << 20) // d)
     for a in range(0, r, chunk):
         srv.db_write(a, synth.records(args.seed, a, min(chunk, r - a), d, n_ch, device=dev))
@@ -545,7 +548,7 @@ def run_oop(args, wl, rank, local):
     stream = torch.cuda.current_stream(dev)
     n_cells, n_ch, d, n = wl["n_cells"], wl["n_ch"], wl["d"], wl["n_chunks"]
     r = n_cells * n_ch
-    srv = P.EnsServer(r, d, device=local)
+    srv = P.EnsServer(r, d, device=local, stable_inputs=True)
     chunk = max(1, (256 << 20) // d)
     for a in range(0, r, chunk):
         srv.db_write(a, synth.records(args.seed, a, min(chunk, r - a), d, n_ch, device=dev))

@@ -420,33 +420,51 @@ __global__ void __launch_bounds__(CONV ? MMA_THREADS + MMA_CONV_THREADS : MMA_TH
         if (live) {
           const uint32_t c0 = kb * (16 * GPB) + 4 * cl;
           const uint32_t g = c0 >> 4;
-          for (uint32_t j = cw; j < nq; j += 4) {
-            uint32_t v[4] = {0u, 0u, 0u, 0u};
-            if (j < a.qB) {
-              const uint32_t* row = a.Q + (size_t)j * a.qm;
-              if (vec && c0 + 4 <= a.qm) {
-                const uint4 x = __ldg(reinterpret_cast<const uint4*>(row + c0));
-                v[0] = x.x; v[1] = x.y; v[2] = x.z; v[3] = x.w;
-              } else {
+          // CU queries per batch: their loads are all in flight before the
+          // first is used (one load per warp at a time left the converters
+          // latency-bound: 0.5 ms per FTR call instead of the GEMM's 0.2 ms)
+          constexpr uint32_t CU = 8;
+          for (uint32_t jb0 = cw; jb0 < nq; jb0 += 4 * CU) {
+            uint4 x[CU];
 #pragma unroll
-                for (int e = 0; e < 4; ++e) v[e] = (c0 + e < a.qm) ? __ldg(row + c0 + e) : 0u;
-              }
-#pragma unroll
-              for (int e = 0; e < 4; ++e) {
-                v[e] = fastmod_u32(v[e], a.pM, a.p);
-                if (v[e] == 65536u && a.exc_cnt) {  // p = 65537 only; padding cells are 0
-                  const uint32_t idx = atomicAdd(a.exc_cnt + j, 1u);
-                  if (idx < a.exc_cap) a.exc_list[(size_t)j * a.exc_cap + idx] = c0 + e;
-                  v[e] = 0u;
+            for (uint32_t u = 0; u < CU; ++u) {
+              const uint32_t j = jb0 + 4 * u;
+              x[u] = make_uint4(0u, 0u, 0u, 0u);
+              if (j < a.qB) {
+                const uint32_t* row = a.Q + (size_t)j * a.qm;
+                if (vec && c0 + 4 <= a.qm) {
+                  x[u] = __ldg(reinterpret_cast<const uint4*>(row + c0));
+                } else {
+                  x[u].x = (c0 + 0 < a.qm) ? __ldg(row + c0 + 0) : 0u;
+                  x[u].y = (c0 + 1 < a.qm) ? __ldg(row + c0 + 1) : 0u;
+                  x[u].z = (c0 + 2 < a.qm) ? __ldg(row + c0 + 2) : 0u;
+                  x[u].w = (c0 + 3 < a.qm) ? __ldg(row + c0 + 3) : 0u;
                 }
               }
             }
-            const uint32_t w0 = __byte_perm(__byte_perm(v[0], v[1], 0x0040), __byte_perm(v[2], v[3], 0x0040), 0x5410);
-            const uint32_t w1 = __byte_perm(__byte_perm(v[0], v[1], 0x0051), __byte_perm(v[2], v[3], 0x0051), 0x5410);
-            const uint32_t n0 = 2 * j;  // limb columns 2j, 2j + 1 (same BN panel: BN even)
-            uint8_t* dst = a.Bw + (((size_t)(n0 / BN) * a.G + g) * BN + (n0 % BN)) * 16 + (cl & 3) * 4;
-            *reinterpret_cast<uint32_t*>(dst) = w0;
-            *reinterpret_cast<uint32_t*>(dst + 16) = w1;
+#pragma unroll
+            for (uint32_t u = 0; u < CU; ++u) {
+              const uint32_t j = jb0 + 4 * u;
+              if (j >= nq) break;
+              uint32_t v[4] = {x[u].x, x[u].y, x[u].z, x[u].w};
+              if (j < a.qB) {
+#pragma unroll
+                for (int e = 0; e < 4; ++e) {
+                  v[e] = fastmod_u32(v[e], a.pM, a.p);
+                  if (v[e] == 65536u && a.exc_cnt) {  // p = 65537 only; padding cells are 0
+                    const uint32_t idx = atomicAdd(a.exc_cnt + j, 1u);
+                    if (idx < a.exc_cap) a.exc_list[(size_t)j * a.exc_cap + idx] = c0 + e;
+                    v[e] = 0u;
+                  }
+                }
+              }
+              const uint32_t w0 = __byte_perm(__byte_perm(v[0], v[1], 0x0040), __byte_perm(v[2], v[3], 0x0040), 0x5410);
+              const uint32_t w1 = __byte_perm(__byte_perm(v[0], v[1], 0x0051), __byte_perm(v[2], v[3], 0x0051), 0x5410);
+              const uint32_t n0 = 2 * j;  // limb columns 2j, 2j + 1 (same BN panel: BN even)
+              uint8_t* dst = a.Bw + (((size_t)(n0 / BN) * a.G + g) * BN + (n0 % BN)) * 16 + (cl & 3) * 4;
+              *reinterpret_cast<uint32_t*>(dst) = w0;
+              *reinterpret_cast<uint32_t*>(dst + 16) = w1;
+            }
           }
           __threadfence();
         }

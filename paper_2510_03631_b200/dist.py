@@ -60,7 +60,7 @@ class DistributedPIR:
 
     def __init__(self, n_cells: int, n_ch: int, rec_bytes: int, *, m: int = 0,
                  lwe_n: int = 1024, seed_A: int = 0, device: int | None = None,
-                 records=None, group=None):
+                 records=None, group=None, stable_inputs: bool = False):
         from . import PirServer
 
         self.group = group
@@ -73,7 +73,8 @@ class DistributedPIR:
         r0, r1 = self.bounds[self.rank]
         dev = torch.cuda.current_device() if device is None else device
         self.server = PirServer(n_cells, n_ch, rec_bytes, m=m, lwe_n=lwe_n, seed_A=seed_A,
-                                row_begin=r0, row_end=r1, device=dev, records=records)
+                                row_begin=r0, row_end=r1, device=dev, records=records,
+                                stable_inputs=stable_inputs)
 
     def answer(self, qu, gather: bool = True):
         a = self.server.answer(qu)
@@ -169,7 +170,7 @@ class DistributedEns:
     records of its shard; the d-byte partials are XOR-combined."""
 
     def __init__(self, n_records: int, rec_bytes: int, *, device: int | None = None,
-                 records=None, group=None):
+                 records=None, group=None, stable_inputs: bool = False):
         from . import EnsServer
 
         self.group = group
@@ -179,7 +180,8 @@ class DistributedEns:
         self.t0, self.t1 = shard_records(n_records, self.world, self.rank, align=8)
         dev = torch.cuda.current_device() if device is None else device
         local = None if records is None else records[self.t0:self.t1]
-        self.server = EnsServer(self.t1 - self.t0, rec_bytes, device=dev, records=local)
+        self.server = EnsServer(self.t1 - self.t0, rec_bytes, device=dev, records=local,
+                                stable_inputs=stable_inputs)
 
     def local_share(self, share_bits: torch.Tensor) -> torch.Tensor:
         """Slice of a full r-bit share for this shard (shards start on byte boundaries)."""

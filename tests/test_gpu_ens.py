@@ -170,8 +170,8 @@ def test_ens_db_write_and_c2_scale(cuda_ok):
 
 
 @pytest.mark.parametrize("r,d", [(20000, 3072), (50000, 64), (4099, 100)])
-@pytest.mark.parametrize("pdl", ["1", "0"])
-def test_ens_oop_back_to_back_no_sync(cuda_ok, r, d, pdl, monkeypatch):
+@pytest.mark.parametrize("pdl,stable", [("1", False), ("0", False), ("1", True)])
+def test_ens_oop_back_to_back_no_sync(cuda_ok, r, d, pdl, stable, monkeypatch):
     """Single-share answers and OOP online answers queued back to back on one
     stream (programmatic dependent launch lets each scan start while the previous
     one drains; the in-kernel finaliser re-zeroes the accumulator): every
@@ -186,7 +186,7 @@ def test_ens_oop_back_to_back_no_sync(cuda_ok, r, d, pdl, monkeypatch):
     shares = [_share(100 + i, r) for i in range(6)]
     qs = [_share(200 + i, k) for i in range(6)]
     As = [synth.uniform_u8_np(300 + i, (d,)) for i in range(6)]
-    with P.EnsServer(r, d, records=rec) as s:
+    with P.EnsServer(r, d, records=rec, stable_inputs=stable) as s:
         st = torch.cuda.Stream()
         dev = [torch.from_numpy(x).cuda() for x in shares]
         dq = [torch.from_numpy(x).cuda() for x in qs]

@@ -312,12 +312,15 @@ def test_c3_nationwide_sampled(cuda_ok):
 
 
 def _channel_slab(seed, ch, n_cells, n_ch, d):
-    """Rows [ch*d, (ch+1)*d) of D for m = n_cells (one row block, DESIGN R10):
-    the channel's records (synth, generated on the GPU only for speed) packed
-    by the oracle as a one-channel DB."""
+    """Rows [ch*d, (ch+1)*d) of D for m = n_cells (one row block, DESIGN R10:
+    D[ch*d + b][cell] = rec_{cell*n_ch + ch}[b]), i.e. the transpose of the
+    channel's records (synth, generated on the GPU only for speed).  That this
+    equals the oracle's pack of a one-channel DB is pinned in
+    tests/test_oracle.py::test_one_channel_pack_is_transpose; the oracle's
+    element-by-element pack is ~9 s per 201 MB channel, too slow for 40."""
     theta = torch.arange(n_cells, device="cuda", dtype=torch.int64) * n_ch + ch
     rec = synth.records_at(seed, theta, d, n_ch, 512).cpu().numpy()
-    return O.pack(rec, n_cells, 1, d, n_cells)
+    return np.ascontiguousarray(rec.T)
 
 
 @pytest.mark.slow
@@ -378,18 +381,23 @@ def test_c5_hint_shard_sampled(cuda_ok):
         assert (left[ch * d:(ch + 1) * d] == right).all(), f"Freivalds fails in channel {ch}"
 
 
+@pytest.mark.parametrize("stable", [False, True])
 @pytest.mark.parametrize("cfg", [dict(), dict(QPIR_GEMV_SPLIT="7"), dict(QPIR_GEMV_PDL="0")])
-def test_back_to_back_answers_pdl(cuda_ok, cfg, monkeypatch):
+def test_back_to_back_answers_pdl(cuda_ok, cfg, stable, monkeypatch):
     """Back-to-back GEMVs on one stream overlap under programmatic dependent
-    launch; split-K scratch and outputs must not race (every answer exact)."""
+    launch; split-K scratch and outputs must not race (every answer exact).
+    stable: QPIR_FLAG_STABLE_INPUTS (the queries were written before the loop),
+    the whole scan runs before griddepcontrol.wait -- the bench's setting."""
     for k, v in cfg.items():
         monkeypatch.setenv(k, v)
     P = _srv()
     n_cells, n_ch, d = 4096, 8, 64
     rec, D = _db(n_cells, n_ch, d, seed=40)
     Qs = [synth.uniform_u32_np(41 + i, (n_cells,)) for i in range(24)]
-    with P.PirServer(n_cells, n_ch, d, records=torch.from_numpy(rec).cuda()) as s:
+    with P.PirServer(n_cells, n_ch, d, records=torch.from_numpy(rec).cuda(),
+                     stable_inputs=stable) as s:
         qd = [torch.from_numpy(q.view(np.int32)).cuda() for q in Qs]
+        torch.cuda.synchronize()
         same = torch.empty(s.ell_local, dtype=torch.int32, device="cuda")
         outs = []
         for i, q in enumerate(qd):

@@ -95,6 +95,14 @@ def test_pack_places_records():
     assert D[2 * n_ch * d:, 2:].sum() == 0
 
 
+@pytest.mark.parametrize("n_cells,d", [(7, 5), (64, 48)])
+def test_one_channel_pack_is_transpose(n_cells, d):
+    """R10 with n_ch = 1 and m = n_cells: D[b][cell] = rec_cell[b], i.e. D = rec^T
+    (the full-size Freivalds tests build their right side this way)."""
+    rec = synth.uniform_u8_np(6 + d, (n_cells, d))
+    assert (O.pack(rec, n_cells, 1, d, n_cells) == rec.T).all()
+
+
 # ------------------------------------------------------------------ answer
 def _np_answer(D, qu):
     # numpy integer matmul (non-BLAS loop in uint32: wraps mod 2^32)
