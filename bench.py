@@ -497,7 +497,7 @@ def run_ens(args, wl, world, rank, local):
             roof_tc = {"bound": "hbm", "achieved": round(ach_h, 1), "peak": hbm, "unit": "GB/s",
                        "frac": round(ach_h / hbm, 4), "tensor_frac": round(ach_t / t_peak, 4)}
         roof_tc.update({"traffic": _traffic(args.workload),
-                        "kernel": "ens_share_expand_kernel + qpir_ens_mma_kernel",
+                        "kernel": "ens_share_pack_kernel + qpir_ens_mma_ts_kernel (shares in TMEM)",
                         "kernel_ms": round(ms, 5),
                         "peak_source": f"{peak_src} (int8 = 2 x bf16 burst)",
                         "algorithmic_bytes_per_launch": meth_bytes,

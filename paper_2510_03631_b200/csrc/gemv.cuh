@@ -109,18 +109,20 @@ struct GemvArgs {
   uint32_t split_major; // 1: blockIdx.x = split, blockIdx.y = row block (page-local order)
   uint32_t pf256;       // 1: L2::256B prefetch hint on the D loads
   uint32_t l2pf;        // 1: bulk L2 prefetch of the CTA's D slice before griddepcontrol.wait
-  uint32_t early;       // 1: qu is not the previous kernel's output: scan before the wait
 };
 
 // U rows per thread (rows r, r + 128, ...); UNR column groups per iteration.
-template <int U, int UNR>
+// EARLY: qu is not the previous kernel's output (see below); a separate
+// instantiation, so its loop is the plain load-then-use loop (a runtime flag
+// with the D loads hoisted out of the first iteration cost 5 % on C2).
+template <int U, int UNR, bool EARLY>
 __global__ void __launch_bounds__(GEMV_THREADS) qpir_gemv_u8_u32_kernel(GemvArgs a) {
   extern __shared__ uint4 sL[];
   // Programmatic dependent launch: the next query's GEMV may start while this
   // grid drains; only the previous kernel's writes are visible after
   // griddepcontrol.wait.  Before the wait a CTA touches only the D shard
   // (library-owned; right after a device-side db_write the GEMV is launched
-  // without PDL, qpir.cu) -- unless a.early: then qu is known not to come from
+  // without PDL, qpir.cu) -- unless EARLY: then qu is known not to come from
   // the previous kernel (staged by the library from host memory, or the caller
   // set QPIR_FLAG_STABLE_INPUTS) and the whole scan runs before the wait.
   // Every global write (partials, tickets, ans) comes after the wait.
@@ -158,17 +160,19 @@ __global__ void __launch_bounds__(GEMV_THREADS) qpir_gemv_u8_u32_kernel(GemvArgs
                             : ldg_stream_v4(Drow[u] + (size_t)(g + i) * gstride);
   };
 
-  // ---- before the wait: D only (first UNR groups in flight; optional bulk L2
-  // prefetch of the whole slice)
-  if (a.l2pf && tid < U) {
-    const uint32_t r = rblk * (GEMV_THREADS * U) + tid * GEMV_THREADS;
-    if (r < a.ell_local)
-      l2_prefetch_bulk(a.D + (size_t)(r >> 7) * a.G * 2048 + (size_t)gb * gstride,
-                       (ge - gb) * (uint32_t)gstride);
-  }
   uint4 d[UNR][U];
-  load(gb, d);
-  if (!a.early) asm volatile("griddepcontrol.wait;" ::: "memory");  // qu may be the previous grid's output
+  if constexpr (!EARLY) {
+    // ---- before the wait: D only (first UNR groups in flight; optional bulk
+    // L2 prefetch of the whole slice)
+    if (a.l2pf && tid < U) {
+      const uint32_t r = rblk * (GEMV_THREADS * U) + tid * GEMV_THREADS;
+      if (r < a.ell_local)
+        l2_prefetch_bulk(a.D + (size_t)(r >> 7) * a.G * 2048 + (size_t)gb * gstride,
+                         (ge - gb) * (uint32_t)gstride);
+    }
+    load(gb, d);
+    asm volatile("griddepcontrol.wait;" ::: "memory");  // qu may be the previous grid's output
+  }
 
   for (uint32_t cb = gb; cb < ge; cb += a.chunk) {
     const uint32_t ce = min(ge, cb + a.chunk);
@@ -177,7 +181,7 @@ __global__ void __launch_bounds__(GEMV_THREADS) qpir_gemv_u8_u32_kernel(GemvArgs
     __syncthreads();
 #pragma unroll 1
     for (uint32_t g = cb; g < ce; g += UNR) {
-      if (g != gb) load(g, d);
+      if (EARLY || g != gb) load(g, d);
 #pragma unroll
       for (int i = 0; i < UNR; ++i) {
         const uint4* l = sL + (size_t)(g + i - cb) * 4;
@@ -187,7 +191,7 @@ __global__ void __launch_bounds__(GEMV_THREADS) qpir_gemv_u8_u32_kernel(GemvArgs
       }
     }
   }
-  if (a.early) asm volatile("griddepcontrol.wait;" ::: "memory");  // before any global write
+  if constexpr (EARLY) asm volatile("griddepcontrol.wait;" ::: "memory");  // before any global write
 
   uint32_t out[U];
 #pragma unroll

@@ -420,10 +420,10 @@ __global__ void __launch_bounds__(CONV ? MMA_THREADS + MMA_CONV_THREADS : MMA_TH
         if (live) {
           const uint32_t c0 = kb * (16 * GPB) + 4 * cl;
           const uint32_t g = c0 >> 4;
-          // CU queries per batch: their loads are all in flight before the
+          // CU queries per batch (32: all of a warp's, nq = 128): their loads are all in flight before the
           // first is used (one load per warp at a time left the converters
           // latency-bound: 0.5 ms per FTR call instead of the GEMM's 0.2 ms)
-          constexpr uint32_t CU = 8;
+          constexpr uint32_t CU = 32;
           for (uint32_t jb0 = cw; jb0 < nq; jb0 += 4 * CU) {
             uint4 x[CU];
 #pragma unroll

@@ -106,7 +106,8 @@ struct qpir_ctx {
   int mma_gpb = 8;     // env QPIR_MMA_GPB (column groups per pipeline stage: 4 or 8)
   int modp3 = 1;       // env QPIR_MODP3 (3 limbs per query for p < 2^24)
   int modp2 = 1;       // env QPIR_MODP2 (2 limbs per query for p <= 65537)
-  int ftr_fuse = 1;    // env QPIR_FTR_FUSE (2-limb split inside the GEMM: converter warps)
+  int ftr_fuse = 0;    // env QPIR_FTR_FUSE (2-limb split inside the GEMM: converter warps; measured
+                       // 0.29 vs 0.27 ms for the separate split kernel on ftr-c2-b128, so off)
   int h2d_stream = 1;  // env QPIR_H2D_STREAM (host inputs copied on a side stream)
   int mma_ls = 16;     // env QPIR_MMA_LOCKSTEP: K-blocks per lockstep chunk (0 = off)
   int mma_drift = 1;   // env QPIR_MMA_DRIFT: chunks a CTA may run ahead of its wave
@@ -339,9 +340,8 @@ int launch_gemv(qpir_ctx* ctx, const uint32_t* qu, uint32_t* ans, cudaStream_t s
   a.split_major = (ctx->gemv_order == 1 && rb <= 65535) ? 1u : 0u;
   a.pf256 = ctx->gemv_pf256 ? 1u : 0u;
   a.l2pf = ctx->gemv_l2pf ? 1u : 0u;
-  a.early = early ? 1u : 0u;
   const size_t smem = (size_t)chunk * 64;
-  auto kern = qpir_gemv_u8_u32_kernel<U, UNR>;
+  auto kern = early ? qpir_gemv_u8_u32_kernel<U, UNR, true> : qpir_gemv_u8_u32_kernel<U, UNR, false>;
   if (smem > 48 * 1024)
     CUDA_TRY(ctx, cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   const dim3 grid = a.split_major ? dim3(S, rb) : dim3(rb, S);
@@ -478,7 +478,7 @@ int qpir_setup(const qpir_params* params, const uint8_t* records, uint64_t recor
   ctx->mma_gpb = env_int("QPIR_MMA_GPB", 8);
   ctx->modp3 = env_int("QPIR_MODP3", 1);
   ctx->modp2 = env_int("QPIR_MODP2", 1);
-  ctx->ftr_fuse = env_int("QPIR_FTR_FUSE", 1);
+  ctx->ftr_fuse = env_int("QPIR_FTR_FUSE", 0);
   ctx->h2d_stream = env_int("QPIR_H2D_STREAM", 1);
   ctx->mma_ls = env_int("QPIR_MMA_LOCKSTEP", 16);
   ctx->mma_drift = env_int("QPIR_MMA_DRIFT", 1);

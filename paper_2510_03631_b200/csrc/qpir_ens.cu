@@ -73,6 +73,7 @@ struct qpir_ens_ctx {
   int tc = -1;                  // env QPIR_ENS_TC: -1 auto, 0 CUDA cores, 1 tensor cores
   int flags = 0;                // qpir_ens_params.flags (QPIR_FLAG_STABLE_INPUTS)
   int mma_split = 0;            // env QPIR_MMA_SPLIT (0 = auto)
+  int ts = 1;                   // env QPIR_ENS_TS: bit-rows in TMEM (1) or shared memory (0)
   std::atomic<uint64_t> launches{0};
   std::atomic<int> last_path{QPIR_ENS_PATH_NONE};
   int rows_per_cta = 0;       // env QPIR_ENS_ROWS (0 = auto)
@@ -218,6 +219,7 @@ int qpir_ens_setup(const qpir_ens_params* p, const uint8_t* records, uint64_t re
   ctx->tc = env_int("QPIR_ENS_TC", -1);
   ctx->flags = p->flags;
   ctx->mma_split = env_int("QPIR_MMA_SPLIT", 0);
+  ctx->ts = env_int("QPIR_ENS_TS", 1);
   cudaStream_t st = (cudaStream_t)stream;
   if (cudaMalloc(&ctx->R, ctx->r * ctx->dp) != cudaSuccess) {
     cudaGetLastError();
@@ -488,8 +490,63 @@ static cudaError_t ens_mma_launch(qpir_ens_ctx* ctx, EnsMmaArgs a, cudaStream_t 
   return cudaGetLastError();
 }
 
+template <uint32_t S, uint32_t SA, uint32_t RS>
+static cudaError_t ens_mma_ts_launch(qpir_ens_ctx* ctx, EnsMmaArgs a, cudaStream_t st) {
+  using C = EtCfg<S, SA, RS>;
+  auto kern = qpir_ens_mma_ts_kernel<S, SA, RS>;
+  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::TOTAL);
+  if (e != cudaSuccess) return e;
+  const uint32_t units = a.s_tiles * a.w_tiles * a.splits;
+  kern<<<std::min<uint32_t>(units, (uint32_t)ctx->num_sms), ET_THREADS, C::TOTAL, st>>>(a);
+  return cudaGetLastError();
+}
+
 static int ens_batch_tc(qpir_ens_ctx* ctx, EnsArena& ar, const uint8_t* Qd, uint64_t B,
                         cudaStream_t st) {
+  if (ctx->ts) {
+    // shares in TMEM (ens_mma.cuh, TS form): units of 128 shares x 32 record bytes
+    const uint32_t rows64 = (uint32_t)((ctx->r + 63) / 64);
+    const uint32_t ld = (uint32_t)round_up(B, 128ull);
+    int rc = grow(ctx, (void**)&ar.Qb, &ar.Qb_bytes, (uint64_t)rows64 * ld * 8);
+    if (rc) return rc;
+    unsigned long long* Qp = reinterpret_cast<unsigned long long*>(ar.Qb);
+    {
+      const uint32_t gy = std::min<uint32_t>(rows64, 65535);
+      const uint32_t gz = (rows64 + gy - 1) / gy;
+      dim3 grid(ld / 128, gy, gz);
+      ens_share_pack_kernel<<<grid, 128, 0, st>>>(Qd, (uint32_t)B, ctx->r, (ctx->r + 7) / 8, Qp,
+                                                  rows64, ld);
+      ENS_LAUNCHED(ctx);
+    }
+    EnsMmaArgs a;
+    a.R = ctx->R;
+    a.Qb = nullptr;
+    a.Qp = Qp;
+    a.qp_ld = ld;
+    a.qp_rows = rows64;
+    a.out = ar.acc;
+    a.r = ctx->r;
+    a.dp = (uint32_t)ctx->dp;
+    a.out_ld = (uint32_t)(ctx->dp / 4);
+    a.B = (uint32_t)B;
+    a.G16 = 0;
+    a.s_tstride = 0;
+    a.s_tiles = ld / 128;
+    a.w_tiles = (uint32_t)((ctx->dp + 31) / 32);
+    a.kblocks = (uint32_t)((ctx->r + ET_KB - 1) / ET_KB);
+    const uint32_t tiles = a.s_tiles * a.w_tiles;
+    a.splits = mma_choose_splits(tiles, a.kblocks, (uint32_t)ctx->num_sms, ctx->mma_split, 1,
+                                 (double)B * ctx->dp, (double)ET_KB * 32 * ctx->num_sms, false);
+    a.kbps = (a.kblocks + a.splits - 1) / a.splits;
+    a.splits = (a.kblocks + a.kbps - 1) / a.kbps;
+    if (a.splits > 1) ENS_CUDA(ctx, cudaMemsetAsync(ar.acc, 0, B * ctx->dp, st));
+    const cudaError_t e = ens_mma_ts_launch<4, 8, 8>(ctx, a, st);
+    if (e != cudaSuccess)
+      return ENS_FAIL(ctx, QPIR_E_CUDA, "tcgen05 GF(2) GEMM (TS): %s", cudaGetErrorString(e));
+    ctx->launches++;
+    ctx->last_path = QPIR_ENS_PATH_TENSOR;
+    return QPIR_OK;
+  }
   // MS share tiles of 128 x NT width tiles of 256 bit-rows (32 record bytes)
   // share the 512 TMEM columns: B <= 128 -> 1 x 2 (64 record bytes per unit),
   // larger B -> 2 x 1 (the expanded record slice feeds 256 shares).

@@ -51,13 +51,15 @@ def test_ens_answer_matches_oracle(cuda_ok, r, d, rows, group, wide, monkeypatch
 
 
 @pytest.mark.parametrize("B", [1, 7, 64, 128, 130, 256, 300])
-@pytest.mark.parametrize("tc", ["0", "1"])
+@pytest.mark.parametrize("tc", ["0", "1", "ss"])
 def test_ens_batch_matches_oracle(cuda_ok, B, tc, monkeypatch):
-    """tc = 1: GF(2) product on tcgen05 (records expanded on chip into weighted
-    bit-rows, ens_mma.cuh; B <= 128: one share tile x 64 record bytes per unit,
-    B > 128: two share tiles x 32 bytes, B > 256: several share-tile groups);
-    tc = 0: CUDA-core predicated-XOR kernel."""
-    monkeypatch.setenv("QPIR_ENS_TC", tc)
+    """tc = 1: GF(2) product on tcgen05 with the bit-rows in TMEM (A operand
+    written by tcgen05.st, ens_mma.cuh TS form; units of 128 shares x 32 record
+    bytes, B > 128: several share tiles); tc = ss: the shared-memory form (B <=
+    128: one share tile x 64 record bytes per unit, B > 128: two share tiles x
+    32 bytes); tc = 0: CUDA-core predicated-XOR kernel."""
+    monkeypatch.setenv("QPIR_ENS_TC", "0" if tc == "0" else "1")
+    monkeypatch.setenv("QPIR_ENS_TS", "0" if tc == "ss" else "1")
     P = _P()
     r, d = 3001, 200
     rec = synth.uniform_u8_np(5, (r, d))
@@ -65,18 +67,20 @@ def test_ens_batch_matches_oracle(cuda_ok, B, tc, monkeypatch):
     want = O.ens_respond_batch(rec, Q)
     with P.EnsServer(r, d, records=torch.from_numpy(rec).cuda()) as s:
         got = s.answer_batch(Q).cpu().numpy()
-        assert s.last_path == ("tensor" if tc == "1" else "cuda_cores")
+        assert s.last_path == ("cuda_cores" if tc == "0" else "tensor")
         assert (got == want).all()
         assert (s.answer(Q[B // 2]).cpu().numpy() == want[B // 2]).all()
         assert s.last_path == "scan"
 
 
-def test_ens_tc_extreme_bits(cuda_ok, monkeypatch):
+@pytest.mark.parametrize("ts", ["1", "0"])
+def test_ens_tc_extreme_bits(cuda_ok, ts, monkeypatch):
     """Tensor-core path on all-0xFF records and all-ones shares: every bit-row
     count is r (accumulated as r * 2^i for bit i, up to r * 128), so the
     response is all-ones iff r is odd -- each weight 2^0..2^7 must land on its
     own bit; then unit shares return single records exactly."""
     monkeypatch.setenv("QPIR_ENS_TC", "1")
+    monkeypatch.setenv("QPIR_ENS_TS", ts)
     P = _P()
     for r in (4097, 4096):
         d = 77
@@ -108,11 +112,13 @@ def test_ens_bruteforce_reconstruct(cuda_ok):
         assert (O.ens_reconstruct(resp[t]) == rec[t]).all()
 
 
+@pytest.mark.parametrize("ts", ["1", "0"])
 @pytest.mark.parametrize("split", ["0", "3"])
-def test_ens_tc_ragged_and_split(cuda_ok, split, monkeypatch):
+def test_ens_tc_ragged_and_split(cuda_ok, split, ts, monkeypatch):
     """Ragged r / d (d not a multiple of 16, r not of 128) and forced K-splits
     (parities combined with atomicXor) on the tensor-core path."""
     monkeypatch.setenv("QPIR_ENS_TC", "1")
+    monkeypatch.setenv("QPIR_ENS_TS", ts)
     monkeypatch.setenv("QPIR_MMA_SPLIT", split)
     P = _P()
     for r, d, B in [(70001, 5, 33), (1000, 37, 40), (4097, 3072, 17)]:
