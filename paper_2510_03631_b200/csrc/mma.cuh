@@ -84,6 +84,12 @@ struct MmaArgs {
   // feeding UBLKCP: an illegal address for the second D panel; see
   // tools/sass_counts.py, which checks every build for that pattern).
   uint64_t a_pstride, b_tstride;
+  // L2 eviction hints on the bulk copies (bit 0: A = D panels evict_first,
+  // bit 1: B tiles evict_last), meant to keep a split's B K range L2-resident
+  // across the waves of that split.  Measured on the C5 hint with 12-24 splits:
+  // DRAM reads unchanged (12.1 GB/launch) and slower than 2 splits, so off
+  // (profiles/r02_c5_l2_experiments.md).
+  uint32_t l2hint = 0;
   // Fused limb split (OUT_MODP2, CONV kernels): converter warps build the B
   // operand (reduced 2-limb planes) from the u32 queries while the GEMM runs.
   // Conversion chunks = K-blocks, taken from a global work counter (so every
@@ -201,6 +207,8 @@ __global__ void __launch_bounds__(CONV ? MMA_THREADS + MMA_CONV_THREADS : MMA_TH
     if (lane == 0) {
       uint32_t stage = 0, phase = 0, wave = 0;
       const uint32_t LS = a.kprog ? a.ls_chunk : 0u;
+      const uint64_t polA = (a.l2hint & 1u) ? l2_policy_evict_first() : l2_policy_evict_normal();
+      const uint64_t polB = (a.l2hint & 2u) ? l2_policy_evict_last() : l2_policy_evict_normal();
       for (uint32_t u = blockIdx.x; u < num_units; u += gridDim.x, ++wave) {
         uint32_t mt, nt, kb0, kb1;
         decode(u, mt, nt, kb0, kb1);
@@ -226,13 +234,13 @@ __global__ void __launch_bounds__(CONV ? MMA_THREADS + MMA_CONV_THREADS : MMA_TH
 #pragma unroll
           for (uint32_t p = 0; p < MT; ++p) {
             const uint64_t panel = (uint64_t)mt * MT + p;
-            bulk_g2s(dst + p * C::PANEL_BYTES,
-                     a.A + panel * a.a_pstride + (uint64_t)kb * (GPB * 2048), C::PANEL_BYTES,
-                     &full[stage]);
+            const uint8_t* src = a.A + panel * a.a_pstride + (uint64_t)kb * (GPB * 2048);
+            if (a.l2hint) bulk_g2s_hint(dst + p * C::PANEL_BYTES, src, C::PANEL_BYTES, &full[stage], polA);
+            else bulk_g2s(dst + p * C::PANEL_BYTES, src, C::PANEL_BYTES, &full[stage]);
           }
-          bulk_g2s(dst + C::A_BYTES,
-                   a.B + (uint64_t)nt * a.b_tstride + (uint64_t)kb * (GPB * BN * 16), C::B_BYTES,
-                   &full[stage]);
+          const uint8_t* srcB = a.B + (uint64_t)nt * a.b_tstride + (uint64_t)kb * (GPB * BN * 16);
+          if (a.l2hint) bulk_g2s_hint(dst + C::A_BYTES, srcB, C::B_BYTES, &full[stage], polB);
+          else bulk_g2s(dst + C::A_BYTES, srcB, C::B_BYTES, &full[stage]);
           if (++stage == STAGES) { stage = 0; phase ^= 1; }
           if (LS && ((kb - kb0) % LS == LS - 1 || kb + 1 == kb1))
             atomicAdd(issued, 1u);  // chunk issued

@@ -33,6 +33,7 @@ struct MmaJob {
   uint32_t* kprog = nullptr;   // K-lockstep scratch (kprog_cap u32), nullptr = off
   uint32_t kprog_cap = 0;
   uint32_t ls_chunk = 0, ls_drift = 1;  // K-blocks per lockstep chunk (0 = off)
+  uint32_t l2hint = 0;                  // MmaArgs::l2hint
   // fused limb split (OUT_MODP2, gpb 8): converter warps build B from the u32
   // queries inside the GEMM (mma.cuh CONV); B is then the writable Q' buffer
   bool conv = false;
@@ -138,6 +139,7 @@ cudaError_t mma_launch_cfg(const MmaJob& j, cudaStream_t st, uint64_t* launches)
   a.kprog = ls ? j.kprog : nullptr;
   a.ls_chunk = j.ls_chunk;
   a.ls_drift = std::max<uint32_t>(1, j.ls_drift);
+  a.l2hint = j.l2hint;
   cudaError_t e = cudaSuccess;
   if (ls) e = cudaMemsetAsync(j.kprog, 0, waves * 8, st);
   if (e != cudaSuccess) return e;

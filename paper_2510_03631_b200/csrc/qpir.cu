@@ -102,6 +102,7 @@ struct qpir_ctx {
   int flags = 0;       // qpir_params.flags (QPIR_FLAG_STABLE_INPUTS)
   std::atomic<bool> d_written{false};  // a device db_write is queued: next GEMV without PDL
   int mma_mt = 2;      // env QPIR_MMA_MT (1 or 2 row panels per CTA tile)
+  int mma_l2hint = 0;  // env QPIR_MMA_L2HINT (MmaArgs::l2hint)
   int mma_split = 0;   // env QPIR_MMA_SPLIT (0 = auto)
   int mma_gpb = 8;     // env QPIR_MMA_GPB (column groups per pipeline stage: 4 or 8)
   int modp3 = 1;       // env QPIR_MODP3 (3 limbs per query for p < 2^24)
@@ -398,6 +399,7 @@ int launch_mma(qpir_ctx* ctx, uint32_t BN, const uint8_t* Bl, uint32_t Npad, uin
   j.gpb = ctx->mma_gpb;
   j.out_prezeroed = prezeroed;
   j.exc = exc;
+  j.l2hint = (uint32_t)ctx->mma_l2hint;
   if (conv) {  // fused limb split (OUT_MODP2): the converter fields of the caller's job
     j.conv = true;
     j.Q = conv->Q;
@@ -474,6 +476,7 @@ int qpir_setup(const qpir_params* params, const uint8_t* records, uint64_t recor
   ctx->gemv_l2pf = env_int("QPIR_GEMV_L2PF", 0);
   ctx->flags = params->flags;
   ctx->mma_mt = env_int("QPIR_MMA_MT", 2);
+  ctx->mma_l2hint = env_int("QPIR_MMA_L2HINT", 0);
   ctx->mma_split = env_int("QPIR_MMA_SPLIT", 0);
   ctx->mma_gpb = env_int("QPIR_MMA_GPB", 8);
   ctx->modp3 = env_int("QPIR_MODP3", 1);
