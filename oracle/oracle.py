@@ -76,6 +76,8 @@ def lib():
         L.qo_oop_respond.argtypes = [_u8p, _u64, _u64, _u32, _u32, _u8p, _u8p, _u8p]
         L.qo_num_threads.restype = ctypes.c_int
         L.qo_set_num_threads.argtypes = [ctypes.c_int]
+        L.qo_hct_puzzle_gen.argtypes = [_u64, _u64, _u32, ctypes.c_uint8, _u8p]
+        L.qo_puzzle_bind_hct.argtypes = [_u8p, _u64, _u64, _u64, _u64, _u32, ctypes.c_uint8, _u64, _u8p]
         _lib = L
     return _lib
 
@@ -341,3 +343,28 @@ def num_threads() -> int:
 
 def set_num_threads(t: int) -> None:
     lib().qo_set_num_threads(t)
+
+
+# ------------------------------------------------------------------ NEXT-4
+HCT_PUZZLE_BYTES = 37     # 32-byte nonce + 4-byte kappa + 1-byte level
+SPECTRUM_BYTES = 560
+
+
+def hct_puzzle_gen(seed_psd: int, theta: int, kappa: int, n_l: int) -> np.ndarray:
+    """HCT.Puzzle.Gen of record theta -> 37 bytes (qo_hct_puzzle_gen)."""
+    out = np.zeros(HCT_PUZZLE_BYTES, np.uint8)
+    lib().qo_hct_puzzle_gen(seed_psd, theta, kappa, n_l, _p(out, _u8p))
+    return out
+
+
+def puzzle_bind_hct(spectrum: np.ndarray, theta0: int, seed_psd: int, kappa: int, n_l: int,
+                    d: int) -> np.ndarray:
+    """PSD.Puzzle.Bind (Alg. 1 step 1, P:553-566) over records theta0 .. theta0 + n - 1;
+    spectrum: n x >= 560 bytes.  Returns n x d records (signature slot zero)."""
+    sp = _c(spectrum, np.uint8)
+    assert sp.ndim == 2 and sp.shape[1] >= SPECTRUM_BYTES and d >= SPECTRUM_BYTES + HCT_PUZZLE_BYTES
+    n = sp.shape[0]
+    out = np.empty((n, d), np.uint8)
+    lib().qo_puzzle_bind_hct(_p(sp, _u8p), sp.shape[1], theta0, n, seed_psd, kappa, n_l, d,
+                             _p(out, _u8p))
+    return out

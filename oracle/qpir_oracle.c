@@ -611,3 +611,48 @@ void qo_oop_respond(const uint8_t *records, uint64_t B, uint64_t d, uint32_t n, 
     }
   }
 }
+
+/* ------------------------------------------------------------------ */
+/* NEXT-4: PSD.Puzzle.Bind with HCT puzzles (Alg. 1 step 1). */
+/* ------------------------------------------------------------------ */
+/* HCT.Puzzle.Gen(1^lambda, kappa): "randomly selects n_s <-$ {0,1}^lambda
+ * and sets the number of leaves n_l based on the difficulty level kappa; the
+ * puzzle is Pi = (h, n_s, kappa, n_l)".  Sizes: "a lambda-bit nonce
+ * (n_s), a 4-byte difficulty (kappa), and a 1-byte level (n_l), totaling 37
+ * bytes" -> lambda = 256.  Encoding (DESIGN R21): n_s || kappa (u32 LE) || n_l;
+ * h (the hash function) is fixed by the system, not stored; n_l is the caller's
+ * level byte (the paper gives no kappa -> n_l map).  Randomness (DESIGN R21):
+ * n_s word w (w = 0..7, little-endian) = Philox4x32-10(key = seed_psd,
+ * ctr = (theta_lo, theta_hi, w >> 2, 0x48))[w & 3]. */
+void qo_hct_puzzle_gen(uint64_t seed_psd, uint64_t theta, uint32_t kappa, uint8_t n_l,
+                       uint8_t out[37]) {
+  uint32_t key[2];
+  key_from_seed(seed_psd, key);
+  for (uint32_t w = 0; w < 8; ++w) {
+    uint32_t ctr[4] = {(uint32_t)(theta & 0xFFFFFFFFu), (uint32_t)(theta >> 32), w >> 2, 0x48u};
+    uint32_t r[4];
+    qo_philox4x32_10(ctr, key, r);
+    for (int b = 0; b < 4; ++b) out[4 * w + b] = (uint8_t)(r[w & 3] >> (8 * b));
+  }
+  for (int b = 0; b < 4; ++b) out[32 + b] = (uint8_t)(kappa >> (8 * b));
+  out[36] = n_l;
+}
+
+/* Puzzle.Bind over records theta0 .. theta0 + n - 1 (Alg. 1 step 1: for every
+ * theta, pi_theta <- Puzzle.Gen; sigma <- ML-DSA.Sign(sk, pi_theta);
+ * DB.Record(pi_theta, sigma)).  Record layout (DESIGN R11): bytes
+ * [0, 560) spectrum data (the caller's, row theta - theta0 of `spectrum`,
+ * stride spec_stride >= 560), [560, 597) pi_theta, [597, 3017) the ML-DSA
+ * signature slot -- ML-DSA is not implemented (no FIPS 204 implementation or
+ * KAT vectors in this environment), so the slot is left zero ("unsigned") --
+ * and zero from 3017 to d.  Requires d >= 597.  out: n x d bytes. */
+void qo_puzzle_bind_hct(const uint8_t *spectrum, uint64_t spec_stride, uint64_t theta0,
+                        uint64_t n, uint64_t seed_psd, uint32_t kappa, uint8_t n_l,
+                        uint64_t d, uint8_t *out) {
+  for (uint64_t i = 0; i < n; ++i) {
+    uint8_t *rec = out + i * d;
+    memset(rec, 0, (size_t)d);
+    memcpy(rec, spectrum + i * spec_stride, 560);
+    qo_hct_puzzle_gen(seed_psd, theta0 + i, kappa, n_l, rec + 560);
+  }
+}
