@@ -116,6 +116,24 @@ int qpir_setup(const qpir_params *params, const uint8_t *records,
 int qpir_db_write(qpir_ctx *ctx, uint64_t theta_begin, uint64_t n_records,
                   const uint8_t *records, uint64_t records_len, void *stream);
 
+/* NEXT-4: PSD.Puzzle.Bind with HCT puzzles, on the GPU (Alg. 1 step 1,
+ * PAPER.md:553-566; HCT.Puzzle.Gen PAPER.md:855; record layout PAPER.md:1686,
+ * DESIGN R11 / R21).  Builds records theta_begin .. theta_begin + n_records - 1
+ * and writes them into the shard exactly as qpir_db_write would:
+ *   record = spectrum row (its first 560 bytes) || n_s (32 B) || kappa (u32 LE)
+ *            || n_l (1 B) || zeros (the 2420-byte ML-DSA signature slot and the
+ *            padding: the DB is bound but NOT signed -- DESIGN R21)
+ * with the 256-bit nonce n_s word w = Philox4x32-10(key = seed_psd,
+ * ctr = (theta_lo, theta_hi, w >> 2, 0x48))[w & 3].
+ * spectrum: n_records rows of spec_stride >= 560 bytes, host or device
+ * (spectrum_len == n_records * spec_stride); requires rec_bytes >= 597.
+ * Errors: QPIR_E_DIMENSION (range, lengths, stride, rec_bytes), QPIR_E_PARAM
+ * (NULL spectrum).  Concurrency as qpir_db_write. */
+int qpir_puzzle_bind_hct(qpir_ctx *ctx, uint64_t theta_begin, uint64_t n_records,
+                         const uint8_t *spectrum, uint64_t spec_stride,
+                         uint64_t spectrum_len, uint64_t seed_psd, uint32_t kappa,
+                         uint8_t n_l, void *stream);
+
 /* Geometry: ell (all rows), m (columns), ell_local (= row_end - row_begin),
  * row_begin.  Any output pointer may be NULL. */
 int qpir_geometry(const qpir_ctx *ctx, uint64_t *ell, uint64_t *m,
@@ -194,6 +212,13 @@ int qpir_ens_setup(const qpir_ens_params *params, const uint8_t *records,
 /* Overwrite records theta_begin .. theta_begin + n_records - 1. */
 int qpir_ens_db_write(qpir_ens_ctx *ctx, uint64_t theta_begin, uint64_t n_records,
                       const uint8_t *records, uint64_t records_len, void *stream);
+
+/* NEXT-4 on an ENS context: as qpir_puzzle_bind_hct, the records written in
+ * place (theta-major rows). */
+int qpir_ens_puzzle_bind_hct(qpir_ens_ctx *ctx, uint64_t theta_begin, uint64_t n_records,
+                             const uint8_t *spectrum, uint64_t spec_stride,
+                             uint64_t spectrum_len, uint64_t seed_psd, uint32_t kappa,
+                             uint8_t n_l, void *stream);
 
 /* Response to one share (len_share == ceil(r/8)) -> out: d bytes (len_out == d).
  * A 4-byte-aligned device share may be read in whole 32-bit words (up to 3

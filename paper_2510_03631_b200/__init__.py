@@ -60,6 +60,16 @@ class PirServer:
         n = int(records.shape[0]) if records.ndim == 2 else records.numel() // self.rec_bytes
         _lib.qpir_db_write(self._ctx, theta_begin, records, n, _st(self.device, stream))
 
+    def puzzle_bind_hct(self, theta_begin: int, spectrum, seed_psd: int, kappa: int = 20,
+                        n_l: int = 3, stream=None) -> None:
+        """NEXT-4 PSD.Puzzle.Bind (Alg. 1 step 1): records theta_begin .. + len(spectrum)
+        built on the GPU (spectrum row || HCT puzzle || unsigned signature slot) and
+        written into the shard (include/qpir.h qpir_puzzle_bind_hct)."""
+        assert spectrum.ndim == 2 and str(spectrum.dtype) in ("uint8", "torch.uint8")
+        _lib.qpir_puzzle_bind_hct(self._ctx, theta_begin, spectrum, int(spectrum.shape[0]),
+                                  int(spectrum.shape[1]), seed_psd, kappa, n_l,
+                                  _st(self.device, stream))
+
     # ------------------------------------------------------------------ answers
     def _dev(self):
         return torch.device("cuda", self.device)
@@ -127,6 +137,14 @@ class EnsServer:
     def db_write(self, theta_begin: int, records, stream=None) -> None:
         n = int(records.shape[0]) if records.ndim == 2 else records.numel() // self.d
         _lib.qpir_ens_db_write(self._ctx, theta_begin, records, n, _st(self.device, stream))
+
+    def puzzle_bind_hct(self, theta_begin: int, spectrum, seed_psd: int, kappa: int = 20,
+                        n_l: int = 3, stream=None) -> None:
+        """NEXT-4 PSD.Puzzle.Bind on the ENS records (qpir_ens_puzzle_bind_hct)."""
+        assert spectrum.ndim == 2 and str(spectrum.dtype) in ("uint8", "torch.uint8")
+        _lib.qpir_ens_puzzle_bind_hct(self._ctx, theta_begin, spectrum, int(spectrum.shape[0]),
+                                      int(spectrum.shape[1]), seed_psd, kappa, n_l,
+                                      _st(self.device, stream))
 
     def answer(self, share, out=None, stream=None):
         if out is None:

@@ -32,6 +32,7 @@ EXPORTS = (
     "qpir_ens_kernel_launches", "qpir_ens_last_error", "qpir_ens_destroy",
     "qpir_oop_preprocess", "qpir_oop_answer", "qpir_ens_last_path",
     "qpir_xor_fold", "qpir_sum_mod_p", "qpir_combine_last_error",
+    "qpir_puzzle_bind_hct", "qpir_ens_puzzle_bind_hct",
 )
 
 # qpir_ens_last_path values (include/qpir.h)
@@ -104,6 +105,9 @@ _vp = ctypes.c_void_p
 _u64 = ctypes.c_uint64
 _L.qpir_setup.argtypes = [ctypes.POINTER(qpir_params), _vp, _u64, _vp, ctypes.POINTER(_vp)]
 _L.qpir_db_write.argtypes = [_vp, _u64, _u64, _vp, _u64, _vp]
+_L.qpir_puzzle_bind_hct.argtypes = [_vp, _u64, _u64, _vp, _u64, _u64, _u64, ctypes.c_uint32,
+                                    ctypes.c_uint8, _vp]
+_L.qpir_ens_puzzle_bind_hct.argtypes = _L.qpir_puzzle_bind_hct.argtypes
 _L.qpir_geometry.argtypes = [_vp, ctypes.POINTER(_u64), ctypes.POINTER(_u64),
                              ctypes.POINTER(_u64), ctypes.POINTER(_u64)]
 _L.qpir_answer.argtypes = [_vp, _vp, _u64, _vp, _u64, _vp]
@@ -197,6 +201,19 @@ def qpir_setup(params: qpir_params, records=None, stream=None) -> int:
 def qpir_db_write(ctx: int, theta_begin: int, records, n_records: int, stream=None):
     _check(_L.qpir_db_write(ctx, theta_begin, n_records, _addr(records), _numel(records),
                             _stream(stream)), ctx)
+
+
+def qpir_puzzle_bind_hct(ctx: int, theta_begin: int, spectrum, n_records: int, spec_stride: int,
+                         seed_psd: int, kappa: int, n_l: int, stream=None):
+    _check(_L.qpir_puzzle_bind_hct(ctx, theta_begin, n_records, _addr(spectrum), spec_stride,
+                                   _numel(spectrum), seed_psd, kappa, n_l, _stream(stream)), ctx)
+
+
+def qpir_ens_puzzle_bind_hct(ctx: int, theta_begin: int, spectrum, n_records: int,
+                             spec_stride: int, seed_psd: int, kappa: int, n_l: int, stream=None):
+    _check_ens(_L.qpir_ens_puzzle_bind_hct(ctx, theta_begin, n_records, _addr(spectrum),
+                                           spec_stride, _numel(spectrum), seed_psd, kappa, n_l,
+                                           _stream(stream)), ctx)
 
 
 def qpir_geometry(ctx: int):

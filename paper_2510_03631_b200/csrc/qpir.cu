@@ -21,6 +21,7 @@
 #include "gemv.cuh"
 #include "host_common.h"
 #include "mma_launch.cuh"
+#include "puzzle.cuh"
 
 using namespace qpir;
 using namespace qpir_host;
@@ -87,6 +88,8 @@ struct qpir_ctx {
   uint8_t* D = nullptr;            // 128-row panels [L/128][G][128][16]
   uint8_t* rec_stage = nullptr;    // host-record staging for db_write
   uint64_t rec_stage_bytes = 0;
+  uint8_t* spec_stage = nullptr;   // host spectrum staging for qpir_puzzle_bind_hct
+  uint64_t spec_stage_bytes = 0;
   std::mutex mu;                   // guards `arenas`
   std::map<cudaStream_t, Arena> arenas;
   uint64_t launches = 0;
@@ -551,6 +554,69 @@ int qpir_db_write(qpir_ctx* ctx, uint64_t theta_begin, uint64_t n_records,
   return QPIR_OK;
 }
 
+int qpir_puzzle_bind_hct(qpir_ctx* ctx, uint64_t theta_begin, uint64_t n_records,
+                         const uint8_t* spectrum, uint64_t spec_stride, uint64_t spectrum_len,
+                         uint64_t seed_psd, uint32_t kappa, uint8_t n_l, void* stream) {
+  NvtxRange nvtx_("qpir_puzzle_bind_hct");
+  if (!ctx) return fail(nullptr, QPIR_E_STATE, "ctx: NULL");
+  const Geometry& g = ctx->geo;
+  const uint64_t n_all = g.n_cells * g.n_ch;
+  if (g.d < HCT_SPECTRUM + HCT_PUZZLE)
+    return fail(ctx, QPIR_E_DIMENSION, "rec_bytes: %llu < 597 (560 B spectrum + 37 B puzzle)",
+                (unsigned long long)g.d);
+  if (theta_begin > n_all || n_records > n_all - theta_begin)
+    return fail(ctx, QPIR_E_DIMENSION, "theta range: [%llu, +%llu) exceeds %llu records",
+                (unsigned long long)theta_begin, (unsigned long long)n_records,
+                (unsigned long long)n_all);
+  if (spec_stride < HCT_SPECTRUM)
+    return fail(ctx, QPIR_E_DIMENSION, "spec_stride: %llu < 560", (unsigned long long)spec_stride);
+  if (spectrum_len != n_records * spec_stride)
+    return fail(ctx, QPIR_E_DIMENSION, "spectrum_len: %llu != %llu",
+                (unsigned long long)spectrum_len, (unsigned long long)(n_records * spec_stride));
+  if (n_records == 0) return QPIR_OK;
+  if (!spectrum) return fail(ctx, QPIR_E_PARAM, "spectrum: NULL");
+  DeviceGuard dg(ctx->device);
+  cudaStream_t st = (cudaStream_t)stream;
+  const int w = where(spectrum, ctx->device);
+  if (w < 0) return fail(ctx, QPIR_E_PARAM, "spectrum: device memory of another device");
+  // records are built in chunks of <= 64 MB into the db_write staging buffer,
+  // then packed into the shard (pack_records_kernel)
+  const uint64_t chunk = std::max<uint64_t>(1, (64ull << 20) / g.d);
+  int rc = ensure(ctx, (void**)&ctx->rec_stage, &ctx->rec_stage_bytes,
+                  std::min(n_records, chunk) * g.d);
+  if (rc) return rc;
+  if (w == 0) {
+    rc = ensure(ctx, (void**)&ctx->spec_stage, &ctx->spec_stage_bytes,
+                std::min(n_records, chunk) * spec_stride);
+    if (rc) return rc;
+  }
+  for (uint64_t t = 0; t < n_records; t += chunk) {
+    const uint64_t n = std::min(chunk, n_records - t);
+    const uint8_t* sp = spectrum + t * spec_stride;
+    if (w == 0) {
+      CUDA_TRY(ctx, cudaMemcpyAsync(ctx->spec_stage, sp, n * spec_stride, cudaMemcpyHostToDevice, st));
+      sp = ctx->spec_stage;
+    }
+    BindArgs b;
+    b.spectrum = sp;
+    b.spec_stride = spec_stride;
+    b.theta0 = theta_begin + t;
+    b.n = n;
+    b.seed_psd = seed_psd;
+    b.kappa = kappa;
+    b.n_l = n_l;
+    b.d = (uint32_t)g.d;
+    b.out = ctx->rec_stage;
+    b.out_stride = g.d;
+    launch_puzzle_bind(b, st);
+    LAUNCH_CHECK(ctx);
+    rc = db_write_device(ctx, theta_begin + t, n, ctx->rec_stage, st);
+    if (rc) return rc;
+  }
+  if (w == 0) CUDA_TRY(ctx, cudaStreamSynchronize(st));  // the staging buffers are reused per call
+  return QPIR_OK;
+}
+
 int qpir_geometry(const qpir_ctx* ctx, uint64_t* ell, uint64_t* m, uint64_t* ell_local,
                   uint64_t* row_begin) {
   if (!ctx) return QPIR_E_STATE;
@@ -843,7 +909,7 @@ const char* qpir_last_error(const qpir_ctx* ctx) {
 void qpir_destroy(qpir_ctx* ctx) {
   if (!ctx) return;
   DeviceGuard dg(ctx->device);
-  void* bufs[] = {ctx->D, ctx->rec_stage};
+  void* bufs[] = {ctx->D, ctx->rec_stage, ctx->spec_stage};
   for (void* b : bufs)
     if (b) cudaFree(b);
   for (auto& kv : ctx->arenas) {

@@ -14,6 +14,7 @@
 #include "ens_mma.cuh"
 #include "host_common.h"
 #include "mma_launch.cuh"
+#include "puzzle.cuh"
 
 using namespace qpir;
 using namespace qpir_host;
@@ -64,6 +65,9 @@ struct qpir_ens_ctx {
   int h2d_stream = 1;           // env QPIR_H2D_STREAM
   int device = 0, num_sms = 148;
   uint8_t* R = nullptr;         // [r][dp]
+  std::atomic<bool> r_written{false};  // a kernel wrote R (puzzle bind): next scan without PDL
+  uint8_t* spec_stage = nullptr;       // host spectrum staging (puzzle bind)
+  uint64_t spec_stage_bytes = 0;
   std::mutex mu;                // guards `arenas`
   std::map<cudaStream_t, EnsArena> arenas;
   int group = 0;                // env QPIR_ENS_GROUP (0 = auto 32; 1 = atomics only)
@@ -266,6 +270,62 @@ int qpir_ens_db_write(qpir_ens_ctx* ctx, uint64_t theta_begin, uint64_t n_record
   return QPIR_OK;
 }
 
+int qpir_ens_puzzle_bind_hct(qpir_ens_ctx* ctx, uint64_t theta_begin, uint64_t n_records,
+                             const uint8_t* spectrum, uint64_t spec_stride,
+                             uint64_t spectrum_len, uint64_t seed_psd, uint32_t kappa,
+                             uint8_t n_l, void* stream) {
+  NvtxRange nvtx_("qpir_ens_puzzle_bind_hct");
+  if (!ctx) return QPIR_E_STATE;
+  if (ctx->d < HCT_SPECTRUM + HCT_PUZZLE)
+    return ENS_FAIL(ctx, QPIR_E_DIMENSION, "rec_bytes: %llu < 597 (560 B spectrum + 37 B puzzle)",
+                    (unsigned long long)ctx->d);
+  if (theta_begin > ctx->r || n_records > ctx->r - theta_begin)
+    return ENS_FAIL(ctx, QPIR_E_DIMENSION, "theta range: [%llu, +%llu) exceeds %llu records",
+                    (unsigned long long)theta_begin, (unsigned long long)n_records,
+                    (unsigned long long)ctx->r);
+  if (spec_stride < HCT_SPECTRUM)
+    return ENS_FAIL(ctx, QPIR_E_DIMENSION, "spec_stride: %llu < 560", (unsigned long long)spec_stride);
+  if (spectrum_len != n_records * spec_stride)
+    return ENS_FAIL(ctx, QPIR_E_DIMENSION, "spectrum_len: %llu != %llu",
+                    (unsigned long long)spectrum_len, (unsigned long long)(n_records * spec_stride));
+  if (n_records == 0) return QPIR_OK;
+  if (!spectrum) return ENS_FAIL(ctx, QPIR_E_PARAM, "spectrum: NULL");
+  DeviceGuard dg(ctx->device);
+  const int w = where(spectrum, ctx->device);
+  if (w < 0) return ENS_FAIL(ctx, QPIR_E_PARAM, "spectrum: memory of another device");
+  cudaStream_t st = (cudaStream_t)stream;
+  const uint64_t chunk = w ? n_records : std::max<uint64_t>(1, (64ull << 20) / spec_stride);
+  if (!w) {
+    int rc = grow(ctx, (void**)&ctx->spec_stage, &ctx->spec_stage_bytes,
+                  std::min(n_records, chunk) * spec_stride);
+    if (rc) return rc;
+  }
+  for (uint64_t t = 0; t < n_records; t += chunk) {
+    const uint64_t n = std::min(chunk, n_records - t);
+    const uint8_t* sp = spectrum + t * spec_stride;
+    if (!w) {
+      ENS_CUDA(ctx, cudaMemcpyAsync(ctx->spec_stage, sp, n * spec_stride, cudaMemcpyHostToDevice, st));
+      sp = ctx->spec_stage;
+    }
+    BindArgs b;
+    b.spectrum = sp;
+    b.spec_stride = spec_stride;
+    b.theta0 = theta_begin + t;
+    b.n = n;
+    b.seed_psd = seed_psd;
+    b.kappa = kappa;
+    b.n_l = n_l;
+    b.d = (uint32_t)ctx->d;
+    b.out = ctx->R + (theta_begin + t) * ctx->dp;  // rows in place (padding bytes stay zero)
+    b.out_stride = ctx->dp;
+    launch_puzzle_bind(b, st);
+    ENS_LAUNCHED(ctx);
+    ctx->r_written.store(true);
+  }
+  if (!w) ENS_CUDA(ctx, cudaStreamSynchronize(st));
+  return QPIR_OK;
+}
+
 // One scan of rows [row_lo, row_hi) selected by share_dev, finalised in the
 // kernel: out_dev (device, d bytes) = init_dev ^ XOR of the selected rows.
 // early: the share was not written by the kernel preceding this launch (staged
@@ -342,7 +402,10 @@ static int scan_range(qpir_ens_ctx* ctx, EnsArena& ar, const uint8_t* share_dev,
   cfg.stream = st;
   cudaLaunchAttribute attr[1];
   attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-  attr[0].val.programmaticStreamSerializationAllowed = ctx->pdl ? 1 : 0;
+  // a scan may read R before griddepcontrol.wait: right after a kernel wrote R
+  // (qpir_ens_puzzle_bind_hct) it is launched without PDL
+  const bool after_write = ctx->r_written.exchange(false);
+  attr[0].val.programmaticStreamSerializationAllowed = (ctx->pdl && !after_write) ? 1 : 0;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
   ENS_CUDA(ctx, cudaLaunchKernelEx(&cfg, kern, a));
@@ -676,6 +739,7 @@ void qpir_ens_destroy(qpir_ens_ctx* ctx) {
   if (!ctx) return;
   DeviceGuard dg(ctx->device);
   if (ctx->R) cudaFree(ctx->R);
+  if (ctx->spec_stage) cudaFree(ctx->spec_stage);
   for (auto& kv : ctx->arenas) {
     EnsArena& a = kv.second;
     if (a.h2d) cudaStreamSynchronize(a.h2d);

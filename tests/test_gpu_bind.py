@@ -1,0 +1,118 @@
+"""NEXT-4: PSD.Puzzle.Bind with HCT puzzles on the GPU (Alg. 1 step 1, P:553-566;
+HCT.Puzzle.Gen P:855; record layout P:1686, DESIGN R21) through the C ABI,
+bit-exact against the oracle's qo_puzzle_bind_hct + qo_pack."""
+import numpy as np
+import pytest
+import torch
+
+import synth
+from oracle import oracle as O
+
+pytestmark = pytest.mark.gpu
+
+
+def _P():
+    import paper_2510_03631_b200 as P
+    return P
+
+
+def _u32(t):
+    return _P().u32(t)
+
+
+def _read_D(s, m):
+    """The whole shard, exactly: ANS for Q = identity (one query per cell) is D^T."""
+    Q = np.eye(m, dtype=np.uint32)
+    return _u32(s.answer_batch(Q)).T.astype(np.uint8)
+
+
+@pytest.mark.parametrize("n_cells,n_ch,m", [(64, 3, 0), (40, 2, 16)])
+def test_bind_whole_db_matches_oracle(cuda_ok, n_cells, n_ch, m):
+    """Every record bound on the GPU (host spectrum, stride 600 > 560): the shard
+    equals the oracle's pack of the oracle's bound records, byte for byte."""
+    P = _P()
+    d = 3072
+    n = n_cells * n_ch
+    spec = synth.uniform_u8_np(11, (n, 600))
+    seed, kappa, n_l = 0xC0FFEE1234, 20, 3
+    want_rec = O.puzzle_bind_hct(spec, 0, seed, kappa, n_l, d)
+    with P.PirServer(n_cells, n_ch, d, m=m, lwe_n=4) as s:
+        s.puzzle_bind_hct(0, spec, seed, kappa, n_l)
+        D = _read_D(s, s.m)
+    assert (D == O.pack(want_rec, n_cells, n_ch, d, m or n_cells)).all()
+
+
+def test_bind_ragged_range_device_spectrum_and_shard(cuda_ok):
+    """A ragged theta range with a device spectrum (stride 560) on top of a
+    written DB, on a row shard: bound records replaced, the rest untouched."""
+    P = _P()
+    n_cells, n_ch, d = 48, 2, 3072
+    n = n_cells * n_ch
+    base = synth.records_np(3, n, d, n_ch)
+    t0, cnt = 5, 77
+    spec = synth.uniform_u8_np(12, (cnt, 560))
+    want = base.copy()
+    want[t0:t0 + cnt] = O.puzzle_bind_hct(spec, t0, 77, 0xDEADBEEF, 9, d)
+    full = O.pack(want, n_cells, n_ch, d, n_cells)
+    r0, r1 = 2000, 4096 + 123
+    with P.PirServer(n_cells, n_ch, d, lwe_n=4, row_begin=r0, row_end=r1, records=base) as s:
+        s.puzzle_bind_hct(t0, torch.from_numpy(spec).cuda(), 77, 0xDEADBEEF, 9)
+        D = _read_D(s, n_cells)
+    assert (D == full[r0:r1]).all()
+
+
+def test_bind_then_answer_without_sync(cuda_ok):
+    """The bind's pack kernel writes D; the next GEMV (launched right after, no
+    sync) must see it (launched without programmatic dependent launch)."""
+    P = _P()
+    n_cells, n_ch, d = 32, 2, 3072
+    n = n_cells * n_ch
+    spec = torch.from_numpy(synth.uniform_u8_np(13, (n, 560))).cuda()
+    qu = synth.uniform_u32_np(14, (n_cells,))
+    want_rec = O.puzzle_bind_hct(spec.cpu().numpy(), 0, 5, 20, 3, d)
+    D = O.pack(want_rec, n_cells, n_ch, d, n_cells)
+    with P.PirServer(n_cells, n_ch, d, lwe_n=4, stable_inputs=True) as s:
+        qd = torch.from_numpy(qu.view(np.int32)).cuda()
+        torch.cuda.synchronize()
+        s.answer(qd)  # a GEMV in flight before the bind
+        s.puzzle_bind_hct(0, spec, 5, 20, 3)
+        got = s.answer(qd)
+        torch.cuda.synchronize()
+        assert (_u32(got) == O.answer(D, qu)).all()
+
+
+@pytest.mark.parametrize("r,d", [(1000, 3072), (333, 600)])
+def test_ens_bind_matches_oracle(cuda_ok, r, d):
+    """ENS records bound in place; unit shares return single bound records and a
+    random share returns the oracle's XOR of the selected bound records; the
+    first scan runs right after the bind with no sync."""
+    P = _P()
+    spec = synth.uniform_u8_np(r + d, (r, 560))
+    want = O.puzzle_bind_hct(spec, 0, 42, 20, 3, d)
+    nb = (r + 7) // 8
+    share = synth.uniform_u8_np(7, (nb,))
+    if r % 8:
+        share[-1] &= (1 << (r % 8)) - 1
+    with P.EnsServer(r, d, stable_inputs=True) as s:
+        sd = torch.from_numpy(share).cuda()
+        torch.cuda.synchronize()
+        s.puzzle_bind_hct(0, torch.from_numpy(spec).cuda(), 42, 20, 3)
+        got = s.answer(sd).cpu().numpy()
+        assert (got == O.ens_respond(want, share)).all()
+        for t in (0, r // 2, r - 1):
+            u = np.zeros(nb, np.uint8)
+            u[t >> 3] = 1 << (t & 7)
+            assert (s.answer(u).cpu().numpy() == want[t]).all()
+
+
+def test_bind_errors_name_the_field(cuda_ok):
+    P = _P()
+    spec = np.zeros((4, 560), np.uint8)
+    with P.PirServer(16, 1, 64, lwe_n=4) as s:  # records too small for a puzzle
+        with pytest.raises(RuntimeError, match="rec_bytes"):
+            s.puzzle_bind_hct(0, spec, 1)
+    with P.PirServer(16, 1, 3072, lwe_n=4) as s:
+        with pytest.raises(RuntimeError, match="spec_stride"):
+            s.puzzle_bind_hct(0, np.zeros((4, 100), np.uint8), 1)
+        with pytest.raises(RuntimeError, match="theta range"):
+            s.puzzle_bind_hct(14, spec, 1)
