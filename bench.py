@@ -3,7 +3,7 @@
 "PIR answer DB-scan GB/s and queries/sec per GPU at 1/2/4/8 B200 vs HBM roof").
 
     python bench.py [--gpus N] [--steps K] [--warmup W]
-                    [--workload c1|c2|c3|c4-64|c4-256|c5|ens-c2|ens-c2-b128|ftr-c2-b128|oop-c2]
+                    [--workload c1|c2|c3|c4-64|c4-256|c5|ens-c2|ens-c2-b128|ftr-c2-b128|oop-c2|bind-c2]
                     [--impl ours|reference] [--no-cpu-baseline] [--no-e2e] [--graph 0|1]
     torchrun --nproc-per-node N bench.py --gpus N ...   (plain `--gpus N` re-runs itself
                                                         under torchrun on 127.0.0.1)
@@ -69,6 +69,10 @@ WORKLOADS = {
     "ftr-c2-b128": dict(name="QPADL-FTR (Goldberg PIR over F_65537, NEXT-2; Alg. 4): 327680 "
                              "paper-shaped 3 KB records = 1.007 GB, 128 Shamir-share queries",
                         n_cells=327680, n_ch=1, d=3072, kind="batch", B=128, modp=65537),
+    "bind-c2": dict(name="NEXT-4 PSD.Puzzle.Bind (Alg. 1 step 1): all 327680 records of the "
+                         "1.007 GB regional DB built on the GPU (560 B spectrum + 37 B HCT puzzle "
+                         "+ unsigned 2420 B signature slot) straight into the D panels",
+                    n_cells=8192, n_ch=40, d=3072, kind="bind"),
     "c5": dict(name="hint D.A, n=1024, one rank's shard of the 32.2 GB DB at G=8 "
                     "(BASELINE configs[4])", n_cells=262144, n_ch=40, d=3072, kind="hint", n=1024,
                shard_of=8),
@@ -629,6 +633,93 @@ def run_oop(args, wl, rank, local):
     print(json.dumps(line), flush=True)
 
 
+def run_bind(args, wl, rank, local):
+    """NEXT-4: one step = Puzzle.Bind of every record of the DB on the GPU (HCT
+    puzzle generation fused into the pack into the D panels), the spectrum data
+    resident in HBM.  Replicas only (every rank binds its own copy)."""
+    import synth
+    import paper_2510_03631_b200 as P
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    stream = torch.cuda.current_stream(dev)
+    n_cells, n_ch, d = wl["n_cells"], wl["n_ch"], wl["d"]
+    r = n_cells * n_ch
+    spec = synth.uniform_u32(args.seed, (r, 140), device=dev).view(torch.uint8).contiguous()  # 560 B rows
+    srv = P.PirServer(n_cells, n_ch, d, lwe_n=4, device=local)
+    seed_psd = 0x5D5EED
+    for _ in range(args.warmup):
+        srv.puzzle_bind_hct(0, spec, seed_psd, 20, 3, stream=stream)
+    torch.cuda.synchronize(dev)
+    sampler = ClockSampler(physical_gpu(local))
+    l0 = srv.kernel_launches
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    sampler.start()
+    e0.record(stream)
+    for _ in range(args.steps):
+        srv.puzzle_bind_hct(0, spec, seed_psd, 20, 3, stream=stream)
+    e1.record(stream)
+    torch.cuda.synchronize(dev)
+    sampler.stop()
+    launches = srv.kernel_launches - l0
+    ms = e0.elapsed_time(e1) / args.steps
+    # e2e: the spectrum from pinned host memory every step (staged by the library)
+    h_spec = spec.cpu().pin_memory()
+    n_e2e = max(3, min(args.steps, 20))
+    srv.puzzle_bind_hct(0, h_spec, seed_psd, 20, 3, stream=stream)
+    torch.cuda.synchronize(dev)
+    a0 = torch.cuda.Event(enable_timing=True)
+    a1 = torch.cuda.Event(enable_timing=True)
+    a0.record(stream)
+    for _ in range(n_e2e):
+        srv.puzzle_bind_hct(0, h_spec, seed_psd, 20, 3, stream=stream)
+    a1.record(stream)
+    torch.cuda.synchronize(dev)
+    te = a0.elapsed_time(a1) / n_e2e
+    srv.close()
+    if rank != 0:
+        return
+    hbm, _, _, peak_src = peaks()
+    db = r * d
+    alg = r * 560 + db  # spectrum read + D written (the bound records)
+    achieved = alg / (ms / 1e3) / 1e9
+    cpu = None
+    if not args.no_cpu_baseline:
+        from oracle import oracle as O
+        O.set_num_threads(os.cpu_count() or 1)
+        ns = 200 * n_ch  # records (whole cells, 24.6 MB of bound DB), oracle bind + pack
+        sp = spec[:ns].cpu().numpy()
+        fn = lambda: O.pack(O.puzzle_bind_hct(sp, 0, seed_psd, 20, 3, d), ns // n_ch, n_ch, d,  # noqa: E731
+                            ns // n_ch)
+        _warm_oracle(fn, 1.0)
+        t0 = time.perf_counter()
+        reps = 0
+        while time.perf_counter() - t0 < 8.0:
+            fn()
+            reps += 1
+        el = time.perf_counter() - t0
+        cpu = {"value": round(reps * ns * d / el / 1e9, 3), "unit": "GB/s", "cores": os.cpu_count(),
+               "kind": "oracle", "sample": f"{ns} records ({ns * d / 1e6:.1f} MB), oracle "
+                                           f"qo_puzzle_bind_hct + qo_pack, {reps} repetitions"}
+    line = {"metric": METRIC, "value": round(db / (ms / 1e3) / 1e9, 2),
+            "unit": "GB/s (bound DB bytes built per second)", "n_gpus": 1, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": round(ms, 5), "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "u8", "data": "synthetic",
+            "config": {"workload": wl["name"], "n_records": r, "rec_bytes": d,
+                       "records_per_s": round(r / (ms / 1e3), 1),
+                       "signature": "not computed (ML-DSA not implemented: DESIGN R21)"},
+            "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": hbm, "unit": "GB/s",
+                         "frac": round(achieved / hbm, 4), "traffic": _traffic(args.workload),
+                         "kernel": "pack_bind_tile_kernel", "kernel_ms": round(ms, 5),
+                         "algorithmic_bytes_per_launch": alg, "peak_source": f"{peak_src} hbm_gbs"},
+            "cpu_baseline": cpu,
+            "e2e": {"value": round(db / (te / 1e3) / 1e9, 2), "unit": "GB/s",
+                    "h2d_bytes_per_step": r * 560, "d2h_bytes_per_step": 0, "ms_per_step": round(te, 4),
+                    "timing": "device events; pinned host spectrum staged by the library each step"},
+            "gpu_launches": launches, "clocks": sampler.summary()}
+    print(json.dumps(line), flush=True)
+
+
 def _traffic(workload):
     """DRAM bytes per launch of the dominant kernel from a committed ncu --set full
     summary (profiles/traffic_<workload>.json), else None."""
@@ -676,6 +767,10 @@ def main():
         args.warmup = args.warmup if args.warmup is not None else 3
         return run_reference(args, wl, world, rank)
 
+    if wl["kind"] == "bind":
+        args.steps = args.steps or 50
+        args.warmup = max(3, args.warmup if args.warmup is not None else 3)
+        return run_bind(args, wl, rank, local if args.device_override is None else args.device_override)
     if wl["kind"] == "oop":
         args.steps = args.steps or 1000
         args.warmup = max(3, args.warmup if args.warmup is not None else 5)

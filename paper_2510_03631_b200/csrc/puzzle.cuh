@@ -84,6 +84,22 @@ static __global__ void puzzle_bind_hct_kernel(BindArgs a) {
   }
 }
 
+// Byte b of the bound record theta (b < d): the same record as
+// puzzle_bind_hct_kernel writes, one byte at a time (for the fused pack below).
+__device__ __forceinline__ uint8_t bound_record_byte(const BindArgs& a, uint64_t theta, uint32_t b) {
+  if (b < HCT_SPECTRUM) return a.spectrum[(theta - a.theta0) * a.spec_stride + b];
+  if (b < HCT_SPECTRUM + 32) {
+    const uint32_t o = b - HCT_SPECTRUM, w = o >> 2;
+    const uint2 key = make_uint2((uint32_t)a.seed_psd, (uint32_t)(a.seed_psd >> 32));
+    const uint4 r = philox4x32_10(make_uint4((uint32_t)theta, (uint32_t)(theta >> 32), w >> 2, 0x48u), key);
+    const uint32_t x = (w & 3) == 0 ? r.x : (w & 3) == 1 ? r.y : (w & 3) == 2 ? r.z : r.w;
+    return (uint8_t)(x >> (8 * (o & 3)));
+  }
+  if (b < HCT_SPECTRUM + 36) return (uint8_t)(a.kappa >> (8 * (b - HCT_SPECTRUM - 32)));
+  if (b == HCT_SPECTRUM + 36) return (uint8_t)a.n_l;
+  return 0;  // the (unsigned) ML-DSA signature slot and the padding
+}
+
 static inline void launch_puzzle_bind(const BindArgs& a, cudaStream_t st) {
   const uint64_t threads = a.n * ((a.d + 15) / 16);
   const uint32_t blocks = (uint32_t)((threads + 255) / 256);

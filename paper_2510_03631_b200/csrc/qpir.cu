@@ -246,8 +246,158 @@ int stage_host(qpir_ctx* ctx, Arena& ar, InRing& ring, const void* src, uint64_t
   return QPIR_OK;
 }
 
+// NEXT-4: pack_records_kernel with the record bytes generated in place (Puzzle.Bind
+// straight into the D panel layout: no record staging buffer).  Same thread map:
+// one thread per (row, 16-cell column group); row b of a channel = byte b of its
+// records, so all but 32 of a 3072-byte record's rows are a spectrum copy or zeros.
+__global__ void pack_bind_kernel(PackArgs a, BindArgs bnd) {
+  const uint32_t rl = blockIdx.y * blockDim.x + threadIdx.x;
+  if (rl >= a.ell_local) return;
+  const uint32_t j = a.g_lo + blockIdx.x;
+  const uint64_t row = a.row_begin + rl;
+  const uint64_t per_blk = (uint64_t)a.n_ch * a.d;
+  const uint64_t blk = row / per_blk;
+  const uint32_t rr = (uint32_t)(row % per_blk);
+  const uint32_t ch = rr / a.d;
+  const uint32_t b = rr % a.d;
+  uint4* dst = reinterpret_cast<uint4*>(a.D + ((size_t)(rl >> 7) * a.G + j) * 2048 +
+                                        (rl & 127u) * 16);
+  uint4 v = make_uint4(0u, 0u, 0u, 0u);
+  uint8_t* bytes = reinterpret_cast<uint8_t*>(&v);
+  uint32_t touched = 0;  // columns written (a full group needs no read of the old bytes)
+#pragma unroll
+  for (int i = 0; i < 16; ++i) {
+    const uint32_t col = j * 16u + i;
+    if (col >= a.m) continue;
+    const uint64_t cell = blk * a.m + col;
+    if (cell >= a.n_cells) continue;
+    const uint64_t theta = cell * a.n_ch + ch;
+    if (theta < a.theta0 || theta >= a.theta0 + a.n_rec) continue;
+    bytes[i] = bound_record_byte(bnd, theta, b);
+    touched |= 1u << i;
+  }
+  if (touched == 0xFFFFu) {
+    *dst = v;
+  } else if (touched) {
+    uint4 o = *dst;
+    const uint8_t* ob = reinterpret_cast<const uint8_t*>(&o);
+#pragma unroll
+    for (int i = 0; i < 16; ++i)
+      if (!((touched >> i) & 1u)) bytes[i] = ob[i];
+    *dst = v;
+  }
+}
+
+// Register-transposed form (d and the spectrum rows 16-byte aligned): one CTA
+// per (16-cell column group j, channel ch, row block blk).  Threads 0..37 each
+// take 16 record-byte rows of the 608-byte data prefix (spectrum + puzzle):
+// bytes 16t .. 16t + 15 of the 16 cells' records (16-byte loads, coalesced
+// across the warp; nonce bytes straight from Philox), a 16 x 16 byte transpose
+// in registers (4 x 4 byte transposes of words, 8 PRMT each) into shared
+// memory; then all threads store the record-byte rows as 16-byte D chunks,
+// consecutive threads on consecutive rows (512 contiguous bytes per warp
+// store), rows past the prefix as zeros (the unsigned signature slot).
+__device__ __forceinline__ void transpose4x4_bytes(uint32_t x0, uint32_t x1, uint32_t x2, uint32_t x3,
+                                                   uint32_t& y0, uint32_t& y1, uint32_t& y2, uint32_t& y3) {
+  const uint32_t t0 = __byte_perm(x0, x1, 0x5140), t1 = __byte_perm(x0, x1, 0x7362);
+  const uint32_t t2 = __byte_perm(x2, x3, 0x5140), t3 = __byte_perm(x2, x3, 0x7362);
+  y0 = __byte_perm(t0, t2, 0x5410);
+  y1 = __byte_perm(t0, t2, 0x7632);
+  y2 = __byte_perm(t1, t3, 0x5410);
+  y3 = __byte_perm(t1, t3, 0x7632);
+}
+
+constexpr uint32_t BIND_HEAD = (HCT_SPECTRUM + HCT_PUZZLE + 15) / 16 * 16;  // 608 rows with data
+
+__global__ void __launch_bounds__(256) pack_bind_tile_kernel(PackArgs a, BindArgs bnd) {
+  // rows [0, 608) of the 16 records, transposed, staged with one pad slot per 16 rows
+  __shared__ uint4 S[BIND_HEAD + BIND_HEAD / 16];
+  const uint32_t j = a.g_lo + blockIdx.x, ch = blockIdx.y, blk = blockIdx.z;
+  const uint32_t tid = threadIdx.x;
+  const uint64_t row0 = ((uint64_t)blk * a.n_ch + ch) * a.d;  // global row of byte 0
+  if (row0 + a.d <= a.row_begin || row0 >= a.row_begin + a.ell_local) return;  // outside the shard
+  uint32_t valid = 0;
+  uint64_t th[16];
+#pragma unroll
+  for (int i = 0; i < 16; ++i) {
+    const uint32_t col = j * 16 + i;
+    const uint64_t cell = (uint64_t)blk * a.m + col;
+    th[i] = cell * a.n_ch + ch;
+    if (col < a.m && cell < a.n_cells && th[i] >= a.theta0 && th[i] < a.theta0 + a.n_rec) valid |= 1u << i;
+  }
+  if (!valid) return;
+  if (tid < BIND_HEAD / 16) {
+    const uint32_t b0 = tid * 16;
+    uint32_t X[16][4];  // X[record][word]: bytes b0 .. b0 + 15 of record i
+    if (b0 + 16 <= HCT_SPECTRUM) {
+#pragma unroll
+      for (int i = 0; i < 16; ++i) {
+        uint4 v = make_uint4(0u, 0u, 0u, 0u);
+        if ((valid >> i) & 1u)
+          v = *reinterpret_cast<const uint4*>(bnd.spectrum + (th[i] - bnd.theta0) * bnd.spec_stride + b0);
+        X[i][0] = v.x; X[i][1] = v.y; X[i][2] = v.z; X[i][3] = v.w;
+      }
+    } else {
+#pragma unroll
+      for (int i = 0; i < 16; ++i) {
+        uint8_t by[16];
+#pragma unroll
+        for (int k = 0; k < 16; ++k) by[k] = 0;
+        if ((valid >> i) & 1u) {
+          if (b0 + 16 <= HCT_SPECTRUM + 32) {  // one Philox block = 16 nonce bytes
+            const uint2 key = make_uint2((uint32_t)bnd.seed_psd, (uint32_t)(bnd.seed_psd >> 32));
+            const uint4 r = philox4x32_10(
+                make_uint4((uint32_t)th[i], (uint32_t)(th[i] >> 32), (b0 - HCT_SPECTRUM) / 16, 0x48u), key);
+            X[i][0] = r.x; X[i][1] = r.y; X[i][2] = r.z; X[i][3] = r.w;
+            continue;
+          }
+#pragma unroll
+          for (int k = 0; k < 16; ++k) by[k] = bound_record_byte(bnd, th[i], b0 + k);
+        }
+#pragma unroll
+        for (int w = 0; w < 4; ++w)
+          X[i][w] = by[4 * w] | (by[4 * w + 1] << 8) | (by[4 * w + 2] << 16) | ((uint32_t)by[4 * w + 3] << 24);
+      }
+    }
+    // row b0 + 4w + k, cells 4v .. 4v + 3: byte k of X[4v .. 4v + 3][w]
+#pragma unroll
+    for (int v = 0; v < 4; ++v)
+#pragma unroll
+      for (int w = 0; w < 4; ++w) {
+        uint32_t y[4];
+        transpose4x4_bytes(X[4 * v][w], X[4 * v + 1][w], X[4 * v + 2][w], X[4 * v + 3][w], y[0], y[1], y[2], y[3]);
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+          const uint32_t rr = b0 + 4 * w + k;
+          reinterpret_cast<uint32_t*>(&S[rr + rr / 16])[v] = y[k];
+        }
+      }
+  }
+  __syncthreads();
+  // every row of the record bytes: consecutive threads, consecutive rows (16-byte chunks)
+  for (uint32_t b = tid; b < a.d; b += blockDim.x) {
+    const uint64_t row = row0 + b;
+    if (row < a.row_begin || row >= a.row_begin + a.ell_local) continue;
+    const uint64_t rl = row - a.row_begin;
+    uint4* dst = reinterpret_cast<uint4*>(a.D + ((size_t)(rl >> 7) * a.G + j) * 2048 + (rl & 127u) * 16);
+    uint4 v = b < BIND_HEAD ? S[b + b / 16] : make_uint4(0u, 0u, 0u, 0u);
+    if (valid != 0xFFFFu) {  // partial group: keep the other cells' bytes
+      const uint4 o = *dst;
+      uint8_t* vb = reinterpret_cast<uint8_t*>(&v);
+      const uint8_t* ob = reinterpret_cast<const uint8_t*>(&o);
+#pragma unroll
+      for (int i = 0; i < 16; ++i)
+        if (!((valid >> i) & 1u)) vb[i] = ob[i];
+    }
+    *dst = v;
+  }
+}
+
 int db_write_device(qpir_ctx* ctx, uint64_t theta0, uint64_t n_rec, const uint8_t* rec,
-                    cudaStream_t st) {
+                    cudaStream_t st, const BindArgs* bind = nullptr);
+
+int db_write_device(qpir_ctx* ctx, uint64_t theta0, uint64_t n_rec, const uint8_t* rec,
+                    cudaStream_t st, const BindArgs* bind) {
   const Geometry& g = ctx->geo;
   if (n_rec == 0) return QPIR_OK;
   // column groups touched: whole range unless the chunk lies in one row block
@@ -280,7 +430,24 @@ int db_write_device(qpir_ctx* ctx, uint64_t theta0, uint64_t n_rec, const uint8_
     b.row_begin = g.row_begin + (uint64_t)y0 * 128;
     b.ell_local = (uint32_t)std::min<uint64_t>(g.ell_local - (uint64_t)y0 * 128, (uint64_t)ny * 128);
     dim3 grid((uint32_t)(j_hi - j_lo + 1), ny);
-    pack_records_kernel<<<grid, 128, 0, st>>>(b);
+    const bool tile = bind && g.d % 16 == 0 && g.d >= BIND_HEAD && bind->spec_stride % 16 == 0 &&
+                      (reinterpret_cast<uintptr_t>(bind->spectrum) & 15u) == 0 &&
+                      g.n_ch <= 65535 && (g.n_cells + g.m - 1) / g.m <= 65535;
+    if (tile) {
+      // register-transposed bind (whole shard in one launch: grid = column groups x
+      // channels x row blocks; threads = 16-row chunks of a record)
+      if (y0 == 0) {
+        const uint32_t nblk = (uint32_t)((g.n_cells + g.m - 1) / g.m);
+        dim3 tg((uint32_t)(j_hi - j_lo + 1), (uint32_t)g.n_ch, nblk);
+        pack_bind_tile_kernel<<<tg, 256, 0, st>>>(a, *bind);
+        LAUNCH_CHECK(ctx);
+      }
+      continue;
+    } else if (bind) {
+      pack_bind_kernel<<<grid, 128, 0, st>>>(b, *bind);
+    } else {
+      pack_records_kernel<<<grid, 128, 0, st>>>(b);
+    }
     LAUNCH_CHECK(ctx);
   }
   ctx->d_written.store(true);
@@ -579,12 +746,10 @@ int qpir_puzzle_bind_hct(qpir_ctx* ctx, uint64_t theta_begin, uint64_t n_records
   cudaStream_t st = (cudaStream_t)stream;
   const int w = where(spectrum, ctx->device);
   if (w < 0) return fail(ctx, QPIR_E_PARAM, "spectrum: device memory of another device");
-  // records are built in chunks of <= 64 MB into the db_write staging buffer,
-  // then packed into the shard (pack_records_kernel)
-  const uint64_t chunk = std::max<uint64_t>(1, (64ull << 20) / g.d);
-  int rc = ensure(ctx, (void**)&ctx->rec_stage, &ctx->rec_stage_bytes,
-                  std::min(n_records, chunk) * g.d);
-  if (rc) return rc;
+  // records are generated inside the pack kernel, straight into the D panels;
+  // a host spectrum is staged in chunks of <= 64 MB
+  const uint64_t chunk = w ? n_records : std::max<uint64_t>(1, (64ull << 20) / spec_stride);
+  int rc = QPIR_OK;
   if (w == 0) {
     rc = ensure(ctx, (void**)&ctx->spec_stage, &ctx->spec_stage_bytes,
                 std::min(n_records, chunk) * spec_stride);
@@ -606,14 +771,12 @@ int qpir_puzzle_bind_hct(qpir_ctx* ctx, uint64_t theta_begin, uint64_t n_records
     b.kappa = kappa;
     b.n_l = n_l;
     b.d = (uint32_t)g.d;
-    b.out = ctx->rec_stage;
-    b.out_stride = g.d;
-    launch_puzzle_bind(b, st);
-    LAUNCH_CHECK(ctx);
-    rc = db_write_device(ctx, theta_begin + t, n, ctx->rec_stage, st);
+    b.out = nullptr;
+    b.out_stride = 0;
+    rc = db_write_device(ctx, theta_begin + t, n, nullptr, st, &b);
     if (rc) return rc;
   }
-  if (w == 0) CUDA_TRY(ctx, cudaStreamSynchronize(st));  // the staging buffers are reused per call
+  if (w == 0) CUDA_TRY(ctx, cudaStreamSynchronize(st));  // the staging buffer is reused per call
   return QPIR_OK;
 }
 

@@ -26,18 +26,21 @@ def _read_D(s, m):
     return _u32(s.answer_batch(Q)).T.astype(np.uint8)
 
 
-@pytest.mark.parametrize("n_cells,n_ch,m", [(64, 3, 0), (40, 2, 16)])
-def test_bind_whole_db_matches_oracle(cuda_ok, n_cells, n_ch, m):
-    """Every record bound on the GPU (host spectrum, stride 600 > 560): the shard
-    equals the oracle's pack of the oracle's bound records, byte for byte."""
+@pytest.mark.parametrize("stride,device", [(600, False), (560, True), (576, False)])
+@pytest.mark.parametrize("n_cells,n_ch,m", [(64, 3, 0), (40, 2, 16), (37, 3, 0)])
+def test_bind_whole_db_matches_oracle(cuda_ok, n_cells, n_ch, m, stride, device):
+    """Every record bound on the GPU: the shard equals the oracle's pack of the
+    oracle's bound records, byte for byte.  Spectrum strides 560 / 576 (16-byte
+    aligned: register-transposed kernel) and 600 (per-byte kernel); ragged cell
+    counts leave partial 16-cell groups."""
     P = _P()
     d = 3072
     n = n_cells * n_ch
-    spec = synth.uniform_u8_np(11, (n, 600))
+    spec = synth.uniform_u8_np(11, (n, stride))
     seed, kappa, n_l = 0xC0FFEE1234, 20, 3
     want_rec = O.puzzle_bind_hct(spec, 0, seed, kappa, n_l, d)
     with P.PirServer(n_cells, n_ch, d, m=m, lwe_n=4) as s:
-        s.puzzle_bind_hct(0, spec, seed, kappa, n_l)
+        s.puzzle_bind_hct(0, torch.from_numpy(spec).cuda() if device else spec, seed, kappa, n_l)
         D = _read_D(s, s.m)
     assert (D == O.pack(want_rec, n_cells, n_ch, d, m or n_cells)).all()
 
@@ -50,7 +53,7 @@ def test_bind_ragged_range_device_spectrum_and_shard(cuda_ok):
     n = n_cells * n_ch
     base = synth.records_np(3, n, d, n_ch)
     t0, cnt = 5, 77
-    spec = synth.uniform_u8_np(12, (cnt, 560))
+    spec = synth.uniform_u8_np(12, (cnt, 560))  # 16-byte aligned rows: the tiled kernel
     want = base.copy()
     want[t0:t0 + cnt] = O.puzzle_bind_hct(spec, t0, 77, 0xDEADBEEF, 9, d)
     full = O.pack(want, n_cells, n_ch, d, n_cells)
