@@ -109,7 +109,7 @@ struct MmaArgs {
   unsigned long long conv_base = 0;        // its value at this launch
 };
 
-constexpr uint32_t MMA_CONV_THREADS = 128;  // 4 converter warps (CONV kernels)
+constexpr uint32_t MMA_CONV_THREADS = 256;  // 8 converter warps (CONV kernels; 16 measured no faster)
 
 __device__ __forceinline__ void st_release_u32(uint32_t* p, uint32_t v) {
   asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
@@ -408,7 +408,7 @@ __global__ void __launch_bounds__(CONV ? MMA_THREADS + MMA_CONV_THREADS : MMA_TH
     // (CONV only) K-block kb of the B operand: limb k of (Q[j][c] mod p), c in
     // the block's 16 * GPB cells, for every padded query slot j; the residue
     // 65536 of p = 65537 (17 bits) is written as 0 and listed for the fixup.
-    // Warp cw takes queries cw, cw + 4, ...; lane l the 4 cells 4l .. 4l + 3.
+    // Warp cw takes queries cw, cw + NCW, ...; lane l the 4 cells 4l .. 4l + 3.
     static_assert(!CONV || (OUT_MODE == OUT_MODP2 && GPB == 8), "fused split: 2 limbs, K-block 128");
     if constexpr (CONV) {
       __shared__ uint32_t s_job[2];
@@ -431,12 +431,13 @@ __global__ void __launch_bounds__(CONV ? MMA_THREADS + MMA_CONV_THREADS : MMA_TH
           // CU queries per batch (32: all of a warp's, nq = 128): their loads are all in flight before the
           // first is used (one load per warp at a time left the converters
           // latency-bound: 0.5 ms per FTR call instead of the GEMM's 0.2 ms)
-          constexpr uint32_t CU = 32;
-          for (uint32_t jb0 = cw; jb0 < nq; jb0 += 4 * CU) {
+          constexpr uint32_t NCW = MMA_CONV_THREADS / 32;
+          constexpr uint32_t CU = 128 / NCW;
+          for (uint32_t jb0 = cw; jb0 < nq; jb0 += NCW * CU) {
             uint4 x[CU];
 #pragma unroll
             for (uint32_t u = 0; u < CU; ++u) {
-              const uint32_t j = jb0 + 4 * u;
+              const uint32_t j = jb0 + NCW * u;
               x[u] = make_uint4(0u, 0u, 0u, 0u);
               if (j < a.qB) {
                 const uint32_t* row = a.Q + (size_t)j * a.qm;
@@ -452,7 +453,7 @@ __global__ void __launch_bounds__(CONV ? MMA_THREADS + MMA_CONV_THREADS : MMA_TH
             }
 #pragma unroll
             for (uint32_t u = 0; u < CU; ++u) {
-              const uint32_t j = jb0 + 4 * u;
+              const uint32_t j = jb0 + NCW * u;
               if (j >= nq) break;
               uint32_t v[4] = {x[u].x, x[u].y, x[u].z, x[u].w};
               if (j < a.qB) {

@@ -110,8 +110,8 @@ struct qpir_ctx {
   int mma_gpb = 8;     // env QPIR_MMA_GPB (column groups per pipeline stage: 4 or 8)
   int modp3 = 1;       // env QPIR_MODP3 (3 limbs per query for p < 2^24)
   int modp2 = 1;       // env QPIR_MODP2 (2 limbs per query for p <= 65537)
-  int ftr_fuse = 0;    // env QPIR_FTR_FUSE (2-limb split inside the GEMM: converter warps; measured
-                       // 0.29 vs 0.27 ms for the separate split kernel on ftr-c2-b128, so off)
+  int ftr_fuse = 1;    // env QPIR_FTR_FUSE (2-limb split inside the GEMM: 8 converter warps;
+                       // ftr-c2-b128 0.262-0.264 ms vs 0.269-0.273 ms with the split kernel)
   int h2d_stream = 1;  // env QPIR_H2D_STREAM (host inputs copied on a side stream)
   int mma_ls = 16;     // env QPIR_MMA_LOCKSTEP: K-blocks per lockstep chunk (0 = off)
   int mma_drift = 1;   // env QPIR_MMA_DRIFT: chunks a CTA may run ahead of its wave
@@ -651,7 +651,7 @@ int qpir_setup(const qpir_params* params, const uint8_t* records, uint64_t recor
   ctx->mma_gpb = env_int("QPIR_MMA_GPB", 8);
   ctx->modp3 = env_int("QPIR_MODP3", 1);
   ctx->modp2 = env_int("QPIR_MODP2", 1);
-  ctx->ftr_fuse = env_int("QPIR_FTR_FUSE", 0);
+  ctx->ftr_fuse = env_int("QPIR_FTR_FUSE", 1);
   ctx->h2d_stream = env_int("QPIR_H2D_STREAM", 1);
   ctx->mma_ls = env_int("QPIR_MMA_LOCKSTEP", 16);
   ctx->mma_drift = env_int("QPIR_MMA_DRIFT", 1);
