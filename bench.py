@@ -1064,7 +1064,9 @@ def main():
         achieved_tc = ops / (k_ms / 1e3) / 1e12
         achieved_hbm = alg_bytes / (k_ms / 1e3) / 1e9
         common = {"traffic": None,
-                  "kernel": "limb_split_kernel + mma_u8_limb_kernel (step time, upper bound)",
+                  "kernel": ("mma_u8_limb_kernel with the fused 2-limb split + modp_fixup_kernel "
+                             "(step time, upper bound)" if limbs == 2 and os.environ.get("QPIR_FTR_FUSE", "1") != "0"
+                             else "limb_split_kernel + mma_u8_limb_kernel (step time, upper bound)"),
                   "limbs_per_query": limbs, "kernel_ms": round(k_ms, 5),
                   "algorithmic_ops_per_launch": ops, "algorithmic_bytes_per_launch": alg_bytes,
                   "roof_ms": {"hbm": round(t_hbm * 1e3, 5), "tensor": round(t_tc * 1e3, 5)}}
