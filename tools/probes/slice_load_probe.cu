@@ -44,6 +44,61 @@ __global__ void __launch_bounds__(256, 1) cpasync_probe(const uint8_t* rec, uint
   if (acc == 0x1234567) sink[0] = acc;
 }
 
+// cp.async probe with K-lockstep among the CTAs of one split: every LS K-blocks a
+// CTA publishes progress and waits until all CTAs that arrived in its split have
+// issued the chunk before the previous one (drift <= 1 chunk).
+template <uint32_t W, uint32_t RS, uint32_t LS>
+__global__ void __launch_bounds__(256, 1) cpasync_ls_probe(const uint8_t* rec, uint32_t splits, unsigned int* prog,
+                                                           unsigned long long* sink) {
+  extern __shared__ __align__(1024) uint8_t smem[];
+  const uint32_t wt_n = DP / W, kblocks = R / KB, kbps = (kblocks + splits - 1) / splits;
+  const uint32_t units = wt_n * splits;
+  const uint32_t t = threadIdx.x;
+  constexpr uint32_t CH = KB * W / 16;
+  unsigned long long acc = 0;
+  for (uint32_t u = blockIdx.x; u < units; u += gridDim.x) {
+    const uint32_t sp = u / wt_n, wt = u % wt_n;
+    const uint32_t kb0 = sp * kbps, kb1 = min(kblocks, kb0 + kbps);
+    unsigned int* issued = prog + 2 * sp;
+    if (t == 0) atomicAdd(issued + 1, 1u);
+    auto issue = [&](uint32_t kb) {
+      if (kb < kb1) {
+        const uint32_t j = (kb - kb0);
+        if (j % LS == 0 && j >= LS) {
+          if (t == 0) {
+            const uint32_t need = j / LS - 1;
+            while (true) {
+              uint32_t a, b;
+              asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(a) : "l"(issued) : "memory");
+              asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(b) : "l"(issued + 1) : "memory");
+              if (a >= b * need) break;
+              __nanosleep(100);
+            }
+          }
+          __syncthreads();
+        }
+        for (uint32_t c = t; c < CH; c += blockDim.x) {
+          const uint32_t rr = c / (W / 16), part = c % (W / 16);
+          cp_async_16(smem + (kb % RS) * KB * W + c * 16, rec + ((size_t)kb * KB + rr) * DP + wt * W + part * 16, true);
+        }
+        if (t == 0 && (j % LS == LS - 1)) atomicAdd(issued, 1u);
+      }
+      cp_async_commit();
+    };
+    for (uint32_t p = 0; p + 1 < RS; ++p) issue(kb0 + p);
+    for (uint32_t kb = kb0; kb < kb1; ++kb) {
+      issue(kb + RS - 1);
+      cp_async_wait<RS - 1>();
+      __syncthreads();
+      acc += reinterpret_cast<const uint32_t*>(smem + (kb % RS) * KB * W)[t % (KB * W / 4)];
+      __syncthreads();
+    }
+    cp_async_wait<0>();
+    if (t == 0) atomicAdd(issued, 100000u);  // done: never block the others
+  }
+  if (acc == 0x1234567) sink[0] = acc;
+}
+
 template <uint32_t W, uint32_t RS>
 __global__ void __launch_bounds__(160, 1) tma_probe(const __grid_constant__ CUtensorMap map, uint32_t splits, unsigned long long* sink) {
   extern __shared__ __align__(1024) uint8_t smem[];
@@ -112,7 +167,11 @@ int main() {
     if (cr) printf("encode %d\n", (int)cr); \
     auto k = tma_probe<W, RS>; size_t sm = RS * KB * W + 2 * RS * 8; cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm); \
     run("TMA W=" #W " RS=" #RS " sp=" #SPL, [&] { k<<<148, 160, sm>>>(map, SPL, sink); }); }
-  CPA(32, 12, 3) CPA(32, 32, 3) CPA(64, 12, 3) CPA(64, 24, 3) CPA(128, 12, 3)
-  TMA(32, 12, 3) TMA(32, 48, 3) TMA(64, 24, 3) TMA(128, 12, 3) TMA(128, 24, 3) TMA(256, 12, 3)
+  unsigned int* prog; cudaMalloc(&prog, 4096);
+#define CPL(W, RS, LS, SPL) { auto k = cpasync_ls_probe<W, RS, LS>; size_t sm = RS * KB * W; cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm); \
+    run("cp.async+LS W=" #W " RS=" #RS " LS=" #LS " sp=" #SPL, [&] { cudaMemsetAsync(prog, 0, 4096); k<<<148, 256, sm>>>(rec, SPL, prog, sink); }); }
+  CPA(32, 12, 3) CPA(32, 24, 3) CPA(64, 12, 3)
+  CPL(32, 12, 8, 3) CPL(32, 12, 16, 3) CPL(32, 24, 16, 3) CPL(32, 12, 4, 3)
+  CPA(32, 12, 6) CPL(32, 12, 8, 6)
   return 0;
 }
