@@ -368,3 +368,17 @@ def puzzle_bind_hct(spectrum: np.ndarray, theta0: int, seed_psd: int, kappa: int
     lib().qo_puzzle_bind_hct(_p(sp, _u8p), sp.shape[1], theta0, n, seed_psd, kappa, n_l, d,
                              _p(out, _u8p))
     return out
+
+
+def puzzle_bind_hct_signed(spectrum: np.ndarray, theta0: int, seed_psd: int, kappa: int, n_l: int,
+                           d: int, mldsa_seed: bytes) -> np.ndarray:
+    """PSD.Puzzle.Bind with the ML-DSA signature of Alg. 1 step 1:
+    record = spectrum || pi_theta || sigma, sigma = ML-DSA-44.Sign(sk_PSD, pi_theta)
+    (deterministic variant, empty context; oracle/mldsa.py), bytes [597, 3017)."""
+    from oracle import mldsa
+    assert d >= 3017
+    rec = puzzle_bind_hct(spectrum, theta0, seed_psd, kappa, n_l, d)
+    for i in range(rec.shape[0]):
+        sig = mldsa.sign(mldsa_seed, rec[i, 560:597].tobytes())
+        rec[i, 597:3017] = np.frombuffer(sig, np.uint8)
+    return rec
