@@ -120,19 +120,25 @@ int qpir_db_write(qpir_ctx *ctx, uint64_t theta_begin, uint64_t n_records,
  * PAPER.md:553-566; HCT.Puzzle.Gen PAPER.md:855; record layout PAPER.md:1686,
  * DESIGN R11 / R21).  Builds records theta_begin .. theta_begin + n_records - 1
  * and writes them into the shard exactly as qpir_db_write would:
- *   record = spectrum row (its first 560 bytes) || n_s (32 B) || kappa (u32 LE)
- *            || n_l (1 B) || zeros (the 2420-byte ML-DSA signature slot and the
- *            padding: the DB is bound but NOT signed -- DESIGN R21)
+ *   record = spectrum row (its first 560 bytes) || pi_theta = n_s (32 B) ||
+ *            kappa (u32 LE) || n_l (1 B) || sigma (2420 B) || zero padding
  * with the 256-bit nonce n_s word w = Philox4x32-10(key = seed_psd,
- * ctr = (theta_lo, theta_hi, w >> 2, 0x48))[w & 3].
+ * ctr = (theta_lo, theta_hi, w >> 2, 0x48))[w & 3], and sigma the ML-DSA-44
+ * signature of the 37-byte pi_theta (FIPS 204, deterministic variant, empty
+ * context) under the key generated from the 32-byte seed mldsa_seed (host or
+ * device; KeyGen and Sign run on the GPU).  mldsa_seed == NULL leaves the
+ * signature slot zero (unsigned DB).  mldsa_pk (1312 bytes, host or device, may
+ * be NULL) receives the public key.
  * spectrum: n_records rows of spec_stride >= 560 bytes, host or device
- * (spectrum_len == n_records * spec_stride); requires rec_bytes >= 597.
+ * (spectrum_len == n_records * spec_stride); requires rec_bytes >= 597 (>= 3017
+ * when signing).
  * Errors: QPIR_E_DIMENSION (range, lengths, stride, rec_bytes), QPIR_E_PARAM
  * (NULL spectrum).  Concurrency as qpir_db_write. */
 int qpir_puzzle_bind_hct(qpir_ctx *ctx, uint64_t theta_begin, uint64_t n_records,
                          const uint8_t *spectrum, uint64_t spec_stride,
                          uint64_t spectrum_len, uint64_t seed_psd, uint32_t kappa,
-                         uint8_t n_l, void *stream);
+                         uint8_t n_l, const uint8_t *mldsa_seed, uint8_t *mldsa_pk,
+                         void *stream);
 
 /* Geometry: ell (all rows), m (columns), ell_local (= row_end - row_begin),
  * row_begin.  Any output pointer may be NULL. */
@@ -218,7 +224,8 @@ int qpir_ens_db_write(qpir_ens_ctx *ctx, uint64_t theta_begin, uint64_t n_record
 int qpir_ens_puzzle_bind_hct(qpir_ens_ctx *ctx, uint64_t theta_begin, uint64_t n_records,
                              const uint8_t *spectrum, uint64_t spec_stride,
                              uint64_t spectrum_len, uint64_t seed_psd, uint32_t kappa,
-                             uint8_t n_l, void *stream);
+                             uint8_t n_l, const uint8_t *mldsa_seed, uint8_t *mldsa_pk,
+                             void *stream);
 
 /* Response to one share (len_share == ceil(r/8)) -> out: d bytes (len_out == d).
  * A 4-byte-aligned device share may be read in whole 32-bit words (up to 3

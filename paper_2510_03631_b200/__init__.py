@@ -37,6 +37,15 @@ def u32(t) -> np.ndarray:
     return t.detach().cpu().numpy().view(np.uint32)
 
 
+def _mldsa_bufs(mldsa_seed):
+    """Host buffers for the ML-DSA key seed (32 bytes) and the public key out."""
+    if mldsa_seed is None:
+        return None, None
+    seed = np.frombuffer(bytes(mldsa_seed), np.uint8).copy()
+    assert seed.size == 32, "mldsa_seed: 32 bytes"
+    return seed, np.zeros(1312, np.uint8)
+
+
 class PirServer:
     """A context over rows [row_begin, row_end) of the DB matrix on one GPU."""
 
@@ -61,14 +70,18 @@ class PirServer:
         _lib.qpir_db_write(self._ctx, theta_begin, records, n, _st(self.device, stream))
 
     def puzzle_bind_hct(self, theta_begin: int, spectrum, seed_psd: int, kappa: int = 20,
-                        n_l: int = 3, stream=None) -> None:
+                        n_l: int = 3, mldsa_seed: bytes | None = None, stream=None):
         """NEXT-4 PSD.Puzzle.Bind (Alg. 1 step 1): records theta_begin .. + len(spectrum)
-        built on the GPU (spectrum row || HCT puzzle || unsigned signature slot) and
-        written into the shard (include/qpir.h qpir_puzzle_bind_hct)."""
+        built on the GPU (spectrum row || HCT puzzle || ML-DSA-44 signature of the
+        puzzle under the key from `mldsa_seed`, or a zero slot without a seed) and
+        written into the shard (include/qpir.h qpir_puzzle_bind_hct).  Returns the
+        1312-byte public key when signing."""
         assert spectrum.ndim == 2 and str(spectrum.dtype) in ("uint8", "torch.uint8")
+        seed, pk = _mldsa_bufs(mldsa_seed)
         _lib.qpir_puzzle_bind_hct(self._ctx, theta_begin, spectrum, int(spectrum.shape[0]),
-                                  int(spectrum.shape[1]), seed_psd, kappa, n_l,
+                                  int(spectrum.shape[1]), seed_psd, kappa, n_l, seed, pk,
                                   _st(self.device, stream))
+        return None if pk is None else pk.tobytes()
 
     # ------------------------------------------------------------------ answers
     def _dev(self):
@@ -139,12 +152,14 @@ class EnsServer:
         _lib.qpir_ens_db_write(self._ctx, theta_begin, records, n, _st(self.device, stream))
 
     def puzzle_bind_hct(self, theta_begin: int, spectrum, seed_psd: int, kappa: int = 20,
-                        n_l: int = 3, stream=None) -> None:
+                        n_l: int = 3, mldsa_seed: bytes | None = None, stream=None):
         """NEXT-4 PSD.Puzzle.Bind on the ENS records (qpir_ens_puzzle_bind_hct)."""
         assert spectrum.ndim == 2 and str(spectrum.dtype) in ("uint8", "torch.uint8")
+        seed, pk = _mldsa_bufs(mldsa_seed)
         _lib.qpir_ens_puzzle_bind_hct(self._ctx, theta_begin, spectrum, int(spectrum.shape[0]),
-                                      int(spectrum.shape[1]), seed_psd, kappa, n_l,
+                                      int(spectrum.shape[1]), seed_psd, kappa, n_l, seed, pk,
                                       _st(self.device, stream))
+        return None if pk is None else pk.tobytes()
 
     def answer(self, share, out=None, stream=None):
         if out is None:

@@ -106,7 +106,7 @@ _u64 = ctypes.c_uint64
 _L.qpir_setup.argtypes = [ctypes.POINTER(qpir_params), _vp, _u64, _vp, ctypes.POINTER(_vp)]
 _L.qpir_db_write.argtypes = [_vp, _u64, _u64, _vp, _u64, _vp]
 _L.qpir_puzzle_bind_hct.argtypes = [_vp, _u64, _u64, _vp, _u64, _u64, _u64, ctypes.c_uint32,
-                                    ctypes.c_uint8, _vp]
+                                    ctypes.c_uint8, _vp, _vp, _vp]
 _L.qpir_ens_puzzle_bind_hct.argtypes = _L.qpir_puzzle_bind_hct.argtypes
 _L.qpir_geometry.argtypes = [_vp, ctypes.POINTER(_u64), ctypes.POINTER(_u64),
                              ctypes.POINTER(_u64), ctypes.POINTER(_u64)]
@@ -204,15 +204,22 @@ def qpir_db_write(ctx: int, theta_begin: int, records, n_records: int, stream=No
 
 
 def qpir_puzzle_bind_hct(ctx: int, theta_begin: int, spectrum, n_records: int, spec_stride: int,
-                         seed_psd: int, kappa: int, n_l: int, stream=None):
+                         seed_psd: int, kappa: int, n_l: int, mldsa_seed=None, mldsa_pk=None,
+                         stream=None):
     _check(_L.qpir_puzzle_bind_hct(ctx, theta_begin, n_records, _addr(spectrum), spec_stride,
-                                   _numel(spectrum), seed_psd, kappa, n_l, _stream(stream)), ctx)
+                                   _numel(spectrum), seed_psd, kappa, n_l,
+                                   None if mldsa_seed is None else _addr(mldsa_seed),
+                                   None if mldsa_pk is None else _addr(mldsa_pk),
+                                   _stream(stream)), ctx)
 
 
 def qpir_ens_puzzle_bind_hct(ctx: int, theta_begin: int, spectrum, n_records: int,
-                             spec_stride: int, seed_psd: int, kappa: int, n_l: int, stream=None):
+                             spec_stride: int, seed_psd: int, kappa: int, n_l: int,
+                             mldsa_seed=None, mldsa_pk=None, stream=None):
     _check_ens(_L.qpir_ens_puzzle_bind_hct(ctx, theta_begin, n_records, _addr(spectrum),
                                            spec_stride, _numel(spectrum), seed_psd, kappa, n_l,
+                                           None if mldsa_seed is None else _addr(mldsa_seed),
+                                           None if mldsa_pk is None else _addr(mldsa_pk),
                                            _stream(stream)), ctx)
 
 

@@ -30,7 +30,14 @@ struct BindArgs {
   uint32_t d;               // record bytes (>= 597)
   uint8_t* out;             // records, row stride out_stride
   uint64_t out_stride;
+  // ML-DSA signatures (mldsa.cuh): n rows of 3024 bytes, the signature of
+  // record i at bytes [597, 3017) of row i (16-byte aligned with the record);
+  // nullptr = unsigned (zero slot)
+  const uint8_t* sig = nullptr;
 };
+
+constexpr uint32_t HCT_SIG_END = 3017;   // 597 + 2420
+constexpr uint32_t HCT_SIG_STRIDE = 3024;
 
 static __global__ void puzzle_bind_hct_kernel(BindArgs a) {
   const uint32_t chunks = (a.d + 15) / 16;
@@ -68,8 +75,10 @@ static __global__ void puzzle_bind_hct_kernel(BindArgs a) {
       x = (uint8_t)(a.kappa >> (8 * (b - HCT_SPECTRUM - 32)));
     } else if (b == HCT_SPECTRUM + 36) {
       x = (uint8_t)a.n_l;
+    } else if (a.sig && b < HCT_SIG_END) {
+      x = a.sig[i * HCT_SIG_STRIDE + b];
     }
-    v[k] = x;  // the signature slot and the padding stay zero
+    v[k] = x;  // unsigned signature slot and padding stay zero
   }
   uint8_t* dst = a.out + i * a.out_stride + b0;
   if (b0 + 16 <= a.d && ((reinterpret_cast<uintptr_t>(dst) & 15u) == 0)) {
@@ -97,7 +106,8 @@ __device__ __forceinline__ uint8_t bound_record_byte(const BindArgs& a, uint64_t
   }
   if (b < HCT_SPECTRUM + 36) return (uint8_t)(a.kappa >> (8 * (b - HCT_SPECTRUM - 32)));
   if (b == HCT_SPECTRUM + 36) return (uint8_t)a.n_l;
-  return 0;  // the (unsigned) ML-DSA signature slot and the padding
+  if (a.sig && b < HCT_SIG_END) return a.sig[(theta - a.theta0) * HCT_SIG_STRIDE + b];
+  return 0;  // unsigned signature slot and the padding
 }
 
 static inline void launch_puzzle_bind(const BindArgs& a, cudaStream_t st) {

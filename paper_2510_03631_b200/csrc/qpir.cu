@@ -22,6 +22,7 @@
 #include "host_common.h"
 #include "mma_launch.cuh"
 #include "puzzle.cuh"
+#include "mldsa.cuh"
 
 using namespace qpir;
 using namespace qpir_host;
@@ -90,6 +91,10 @@ struct qpir_ctx {
   uint64_t rec_stage_bytes = 0;
   uint8_t* spec_stage = nullptr;   // host spectrum staging for qpir_puzzle_bind_hct
   uint64_t spec_stage_bytes = 0;
+  uint8_t* mldsa_buf = nullptr;    // ML-DSA: expanded key + 32-byte seed
+  uint64_t mldsa_buf_bytes = 0;
+  uint8_t* sig_stage = nullptr;    // ML-DSA signatures, 3024-byte rows
+  uint64_t sig_stage_bytes = 0;
   std::mutex mu;                   // guards `arenas`
   std::map<cudaStream_t, Arena> arenas;
   uint64_t launches = 0;
@@ -308,10 +313,12 @@ __device__ __forceinline__ void transpose4x4_bytes(uint32_t x0, uint32_t x1, uin
 }
 
 constexpr uint32_t BIND_HEAD = (HCT_SPECTRUM + HCT_PUZZLE + 15) / 16 * 16;  // 608 rows with data
+constexpr uint32_t BIND_HEAD_SIG = HCT_SIG_STRIDE;                              // 3024 with the signature
 
 __global__ void __launch_bounds__(256) pack_bind_tile_kernel(PackArgs a, BindArgs bnd) {
-  // rows [0, 608) of the 16 records, transposed, staged with one pad slot per 16 rows
-  __shared__ uint4 S[BIND_HEAD + BIND_HEAD / 16];
+  // rows [0, head) of the 16 records, transposed, staged with one pad slot per 16 rows
+  extern __shared__ uint4 S[];
+  const uint32_t head = bnd.sig ? BIND_HEAD_SIG : BIND_HEAD;
   const uint32_t j = a.g_lo + blockIdx.x, ch = blockIdx.y, blk = blockIdx.z;
   const uint32_t tid = threadIdx.x;
   const uint64_t row0 = ((uint64_t)blk * a.n_ch + ch) * a.d;  // global row of byte 0
@@ -326,15 +333,17 @@ __global__ void __launch_bounds__(256) pack_bind_tile_kernel(PackArgs a, BindArg
     if (col < a.m && cell < a.n_cells && th[i] >= a.theta0 && th[i] < a.theta0 + a.n_rec) valid |= 1u << i;
   }
   if (!valid) return;
-  if (tid < BIND_HEAD / 16) {
+  if (tid < head / 16) {
     const uint32_t b0 = tid * 16;
     uint32_t X[16][4];  // X[record][word]: bytes b0 .. b0 + 15 of record i
-    if (b0 + 16 <= HCT_SPECTRUM) {
+    const bool sig_chunk = bnd.sig && b0 >= BIND_HEAD;  // whole chunk inside the signature rows
+    if (b0 + 16 <= HCT_SPECTRUM || sig_chunk) {
 #pragma unroll
       for (int i = 0; i < 16; ++i) {
         uint4 v = make_uint4(0u, 0u, 0u, 0u);
         if ((valid >> i) & 1u)
-          v = *reinterpret_cast<const uint4*>(bnd.spectrum + (th[i] - bnd.theta0) * bnd.spec_stride + b0);
+          v = sig_chunk ? *reinterpret_cast<const uint4*>(bnd.sig + (th[i] - bnd.theta0) * HCT_SIG_STRIDE + b0)
+                        : *reinterpret_cast<const uint4*>(bnd.spectrum + (th[i] - bnd.theta0) * bnd.spec_stride + b0);
         X[i][0] = v.x; X[i][1] = v.y; X[i][2] = v.z; X[i][3] = v.w;
       }
     } else {
@@ -380,7 +389,7 @@ __global__ void __launch_bounds__(256) pack_bind_tile_kernel(PackArgs a, BindArg
     if (row < a.row_begin || row >= a.row_begin + a.ell_local) continue;
     const uint64_t rl = row - a.row_begin;
     uint4* dst = reinterpret_cast<uint4*>(a.D + ((size_t)(rl >> 7) * a.G + j) * 2048 + (rl & 127u) * 16);
-    uint4 v = b < BIND_HEAD ? S[b + b / 16] : make_uint4(0u, 0u, 0u, 0u);
+    uint4 v = b < head ? S[b + b / 16] : make_uint4(0u, 0u, 0u, 0u);
     if (valid != 0xFFFFu) {  // partial group: keep the other cells' bytes
       const uint4 o = *dst;
       uint8_t* vb = reinterpret_cast<uint8_t*>(&v);
@@ -430,7 +439,8 @@ int db_write_device(qpir_ctx* ctx, uint64_t theta0, uint64_t n_rec, const uint8_
     b.row_begin = g.row_begin + (uint64_t)y0 * 128;
     b.ell_local = (uint32_t)std::min<uint64_t>(g.ell_local - (uint64_t)y0 * 128, (uint64_t)ny * 128);
     dim3 grid((uint32_t)(j_hi - j_lo + 1), ny);
-    const bool tile = bind && g.d % 16 == 0 && g.d >= BIND_HEAD && bind->spec_stride % 16 == 0 &&
+    const bool tile = bind && g.d % 16 == 0 && g.d >= (bind->sig ? BIND_HEAD_SIG : BIND_HEAD) &&
+                      bind->spec_stride % 16 == 0 &&
                       (reinterpret_cast<uintptr_t>(bind->spectrum) & 15u) == 0 &&
                       g.n_ch <= 65535 && (g.n_cells + g.m - 1) / g.m <= 65535;
     if (tile) {
@@ -439,7 +449,11 @@ int db_write_device(qpir_ctx* ctx, uint64_t theta0, uint64_t n_rec, const uint8_
       if (y0 == 0) {
         const uint32_t nblk = (uint32_t)((g.n_cells + g.m - 1) / g.m);
         dim3 tg((uint32_t)(j_hi - j_lo + 1), (uint32_t)g.n_ch, nblk);
-        pack_bind_tile_kernel<<<tg, 256, 0, st>>>(a, *bind);
+        const uint32_t head = bind->sig ? BIND_HEAD_SIG : BIND_HEAD;
+        const size_t sm = (size_t)(head + head / 16) * 16;
+        CUDA_TRY(ctx, cudaFuncSetAttribute(pack_bind_tile_kernel,
+                                           cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+        pack_bind_tile_kernel<<<tg, 256, sm, st>>>(a, *bind);
         LAUNCH_CHECK(ctx);
       }
       continue;
@@ -723,13 +737,17 @@ int qpir_db_write(qpir_ctx* ctx, uint64_t theta_begin, uint64_t n_records,
 
 int qpir_puzzle_bind_hct(qpir_ctx* ctx, uint64_t theta_begin, uint64_t n_records,
                          const uint8_t* spectrum, uint64_t spec_stride, uint64_t spectrum_len,
-                         uint64_t seed_psd, uint32_t kappa, uint8_t n_l, void* stream) {
+                         uint64_t seed_psd, uint32_t kappa, uint8_t n_l, const uint8_t* mldsa_seed,
+                         uint8_t* mldsa_pk, void* stream) {
   NvtxRange nvtx_("qpir_puzzle_bind_hct");
   if (!ctx) return fail(nullptr, QPIR_E_STATE, "ctx: NULL");
   const Geometry& g = ctx->geo;
   const uint64_t n_all = g.n_cells * g.n_ch;
   if (g.d < HCT_SPECTRUM + HCT_PUZZLE)
     return fail(ctx, QPIR_E_DIMENSION, "rec_bytes: %llu < 597 (560 B spectrum + 37 B puzzle)",
+                (unsigned long long)g.d);
+  if (mldsa_seed && g.d < HCT_SIG_END)
+    return fail(ctx, QPIR_E_DIMENSION, "rec_bytes: %llu < 3017 (spectrum + puzzle + ML-DSA signature)",
                 (unsigned long long)g.d);
   if (theta_begin > n_all || n_records > n_all - theta_begin)
     return fail(ctx, QPIR_E_DIMENSION, "theta range: [%llu, +%llu) exceeds %llu records",
@@ -747,9 +765,26 @@ int qpir_puzzle_bind_hct(qpir_ctx* ctx, uint64_t theta_begin, uint64_t n_records
   const int w = where(spectrum, ctx->device);
   if (w < 0) return fail(ctx, QPIR_E_PARAM, "spectrum: device memory of another device");
   // records are generated inside the pack kernel, straight into the D panels;
-  // a host spectrum is staged in chunks of <= 64 MB
-  const uint64_t chunk = w ? n_records : std::max<uint64_t>(1, (64ull << 20) / spec_stride);
+  // a host spectrum is staged in chunks of <= 64 MB; signatures in chunks of 16K
+  uint64_t chunk = w ? n_records : std::max<uint64_t>(1, (64ull << 20) / spec_stride);
   int rc = QPIR_OK;
+  mldsa::MldsaKey* key = nullptr;
+  if (mldsa_seed) {
+    chunk = std::min<uint64_t>(chunk, 16384);
+    rc = ensure(ctx, (void**)&ctx->mldsa_buf, &ctx->mldsa_buf_bytes, sizeof(mldsa::MldsaKey) + 64);
+    if (rc) return rc;
+    key = reinterpret_cast<mldsa::MldsaKey*>(ctx->mldsa_buf);
+    uint8_t* xi_dev = ctx->mldsa_buf + sizeof(mldsa::MldsaKey);
+    CUDA_TRY(ctx, cudaMemcpyAsync(xi_dev, mldsa_seed, 32, cudaMemcpyDefault, st));
+    CUDA_TRY(ctx, mldsa::keygen(xi_dev, key, st));
+    ctx->launches++;
+    if (mldsa_pk) CUDA_TRY(ctx, cudaMemcpyAsync(mldsa_pk, key->pk, mldsa::PK_BYTES, cudaMemcpyDefault, st));
+    rc = ensure(ctx, (void**)&ctx->sig_stage, &ctx->sig_stage_bytes,
+                std::min(n_records, chunk) * HCT_SIG_STRIDE);
+    if (rc) return rc;
+    // bytes outside [597, 3017) of a staging row are never written: zero once per call
+    CUDA_TRY(ctx, cudaMemsetAsync(ctx->sig_stage, 0, std::min(n_records, chunk) * HCT_SIG_STRIDE, st));
+  }
   if (w == 0) {
     rc = ensure(ctx, (void**)&ctx->spec_stage, &ctx->spec_stage_bytes,
                 std::min(n_records, chunk) * spec_stride);
@@ -773,9 +808,15 @@ int qpir_puzzle_bind_hct(qpir_ctx* ctx, uint64_t theta_begin, uint64_t n_records
     b.d = (uint32_t)g.d;
     b.out = nullptr;
     b.out_stride = 0;
+    if (key) {
+      CUDA_TRY(ctx, mldsa::sign_records(key, theta_begin + t, n, seed_psd, kappa, n_l, ctx->sig_stage, st));
+      ctx->launches++;
+      b.sig = ctx->sig_stage;
+    }
     rc = db_write_device(ctx, theta_begin + t, n, nullptr, st, &b);
     if (rc) return rc;
   }
+  if (mldsa_pk && where(mldsa_pk, ctx->device) == 0) CUDA_TRY(ctx, cudaStreamSynchronize(st));
   if (w == 0) CUDA_TRY(ctx, cudaStreamSynchronize(st));  // the staging buffer is reused per call
   return QPIR_OK;
 }
@@ -1072,7 +1113,7 @@ const char* qpir_last_error(const qpir_ctx* ctx) {
 void qpir_destroy(qpir_ctx* ctx) {
   if (!ctx) return;
   DeviceGuard dg(ctx->device);
-  void* bufs[] = {ctx->D, ctx->rec_stage, ctx->spec_stage};
+  void* bufs[] = {ctx->D, ctx->rec_stage, ctx->spec_stage, ctx->mldsa_buf, ctx->sig_stage};
   for (void* b : bufs)
     if (b) cudaFree(b);
   for (auto& kv : ctx->arenas) {

@@ -15,6 +15,7 @@
 #include "host_common.h"
 #include "mma_launch.cuh"
 #include "puzzle.cuh"
+#include "mldsa.cuh"
 
 using namespace qpir;
 using namespace qpir_host;
@@ -68,6 +69,10 @@ struct qpir_ens_ctx {
   std::atomic<bool> r_written{false};  // a kernel wrote R (puzzle bind): next scan without PDL
   uint8_t* spec_stage = nullptr;       // host spectrum staging (puzzle bind)
   uint64_t spec_stage_bytes = 0;
+  uint8_t* mldsa_buf = nullptr;        // ML-DSA expanded key + seed (puzzle bind)
+  uint64_t mldsa_buf_bytes = 0;
+  uint8_t* sig_stage = nullptr;        // ML-DSA signatures, 3024-byte rows
+  uint64_t sig_stage_bytes = 0;
   std::mutex mu;                // guards `arenas`
   std::map<cudaStream_t, EnsArena> arenas;
   int group = 0;                // env QPIR_ENS_GROUP (0 = auto 32; 1 = atomics only)
@@ -273,11 +278,15 @@ int qpir_ens_db_write(qpir_ens_ctx* ctx, uint64_t theta_begin, uint64_t n_record
 int qpir_ens_puzzle_bind_hct(qpir_ens_ctx* ctx, uint64_t theta_begin, uint64_t n_records,
                              const uint8_t* spectrum, uint64_t spec_stride,
                              uint64_t spectrum_len, uint64_t seed_psd, uint32_t kappa,
-                             uint8_t n_l, void* stream) {
+                             uint8_t n_l, const uint8_t* mldsa_seed, uint8_t* mldsa_pk,
+                             void* stream) {
   NvtxRange nvtx_("qpir_ens_puzzle_bind_hct");
   if (!ctx) return QPIR_E_STATE;
   if (ctx->d < HCT_SPECTRUM + HCT_PUZZLE)
     return ENS_FAIL(ctx, QPIR_E_DIMENSION, "rec_bytes: %llu < 597 (560 B spectrum + 37 B puzzle)",
+                    (unsigned long long)ctx->d);
+  if (mldsa_seed && ctx->d < HCT_SIG_END)
+    return ENS_FAIL(ctx, QPIR_E_DIMENSION, "rec_bytes: %llu < 3017 (spectrum + puzzle + ML-DSA signature)",
                     (unsigned long long)ctx->d);
   if (theta_begin > ctx->r || n_records > ctx->r - theta_begin)
     return ENS_FAIL(ctx, QPIR_E_DIMENSION, "theta range: [%llu, +%llu) exceeds %llu records",
@@ -294,7 +303,23 @@ int qpir_ens_puzzle_bind_hct(qpir_ens_ctx* ctx, uint64_t theta_begin, uint64_t n
   const int w = where(spectrum, ctx->device);
   if (w < 0) return ENS_FAIL(ctx, QPIR_E_PARAM, "spectrum: memory of another device");
   cudaStream_t st = (cudaStream_t)stream;
-  const uint64_t chunk = w ? n_records : std::max<uint64_t>(1, (64ull << 20) / spec_stride);
+  uint64_t chunk = w ? n_records : std::max<uint64_t>(1, (64ull << 20) / spec_stride);
+  qpir::mldsa::MldsaKey* key = nullptr;
+  if (mldsa_seed) {
+    chunk = std::min<uint64_t>(chunk, 16384);
+    int rc = grow(ctx, (void**)&ctx->mldsa_buf, &ctx->mldsa_buf_bytes, sizeof(qpir::mldsa::MldsaKey) + 64);
+    if (rc) return rc;
+    key = reinterpret_cast<qpir::mldsa::MldsaKey*>(ctx->mldsa_buf);
+    uint8_t* xi_dev = ctx->mldsa_buf + sizeof(qpir::mldsa::MldsaKey);
+    ENS_CUDA(ctx, cudaMemcpyAsync(xi_dev, mldsa_seed, 32, cudaMemcpyDefault, st));
+    ENS_CUDA(ctx, qpir::mldsa::keygen(xi_dev, key, st));
+    ctx->launches++;
+    if (mldsa_pk)
+      ENS_CUDA(ctx, cudaMemcpyAsync(mldsa_pk, key->pk, qpir::mldsa::PK_BYTES, cudaMemcpyDefault, st));
+    rc = grow(ctx, (void**)&ctx->sig_stage, &ctx->sig_stage_bytes, std::min(n_records, chunk) * HCT_SIG_STRIDE);
+    if (rc) return rc;
+    ENS_CUDA(ctx, cudaMemsetAsync(ctx->sig_stage, 0, std::min(n_records, chunk) * HCT_SIG_STRIDE, st));
+  }
   if (!w) {
     int rc = grow(ctx, (void**)&ctx->spec_stage, &ctx->spec_stage_bytes,
                   std::min(n_records, chunk) * spec_stride);
@@ -318,10 +343,16 @@ int qpir_ens_puzzle_bind_hct(qpir_ens_ctx* ctx, uint64_t theta_begin, uint64_t n
     b.d = (uint32_t)ctx->d;
     b.out = ctx->R + (theta_begin + t) * ctx->dp;  // rows in place (padding bytes stay zero)
     b.out_stride = ctx->dp;
+    if (key) {
+      ENS_CUDA(ctx, qpir::mldsa::sign_records(key, theta_begin + t, n, seed_psd, kappa, n_l, ctx->sig_stage, st));
+      ctx->launches++;
+      b.sig = ctx->sig_stage;
+    }
     launch_puzzle_bind(b, st);
     ENS_LAUNCHED(ctx);
     ctx->r_written.store(true);
   }
+  if (mldsa_pk && where(mldsa_pk, ctx->device) == 0) ENS_CUDA(ctx, cudaStreamSynchronize(st));
   if (!w) ENS_CUDA(ctx, cudaStreamSynchronize(st));
   return QPIR_OK;
 }
@@ -740,6 +771,8 @@ void qpir_ens_destroy(qpir_ens_ctx* ctx) {
   DeviceGuard dg(ctx->device);
   if (ctx->R) cudaFree(ctx->R);
   if (ctx->spec_stage) cudaFree(ctx->spec_stage);
+  if (ctx->mldsa_buf) cudaFree(ctx->mldsa_buf);
+  if (ctx->sig_stage) cudaFree(ctx->sig_stage);
   for (auto& kv : ctx->arenas) {
     EnsArena& a = kv.second;
     if (a.h2d) cudaStreamSynchronize(a.h2d);

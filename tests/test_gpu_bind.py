@@ -119,3 +119,68 @@ def test_bind_errors_name_the_field(cuda_ok):
             s.puzzle_bind_hct(0, np.zeros((4, 100), np.uint8), 1)
         with pytest.raises(RuntimeError, match="theta range"):
             s.puzzle_bind_hct(14, spec, 1)
+
+
+# ------------------------------------------------------------------ ML-DSA-44 signatures
+_XI = bytes((7 * j + 3) & 0xFF for j in range(32))
+
+
+@pytest.mark.parametrize("device_spec", [True, False])
+def test_signed_bind_matches_oracle(cuda_ok, device_spec):
+    """Puzzle.Bind with the ML-DSA-44 signature of every puzzle (Alg. 1 step 1):
+    the GPU's public key equals the oracle's (and OpenSSL's), and the whole shard
+    -- spectrum, puzzle and 2420-byte signature of every record -- equals the
+    oracle's pack of the oracle's signed records byte for byte (deterministic
+    FIPS 204 signing); ragged cells leave partial 16-cell groups."""
+    P = _P()
+    n_cells, n_ch, d = 21, 2, 3072
+    n = n_cells * n_ch
+    spec = synth.uniform_u8_np(21, (n, 560))
+    want = O.puzzle_bind_hct_signed(spec, 0, 99, 20, 3, d, _XI)
+    with P.PirServer(n_cells, n_ch, d, lwe_n=4) as s:
+        pk = s.puzzle_bind_hct(0, torch.from_numpy(spec).cuda() if device_spec else spec, 99, 20, 3,
+                               mldsa_seed=_XI)
+        D = _read_D(s, n_cells)
+    from oracle import mldsa
+    assert pk == mldsa.keygen(_XI)[0]
+    assert (D == O.pack(want, n_cells, n_ch, d, n_cells)).all()
+
+
+def test_signed_bind_signatures_verify_with_openssl(cuda_ok):
+    """Independent check: signatures read back from the GPU-bound ENS records
+    verify under OpenSSL's ML-DSA-44 (cryptography) with the GPU's public key,
+    and a corrupted record does not."""
+    lib = pytest.importorskip("cryptography.hazmat.primitives.asymmetric.mldsa")
+    P = _P()
+    r, d = 64, 3072
+    spec = synth.uniform_u8_np(22, (r, 560))
+    with P.EnsServer(r, d) as s:
+        pk = s.puzzle_bind_hct(0, torch.from_numpy(spec).cuda(), 123, 20, 3, mldsa_seed=_XI)
+        nb = (r + 7) // 8
+        recs = []
+        for t in (0, 17, r - 1):
+            u = np.zeros(nb, np.uint8)
+            u[t >> 3] = 1 << (t & 7)
+            recs.append((t, s.answer(u).cpu().numpy()))
+    pub = lib.MLDSA44PublicKey.from_public_bytes(pk)
+    for t, rec in recs:
+        assert (rec[:560] == spec[t]).all()
+        pub.verify(rec[597:3017].tobytes(), rec[560:597].tobytes())
+    bad = recs[0][1].copy()
+    bad[700] ^= 1
+    with pytest.raises(Exception):
+        pub.verify(bad[597:3017].tobytes(), bad[560:597].tobytes())
+
+
+def test_signed_bind_ens_matches_oracle(cuda_ok):
+    P = _P()
+    r, d = 40, 3100
+    spec = synth.uniform_u8_np(23, (r, 560))
+    want = O.puzzle_bind_hct_signed(spec, 0, 5, 7, 1, d, _XI)
+    with P.EnsServer(r, d) as s:
+        s.puzzle_bind_hct(0, spec, 5, 7, 1, mldsa_seed=_XI)
+        Q = np.zeros((r, (r + 7) // 8), np.uint8)
+        for t in range(r):
+            Q[t, t >> 3] = 1 << (t & 7)
+        got = s.answer_batch(Q).cpu().numpy()
+    assert (got == want).all()
