@@ -71,8 +71,11 @@ WORKLOADS = {
                         n_cells=327680, n_ch=1, d=3072, kind="batch", B=128, modp=65537),
     "bind-c2": dict(name="NEXT-4 PSD.Puzzle.Bind (Alg. 1 step 1): all 327680 records of the "
                          "1.007 GB regional DB built on the GPU (560 B spectrum + 37 B HCT puzzle "
-                         "+ unsigned 2420 B signature slot) straight into the D panels",
-                    n_cells=8192, n_ch=40, d=3072, kind="bind"),
+                         "+ 2420 B ML-DSA-44 signature of the puzzle) straight into the D panels",
+                    n_cells=8192, n_ch=40, d=3072, kind="bind", sign=True),
+    "bind-c2-unsigned": dict(name="NEXT-4 Puzzle.Bind without the signatures (spectrum + HCT "
+                                  "puzzle + zero slot): the packing alone", n_cells=8192, n_ch=40,
+                             d=3072, kind="bind", sign=False),
     "c5": dict(name="hint D.A, n=1024, one rank's shard of the 32.2 GB DB at G=8 "
                     "(BASELINE configs[4])", n_cells=262144, n_ch=40, d=3072, kind="hint", n=1024,
                shard_of=8),
@@ -647,8 +650,9 @@ def run_bind(args, wl, rank, local):
     spec = synth.uniform_u32(args.seed, (r, 140), device=dev).view(torch.uint8).contiguous()  # 560 B rows
     srv = P.PirServer(n_cells, n_ch, d, lwe_n=4, device=local)
     seed_psd = 0x5D5EED
+    xi = bytes(range(32)) if wl.get("sign") else None  # the PSD's ML-DSA-44 key seed
     for _ in range(args.warmup):
-        srv.puzzle_bind_hct(0, spec, seed_psd, 20, 3, stream=stream)
+        srv.puzzle_bind_hct(0, spec, seed_psd, 20, 3, mldsa_seed=xi, stream=stream)
     torch.cuda.synchronize(dev)
     sampler = ClockSampler(physical_gpu(local))
     l0 = srv.kernel_launches
@@ -657,7 +661,7 @@ def run_bind(args, wl, rank, local):
     sampler.start()
     e0.record(stream)
     for _ in range(args.steps):
-        srv.puzzle_bind_hct(0, spec, seed_psd, 20, 3, stream=stream)
+        srv.puzzle_bind_hct(0, spec, seed_psd, 20, 3, mldsa_seed=xi, stream=stream)
     e1.record(stream)
     torch.cuda.synchronize(dev)
     sampler.stop()
@@ -666,13 +670,13 @@ def run_bind(args, wl, rank, local):
     # e2e: the spectrum from pinned host memory every step (staged by the library)
     h_spec = spec.cpu().pin_memory()
     n_e2e = max(3, min(args.steps, 20))
-    srv.puzzle_bind_hct(0, h_spec, seed_psd, 20, 3, stream=stream)
+    srv.puzzle_bind_hct(0, h_spec, seed_psd, 20, 3, mldsa_seed=xi, stream=stream)
     torch.cuda.synchronize(dev)
     a0 = torch.cuda.Event(enable_timing=True)
     a1 = torch.cuda.Event(enable_timing=True)
     a0.record(stream)
     for _ in range(n_e2e):
-        srv.puzzle_bind_hct(0, h_spec, seed_psd, 20, 3, stream=stream)
+        srv.puzzle_bind_hct(0, h_spec, seed_psd, 20, 3, mldsa_seed=xi, stream=stream)
     a1.record(stream)
     torch.cuda.synchronize(dev)
     te = a0.elapsed_time(a1) / n_e2e
@@ -687,10 +691,14 @@ def run_bind(args, wl, rank, local):
     if not args.no_cpu_baseline:
         from oracle import oracle as O
         O.set_num_threads(os.cpu_count() or 1)
-        ns = 200 * n_ch  # records (whole cells, 24.6 MB of bound DB), oracle bind + pack
+        ns = (200 if not xi else 2) * n_ch  # records (whole cells), oracle bind (+ sign) + pack
         sp = spec[:ns].cpu().numpy()
-        fn = lambda: O.pack(O.puzzle_bind_hct(sp, 0, seed_psd, 20, 3, d), ns // n_ch, n_ch, d,  # noqa: E731
-                            ns // n_ch)
+        if xi:
+            fn = lambda: O.pack(O.puzzle_bind_hct_signed(sp, 0, seed_psd, 20, 3, d, xi),  # noqa: E731
+                                ns // n_ch, n_ch, d, ns // n_ch)
+        else:
+            fn = lambda: O.pack(O.puzzle_bind_hct(sp, 0, seed_psd, 20, 3, d), ns // n_ch, n_ch, d,  # noqa: E731
+                                ns // n_ch)
         _warm_oracle(fn, 1.0)
         t0 = time.perf_counter()
         reps = 0
@@ -698,16 +706,21 @@ def run_bind(args, wl, rank, local):
             fn()
             reps += 1
         el = time.perf_counter() - t0
-        cpu = {"value": round(reps * ns * d / el / 1e9, 3), "unit": "GB/s", "cores": os.cpu_count(),
-               "kind": "oracle", "sample": f"{ns} records ({ns * d / 1e6:.1f} MB), oracle "
-                                           f"qo_puzzle_bind_hct + qo_pack, {reps} repetitions"}
+        cpu = {"value": round(reps * ns * d / el / 1e9, 6), "unit": "GB/s", "cores": 1 if xi else os.cpu_count(),
+               "kind": "oracle", "sample": f"{ns} records ({ns * d / 1e6:.2f} MB), oracle "
+                                           f"{'puzzle_bind_hct_signed (Python ML-DSA-44)' if xi else 'qo_puzzle_bind_hct'}"
+                                           f" + qo_pack, {reps} repetitions",
+               "records_per_s": round(reps * ns / el, 2)}
     line = {"metric": METRIC, "value": round(db / (ms / 1e3) / 1e9, 2),
             "unit": "GB/s (bound DB bytes built per second)", "n_gpus": 1, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": round(ms, 5), "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "u8", "data": "synthetic",
             "config": {"workload": wl["name"], "n_records": r, "rec_bytes": d,
                        "records_per_s": round(r / (ms / 1e3), 1),
-                       "signature": "not computed (ML-DSA not implemented: DESIGN R21)"},
+                       "signature": ("ML-DSA-44 (FIPS 204, deterministic variant) of every puzzle, "
+                                     "signed on the GPU" if xi else "none (zero slot)"),
+                       "paper_context": "Table 1 (P:1448): PSD-HCT Puzzle.Bind on GPU 346 ms for 2^12 "
+                                        "records, 21825 ms for 2^18 (RTX 3060 + CPU signing)"},
             "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": hbm, "unit": "GB/s",
                          "frac": round(achieved / hbm, 4), "traffic": _traffic(args.workload),
                          "kernel": "pack_bind_tile_kernel", "kernel_ms": round(ms, 5),
