@@ -138,9 +138,165 @@ struct Shake {
   }
 };
 
+// Register-resident sponge for the signing hot loop: the state stays in
+// registers (static indices only), message bytes are staged block by block in an
+// 8-byte aligned shared-memory scratch and absorbed / squeezed as 64-bit words
+// (the byte-serial Shake above keeps its state in local memory: one
+// read-modify-write per byte).
+static __device__ __forceinline__ void keccak_reg(uint64_t (&st)[25]) {
+  constexpr int rotc[24] = {1, 3, 6, 10, 15, 21, 28, 36, 45, 55, 2, 14, 27, 41, 56, 8, 25, 43, 62, 18, 39, 61, 20, 44};
+  constexpr int piln[24] = {10, 7, 11, 17, 18, 3, 5, 16, 8, 21, 24, 4, 15, 23, 19, 13, 12, 2, 20, 14, 22, 9, 6, 1};
+#pragma unroll 1
+  for (int r = 0; r < 24; ++r) {
+    uint64_t bc[5];
+#pragma unroll
+    for (int i = 0; i < 5; ++i) bc[i] = st[i] ^ st[i + 5] ^ st[i + 10] ^ st[i + 15] ^ st[i + 20];
+#pragma unroll
+    for (int i = 0; i < 5; ++i) {
+      const uint64_t t = bc[(i + 4) % 5] ^ rol64(bc[(i + 1) % 5], 1);
+#pragma unroll
+      for (int j = 0; j < 25; j += 5) st[j + i] ^= t;
+    }
+    uint64_t t = st[1];
+#pragma unroll
+    for (int i = 0; i < 24; ++i) {
+      const uint64_t b = st[piln[i]];
+      st[piln[i]] = rol64(t, rotc[i]);
+      t = b;
+    }
+#pragma unroll
+    for (int j = 0; j < 25; j += 5) {
+      uint64_t b[5];
+#pragma unroll
+      for (int i = 0; i < 5; ++i) b[i] = st[j + i];
+#pragma unroll
+      for (int i = 0; i < 5; ++i) st[j + i] ^= (~b[(i + 1) % 5]) & b[(i + 2) % 5];
+    }
+    st[0] ^= kRC[r];
+  }
+}
+
+template <int RATE>
+struct RSponge {
+  uint64_t a[25];
+  __device__ __forceinline__ void zero() {
+#pragma unroll
+    for (int i = 0; i < 25; ++i) a[i] = 0;
+  }
+  __device__ __forceinline__ void absorb_block(const uint8_t* blk) {  // 8-byte aligned
+#pragma unroll
+    for (int w = 0; w < RATE / 8; ++w) a[w] ^= reinterpret_cast<const uint64_t*>(blk)[w];
+    keccak_reg(a);
+  }
+  __device__ __forceinline__ void out_block(uint8_t* blk) const {  // RATE bytes of output
+#pragma unroll
+    for (int w = 0; w < RATE / 8; ++w) reinterpret_cast<uint64_t*>(blk)[w] = a[w];
+  }
+  __device__ __forceinline__ void next() { keccak_reg(a); }
+  // absorb p0 || p1 || p2 with the SHAKE padding (one thread; scratch: RATE bytes, 8-aligned)
+  __device__ void absorb_msg(const uint8_t* p0, int n0, const uint8_t* p1, int n1, const uint8_t* p2, int n2,
+                             uint8_t* scratch) {
+    const int total = n0 + n1 + n2;
+    for (int off = 0;; off += RATE) {
+      const int take = min(RATE, total - off);
+#pragma unroll
+      for (int w = 0; w < RATE / 8; ++w) reinterpret_cast<uint64_t*>(scratch)[w] = 0;
+      for (int i = 0; i < take; ++i) {
+        const int m = off + i;
+        scratch[i] = m < n0 ? p0[m] : m < n0 + n1 ? p1[m - n0] : p2[m - n0 - n1];
+      }
+      if (take < RATE) {
+        scratch[take] ^= 0x1F;
+        scratch[RATE - 1] ^= 0x80;
+        absorb_block(scratch);
+        return;
+      }
+      absorb_block(scratch);
+    }
+  }
+};
+
+// Warp-cooperative Keccak-f[1600]: lane i < 25 holds state word A[x + 5y]
+// (x = i % 5, y = i / 5); theta's column parities, pi's lane permutation and
+// chi's row neighbours move through warp shuffles (FIPS 202 Sec. 3.2 steps).
+// Lanes 25..31 take part in the shuffles with a dummy word.
+__device__ __forceinline__ uint64_t shfl64(uint64_t v, int src) {
+  const uint32_t lo = __shfl_sync(0xffffffffu, (uint32_t)v, src);
+  const uint32_t hi = __shfl_sync(0xffffffffu, (uint32_t)(v >> 32), src);
+  return ((uint64_t)hi << 32) | lo;
+}
+__device__ __forceinline__ uint64_t rolv(uint64_t x, int s) { return s ? (x << s) | (x >> (64 - s)) : x; }
+
+static __device__ __noinline__ uint64_t keccak_warp(uint64_t a, int lane) {
+  // rho offsets r[x][y] (FIPS 202 Table 2), indexed x + 5y
+  constexpr int rho[25] = {0, 1, 62, 28, 27, 36, 44, 6, 55, 20, 3, 10, 43, 25, 39,
+                           41, 45, 15, 21, 8, 18, 2, 61, 56, 14};
+  const int l = lane < 25 ? lane : 0;
+  const int x = l % 5, y = l / 5;
+  const int r = rho[l];
+  // pi: B[X][Y] = A[x][y] with X = y, Y = 2x + 3y: destination lane (X, Y) reads
+  // source x = 3 (Y - 3X) mod 5, y = X
+  const int sx = (3 * ((y - 3 * x) % 5 + 10)) % 5;  // here (x, y) play (X, Y)
+  const int pi_src = sx + 5 * x;
+  const int col[4] = {x + 5 * ((y + 1) % 5), x + 5 * ((y + 2) % 5), x + 5 * ((y + 3) % 5), x + 5 * ((y + 4) % 5)};
+  const int xm1 = (x + 4) % 5 + 5 * y, xp1 = (x + 1) % 5 + 5 * y, xp2 = (x + 2) % 5 + 5 * y;
+#pragma unroll 1
+  for (int rd = 0; rd < 24; ++rd) {
+    // theta
+    uint64_t c = a;
+#pragma unroll
+    for (int k = 0; k < 4; ++k) c ^= shfl64(a, col[k]);
+    const uint64_t cm = shfl64(c, xm1), cp = shfl64(c, xp1);
+    a ^= cm ^ rolv(cp, 1);
+    // rho, pi
+    const uint64_t b = shfl64(rolv(a, r), pi_src);
+    // chi
+    const uint64_t b1 = shfl64(b, xp1), b2 = shfl64(b, xp2);
+    a = b ^ (~b1 & b2);
+    // iota
+    if (lane == 0) a ^= kRC[rd];
+  }
+  return a;
+}
+
+// Warp sponge (SHAKE rate RATE): absorb p0 || p1 || p2 with the SHAKE padding;
+// the whole warp calls it; scratch: RATE bytes, 8-byte aligned, per warp.
+template <int RATE>
+__device__ void wsp_absorb(uint64_t& a, const uint8_t* p0, int n0, const uint8_t* p1, int n1,
+                           const uint8_t* p2, int n2, uint8_t* scratch, int lane) {
+  const int total = n0 + n1 + n2;
+  for (int off = 0;; off += RATE) {
+    const int take = min(RATE, total - off);
+    for (int i = lane; i < RATE; i += 32) {
+      const int m = off + i;
+      uint8_t v = 0;
+      if (i < take) v = m < n0 ? p0[m] : m < n0 + n1 ? p1[m - n0] : p2[m - n0 - n1];
+      if (take < RATE) {
+        if (i == take) v ^= 0x1F;
+        if (i == RATE - 1) v ^= 0x80;
+      }
+      scratch[i] = v;
+    }
+    __syncwarp();
+    if (lane < RATE / 8) a ^= reinterpret_cast<const uint64_t*>(scratch)[lane];
+    a = keccak_warp(a, lane);
+    __syncwarp();
+    if (take < RATE) return;
+  }
+}
+template <int RATE>
+__device__ __forceinline__ void wsp_out(uint64_t a, uint8_t* out, int lane) {  // RATE bytes
+  if (lane < RATE / 8) reinterpret_cast<uint64_t*>(out)[lane] = a;
+  __syncwarp();
+}
+
 // ------------------------------------------------------------------ arithmetic
-__device__ __forceinline__ int32_t mulq(int32_t a, int32_t b) {
-  return (int32_t)(((int64_t)a * b) % Q);  // a, b in [0, q)
+__device__ __forceinline__ int32_t mulq(int32_t a, int32_t b) {  // a, b in [0, q)
+  // Barrett: x < 2^46, qt = floor(x * floor(2^64 / q) / 2^64) is floor(x / q) or one less
+  const uint64_t x = (uint64_t)(uint32_t)a * (uint32_t)b;
+  const uint64_t qt = __umul64hi(x, 2201172575745ull);
+  uint32_t r = (uint32_t)(x - qt * (uint64_t)Q);
+  return (int32_t)(r >= (uint32_t)Q ? r - Q : r);
 }
 __device__ __forceinline__ int32_t addq(int32_t a, int32_t b) {
   int32_t s = a + b;
@@ -338,66 +494,116 @@ __device__ __forceinline__ uint4 philox_nonce_block(uint64_t seed, uint64_t thet
                        make_uint2((uint32_t)seed, (uint32_t)(seed >> 32)));
 }
 
+// One signature per warp (WPB warps per CTA): the sponges run in lane 0 (lanes
+// 0..3 for the four mask streams), the polynomial work across the 32 lanes,
+// __syncwarp between steps -- many signatures in flight per SM hide the serial
+// Keccak latency (one signature per 256-thread CTA ran at 319 k/s on C2).
+struct SignSmem {                   // per warp
+  int32_t y[L][256];                // y, then z
+  union {
+    int32_t tmp[K][256];            // NTT(y), then c.s1 / c.s2 / c.t0 products
+    uint8_t w1enc[K * 192];         // w1Encode(w1), hashed before tmp is reused
+  };
+  union {
+    int32_t w[K][256];              // w, then w - c s2, then the hint bits
+    uint8_t ymask[L * 576];         // ExpandMask bytes, unpacked before w is computed
+  };
+  int32_t c[256];
+  alignas(8) uint8_t scratch[L][136];  // sponge block staging (lanes 0..3)
+  alignas(8) uint8_t mu[64];
+  uint8_t rhopp[64], ctilde[32], msg[40], zeros[32];
+  int count[K];
+};
+constexpr int WPB = 3;  // ~14 KB of shared memory per warp: 5 CTAs x 3 warps per SM
+
+static __device__ void ntt_w(int32_t* p, int n, const int32_t* zetas, int lane) {
+  for (int len = 128, lg = 7; len >= 1; len >>= 1, --lg) {
+    for (int t = lane; t < n * 128; t += 32) {
+      const int poly = t >> 7, b = t & 127;
+      const int grp = b >> lg, j = (grp << (lg + 1)) + (b & (len - 1));
+      const int32_t z = zetas[(256 / (2 * len)) + grp];
+      int32_t* w = p + poly * 256;
+      const int32_t tt = mulq(z, w[j + len]);
+      const int32_t a = w[j];
+      w[j + len] = subq(a, tt);
+      w[j] = addq(a, tt);
+    }
+    __syncwarp();
+  }
+}
+
+static __device__ void ntt_inv_w(int32_t* p, int n, const int32_t* zetas, int lane) {
+  for (int len = 1, lg = 0; len < 256; len <<= 1, ++lg) {
+    for (int t = lane; t < n * 128; t += 32) {
+      const int poly = t >> 7, b = t & 127;
+      const int grp = b >> lg, j = (grp << (lg + 1)) + (b & (len - 1));
+      const int32_t z = Q - zetas[(256 / len) - 1 - grp];
+      int32_t* w = p + poly * 256;
+      const int32_t a = w[j], c = w[j + len];
+      w[j] = addq(a, c);
+      w[j + len] = mulq(z, subq(a, c));
+    }
+    __syncwarp();
+  }
+  for (int t = lane; t < n * 256; t += 32) p[t] = mulq(8347681, p[t]);
+  __syncwarp();
+}
+
 // Sign_internal (Alg. 7) of M' = 0 || 0 || pi_theta, rnd = {0}^32.
-static __global__ void __launch_bounds__(THREADS) mldsa_sign_kernel(SignArgs a) {
+static __global__ void __launch_bounds__(32 * WPB) mldsa_sign_kernel(SignArgs a) {
   __shared__ int32_t zetas[256];
-  __shared__ int32_t y[L][256];     // y (normal domain)
-  __shared__ int32_t tmp[K][256];   // NTT(y), then c.s1 / c.s2 / c.t0 products
-  __shared__ int32_t w[K][256];     // w = NTT^-1(A-hat o NTT(y))
-  __shared__ int32_t c[256];
-  __shared__ uint8_t buf[K * 192];  // ExpandMask bytes (4 x 576 > 768) / w1Encode (768)
-  __shared__ uint8_t ymask[L * 576];
-  __shared__ uint8_t mu[64], rhopp[64], ctilde[32], msg[39];
-  __shared__ int s_count[K];
-  const int tid = threadIdx.x;
-  const uint64_t i_rec = blockIdx.x;
+  extern __shared__ __align__(16) uint8_t dsm[];
+  fill_zetas(zetas);
+  __syncthreads();
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  const uint64_t i_rec = (uint64_t)blockIdx.x * WPB + wid;
   if (i_rec >= a.n) return;
+  SignSmem& S = reinterpret_cast<SignSmem*>(dsm)[wid];
   const uint64_t theta = a.theta0 + i_rec;
   const MldsaKey* key = a.key;
-  fill_zetas(zetas);
-  if (tid < 2) {  // the message pi_theta: n_s (Philox, R21) || kappa || n_l
-    const uint4 r = philox_nonce_block(a.seed_psd, theta, tid);
+  S.zeros[lane] = 0;
+  if (lane < 2) {  // the message pi_theta: n_s (Philox, R21) || kappa || n_l
+    const uint4 r = philox_nonce_block(a.seed_psd, theta, lane);
     const uint32_t wds[4] = {r.x, r.y, r.z, r.w};
-    for (int k = 0; k < 16; ++k) msg[2 + 16 * tid + k] = (uint8_t)(wds[k >> 2] >> (8 * (k & 3)));
-  } else if (tid == 2) {
-    msg[0] = 0;  // M' = IntegerToBytes(0, 1) || IntegerToBytes(|ctx| = 0, 1) || M
-    msg[1] = 0;
-    for (int k = 0; k < 4; ++k) msg[34 + k] = (uint8_t)(a.kappa >> (8 * k));
-    msg[38] = (uint8_t)a.n_l;
+    for (int k = 0; k < 16; ++k) S.msg[2 + 16 * lane + k] = (uint8_t)(wds[k >> 2] >> (8 * (k & 3)));
+  } else if (lane == 2) {
+    S.msg[0] = 0;  // M' = IntegerToBytes(0, 1) || IntegerToBytes(|ctx| = 0, 1) || M
+    S.msg[1] = 0;
+    for (int k = 0; k < 4; ++k) S.msg[34 + k] = (uint8_t)(a.kappa >> (8 * k));
+    S.msg[38] = (uint8_t)a.n_l;
   }
-  __syncthreads();
-  if (tid == 0) {
-    Shake h;  // mu = H(tr || M', 64)
-    h.init(136);
-    h.absorb(key->tr, 64);
-    h.absorb(msg, 39);
-    h.finalize();
-    h.squeeze(mu, 64);
-    Shake h2;  // rho'' = H(K || rnd || mu, 64)
-    h2.init(136);
-    h2.absorb(key->Kseed, 32);
-    for (int k = 0; k < 32; ++k) h2.absorb_byte(0);
-    h2.absorb(mu, 64);
-    h2.finalize();
-    h2.squeeze(rhopp, 64);
+  __syncwarp();
+  {
+    uint64_t h = 0;  // mu = H(tr || M', 64)
+    wsp_absorb<136>(h, key->tr, 64, S.msg, 39, nullptr, 0, S.scratch[0], lane);
+    wsp_out<136>(h, S.scratch[0], lane);
+    for (int k = lane; k < 64; k += 32) S.mu[k] = S.scratch[0][k];
+    __syncwarp();
+    uint64_t h2 = 0;  // rho'' = H(K || rnd || mu, 64), rnd = {0}^32
+    wsp_absorb<136>(h2, key->Kseed, 32, S.zeros, 32, S.mu, 64, S.scratch[0], lane);
+    wsp_out<136>(h2, S.scratch[0], lane);
+    for (int k = lane; k < 64; k += 32) S.rhopp[k] = S.scratch[0][k];
+    __syncwarp();
   }
-  __syncthreads();
   for (uint32_t kappa_ctr = 0;; kappa_ctr += L) {
     // ExpandMask (Alg. 34): y[r] = BitUnpack(H(rho'' || (kappa + r), 576), gamma1 - 1, gamma1)
-    if (tid < L) {
-      Shake h;
-      h.init(136);
-      h.absorb(rhopp, 64);
-      const uint32_t idx = kappa_ctr + tid;
-      h.absorb_byte((uint8_t)(idx & 255));
-      h.absorb_byte((uint8_t)(idx >> 8));
-      h.finalize();
-      h.squeeze(ymask + tid * 576, 576);
+    for (int r = 0; r < L; ++r) {
+      uint64_t h = 0;
+      const uint32_t idx = kappa_ctr + r;
+      const uint8_t ib[2] = {(uint8_t)(idx & 255), (uint8_t)(idx >> 8)};
+      wsp_absorb<136>(h, S.rhopp, 64, ib, 2, nullptr, 0, S.scratch[0], lane);
+      for (int o = 0; o < 576; o += 136) {  // 5 blocks (680 >= 576 bytes)
+        if (o) h = keccak_warp(h, lane);
+        const int w = lane, nb = min(136, 576 - o);
+        if (w < 17 && 8 * w < nb) {
+          for (int k = 0; k < 8 && 8 * w + k < nb; ++k) S.ymask[r * 576 + o + 8 * w + k] = (uint8_t)(h >> (8 * k));
+        }
+      }
     }
-    __syncthreads();
-    for (int e = tid; e < L * 64; e += blockDim.x) {  // 4 coefficients per 9 bytes
+    __syncwarp();
+    for (int e = lane; e < L * 64; e += 32) {  // 4 coefficients per 9 bytes
       const int r = e >> 6, g4 = e & 63;
-      const uint8_t* v = ymask + r * 576 + g4 * 9;
+      const uint8_t* v = S.ymask + r * 576 + g4 * 9;
       uint64_t lo = 0;
       for (int b = 0; b < 8; ++b) lo |= (uint64_t)v[b] << (8 * b);
       const uint64_t hi = v[8];
@@ -406,122 +612,130 @@ static __global__ void __launch_bounds__(THREADS) mldsa_sign_kernel(SignArgs a) 
         uint32_t f;
         if (bit + 18 <= 64) f = (uint32_t)(lo >> bit) & 0x3FFFFu;
         else f = (uint32_t)((lo >> bit) | (hi << (64 - bit))) & 0x3FFFFu;
-        const int32_t yv = GAMMA1 - (int32_t)f;
-        y[r][4 * g4 + k] = modq(yv);
-        tmp[r][4 * g4 + k] = modq(yv);
+        const int32_t yv = modq(GAMMA1 - (int32_t)f);
+        S.y[r][4 * g4 + k] = yv;
+        S.tmp[r][4 * g4 + k] = yv;
       }
     }
-    __syncthreads();
-    ntt(&tmp[0][0], L, zetas);
-    for (int cc = tid; cc < 256; cc += blockDim.x)
+    __syncwarp();
+    ntt_w(&S.tmp[0][0], L, zetas, lane);
+    for (int cc = lane; cc < 256; cc += 32)
       for (int i = 0; i < K; ++i) {
         int32_t acc = 0;
-        for (int j = 0; j < L; ++j) acc = addq(acc, mulq(key->A[i][j][cc], tmp[j][cc]));
-        w[i][cc] = acc;
+        for (int j = 0; j < L; ++j) acc = addq(acc, mulq(key->A[i][j][cc], S.tmp[j][cc]));
+        S.w[i][cc] = acc;
       }
-    __syncthreads();
-    ntt_inv(&w[0][0], K, zetas);
+    __syncwarp();
+    ntt_inv_w(&S.w[0][0], K, zetas, lane);
     // w1Encode (Alg. 28): HighBits, 6 bits per coefficient, 4 coefficients -> 3 bytes
-    for (int e = tid; e < K * 64; e += blockDim.x) {
+    for (int e = lane; e < K * 64; e += 32) {
       const int i = e >> 6, g4 = e & 63;
       uint32_t v = 0;
       for (int k = 0; k < 4; ++k) {
         int32_t r1, r0;
-        decompose(w[i][4 * g4 + k], r1, r0);
+        decompose(S.w[i][4 * g4 + k], r1, r0);
         v |= (uint32_t)r1 << (6 * k);
       }
-      buf[i * 192 + g4 * 3 + 0] = (uint8_t)v;
-      buf[i * 192 + g4 * 3 + 1] = (uint8_t)(v >> 8);
-      buf[i * 192 + g4 * 3 + 2] = (uint8_t)(v >> 16);
+      S.w1enc[i * 192 + g4 * 3 + 0] = (uint8_t)v;
+      S.w1enc[i * 192 + g4 * 3 + 1] = (uint8_t)(v >> 8);
+      S.w1enc[i * 192 + g4 * 3 + 2] = (uint8_t)(v >> 16);
     }
-    __syncthreads();
-    if (tid == 0) {
-      Shake h;  // c~ = H(mu || w1Encode(w1), 32)
-      h.init(136);
-      h.absorb(mu, 64);
-      h.absorb(buf, K * 192);
-      h.finalize();
-      h.squeeze(ctilde, 32);
-      // SampleInBall (Alg. 29)
-      for (int k = 0; k < 256; ++k) c[k] = 0;
-      Shake s;
-      s.init(136);
-      s.absorb(ctilde, 32);
-      s.finalize();
+    for (int k = lane; k < 256; k += 32) S.c[k] = 0;
+    __syncwarp();
+    {
+      uint64_t h = 0;  // c~ = H(mu || w1Encode(w1), 32)
+      uint8_t* sc = S.scratch[0];
+      wsp_absorb<136>(h, S.mu, 64, S.w1enc, K * 192, nullptr, 0, sc, lane);
+      wsp_out<136>(h, sc, lane);
+      if (lane < 32) S.ctilde[lane] = sc[lane];
+      __syncwarp();
+      // SampleInBall (Alg. 29): lane 0 samples, the warp squeezes further blocks
+      uint64_t sb = 0;
+      wsp_absorb<136>(sb, S.ctilde, 32, nullptr, 0, nullptr, 0, sc, lane);
+      wsp_out<136>(sb, sc, lane);
       uint64_t hb = 0;
-      for (int k = 0; k < 8; ++k) hb |= (uint64_t)s.squeeze_byte() << (8 * k);
-      for (int i = 256 - TAU; i < 256; ++i) {
-        int j = s.squeeze_byte();
-        while (j > i) j = s.squeeze_byte();
-        c[i] = c[j];
-        c[j] = ((hb >> (i + TAU - 256)) & 1) ? Q - 1 : 1;
+      for (int k = 0; k < 8; ++k) hb |= (uint64_t)sc[k] << (8 * k);
+      int i = 256 - TAU, pos = 8;
+      while (true) {
+        if (lane == 0) {
+          while (i < 256 && pos < 136) {
+            const int j = sc[pos++];
+            if (j > i) continue;
+            S.c[i] = S.c[j];
+            S.c[j] = ((hb >> (i + TAU - 256)) & 1) ? Q - 1 : 1;
+            ++i;
+          }
+        }
+        i = __shfl_sync(0xffffffffu, i, 0);
+        if (i == 256) break;
+        sb = keccak_warp(sb, lane);
+        __syncwarp();
+        wsp_out<136>(sb, sc, lane);
+        pos = 0;
       }
+      __syncwarp();
     }
-    __syncthreads();
-    ntt(c, 1, zetas);
+    ntt_w(S.c, 1, zetas, lane);
     // z = y + NTT^-1(c o s1); checked against gamma1 - beta
-    for (int e = tid; e < L * 256; e += blockDim.x) tmp[e >> 8][e & 255] = mulq(c[e & 255], key->s1[e >> 8][e & 255]);
-    __syncthreads();
-    ntt_inv(&tmp[0][0], L, zetas);
+    for (int e = lane; e < L * 256; e += 32) S.tmp[e >> 8][e & 255] = mulq(S.c[e & 255], key->s1[e >> 8][e & 255]);
+    __syncwarp();
+    ntt_inv_w(&S.tmp[0][0], L, zetas, lane);
     int bad = 0;
-    for (int e = tid; e < L * 256; e += blockDim.x) {
-      const int32_t z = addq(y[e >> 8][e & 255], tmp[e >> 8][e & 255]);
-      y[e >> 8][e & 255] = z;  // y now holds z
+    for (int e = lane; e < L * 256; e += 32) {
+      const int32_t z = addq(S.y[e >> 8][e & 255], S.tmp[e >> 8][e & 255]);
+      S.y[e >> 8][e & 255] = z;  // y now holds z
       const int32_t zc = centered(z);
       if (zc >= GAMMA1 - BETA || zc <= -(GAMMA1 - BETA)) bad = 1;
     }
     // r0 = LowBits(w - c s2), checked against gamma2 - beta; w <- w - c s2
-    for (int e = tid; e < K * 256; e += blockDim.x) tmp[e >> 8][e & 255] = mulq(c[e & 255], key->s2[e >> 8][e & 255]);
-    __syncthreads();
-    ntt_inv(&tmp[0][0], K, zetas);
-    for (int e = tid; e < K * 256; e += blockDim.x) {
-      const int32_t v = subq(w[e >> 8][e & 255], tmp[e >> 8][e & 255]);
-      w[e >> 8][e & 255] = v;
+    for (int e = lane; e < K * 256; e += 32) S.tmp[e >> 8][e & 255] = mulq(S.c[e & 255], key->s2[e >> 8][e & 255]);
+    __syncwarp();
+    ntt_inv_w(&S.tmp[0][0], K, zetas, lane);
+    for (int e = lane; e < K * 256; e += 32) {
+      const int32_t v = subq(S.w[e >> 8][e & 255], S.tmp[e >> 8][e & 255]);
+      S.w[e >> 8][e & 255] = v;
       int32_t r1, r0;
       decompose(v, r1, r0);
       if (r0 >= GAMMA2 - BETA || r0 <= -(GAMMA2 - BETA)) bad = 1;
     }
-    if (__syncthreads_or(bad)) continue;
+    if (__any_sync(0xffffffffu, bad)) continue;
     // c t0; h = MakeHint(-ct0, w - cs2 + ct0); ||ct0|| < gamma2, #h <= omega
-    for (int e = tid; e < K * 256; e += blockDim.x) tmp[e >> 8][e & 255] = mulq(c[e & 255], key->t0[e >> 8][e & 255]);
-    __syncthreads();
-    ntt_inv(&tmp[0][0], K, zetas);
-    int ones = 0;
-    for (int e = tid; e < K * 256; e += blockDim.x) {
-      const int32_t ct0 = tmp[e >> 8][e & 255];
+    for (int e = lane; e < K * 256; e += 32) S.tmp[e >> 8][e & 255] = mulq(S.c[e & 255], key->t0[e >> 8][e & 255]);
+    __syncwarp();
+    ntt_inv_w(&S.tmp[0][0], K, zetas, lane);
+    int cnt[K] = {0, 0, 0, 0};
+    for (int e = lane; e < K * 256; e += 32) {
+      const int32_t ct0 = S.tmp[e >> 8][e & 255];
       const int32_t cc = centered(ct0);
       if (cc >= GAMMA2 || cc <= -GAMMA2) bad = 1;
-      const int32_t r = addq(w[e >> 8][e & 255], ct0);  // w - cs2 + ct0
-      const int32_t zz = subq(0, ct0);                    // -ct0
+      const int32_t r = addq(S.w[e >> 8][e & 255], ct0);  // w - cs2 + ct0
       int32_t h1, h0, v1, v0;
       decompose(r, h1, h0);
-      decompose(addq(r, zz), v1, v0);
+      decompose(subq(r, ct0), v1, v0);                     // r + (-ct0)
       const int hint = h1 != v1;
-      w[e >> 8][e & 255] = hint;  // w now holds the hint bits
-      ones += hint;
+      S.w[e >> 8][e & 255] = hint;  // w now holds the hint bits
+      cnt[e >> 8] += hint;
     }
-    if (__syncthreads_or(bad)) continue;
-    // count hint ones per polynomial
-    if (tid < K) s_count[tid] = 0;
-    __syncthreads();
-    if (ones) {
-      for (int e = tid; e < K * 256; e += blockDim.x)
-        if (w[e >> 8][e & 255]) atomicAdd(&s_count[e >> 8], 1);
+    if (__any_sync(0xffffffffu, bad)) continue;
+    int total = 0;
+#pragma unroll
+    for (int i = 0; i < K; ++i) {
+      const int ci = __reduce_add_sync(0xffffffffu, cnt[i]);
+      if (lane == 0) S.count[i] = ci;
+      total += ci;
     }
-    __syncthreads();
-    if (s_count[0] + s_count[1] + s_count[2] + s_count[3] > OMEGA) {
-      __syncthreads();
-      continue;
-    }
+    if (total > OMEGA) continue;
+    __syncwarp();
     // sigEncode (Alg. 26): c~ || BitPack(z, gamma1 - 1, gamma1) || HintBitPack(h)
     uint8_t* sig = a.out + i_rec * REC_STAGE + SIG_OFF;
-    for (int k = tid; k < 32; k += blockDim.x) sig[k] = ctilde[k];
-    for (int e = tid; e < L * 64; e += blockDim.x) {  // 4 coefficients -> 9 bytes
+    if (lane < 8)
+      for (int k = 0; k < 4; ++k) sig[4 * lane + k] = S.ctilde[4 * lane + k];
+    for (int e = lane; e < L * 64; e += 32) {  // 4 coefficients -> 9 bytes
       const int r = e >> 6, g4 = e & 63;
       uint64_t lo = 0;
       uint32_t hi = 0;
       for (int k = 0; k < 4; ++k) {
-        const uint32_t f = (uint32_t)(GAMMA1 - centered(y[r][4 * g4 + k]));  // 18 bits
+        const uint32_t f = (uint32_t)(GAMMA1 - centered(S.y[r][4 * g4 + k]));  // 18 bits
         const int bit = 18 * k;
         lo |= (uint64_t)f << bit;
         if (bit + 18 > 64) hi |= f >> (64 - bit);
@@ -530,14 +744,14 @@ static __global__ void __launch_bounds__(THREADS) mldsa_sign_kernel(SignArgs a) 
       for (int b = 0; b < 8; ++b) o[b] = (uint8_t)(lo >> (8 * b));
       o[8] = (uint8_t)hi;
     }
-    if (tid < K) {  // HintBitPack (Alg. 20): indices of poly tid after the previous polys'
+    if (lane < K) {  // HintBitPack (Alg. 20): indices of poly `lane` after the previous polys'
       uint8_t* hp = sig + 32 + L * 576;
       int index = 0;
-      for (int i = 0; i < tid; ++i) index += s_count[i];
+      for (int i = 0; i < lane; ++i) index += S.count[i];
       for (int j = 0; j < 256; ++j)
-        if (w[tid][j]) hp[index++] = (uint8_t)j;
-      hp[OMEGA + tid] = (uint8_t)index;
-      if (tid == K - 1)
+        if (S.w[lane][j]) hp[index++] = (uint8_t)j;
+      hp[OMEGA + lane] = (uint8_t)index;
+      if (lane == K - 1)
         for (int k = index; k < OMEGA; ++k) hp[k] = 0;
     }
     return;
@@ -559,7 +773,10 @@ static inline cudaError_t sign_records(const MldsaKey* key, uint64_t theta0, uin
   a.kappa = kappa;
   a.n_l = n_l;
   a.out = stage;
-  mldsa_sign_kernel<<<(uint32_t)n, THREADS, 0, st>>>(a);
+  const size_t sm = WPB * sizeof(SignSmem);
+  cudaError_t e = cudaFuncSetAttribute(mldsa_sign_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+  if (e != cudaSuccess) return e;
+  mldsa_sign_kernel<<<(uint32_t)((n + WPB - 1) / WPB), 32 * WPB, sm, st>>>(a);
   return cudaGetLastError();
 }
 
