@@ -8,9 +8,9 @@
  * paper_2510_03631_b200/ (the CUDA path) and includes none of its headers.
  *
  * Citation keys: P:NNN = PAPER.md line, S:NNN = SPEC.md line, SURVEY = SURVEY.md
- * section, DESIGN = DESIGN.md "Readings" table (R1..R12).
+ * section, DESIGN = DESIGN.md "Readings" table (R1..R21).
  *
- * What is computed (plain definitions, DESIGN R1..R12 for everything the paper
+ * What is computed (plain definitions, DESIGN R1..R21 for everything the paper
  * leaves open):
  *   - the PIR response rho <- PIR.Query.Response(q, DB)  (Def. 1, P:241;
  *     Alg. 1 step 18) read as the LWE answer ans = D.qu mod 2^32,
@@ -21,7 +21,11 @@
  *   - the offline precomputation (Offline-online mode) read as
  *     the LWE hint H = D.A mod 2^32 (DESIGN R7);
  *   - client side (Def. 1 Client.Query / BlockReconst):
- *     keygen, query, decode of a Regev-LWE PIR (DESIGN R1, R4-R8).
+ *     keygen, query, decode of a Regev-LWE PIR (DESIGN R1, R4-R8);
+ *   - the NEXT rows: Chor XOR PIR (Alg. 3, R15/R16), Goldberg PIR over F_p
+ *     with Lagrange and Berlekamp-Welch reconstruction (Alg. 4, R17/R18),
+ *     CIP-PIR offline/online (R19), HCT Puzzle.Gen / Puzzle.Bind (Alg. 1
+ *     step 1, R21; the ML-DSA-44 signatures are in oracle/mldsa.py).
  *
  * Every server-side result is the plain modular matrix product in Z_{2^32};
  * the loops below are the textbook triple loops in uint32_t arithmetic
