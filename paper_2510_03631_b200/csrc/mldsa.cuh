@@ -498,8 +498,7 @@ __device__ __forceinline__ uint4 philox_nonce_block(uint64_t seed, uint64_t thet
 // 0..3 for the four mask streams), the polynomial work across the 32 lanes,
 // __syncwarp between steps -- many signatures in flight per SM hide the serial
 // Keccak latency (one signature per 256-thread CTA ran at 319 k/s on C2).
-struct SignSmem {                   // per warp
-  int32_t y[L][256];                // y, then z
+struct SignSmem {                   // per warp (y / z live in registers: 32 per lane)
   union {
     int32_t tmp[K][256];            // NTT(y), then c.s1 / c.s2 / c.t0 products
     uint8_t w1enc[K * 192];         // w1Encode(w1), hashed before tmp is reused
@@ -514,7 +513,7 @@ struct SignSmem {                   // per warp
   uint8_t rhopp[64], ctilde[32], msg[40], zeros[32];
   int count[K];
 };
-constexpr int WPB = 3;  // ~14 KB of shared memory per warp: 5 CTAs x 3 warps per SM
+constexpr int WPB = 4;  // ~10 KB of shared memory per warp: 5 CTAs x 4 warps per SM
 
 static __device__ void ntt_w(int32_t* p, int n, const int32_t* zetas, int lane) {
   for (int len = 128, lg = 7; len >= 1; len >>= 1, --lg) {
@@ -585,6 +584,7 @@ static __global__ void __launch_bounds__(32 * WPB) mldsa_sign_kernel(SignArgs a)
     for (int k = lane; k < 64; k += 32) S.rhopp[k] = S.scratch[0][k];
     __syncwarp();
   }
+  int32_t yr[32];  // y, then z: coefficient lane + 32 j of the four polynomials
   for (uint32_t kappa_ctr = 0;; kappa_ctr += L) {
     // ExpandMask (Alg. 34): y[r] = BitUnpack(H(rho'' || (kappa + r), 576), gamma1 - 1, gamma1)
     for (int r = 0; r < L; ++r) {
@@ -601,21 +601,16 @@ static __global__ void __launch_bounds__(32 * WPB) mldsa_sign_kernel(SignArgs a)
       }
     }
     __syncwarp();
-    for (int e = lane; e < L * 64; e += 32) {  // 4 coefficients per 9 bytes
-      const int r = e >> 6, g4 = e & 63;
-      const uint8_t* v = S.ymask + r * 576 + g4 * 9;
-      uint64_t lo = 0;
-      for (int b = 0; b < 8; ++b) lo |= (uint64_t)v[b] << (8 * b);
-      const uint64_t hi = v[8];
-      for (int k = 0; k < 4; ++k) {
-        const int bit = 18 * k;
-        uint32_t f;
-        if (bit + 18 <= 64) f = (uint32_t)(lo >> bit) & 0x3FFFFu;
-        else f = (uint32_t)((lo >> bit) | (hi << (64 - bit))) & 0x3FFFFu;
-        const int32_t yv = modq(GAMMA1 - (int32_t)f);
-        S.y[r][4 * g4 + k] = yv;
-        S.tmp[r][4 * g4 + k] = yv;
-      }
+#pragma unroll
+    for (int j = 0; j < 32; ++j) {  // coefficient lane + 32 j of the flattened y
+      const int r = j >> 3, cidx = lane + 32 * (j & 7);
+      const int bit = 18 * cidx, b = bit >> 3;
+      const uint8_t* v = S.ymask + r * 576 + b;
+      uint32_t word = v[0] | ((uint32_t)v[1] << 8) | ((uint32_t)v[2] << 16);
+      if (b + 3 < 576) word |= (uint32_t)v[3] << 24;
+      const uint32_t f = (word >> (bit & 7)) & 0x3FFFFu;
+      yr[j] = modq(GAMMA1 - (int32_t)f);
+      S.tmp[r][cidx] = yr[j];
     }
     __syncwarp();
     ntt_w(&S.tmp[0][0], L, zetas, lane);
@@ -681,9 +676,11 @@ static __global__ void __launch_bounds__(32 * WPB) mldsa_sign_kernel(SignArgs a)
     __syncwarp();
     ntt_inv_w(&S.tmp[0][0], L, zetas, lane);
     int bad = 0;
-    for (int e = lane; e < L * 256; e += 32) {
-      const int32_t z = addq(S.y[e >> 8][e & 255], S.tmp[e >> 8][e & 255]);
-      S.y[e >> 8][e & 255] = z;  // y now holds z
+#pragma unroll
+    for (int j = 0; j < 32; ++j) {
+      const int e = lane + 32 * j;
+      const int32_t z = addq(yr[j], S.tmp[e >> 8][e & 255]);
+      yr[j] = z;  // y now holds z
       const int32_t zc = centered(z);
       if (zc >= GAMMA1 - BETA || zc <= -(GAMMA1 - BETA)) bad = 1;
     }
@@ -726,6 +723,12 @@ static __global__ void __launch_bounds__(32 * WPB) mldsa_sign_kernel(SignArgs a)
     }
     if (total > OMEGA) continue;
     __syncwarp();
+#pragma unroll
+    for (int j = 0; j < 32; ++j) {  // z (centred) into tmp for the packing
+      const int e = lane + 32 * j;
+      S.tmp[e >> 8][e & 255] = centered(yr[j]);
+    }
+    __syncwarp();
     // sigEncode (Alg. 26): c~ || BitPack(z, gamma1 - 1, gamma1) || HintBitPack(h)
     uint8_t* sig = a.out + i_rec * REC_STAGE + SIG_OFF;
     if (lane < 8)
@@ -735,7 +738,7 @@ static __global__ void __launch_bounds__(32 * WPB) mldsa_sign_kernel(SignArgs a)
       uint64_t lo = 0;
       uint32_t hi = 0;
       for (int k = 0; k < 4; ++k) {
-        const uint32_t f = (uint32_t)(GAMMA1 - centered(S.y[r][4 * g4 + k]));  // 18 bits
+        const uint32_t f = (uint32_t)(GAMMA1 - S.tmp[r][4 * g4 + k]);  // 18 bits
         const int bit = 18 * k;
         lo |= (uint64_t)f << bit;
         if (bit + 18 > 64) hi |= f >> (64 - bit);

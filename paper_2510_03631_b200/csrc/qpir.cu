@@ -315,10 +315,16 @@ __device__ __forceinline__ void transpose4x4_bytes(uint32_t x0, uint32_t x1, uin
 constexpr uint32_t BIND_HEAD = (HCT_SPECTRUM + HCT_PUZZLE + 15) / 16 * 16;  // 608 rows with data
 constexpr uint32_t BIND_HEAD_SIG = HCT_SIG_STRIDE;                              // 3024 with the signature
 
-__global__ void __launch_bounds__(256) pack_bind_tile_kernel(PackArgs a, BindArgs bnd) {
+// SIG: the records carry ML-DSA signatures (rows [597, 3017) from bnd.sig); a
+// separate instantiation keeps the unsigned kernel free of the signature branches.
+template <bool SIG>
+__global__ void __launch_bounds__(256, 3) pack_bind_tile_kernel(PackArgs a, BindArgs bnd) {
   // rows [0, head) of the 16 records, transposed, staged with one pad slot per 16 rows
-  extern __shared__ uint4 S[];
-  const uint32_t head = bnd.sig ? BIND_HEAD_SIG : BIND_HEAD;
+  // (static shared memory for the 608-row unsigned prefix, dynamic for 3024 rows)
+  extern __shared__ uint4 S_dyn[];
+  __shared__ uint4 S_st[SIG ? 1 : BIND_HEAD + BIND_HEAD / 16];
+  uint4* S = SIG ? S_dyn : S_st;
+  constexpr uint32_t head = SIG ? BIND_HEAD_SIG : BIND_HEAD;
   const uint32_t j = a.g_lo + blockIdx.x, ch = blockIdx.y, blk = blockIdx.z;
   const uint32_t tid = threadIdx.x;
   const uint64_t row0 = ((uint64_t)blk * a.n_ch + ch) * a.d;  // global row of byte 0
@@ -336,7 +342,7 @@ __global__ void __launch_bounds__(256) pack_bind_tile_kernel(PackArgs a, BindArg
   if (tid < head / 16) {
     const uint32_t b0 = tid * 16;
     uint32_t X[16][4];  // X[record][word]: bytes b0 .. b0 + 15 of record i
-    const bool sig_chunk = bnd.sig && b0 >= BIND_HEAD;  // whole chunk inside the signature rows
+    const bool sig_chunk = SIG && b0 >= BIND_HEAD;  // whole chunk inside the signature rows
     if (b0 + 16 <= HCT_SPECTRUM || sig_chunk) {
 #pragma unroll
       for (int i = 0; i < 16; ++i) {
@@ -360,8 +366,16 @@ __global__ void __launch_bounds__(256) pack_bind_tile_kernel(PackArgs a, BindArg
             X[i][0] = r.x; X[i][1] = r.y; X[i][2] = r.z; X[i][3] = r.w;
             continue;
           }
+          // the chunk at 592: kappa (4 B) || n_l || signature bytes 0..10 (or zeros)
+          static_assert(HCT_SPECTRUM + 32 == BIND_HEAD - 16, "one straddling chunk");
 #pragma unroll
-          for (int k = 0; k < 16; ++k) by[k] = bound_record_byte(bnd, th[i], b0 + k);
+          for (int k = 0; k < 4; ++k) by[k] = (uint8_t)(bnd.kappa >> (8 * k));
+          by[4] = (uint8_t)bnd.n_l;
+          if constexpr (SIG) {
+            const uint8_t* sg = bnd.sig + (th[i] - bnd.theta0) * HCT_SIG_STRIDE;
+#pragma unroll
+            for (int k = 5; k < 16; ++k) by[k] = sg[b0 + k];
+          }
         }
 #pragma unroll
         for (int w = 0; w < 4; ++w)
@@ -449,11 +463,16 @@ int db_write_device(qpir_ctx* ctx, uint64_t theta0, uint64_t n_rec, const uint8_
       if (y0 == 0) {
         const uint32_t nblk = (uint32_t)((g.n_cells + g.m - 1) / g.m);
         dim3 tg((uint32_t)(j_hi - j_lo + 1), (uint32_t)g.n_ch, nblk);
-        const uint32_t head = bind->sig ? BIND_HEAD_SIG : BIND_HEAD;
-        const size_t sm = (size_t)(head + head / 16) * 16;
-        CUDA_TRY(ctx, cudaFuncSetAttribute(pack_bind_tile_kernel,
-                                           cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
-        pack_bind_tile_kernel<<<tg, 256, sm, st>>>(a, *bind);
+        const size_t sm = bind->sig ? (size_t)(BIND_HEAD_SIG + BIND_HEAD_SIG / 16) * 16 : 0;
+        auto kern = bind->sig ? pack_bind_tile_kernel<true> : pack_bind_tile_kernel<false>;
+        // the attribute call costs host time on every launch (measured: 0.29 -> 0.46 ms
+        // per unsigned C2 bind): set it once, and only for the dynamic-smem form
+        static std::atomic<bool> sig_attr{false};
+        if (bind->sig && !sig_attr.load()) {
+          CUDA_TRY(ctx, cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+          sig_attr.store(true);
+        }
+        kern<<<tg, 256, sm, st>>>(a, *bind);
         LAUNCH_CHECK(ctx);
       }
       continue;
