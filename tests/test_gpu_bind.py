@@ -184,3 +184,35 @@ def test_signed_bind_ens_matches_oracle(cuda_ok):
             Q[t, t >> 3] = 1 << (t & 7)
         got = s.answer_batch(Q).cpu().numpy()
     assert (got == want).all()
+
+
+@pytest.mark.parametrize("seed", range(6))
+def test_bind_fuzz_geometries(cuda_ok, seed):
+    """Random geometries (cells, channels, m, record size, row shard, bound theta
+    range, spectrum stride / placement) through both packing kernels: the
+    shard equals the oracle's pack of the oracle's bound records, with the
+    unbound records left as written."""
+    P = _P()
+    rng = np.random.default_rng(1000 + seed)
+    n_ch = int(rng.integers(1, 4))
+    n_cells = int(rng.integers(5, 70))
+    m = int(rng.choice([0, 16, 32]))
+    d = int(rng.choice([608, 640, 1000, 3072]))
+    n = n_cells * n_ch
+    t0 = int(rng.integers(0, n // 2))
+    cnt = int(rng.integers(1, n - t0 + 1))
+    stride = int(rng.choice([560, 576, 600]))
+    base = synth.uniform_u8_np(2000 + seed, (n, d))
+    spec = synth.uniform_u8_np(3000 + seed, (cnt, stride))
+    want = base.copy()
+    want[t0:t0 + cnt] = O.puzzle_bind_hct(spec, t0, 55 + seed, 20 + seed, seed, d)
+    mm = m or n_cells
+    full = O.pack(want, n_cells, n_ch, d, mm)
+    ell = full.shape[0]
+    r0 = int(rng.integers(0, ell // 2))
+    r1 = int(rng.integers(r0 + 1, ell + 1))
+    with P.PirServer(n_cells, n_ch, d, m=m, lwe_n=4, row_begin=r0, row_end=r1, records=base) as s:
+        sp = torch.from_numpy(spec).cuda() if seed % 2 else spec
+        s.puzzle_bind_hct(t0, sp, 55 + seed, 20 + seed, seed)
+        D = _read_D(s, s.m)
+    assert (D == full[r0:r1]).all()
