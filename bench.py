@@ -3,7 +3,8 @@
 "PIR answer DB-scan GB/s and queries/sec per GPU at 1/2/4/8 B200 vs HBM roof").
 
     python bench.py [--gpus N] [--steps K] [--warmup W]
-                    [--workload c1|c2|c3|c4-64|c4-256|c5|ens-c2|ens-c2-b128|ftr-c2-b128|oop-c2|bind-c2]
+                    [--workload c1|c2|c3|c4-64|c4-256|c5|ens-c2|ens-c2-b128|ftr-c2-b128|oop-c2|
+                                bind-c2|bind-c2-unsigned]
                     [--impl ours|reference] [--no-cpu-baseline] [--no-e2e] [--graph 0|1]
     torchrun --nproc-per-node N bench.py --gpus N ...   (plain `--gpus N` re-runs itself
                                                         under torchrun on 127.0.0.1)
@@ -14,6 +15,10 @@ A step = one pass of the whole hot path over one batch of synthetic input:
   c3            single query on the 32.2 GB nationwide DB row-sharded over N GPUs
   c4-64/256     batch of 64/256 queries on the 8.05 GB DB (limb split + tcgen05 GEMM)
   c5            hint H = D.A (n = 1024) for one rank's shard of the 32 GB DB
+  ens-c2 / ens-c2-b128 / ftr-c2-b128 / oop-c2   the NEXT rows (Chor XOR PIR: 1 and 128
+                shares; Goldberg PIR over F_65537, 128 queries; CIP-PIR online answer)
+  bind-c2       Puzzle.Bind of every C2 record: HCT puzzle + ML-DSA-44 signature on the
+                GPU, packed into D (bind-c2-unsigned: the packing alone)
 At N > 1, c2 is weak scaling (each rank holds a 40-channel 1.007 GB slice; the
 DB grows with N), c3 is strong scaling (fixed 32.2 GB).
 value = DB bytes scanned by all ranks / max-over-ranks device time.
