@@ -222,12 +222,6 @@ __global__ void __launch_bounds__(CONV ? MMA_THREADS + MMA_CONV_THREADS : MMA_TH
               while (ld_acquire_u32(issued) < ld_acquire_u32(issued + 1) * need) __nanosleep(128);
             }
           }
-          if constexpr (CONV) {
-            // the converters' generic-proxy stores of this K-block's limb planes
-            // are visible (acquire) before the async-proxy bulk copy reads them
-            while (ld_acquire_u32(a.kb_done + kb) != a.epoch) __nanosleep(64);
-            fence_proxy_async_global();
-          }
           mbar_wait(&empty[stage], phase ^ 1);
           mbar_arrive_expect_tx(&full[stage], C::STAGE_BYTES);
           uint8_t* dst = smem + stage * C::STAGE_BYTES;
@@ -237,6 +231,13 @@ __global__ void __launch_bounds__(CONV ? MMA_THREADS + MMA_CONV_THREADS : MMA_TH
             const uint8_t* src = a.A + panel * a.a_pstride + (uint64_t)kb * (GPB * 2048);
             if (a.l2hint) bulk_g2s_hint(dst + p * C::PANEL_BYTES, src, C::PANEL_BYTES, &full[stage], polA);
             else bulk_g2s(dst + p * C::PANEL_BYTES, src, C::PANEL_BYTES, &full[stage]);
+          }
+          if constexpr (CONV) {
+            // the D panels above do not depend on the conversion: only the limb
+            // tile waits until the converters' generic-proxy stores of this
+            // K-block are visible (acquire) to the async-proxy bulk copy
+            while (ld_acquire_u32(a.kb_done + kb) != a.epoch) __nanosleep(64);
+            fence_proxy_async_global();
           }
           const uint8_t* srcB = a.B + (uint64_t)nt * a.b_tstride + (uint64_t)kb * (GPB * BN * 16);
           if (a.l2hint) bulk_g2s_hint(dst + C::A_BYTES, srcB, C::B_BYTES, &full[stage], polB);
