@@ -95,6 +95,7 @@ struct qpir_ctx {
   uint64_t mldsa_buf_bytes = 0;
   uint8_t* sig_stage = nullptr;    // ML-DSA signatures, 3024-byte rows
   uint64_t sig_stage_bytes = 0;
+  bool bind_sig_attr = false;      // dynamic-smem attribute of the signed packing kernel set
   std::mutex mu;                   // guards `arenas`
   std::map<cudaStream_t, Arena> arenas;
   uint64_t launches = 0;
@@ -467,10 +468,9 @@ int db_write_device(qpir_ctx* ctx, uint64_t theta0, uint64_t n_rec, const uint8_
         auto kern = bind->sig ? pack_bind_tile_kernel<true> : pack_bind_tile_kernel<false>;
         // the attribute call costs host time on every launch (measured: 0.29 -> 0.46 ms
         // per unsigned C2 bind): set it once, and only for the dynamic-smem form
-        static std::atomic<bool> sig_attr{false};
-        if (bind->sig && !sig_attr.load()) {
+        if (bind->sig && !ctx->bind_sig_attr) {  // per context: attributes are per device
           CUDA_TRY(ctx, cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
-          sig_attr.store(true);
+          ctx->bind_sig_attr = true;
         }
         kern<<<tg, 256, sm, st>>>(a, *bind);
         LAUNCH_CHECK(ctx);
