@@ -762,6 +762,34 @@ def run_bind(args, wl, rank, local, world=1):
     print(json.dumps(line), flush=True)
 
 
+# The default run (c2) also measures the other hot-path rows in child processes on
+# the same GPU, after its own timed region, and attaches a compact summary of each
+# line ("secondary"), so every row has numbers from the driver's own run; the
+# headline fields above are the c2 measurement alone.
+SECONDARY = [("c4-64", []), ("c4-256", []), ("c5", []), ("ens-c2", []), ("ens-c2-b128", []),
+             ("ftr-c2-b128", []), ("oop-c2", []), ("bind-c2", ["--steps", "8"])]
+
+
+def _secondary_workloads():
+    out = []
+    for w, extra in SECONDARY:
+        cmd = [sys.executable, os.path.abspath(__file__), "--workload", w, "--no-cpu-baseline",
+               "--no-e2e", *extra]
+        try:
+            p = subprocess.run(cmd, capture_output=True, text=True, timeout=240)
+            d = json.loads(p.stdout.strip().splitlines()[-1])
+            r = d.get("roofline") or {}
+            c = d.get("clocks") or {}
+            out.append({"workload": w, "value": d.get("value"), "unit": d.get("unit"),
+                        "ms_per_step": d.get("ms_per_step"), "steps": d.get("steps"),
+                        "queries_per_s": d.get("queries_per_s"), "bound": r.get("bound"),
+                        "frac": r.get("frac"), "gpu_launches": d.get("gpu_launches"),
+                        "sm_mhz": c.get("sm_mhz"), "reasons": c.get("reasons")})
+        except Exception as e:  # a failed child is reported, never hidden
+            out.append({"workload": w, "error": f"{type(e).__name__}: {str(e)[:200]}"})
+    return out
+
+
 def _traffic(workload):
     """DRAM bytes per launch of the dominant kernel from a committed ncu --set full
     summary (profiles/traffic_<workload>.json), else None."""
@@ -783,6 +811,8 @@ def main():
     ap.add_argument("--seed", type=int, default=2025)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-secondary", action="store_true",
+                    help="default run only: skip the summaries of the other workloads")
     ap.add_argument("--graph", type=int, default=None,
                     help="1: capture the K timed steps into one CUDA graph and replay it "
                          "(N = 1; default on for the launch-bound c1 workload only)")
@@ -1187,8 +1217,10 @@ def main():
             "queries_per_s": round(qps, 1) if qps else None,
             "roofline": roof, "cpu_baseline": cpu_base, "e2e": e2e, "gpu_launches": launches,
             "clocks": clocks}
-    print(json.dumps(line), flush=True)
     srv.close()
+    if world == 1 and args.workload == "c2" and not args.no_secondary:
+        line["secondary"] = _secondary_workloads()
+    print(json.dumps(line), flush=True)
     if world > 1:
         torch.distributed.destroy_process_group()
 
