@@ -119,6 +119,11 @@ def test_bind_errors_name_the_field(cuda_ok):
             s.puzzle_bind_hct(0, np.zeros((4, 100), np.uint8), 1)
         with pytest.raises(RuntimeError, match="theta range"):
             s.puzzle_bind_hct(14, spec, 1)
+        s.puzzle_bind_hct(3, np.zeros((0, 560), np.uint8), 1)  # empty range: a no-op
+    with P.PirServer(16, 1, 1000, lwe_n=4) as s:  # room for the puzzle, not for a signature
+        s.puzzle_bind_hct(0, spec, 1)
+        with pytest.raises(RuntimeError, match="rec_bytes"):
+            s.puzzle_bind_hct(0, spec, 1, mldsa_seed=bytes(32))
 
 
 # ------------------------------------------------------------------ ML-DSA-44 signatures
