@@ -170,8 +170,7 @@ int main() {
   unsigned int* prog; cudaMalloc(&prog, 4096);
 #define CPL(W, RS, LS, SPL) { auto k = cpasync_ls_probe<W, RS, LS>; size_t sm = RS * KB * W; cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm); \
     run("cp.async+LS W=" #W " RS=" #RS " LS=" #LS " sp=" #SPL, [&] { cudaMemsetAsync(prog, 0, 4096); k<<<148, 256, sm>>>(rec, SPL, prog, sink); }); }
-  CPA(32, 12, 3) CPA(32, 24, 3) CPA(64, 12, 3)
-  CPL(32, 12, 8, 3) CPL(32, 12, 16, 3) CPL(32, 24, 16, 3) CPL(32, 12, 4, 3)
-  CPA(32, 12, 6) CPL(32, 12, 8, 6)
+  CPA(32, 12, 3) CPA(48, 12, 3) CPA(64, 12, 3) CPA(32, 12, 2) CPA(48, 12, 2)
+  TMA(32, 12, 3) TMA(48, 12, 3) TMA(64, 12, 3)
   return 0;
 }
