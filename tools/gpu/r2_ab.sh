@@ -1,5 +1,6 @@
 #!/usr/bin/env bash
-# Same-box A/B: round-1 build (ab_r01/) vs current, C2 / ENS / FTR variants.
+# Same-box A/B: round-1 build vs current (C2 / ENS / FTR variants).  Create the
+# round-1 tree first: git worktree add ab_r01 6a560f7 && (cd ab_r01 && python paper_2510_03631_b200/build.py)
 cd $GRAFT_REPO_ROOT
 O=gpurun_out/r2ab; mkdir -p $O
 j() { python -c "import json,sys;d=json.loads(sys.stdin.read().strip().splitlines()[-1]);print(d['ms_per_step'],d['value'],d.get('roofline',{}).get('frac'),d['clocks']['sm_mhz'],d['clocks']['reasons'])"; }
