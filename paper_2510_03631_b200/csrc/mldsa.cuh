@@ -259,6 +259,46 @@ static __device__ __noinline__ uint64_t keccak_warp(uint64_t a, int lane) {
   return a;
 }
 
+// Four independent states in one pass (the four ExpandMask streams): the same
+// round code with the states interleaved, so their shuffles overlap.
+static __device__ __noinline__ void keccak_warp4(uint64_t (&a)[4], int lane) {
+  constexpr int rho[25] = {0, 1, 62, 28, 27, 36, 44, 6, 55, 20, 3, 10, 43, 25, 39,
+                           41, 45, 15, 21, 8, 18, 2, 61, 56, 14};
+  const int l = lane < 25 ? lane : 0;
+  const int x = l % 5, y = l / 5;
+  const int r = rho[l];
+  const int sx = (3 * ((y - 3 * x) % 5 + 10)) % 5;
+  const int pi_src = sx + 5 * x;
+  const int col[4] = {x + 5 * ((y + 1) % 5), x + 5 * ((y + 2) % 5), x + 5 * ((y + 3) % 5), x + 5 * ((y + 4) % 5)};
+  const int xm1 = (x + 4) % 5 + 5 * y, xp1 = (x + 1) % 5 + 5 * y, xp2 = (x + 2) % 5 + 5 * y;
+#pragma unroll 1
+  for (int rd = 0; rd < 24; ++rd) {
+    uint64_t c[4], b[4];
+#pragma unroll
+    for (int s = 0; s < 4; ++s) c[s] = a[s];
+#pragma unroll
+    for (int k = 0; k < 4; ++k)
+#pragma unroll
+      for (int s = 0; s < 4; ++s) c[s] ^= shfl64(a[s], col[k]);
+#pragma unroll
+    for (int s = 0; s < 4; ++s) {
+      const uint64_t cm = shfl64(c[s], xm1), cp = shfl64(c[s], xp1);
+      a[s] ^= cm ^ rolv(cp, 1);
+    }
+#pragma unroll
+    for (int s = 0; s < 4; ++s) b[s] = shfl64(rolv(a[s], r), pi_src);
+#pragma unroll
+    for (int s = 0; s < 4; ++s) {
+      const uint64_t b1 = shfl64(b[s], xp1), b2 = shfl64(b[s], xp2);
+      a[s] = b[s] ^ (~b1 & b2);
+    }
+    if (lane == 0) {
+#pragma unroll
+      for (int s = 0; s < 4; ++s) a[s] ^= kRC[rd];
+    }
+  }
+}
+
 // Warp sponge (SHAKE rate RATE): absorb p0 || p1 || p2 with the SHAKE padding;
 // the whole warp calls it; scratch: RATE bytes, 8-byte aligned, per warp.
 template <int RATE>
@@ -587,16 +627,31 @@ static __global__ void __launch_bounds__(32 * WPB) mldsa_sign_kernel(SignArgs a)
   int32_t yr[32];  // y, then z: coefficient lane + 32 j of the four polynomials
   for (uint32_t kappa_ctr = 0;; kappa_ctr += L) {
     // ExpandMask (Alg. 34): y[r] = BitUnpack(H(rho'' || (kappa + r), 576), gamma1 - 1, gamma1)
-    for (int r = 0; r < L; ++r) {
-      uint64_t h = 0;
-      const uint32_t idx = kappa_ctr + r;
-      const uint8_t ib[2] = {(uint8_t)(idx & 255), (uint8_t)(idx >> 8)};
-      wsp_absorb<136>(h, S.rhopp, 64, ib, 2, nullptr, 0, S.scratch[0], lane);
+    {
+      // the four streams H(rho'' || IntegerToBytes(kappa + r, 2)) side by side:
+      // one padded block each (66 message bytes < 136), then 5 output blocks
+      uint64_t h[L];
+#pragma unroll
+      for (int r = 0; r < L; ++r) {
+        const uint32_t idx = kappa_ctr + r;
+        for (int i = lane; i < 136; i += 32) {
+          uint8_t v = i < 64 ? S.rhopp[i] : i == 64 ? (uint8_t)(idx & 255) : i == 65 ? (uint8_t)(idx >> 8) : 0;
+          if (i == 66) v ^= 0x1F;
+          if (i == 135) v ^= 0x80;
+          S.scratch[r][i] = v;
+        }
+      }
+      __syncwarp();
+#pragma unroll
+      for (int r = 0; r < L; ++r) h[r] = lane < 17 ? reinterpret_cast<const uint64_t*>(S.scratch[r])[lane] : 0ull;
       for (int o = 0; o < 576; o += 136) {  // 5 blocks (680 >= 576 bytes)
-        if (o) h = keccak_warp(h, lane);
-        const int w = lane, nb = min(136, 576 - o);
-        if (w < 17 && 8 * w < nb) {
-          for (int k = 0; k < 8 && 8 * w + k < nb; ++k) S.ymask[r * 576 + o + 8 * w + k] = (uint8_t)(h >> (8 * k));
+        keccak_warp4(h, lane);
+        const int nb = min(136, 576 - o);
+        if (lane < 17 && 8 * lane < nb) {
+#pragma unroll
+          for (int r = 0; r < L; ++r)
+            for (int k = 0; k < 8 && 8 * lane + k < nb; ++k)
+              S.ymask[r * 576 + o + 8 * lane + k] = (uint8_t)(h[r] >> (8 * k));
         }
       }
     }
