@@ -261,7 +261,7 @@ static __device__ __noinline__ uint64_t keccak_warp(uint64_t a, int lane) {
 
 // Four independent states in one pass (the four ExpandMask streams): the same
 // round code with the states interleaved, so their shuffles overlap.
-static __device__ __noinline__ void keccak_warp4(uint64_t (&a)[4], int lane) {
+static __device__ __forceinline__ void keccak_warp4(uint64_t (&a)[4], int lane) {
   constexpr int rho[25] = {0, 1, 62, 28, 27, 36, 44, 6, 55, 20, 3, 10, 43, 25, 39,
                            41, 45, 15, 21, 8, 18, 2, 61, 56, 14};
   const int l = lane < 25 ? lane : 0;
