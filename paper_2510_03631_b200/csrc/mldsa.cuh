@@ -17,6 +17,7 @@
 // arithmetic runs across the CTA (256 threads: one coefficient or one NTT
 // butterfly per thread per step).
 #pragma once
+#include <algorithm>
 #include <cstdint>
 
 #include "philox.cuh"
@@ -525,6 +526,7 @@ struct SignArgs {
   uint64_t seed_psd;   // the puzzles' nonce key (DESIGN R21)
   uint32_t kappa, n_l;
   uint8_t* out;        // n rows of REC_STAGE bytes; signature at SIG_OFF
+  uint32_t* ticket;    // zeroed before the launch: the warps' record counter
 };
 
 // nonce block blk (16 bytes) of pi_theta: Philox(key = seed_psd, ctr = (theta_lo,
@@ -588,16 +590,10 @@ static __device__ void ntt_inv_w(int32_t* p, int n, const int32_t* zetas, int la
   __syncwarp();
 }
 
-// Sign_internal (Alg. 7) of M' = 0 || 0 || pi_theta, rnd = {0}^32.
-static __global__ void __launch_bounds__(32 * WPB) mldsa_sign_kernel(SignArgs a) {
-  __shared__ int32_t zetas[256];
-  extern __shared__ __align__(16) uint8_t dsm[];
-  fill_zetas(zetas);
-  __syncthreads();
-  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-  const uint64_t i_rec = (uint64_t)blockIdx.x * WPB + wid;
-  if (i_rec >= a.n) return;
-  SignSmem& S = reinterpret_cast<SignSmem*>(dsm)[wid];
+// Sign_internal (Alg. 7) of M' = 0 || 0 || pi_theta, rnd = {0}^32, for record
+// i_rec; the whole warp calls it.
+static __device__ __forceinline__ void sign_one(const SignArgs& a, SignSmem& S, const int32_t* zetas,
+                                                uint64_t i_rec, int lane) {
   const uint64_t theta = a.theta0 + i_rec;
   const MldsaKey* key = a.key;
   S.zeros[lane] = 0;
@@ -816,13 +812,37 @@ static __global__ void __launch_bounds__(32 * WPB) mldsa_sign_kernel(SignArgs a)
   }
 }
 
+// Persistent warps: each warp takes the next record from a.ticket until all n
+// are signed. The rejection loop's iteration count is geometric (FIPS 204: ~4.25
+// expected for ML-DSA-44), so warps finish at different times; one record per
+// warp with CTAs of WPB warps kept each CTA resident until its slowest
+// signature was done (ncu: 15 % warps active of a 31 % occupancy limit).
+static __global__ void __launch_bounds__(32 * WPB) mldsa_sign_kernel(SignArgs a) {
+  __shared__ int32_t zetas[256];
+  extern __shared__ __align__(16) uint8_t dsm[];
+  fill_zetas(zetas);
+  __syncthreads();
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  SignSmem& S = reinterpret_cast<SignSmem*>(dsm)[wid];
+  for (;;) {
+    uint32_t t = 0;
+    if (lane == 0) t = atomicAdd(a.ticket, 1u);
+    const uint64_t i_rec = __shfl_sync(0xffffffffu, t, 0);
+    if (i_rec >= a.n) return;
+    sign_one(a, S, zetas, i_rec, lane);
+    __syncwarp();
+  }
+}
+
 // host launchers (the caller owns `key`, `xi_dev` (32 bytes) and `stage`)
 static inline cudaError_t keygen(const uint8_t* xi_dev, MldsaKey* key, cudaStream_t st) {
   mldsa_keygen_kernel<<<1, THREADS, 0, st>>>(xi_dev, key);
   return cudaGetLastError();
 }
+// `ticket`: one device u32 the launcher zeroes on `st` (n < 2^32 per launch).
 static inline cudaError_t sign_records(const MldsaKey* key, uint64_t theta0, uint64_t n, uint64_t seed_psd,
-                                       uint32_t kappa, uint32_t n_l, uint8_t* stage, cudaStream_t st) {
+                                       uint32_t kappa, uint32_t n_l, uint8_t* stage, uint32_t* ticket,
+                                       cudaStream_t st) {
   SignArgs a;
   a.key = key;
   a.theta0 = theta0;
@@ -831,10 +851,18 @@ static inline cudaError_t sign_records(const MldsaKey* key, uint64_t theta0, uin
   a.kappa = kappa;
   a.n_l = n_l;
   a.out = stage;
+  a.ticket = ticket;
   const size_t sm = WPB * sizeof(SignSmem);
   cudaError_t e = cudaFuncSetAttribute(mldsa_sign_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
   if (e != cudaSuccess) return e;
-  mldsa_sign_kernel<<<(uint32_t)((n + WPB - 1) / WPB), 32 * WPB, sm, st>>>(a);
+  int dev = 0, n_sm = 0, per_sm = 0;
+  if ((e = cudaGetDevice(&dev)) != cudaSuccess) return e;
+  if ((e = cudaDeviceGetAttribute(&n_sm, cudaDevAttrMultiProcessorCount, dev)) != cudaSuccess) return e;
+  if ((e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, mldsa_sign_kernel, 32 * WPB, sm)) != cudaSuccess)
+    return e;
+  const uint64_t blocks = std::min<uint64_t>((n + WPB - 1) / WPB, (uint64_t)n_sm * std::max(per_sm, 1));
+  if ((e = cudaMemsetAsync(ticket, 0, sizeof(uint32_t), st)) != cudaSuccess) return e;
+  mldsa_sign_kernel<<<(uint32_t)blocks, 32 * WPB, sm, st>>>(a);
   return cudaGetLastError();
 }
 

@@ -784,16 +784,18 @@ int qpir_puzzle_bind_hct(qpir_ctx* ctx, uint64_t theta_begin, uint64_t n_records
   const int w = where(spectrum, ctx->device);
   if (w < 0) return fail(ctx, QPIR_E_PARAM, "spectrum: device memory of another device");
   // records are generated inside the pack kernel, straight into the D panels;
-  // a host spectrum is staged in chunks of <= 64 MB; signatures in chunks of 16K
+  // a host spectrum is staged in chunks of <= 64 MB; signatures in chunks of 64K (198 MB of staging rows)
   uint64_t chunk = w ? n_records : std::max<uint64_t>(1, (64ull << 20) / spec_stride);
   int rc = QPIR_OK;
   mldsa::MldsaKey* key = nullptr;
+  uint32_t* ticket = nullptr;  // the signer's record counter (after xi in mldsa_buf)
   if (mldsa_seed) {
-    chunk = std::min<uint64_t>(chunk, 16384);
+    chunk = std::min<uint64_t>(chunk, 65536);
     rc = ensure(ctx, (void**)&ctx->mldsa_buf, &ctx->mldsa_buf_bytes, sizeof(mldsa::MldsaKey) + 64);
     if (rc) return rc;
     key = reinterpret_cast<mldsa::MldsaKey*>(ctx->mldsa_buf);
     uint8_t* xi_dev = ctx->mldsa_buf + sizeof(mldsa::MldsaKey);
+    ticket = reinterpret_cast<uint32_t*>(xi_dev + 32);
     CUDA_TRY(ctx, cudaMemcpyAsync(xi_dev, mldsa_seed, 32, cudaMemcpyDefault, st));
     CUDA_TRY(ctx, mldsa::keygen(xi_dev, key, st));
     ctx->launches++;
@@ -828,7 +830,8 @@ int qpir_puzzle_bind_hct(qpir_ctx* ctx, uint64_t theta_begin, uint64_t n_records
     b.out = nullptr;
     b.out_stride = 0;
     if (key) {
-      CUDA_TRY(ctx, mldsa::sign_records(key, theta_begin + t, n, seed_psd, kappa, n_l, ctx->sig_stage, st));
+      CUDA_TRY(ctx, mldsa::sign_records(key, theta_begin + t, n, seed_psd, kappa, n_l, ctx->sig_stage,
+                                            ticket, st));
       ctx->launches++;
       b.sig = ctx->sig_stage;
     }

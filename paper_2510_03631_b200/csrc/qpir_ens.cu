@@ -305,12 +305,14 @@ int qpir_ens_puzzle_bind_hct(qpir_ens_ctx* ctx, uint64_t theta_begin, uint64_t n
   cudaStream_t st = (cudaStream_t)stream;
   uint64_t chunk = w ? n_records : std::max<uint64_t>(1, (64ull << 20) / spec_stride);
   qpir::mldsa::MldsaKey* key = nullptr;
+  uint32_t* ticket = nullptr;  // the signer's record counter (after xi in mldsa_buf)
   if (mldsa_seed) {
-    chunk = std::min<uint64_t>(chunk, 16384);
+    chunk = std::min<uint64_t>(chunk, 65536);
     int rc = grow(ctx, (void**)&ctx->mldsa_buf, &ctx->mldsa_buf_bytes, sizeof(qpir::mldsa::MldsaKey) + 64);
     if (rc) return rc;
     key = reinterpret_cast<qpir::mldsa::MldsaKey*>(ctx->mldsa_buf);
     uint8_t* xi_dev = ctx->mldsa_buf + sizeof(qpir::mldsa::MldsaKey);
+    ticket = reinterpret_cast<uint32_t*>(xi_dev + 32);
     ENS_CUDA(ctx, cudaMemcpyAsync(xi_dev, mldsa_seed, 32, cudaMemcpyDefault, st));
     ENS_CUDA(ctx, qpir::mldsa::keygen(xi_dev, key, st));
     ctx->launches++;
@@ -344,7 +346,8 @@ int qpir_ens_puzzle_bind_hct(qpir_ens_ctx* ctx, uint64_t theta_begin, uint64_t n
     b.out = ctx->R + (theta_begin + t) * ctx->dp;  // rows in place (padding bytes stay zero)
     b.out_stride = ctx->dp;
     if (key) {
-      ENS_CUDA(ctx, qpir::mldsa::sign_records(key, theta_begin + t, n, seed_psd, kappa, n_l, ctx->sig_stage, st));
+      ENS_CUDA(ctx, qpir::mldsa::sign_records(key, theta_begin + t, n, seed_psd, kappa, n_l, ctx->sig_stage,
+                                            ticket, st));
       ctx->launches++;
       b.sig = ctx->sig_stage;
     }
