@@ -228,76 +228,86 @@ __device__ __forceinline__ uint64_t shfl64(uint64_t v, int src) {
 }
 __device__ __forceinline__ uint64_t rolv(uint64_t x, int s) { return s ? (x << s) | (x >> (64 - s)) : x; }
 
-static __device__ __noinline__ uint64_t keccak_warp(uint64_t a, int lane) {
-  // rho offsets r[x][y] (FIPS 202 Table 2), indexed x + 5y
-  constexpr int rho[25] = {0, 1, 62, 28, 27, 36, 44, 6, 55, 20, 3, 10, 43, 25, 39,
-                           41, 45, 15, 21, 8, 18, 2, 61, 56, 14};
-  const int l = lane < 25 ? lane : 0;
-  const int x = l % 5, y = l / 5;
-  const int r = rho[l];
-  // pi: B[X][Y] = A[x][y] with X = y, Y = 2x + 3y: destination lane (X, Y) reads
-  // source x = 3 (Y - 3X) mod 5, y = X
-  const int sx = (3 * ((y - 3 * x) % 5 + 10)) % 5;  // here (x, y) play (X, Y)
-  const int pi_src = sx + 5 * x;
-  const int col[4] = {x + 5 * ((y + 1) % 5), x + 5 * ((y + 2) % 5), x + 5 * ((y + 3) % 5), x + 5 * ((y + 4) % 5)};
-  const int xm1 = (x + 4) % 5 + 5 * y, xp1 = (x + 1) % 5 + 5 * y, xp2 = (x + 2) % 5 + 5 * y;
-#pragma unroll 1
-  for (int rd = 0; rd < 24; ++rd) {
-    // theta
-    uint64_t c = a;
+// Per-lane constants of the warp-cooperative round (lane i < 25 holds A[x + 5y];
+// lanes 25..31 shadow lane 0 and are never read).
+struct KLane {
+  int c1, c2, c4;   // A[x][y+1], A[x][y+2]-partner, A[x][y+4]: theta's column sum in 3 shuffles
+  int xm1, xp1;     // C[x-1], C[x+1]
+  int p0, p1, p2;   // pi sources of B[x][y], B[x+1][y], B[x+2][y] (chi reads them directly)
+  int sw, rr;       // rho offset r[x][y] = 32 sw + rr
+  uint64_t rcmask;  // lane 0: iota applies
+  __device__ __forceinline__ explicit KLane(int lane) {
+    // rho offsets r[x][y] (FIPS 202 Table 2), indexed x + 5y
+    constexpr uint32_t rho[25] = {0, 1, 62, 28, 27, 36, 44, 6, 55, 20, 3, 10, 43, 25, 39,
+                                  41, 45, 15, 21, 8, 18, 2, 61, 56, 14};
+    const int l = lane < 25 ? lane : 0;
+    const int x = l % 5, y = l / 5;
+    c1 = x + 5 * ((y + 1) % 5);
+    c2 = x + 5 * ((y + 2) % 5);
+    c4 = x + 5 * ((y + 4) % 5);
+    xm1 = (x + 4) % 5 + 5 * y;
+    xp1 = (x + 1) % 5 + 5 * y;
+    // pi: B[X][Y] = A[x][y] with X = y, Y = 2x + 3y: lane (X, Y) reads source
+    // x = 3 (Y - 3X) mod 5, y = X
+    auto pisrc = [](int X, int Y) { return (3 * ((Y - 3 * X) % 5 + 10)) % 5 + 5 * X; };
+    p0 = pisrc(x, y);
+    p1 = pisrc((x + 1) % 5, y);
+    p2 = pisrc((x + 2) % 5, y);
+    uint32_t r = 0;
 #pragma unroll
-    for (int k = 0; k < 4; ++k) c ^= shfl64(a, col[k]);
-    const uint64_t cm = shfl64(c, xm1), cp = shfl64(c, xp1);
-    a ^= cm ^ rolv(cp, 1);
-    // rho, pi
-    const uint64_t b = shfl64(rolv(a, r), pi_src);
-    // chi
-    const uint64_t b1 = shfl64(b, xp1), b2 = shfl64(b, xp2);
-    a = b ^ (~b1 & b2);
-    // iota
-    if (lane == 0) a ^= kRC[rd];
+    for (int i = 0; i < 25; ++i) r = i == l ? rho[i] : r;  // no local-memory table
+    sw = r >= 32;
+    rr = r & 31;
+    rcmask = lane == 0 ? ~0ull : 0ull;
   }
-  return a;
+};
+
+// rotate left by the lane's rho offset: a half swap, then two funnel shifts
+__device__ __forceinline__ uint64_t rol_lane(uint64_t v, int sw, int rr) {
+  const uint32_t lo = (uint32_t)v, hi = (uint32_t)(v >> 32);
+  const uint32_t x0 = sw ? hi : lo, x1 = sw ? lo : hi;
+  return ((uint64_t)__funnelshift_l(x0, x1, rr) << 32) | __funnelshift_l(x1, x0, rr);
 }
 
-// Four independent states in one pass (the four ExpandMask streams): the same
-// round code with the states interleaved, so their shuffles overlap.
-static __device__ __forceinline__ void keccak_warp4(uint64_t (&a)[4], int lane) {
-  constexpr int rho[25] = {0, 1, 62, 28, 27, 36, 44, 6, 55, 20, 3, 10, 43, 25, 39,
-                           41, 45, 15, 21, 8, 18, 2, 61, 56, 14};
-  const int l = lane < 25 ? lane : 0;
-  const int x = l % 5, y = l / 5;
-  const int r = rho[l];
-  const int sx = (3 * ((y - 3 * x) % 5 + 10)) % 5;
-  const int pi_src = sx + 5 * x;
-  const int col[4] = {x + 5 * ((y + 1) % 5), x + 5 * ((y + 2) % 5), x + 5 * ((y + 3) % 5), x + 5 * ((y + 4) % 5)};
-  const int xm1 = (x + 4) % 5 + 5 * y, xp1 = (x + 1) % 5 + 5 * y, xp2 = (x + 2) % 5 + 5 * y;
+// S independent states, one Keccak-f[1600] each (FIPS 202 Sec. 3.2 steps), their
+// rounds interleaved so the shuffles of one state overlap the others' arithmetic.
+// Per round and state 8 64-bit shuffles: theta's column sum as a 3-step chain,
+// C[x -/+ 1], and B[x], B[x+1], B[x+2] straight from the rho-rotated words.
+template <int S>
+__device__ __forceinline__ void keccak_warp_n(uint64_t (&a)[S], const KLane& k) {
 #pragma unroll 1
   for (int rd = 0; rd < 24; ++rd) {
-    uint64_t c[4], b[4];
+    uint64_t c[S];
 #pragma unroll
-    for (int s = 0; s < 4; ++s) c[s] = a[s];
-#pragma unroll
-    for (int k = 0; k < 4; ++k)
-#pragma unroll
-      for (int s = 0; s < 4; ++s) c[s] ^= shfl64(a[s], col[k]);
-#pragma unroll
-    for (int s = 0; s < 4; ++s) {
-      const uint64_t cm = shfl64(c[s], xm1), cp = shfl64(c[s], xp1);
-      a[s] ^= cm ^ rolv(cp, 1);
+    for (int s = 0; s < S; ++s) {
+      const uint64_t t4 = shfl64(a[s], k.c4);
+      const uint64_t s1 = a[s] ^ shfl64(a[s], k.c1);      // A[y] ^ A[y+1]
+      c[s] = s1 ^ shfl64(s1, k.c2) ^ t4;                   // ^ A[y+2] ^ A[y+3], ^ A[y+4]
     }
 #pragma unroll
-    for (int s = 0; s < 4; ++s) b[s] = shfl64(rolv(a[s], r), pi_src);
-#pragma unroll
-    for (int s = 0; s < 4; ++s) {
-      const uint64_t b1 = shfl64(b[s], xp1), b2 = shfl64(b[s], xp2);
-      a[s] = b[s] ^ (~b1 & b2);
+    for (int s = 0; s < S; ++s) {
+      const uint64_t cm = shfl64(c[s], k.xm1), cp = shfl64(c[s], k.xp1);
+      a[s] = rol_lane(a[s] ^ cm ^ rolv(cp, 1), k.sw, k.rr);  // theta, then rho
     }
-    if (lane == 0) {
 #pragma unroll
-      for (int s = 0; s < 4; ++s) a[s] ^= kRC[rd];
+    for (int s = 0; s < S; ++s) {
+      const uint64_t b0 = shfl64(a[s], k.p0), b1 = shfl64(a[s], k.p1), b2 = shfl64(a[s], k.p2);
+      a[s] = b0 ^ (~b1 & b2) ^ (kRC[rd] & k.rcmask);     // pi, chi, iota
     }
   }
+}
+
+static __device__ __noinline__ uint64_t keccak_warp(uint64_t a, int lane) {
+  const KLane k(lane);
+  uint64_t st[1] = {a};
+  keccak_warp_n<1>(st, k);
+  return st[0];
+}
+
+// The four ExpandMask streams side by side.
+static __device__ __forceinline__ void keccak_warp4(uint64_t (&a)[4], int lane) {
+  const KLane k(lane);
+  keccak_warp_n<4>(a, k);
 }
 
 // Warp sponge (SHAKE rate RATE): absorb p0 || p1 || p2 with the SHAKE padding;
