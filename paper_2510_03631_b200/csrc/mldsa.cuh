@@ -39,10 +39,10 @@ constexpr int SIG_OFF = 597;      // record byte of the signature (560 spectrum 
 constexpr int REC_STAGE = 3024;   // staging row: 3017 bytes rounded up to 16
 constexpr int THREADS = 256;
 
-struct MldsaKey {                 // expanded signing key (global memory)
-  int32_t A[K][L][256];           // A-hat (NTT domain)
-  int32_t s1[L][256];             // NTT(s1)
-  int32_t s2[K][256];             // NTT(s2)
+struct MldsaKey {                 // expanded signing key (global memory); the four
+  int32_t A[K][L][256];           // A-hat (NTT domain)      polynomial arrays end in
+  int32_t s1[L][256];             // NTT(s1)                 Montgomery form (x 2^32 mod q)
+  int32_t s2[K][256];             // NTT(s2)                 for the signer's montq
   int32_t t0[K][256];             // NTT(t0)
   uint8_t Kseed[32];
   uint8_t tr[64];
@@ -349,6 +349,18 @@ __device__ __forceinline__ int32_t mulq(int32_t a, int32_t b) {  // a, b in [0, 
   uint32_t r = (uint32_t)(x - qt * (uint64_t)Q);
   return (int32_t)(r >= (uint32_t)Q ? r - Q : r);
 }
+// Montgomery product a b 2^-32 mod q for a, b in [0, q) (one operand carries the
+// factor 2^32: the signer's twiddles and key polynomials): x + m q is divisible
+// by 2^32 with m = -x q^-1 mod 2^32, and (x + m q) / 2^32 < 2q.
+constexpr uint32_t MONT_QINV_NEG = 4236238847u;  // -q^-1 mod 2^32
+constexpr int32_t MONT_R = 4193792;              // 2^32 mod q
+constexpr int32_t MONT_F = 16382;                // 256^-1 2^32 mod q = 2^24 mod q
+__device__ __forceinline__ int32_t montq(int32_t a, int32_t b) {
+  const uint64_t x = (uint64_t)(uint32_t)a * (uint32_t)b;
+  const uint32_t m = (uint32_t)x * MONT_QINV_NEG;
+  const uint32_t t = (uint32_t)((x + (uint64_t)m * (uint32_t)Q) >> 32);
+  return (int32_t)min(t, t - (uint32_t)Q);
+}
 __device__ __forceinline__ int32_t addq(int32_t a, int32_t b) {
   int32_t s = a + b;
   return s >= Q ? s - Q : s;
@@ -527,6 +539,14 @@ static __global__ void __launch_bounds__(THREADS) mldsa_keygen_kernel(const uint
     key->s2[e >> 8][e & 255] = s2[e >> 8][e & 255];
     key->t0[e >> 8][e & 255] = t[e >> 8][e & 255];
   }
+  __syncthreads();
+  // Montgomery form for the signer: every product it takes has one key operand
+  for (int e = tid; e < K * L * 256; e += blockDim.x) (&key->A[0][0][0])[e] = mulq((&key->A[0][0][0])[e], MONT_R);
+  for (int e = tid; e < L * 256; e += blockDim.x) (&key->s1[0][0])[e] = mulq((&key->s1[0][0])[e], MONT_R);
+  for (int e = tid; e < K * 256; e += blockDim.x) {
+    (&key->s2[0][0])[e] = mulq((&key->s2[0][0])[e], MONT_R);
+    (&key->t0[0][0])[e] = mulq((&key->t0[0][0])[e], MONT_R);
+  }
 }
 
 // ------------------------------------------------------------------ signing
@@ -574,7 +594,7 @@ static __device__ void ntt_w(int32_t* p, int n, const int32_t* zetas, int lane) 
       const int grp = b >> lg, j = (grp << (lg + 1)) + (b & (len - 1));
       const int32_t z = zetas[(256 / (2 * len)) + grp];
       int32_t* w = p + poly * 256;
-      const int32_t tt = mulq(z, w[j + len]);
+      const int32_t tt = montq(z, w[j + len]);
       const int32_t a = w[j];
       w[j + len] = subq(a, tt);
       w[j] = addq(a, tt);
@@ -592,11 +612,11 @@ static __device__ void ntt_inv_w(int32_t* p, int n, const int32_t* zetas, int la
       int32_t* w = p + poly * 256;
       const int32_t a = w[j], c = w[j + len];
       w[j] = addq(a, c);
-      w[j + len] = mulq(z, subq(a, c));
+      w[j + len] = montq(z, subq(a, c));
     }
     __syncwarp();
   }
-  for (int t = lane; t < n * 256; t += 32) p[t] = mulq(8347681, p[t]);
+  for (int t = lane; t < n * 256; t += 32) p[t] = montq(MONT_F, p[t]);
   __syncwarp();
 }
 
@@ -678,7 +698,7 @@ static __device__ __forceinline__ void sign_one(const SignArgs& a, SignSmem& S, 
     for (int cc = lane; cc < 256; cc += 32)
       for (int i = 0; i < K; ++i) {
         int32_t acc = 0;
-        for (int j = 0; j < L; ++j) acc = addq(acc, mulq(key->A[i][j][cc], S.tmp[j][cc]));
+        for (int j = 0; j < L; ++j) acc = addq(acc, montq(key->A[i][j][cc], S.tmp[j][cc]));
         S.w[i][cc] = acc;
       }
     __syncwarp();
@@ -733,7 +753,7 @@ static __device__ __forceinline__ void sign_one(const SignArgs& a, SignSmem& S, 
     }
     ntt_w(S.c, 1, zetas, lane);
     // z = y + NTT^-1(c o s1); checked against gamma1 - beta
-    for (int e = lane; e < L * 256; e += 32) S.tmp[e >> 8][e & 255] = mulq(S.c[e & 255], key->s1[e >> 8][e & 255]);
+    for (int e = lane; e < L * 256; e += 32) S.tmp[e >> 8][e & 255] = montq(S.c[e & 255], key->s1[e >> 8][e & 255]);
     __syncwarp();
     ntt_inv_w(&S.tmp[0][0], L, zetas, lane);
     int bad = 0;
@@ -746,7 +766,7 @@ static __device__ __forceinline__ void sign_one(const SignArgs& a, SignSmem& S, 
       if (zc >= GAMMA1 - BETA || zc <= -(GAMMA1 - BETA)) bad = 1;
     }
     // r0 = LowBits(w - c s2), checked against gamma2 - beta; w <- w - c s2
-    for (int e = lane; e < K * 256; e += 32) S.tmp[e >> 8][e & 255] = mulq(S.c[e & 255], key->s2[e >> 8][e & 255]);
+    for (int e = lane; e < K * 256; e += 32) S.tmp[e >> 8][e & 255] = montq(S.c[e & 255], key->s2[e >> 8][e & 255]);
     __syncwarp();
     ntt_inv_w(&S.tmp[0][0], K, zetas, lane);
     for (int e = lane; e < K * 256; e += 32) {
@@ -758,7 +778,7 @@ static __device__ __forceinline__ void sign_one(const SignArgs& a, SignSmem& S, 
     }
     if (__any_sync(0xffffffffu, bad)) continue;
     // c t0; h = MakeHint(-ct0, w - cs2 + ct0); ||ct0|| < gamma2, #h <= omega
-    for (int e = lane; e < K * 256; e += 32) S.tmp[e >> 8][e & 255] = mulq(S.c[e & 255], key->t0[e >> 8][e & 255]);
+    for (int e = lane; e < K * 256; e += 32) S.tmp[e >> 8][e & 255] = montq(S.c[e & 255], key->t0[e >> 8][e & 255]);
     __syncwarp();
     ntt_inv_w(&S.tmp[0][0], K, zetas, lane);
     int cnt[K] = {0, 0, 0, 0};
@@ -831,6 +851,8 @@ static __global__ void __launch_bounds__(32 * WPB) mldsa_sign_kernel(SignArgs a)
   __shared__ int32_t zetas[256];
   extern __shared__ __align__(16) uint8_t dsm[];
   fill_zetas(zetas);
+  __syncthreads();
+  for (int m = threadIdx.x; m < 256; m += blockDim.x) zetas[m] = mulq(zetas[m], MONT_R);  // Montgomery form
   __syncthreads();
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   SignSmem& S = reinterpret_cast<SignSmem*>(dsm)[wid];
