@@ -304,10 +304,50 @@ static __device__ __noinline__ uint64_t keccak_warp(uint64_t a, int lane) {
   return st[0];
 }
 
-// The four ExpandMask streams side by side.
-static __device__ __forceinline__ void keccak_warp4(uint64_t (&a)[4], int lane) {
-  const KLane k(lane);
-  keccak_warp_n<4>(a, k);
+// Four independent states in column layout: lane 5s + x (s < 4, x < 5) holds
+// column x of state s, a[y] = A[x][y]. theta's column sum is local, C[x -/+ 1]
+// two shuffles; rho rotates in registers; pi and chi's row neighbours go through
+// 800 bytes of shared memory (each lane stores its five rotated words at their
+// pi destinations B[y][2x + 3y], then reads row Y of columns x, x+1, x+2).
+// Per round for all four states: 4 shuffles, 5 stores, 15 loads, ~50 ALU
+// instructions (the 25-lane layout above: 64 shuffles, ~120 ALU).
+// Lanes 20..31 compute on garbage and never store. `pis`: 200 words per warp.
+__device__ __forceinline__ void keccak_col4(uint64_t (&a)[5], uint64_t* pis, int lane) {
+  constexpr uint32_t rho[25] = {0, 1, 62, 28, 27, 36, 44, 6, 55, 20, 3, 10, 43, 25, 39,
+                                41, 45, 15, 21, 8, 18, 2, 61, 56, 14};
+  const int s = lane / 5, x = lane % 5;
+  const int xm1 = 5 * s + (x + 4) % 5, xp1 = 5 * s + (x + 1) % 5;
+  const bool st = lane < 20;
+  int sw[5], rr[5], dst[5];
+#pragma unroll
+  for (int y = 0; y < 5; ++y) {
+    uint32_t r = 0;
+#pragma unroll
+    for (int i = 0; i < 5; ++i) r = i == x ? rho[i + 5 * y] : r;
+    sw[y] = r >= 32;
+    rr[y] = r & 31;
+    dst[y] = 25 * s + y + 5 * ((2 * x + 3 * y) % 5);
+  }
+  const uint64_t* r0 = pis + 25 * s + x;
+  const uint64_t* r1 = pis + 25 * s + (x + 1) % 5;
+  const uint64_t* r2 = pis + 25 * s + (x + 2) % 5;
+  const uint64_t rcm = x == 0 ? ~0ull : 0ull;
+#pragma unroll 1
+  for (int rd = 0; rd < 24; ++rd) {
+    const uint64_t c = a[0] ^ a[1] ^ a[2] ^ a[3] ^ a[4];
+    const uint64_t cm = shfl64(c, xm1), cp = shfl64(c, xp1);
+    const uint64_t d = cm ^ rolv(cp, 1);
+#pragma unroll
+    for (int y = 0; y < 5; ++y) {
+      const uint64_t v = rol_lane(a[y] ^ d, sw[y], rr[y]);
+      if (st) pis[dst[y]] = v;
+    }
+    __syncwarp();
+#pragma unroll
+    for (int y = 0; y < 5; ++y) a[y] = r0[5 * y] ^ (~r1[5 * y] & r2[5 * y]);
+    a[0] ^= kRC[rd] & rcm;
+    __syncwarp();
+  }
 }
 
 // Warp sponge (SHAKE rate RATE): absorb p0 || p1 || p2 with the SHAKE padding;
@@ -566,23 +606,25 @@ __device__ __forceinline__ uint4 philox_nonce_block(uint64_t seed, uint64_t thet
                        make_uint2((uint32_t)seed, (uint32_t)(seed >> 32)));
 }
 
-// One signature per warp (WPB warps per CTA): the sponges run in lane 0 (lanes
-// 0..3 for the four mask streams), the polynomial work across the 32 lanes,
-// __syncwarp between steps -- many signatures in flight per SM hide the serial
-// Keccak latency (one signature per 256-thread CTA ran at 319 k/s on C2).
+// One signature per warp (WPB warps per CTA): the single sponges (mu, rho'', c~,
+// SampleInBall) run warp-cooperatively on 25 lanes, the four ExpandMask streams in
+// column layout on 20 lanes, the polynomial work across the 32 lanes, __syncwarp
+// between steps -- many signatures in flight per SM hide the serial Keccak
+// latency (one signature per 256-thread CTA ran at 319 k/s on C2).
 struct SignSmem {                   // per warp (y / z live in registers: 32 per lane)
-  union {
+  union alignas(8) {
     int32_t tmp[K][256];            // NTT(y), then c.s1 / c.s2 / c.t0 products
     uint8_t w1enc[K * 192];         // w1Encode(w1), hashed before tmp is reused
   };
-  union {
+  union alignas(8) {
     int32_t w[K][256];              // w, then w - c s2, then the hint bits
     uint8_t ymask[L * 576];         // ExpandMask bytes, unpacked before w is computed
   };
   int32_t c[256];
-  alignas(8) uint8_t scratch[L][136];  // sponge block staging (lanes 0..3)
+  alignas(8) uint8_t scratch[1][136];  // sponge block staging
   alignas(8) uint8_t mu[64];
-  uint8_t rhopp[64], ctilde[32], msg[40], zeros[32];
+  alignas(8) uint8_t rhopp[64];
+  uint8_t ctilde[32], msg[40], zeros[32];
   int count[K];
 };
 constexpr int WPB = 4;  // ~10 KB of shared memory per warp: 5 CTAs x 4 warps per SM
@@ -654,30 +696,29 @@ static __device__ __forceinline__ void sign_one(const SignArgs& a, SignSmem& S, 
   for (uint32_t kappa_ctr = 0;; kappa_ctr += L) {
     // ExpandMask (Alg. 34): y[r] = BitUnpack(H(rho'' || (kappa + r), 576), gamma1 - 1, gamma1)
     {
-      // the four streams H(rho'' || IntegerToBytes(kappa + r, 2)) side by side:
-      // one padded block each (66 message bytes < 136), then 5 output blocks
-      uint64_t h[L];
+      // the four streams H(rho'' || IntegerToBytes(kappa + r, 2)), one per lane
+      // group (column layout): one padded block each (66 message bytes < 136),
+      // then 5 output blocks; tmp (free until y is unpacked) holds the pi buffer
+      const int sg = lane / 5, x = lane % 5;
+      const uint32_t idx = kappa_ctr + (uint32_t)min(sg, L - 1);
+      uint64_t st[5];
 #pragma unroll
-      for (int r = 0; r < L; ++r) {
-        const uint32_t idx = kappa_ctr + r;
-        for (int i = lane; i < 136; i += 32) {
-          uint8_t v = i < 64 ? S.rhopp[i] : i == 64 ? (uint8_t)(idx & 255) : i == 65 ? (uint8_t)(idx >> 8) : 0;
-          if (i == 66) v ^= 0x1F;
-          if (i == 135) v ^= 0x80;
-          S.scratch[r][i] = v;
-        }
+      for (int y = 0; y < 5; ++y) {
+        const int i = x + 5 * y;
+        uint64_t v = 0;
+        if (i < 8) v = reinterpret_cast<const uint64_t*>(S.rhopp)[i];
+        if (i == 8) v = (uint64_t)(idx & 0xFFFFu) | (0x1Full << 16);
+        if (i == 16) v = 0x80ull << 56;
+        st[y] = v;
       }
-      __syncwarp();
-#pragma unroll
-      for (int r = 0; r < L; ++r) h[r] = lane < 17 ? reinterpret_cast<const uint64_t*>(S.scratch[r])[lane] : 0ull;
+      uint64_t* pis = reinterpret_cast<uint64_t*>(&S.tmp[0][0]);
       for (int o = 0; o < 576; o += 136) {  // 5 blocks (680 >= 576 bytes)
-        keccak_warp4(h, lane);
-        const int nb = min(136, 576 - o);
-        if (lane < 17 && 8 * lane < nb) {
+        keccak_col4(st, pis, lane);
+        const int nw = min(17, (576 - o) / 8);
+        if (lane < 5 * L) {
 #pragma unroll
-          for (int r = 0; r < L; ++r)
-            for (int k = 0; k < 8 && 8 * lane + k < nb; ++k)
-              S.ymask[r * 576 + o + 8 * lane + k] = (uint8_t)(h[r] >> (8 * k));
+          for (int y = 0; y < 4; ++y)
+            if (x + 5 * y < nw) reinterpret_cast<uint64_t*>(S.ymask + sg * 576 + o)[x + 5 * y] = st[y];
         }
       }
     }
@@ -847,7 +888,7 @@ static __device__ __forceinline__ void sign_one(const SignArgs& a, SignSmem& S, 
 // expected for ML-DSA-44), so warps finish at different times; one record per
 // warp with CTAs of WPB warps kept each CTA resident until its slowest
 // signature was done (ncu: 15 % warps active of a 31 % occupancy limit).
-static __global__ void __launch_bounds__(32 * WPB) mldsa_sign_kernel(SignArgs a) {
+static __global__ void __launch_bounds__(32 * WPB, 5) mldsa_sign_kernel(SignArgs a) {
   __shared__ int32_t zetas[256];
   extern __shared__ __align__(16) uint8_t dsm[];
   fill_zetas(zetas);
