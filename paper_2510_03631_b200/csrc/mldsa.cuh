@@ -326,11 +326,11 @@ __device__ __forceinline__ void keccak_col4(uint64_t (&a)[5], uint64_t* pis, int
     for (int i = 0; i < 5; ++i) r = i == x ? rho[i + 5 * y] : r;
     sw[y] = r >= 32;
     rr[y] = r & 31;
-    dst[y] = 25 * s + y + 5 * ((2 * x + 3 * y) % 5);
+    dst[y] = 20 * ((2 * x + 3 * y) % 5) + 5 * s + y;  // B[y][2x + 3y]: word 20 Y + 5 s + X
   }
-  const uint64_t* r0 = pis + 25 * s + x;
-  const uint64_t* r1 = pis + 25 * s + (x + 1) % 5;
-  const uint64_t* r2 = pis + 25 * s + (x + 2) % 5;
+  const uint64_t* r0 = pis + 5 * s + x;  // row Y at + 20 Y: a warp's loads hit consecutive words
+  const uint64_t* r1 = pis + 5 * s + (x + 1) % 5;
+  const uint64_t* r2 = pis + 5 * s + (x + 2) % 5;
   const uint64_t rcm = x == 0 ? ~0ull : 0ull;
 #pragma unroll 1
   for (int rd = 0; rd < 24; ++rd) {
@@ -344,7 +344,7 @@ __device__ __forceinline__ void keccak_col4(uint64_t (&a)[5], uint64_t* pis, int
     }
     __syncwarp();
 #pragma unroll
-    for (int y = 0; y < 5; ++y) a[y] = r0[5 * y] ^ (~r1[5 * y] & r2[5 * y]);
+    for (int y = 0; y < 5; ++y) a[y] = r0[20 * y] ^ (~r1[20 * y] & r2[20 * y]);
     a[0] ^= kRC[rd] & rcm;
     __syncwarp();
   }
