@@ -307,15 +307,17 @@ static __device__ __noinline__ uint64_t keccak_warp(uint64_t a, int lane) {
 // Four independent states in column layout: lane 5s + x (s < 4, x < 5) holds
 // column x of state s, a[y] = A[x][y]. theta's column sum is local, C[x -/+ 1]
 // two shuffles; rho rotates in registers; pi and chi's row neighbours go through
-// 800 bytes of shared memory (each lane stores its five rotated words at their
+// 864 bytes of shared memory (each lane stores its five rotated words at their
 // pi destinations B[y][2x + 3y], then reads row Y of columns x, x+1, x+2).
 // Per round for all four states: 4 shuffles, 5 stores, 15 loads, ~50 ALU
 // instructions (the 25-lane layout above: 64 shuffles, ~120 ALU).
 // Lanes 20..31 compute on garbage and never store. `pis`: 200 words per warp.
+constexpr int KC_ROW = 22;  // pi buffer row stride in words (bank spread of the stores)
 __device__ __forceinline__ void keccak_col4(uint64_t (&a)[5], uint64_t* pis, int lane) {
   constexpr uint32_t rho[25] = {0, 1, 62, 28, 27, 36, 44, 6, 55, 20, 3, 10, 43, 25, 39,
                                 41, 45, 15, 21, 8, 18, 2, 61, 56, 14};
-  const int s = lane / 5, x = lane % 5;
+  // lanes 20..31 shadow state 3 (same words: their loads broadcast, no conflicts)
+  const int s = min(lane / 5, 3), x = lane % 5;
   const int xm1 = 5 * s + (x + 4) % 5, xp1 = 5 * s + (x + 1) % 5;
   const bool st = lane < 20;
   int sw[5], rr[5], dst[5];
@@ -326,9 +328,9 @@ __device__ __forceinline__ void keccak_col4(uint64_t (&a)[5], uint64_t* pis, int
     for (int i = 0; i < 5; ++i) r = i == x ? rho[i + 5 * y] : r;
     sw[y] = r >= 32;
     rr[y] = r & 31;
-    dst[y] = 20 * ((2 * x + 3 * y) % 5) + 5 * s + y;  // B[y][2x + 3y]: word 20 Y + 5 s + X
+    dst[y] = KC_ROW * ((2 * x + 3 * y) % 5) + 5 * s + y;  // B[y][2x + 3y]: word 22 Y + 5 s + X
   }
-  const uint64_t* r0 = pis + 5 * s + x;  // row Y at + 20 Y: a warp's loads hit consecutive words
+  const uint64_t* r0 = pis + 5 * s + x;  // row Y at + 22 Y: a warp's loads hit consecutive words
   const uint64_t* r1 = pis + 5 * s + (x + 1) % 5;
   const uint64_t* r2 = pis + 5 * s + (x + 2) % 5;
   const uint64_t rcm = x == 0 ? ~0ull : 0ull;
@@ -344,7 +346,7 @@ __device__ __forceinline__ void keccak_col4(uint64_t (&a)[5], uint64_t* pis, int
     }
     __syncwarp();
 #pragma unroll
-    for (int y = 0; y < 5; ++y) a[y] = r0[20 * y] ^ (~r1[20 * y] & r2[20 * y]);
+    for (int y = 0; y < 5; ++y) a[y] = r0[KC_ROW * y] ^ (~r1[KC_ROW * y] & r2[KC_ROW * y]);
     a[0] ^= kRC[rd] & rcm;
     __syncwarp();
   }
