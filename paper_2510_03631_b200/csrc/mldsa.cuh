@@ -631,37 +631,86 @@ struct SignSmem {                   // per warp (y / z live in registers: 32 per
 };
 constexpr int WPB = 4;  // ~10 KB of shared memory per warp: 5 CTAs x 4 warps per SM
 
-static __device__ void ntt_w(int32_t* p, int n, const int32_t* zetas, int lane) {
-  for (int len = 128, lg = 7; len >= 1; len >>= 1, --lg) {
-    for (int t = lane; t < n * 128; t += 32) {
-      const int poly = t >> 7, b = t & 127;
-      const int grp = b >> lg, j = (grp << (lg + 1)) + (b & (len - 1));
-      const int32_t z = zetas[(256 / (2 * len)) + grp];
-      int32_t* w = p + poly * 256;
-      const int32_t tt = montq(z, w[j + len]);
-      const int32_t a = w[j];
-      w[j + len] = subq(a, tt);
-      w[j] = addq(a, tt);
+// Warp NTT / NTT^-1 of N polynomials in shared memory, two layers per pass
+// (radix 4: each lane loads 4 coefficients, applies both butterfly layers,
+// stores them back -- half the shared-memory traffic of one layer per pass).
+// Same butterflies, zeta indices and order of operations per coefficient as
+// Alg. 41 / 42; the twiddles are in Montgomery form (x 2^32 mod q).
+template <int N>
+static __device__ __noinline__ void ntt_w(int32_t* p, const int32_t* zetas, int lane) {
+#pragma unroll 1
+  for (int lg = 7; lg >= 1; lg -= 2) {  // layers (len, len / 2), len = 2^lg
+    const int len = 1 << lg, h = len >> 1;
+#pragma unroll 2
+    for (int k = 0; k < 2 * N; ++k) {
+      const int u = lane + 32 * k, uu = u & 63;
+      const int grp = uu >> (lg - 1);                       // block of the len layer
+      int32_t* w = p + (u >> 6) * 256 + (grp << (lg + 1)) + (uu & (h - 1));
+      const int32_t z1 = zetas[(128 >> lg) + grp];          // m = 256 / (2 len) + grp
+      const int32_t z2 = zetas[(256 >> lg) + 2 * grp];      // the two len / 2 blocks
+      const int32_t z3 = zetas[(256 >> lg) + 2 * grp + 1];
+      int32_t a0 = w[0], a1 = w[h], a2 = w[len], a3 = w[len + h];
+      int32_t t = montq(z1, a2);
+      a2 = subq(a0, t);
+      a0 = addq(a0, t);
+      t = montq(z1, a3);
+      a3 = subq(a1, t);
+      a1 = addq(a1, t);
+      t = montq(z2, a1);
+      a1 = subq(a0, t);
+      a0 = addq(a0, t);
+      t = montq(z3, a3);
+      a3 = subq(a2, t);
+      a2 = addq(a2, t);
+      w[0] = a0;
+      w[h] = a1;
+      w[len] = a2;
+      w[len + h] = a3;
     }
     __syncwarp();
   }
 }
 
-static __device__ void ntt_inv_w(int32_t* p, int n, const int32_t* zetas, int lane) {
-  for (int len = 1, lg = 0; len < 256; len <<= 1, ++lg) {
-    for (int t = lane; t < n * 128; t += 32) {
-      const int poly = t >> 7, b = t & 127;
-      const int grp = b >> lg, j = (grp << (lg + 1)) + (b & (len - 1));
-      const int32_t z = Q - zetas[(256 / len) - 1 - grp];
-      int32_t* w = p + poly * 256;
-      const int32_t a = w[j], c = w[j + len];
-      w[j] = addq(a, c);
-      w[j + len] = montq(z, subq(a, c));
+// NTT^-1 (Alg. 42), the multiplication by 256^-1 fused into the last pass.
+template <int N>
+static __device__ __noinline__ void ntt_inv_w(int32_t* p, const int32_t* zetas, int lane) {
+#pragma unroll 1
+  for (int lg = 0; lg <= 6; lg += 2) {  // layers (len, 2 len), len = 2^lg
+    const int len = 1 << lg;
+#pragma unroll 2
+    for (int k = 0; k < 2 * N; ++k) {
+      const int u = lane + 32 * k, uu = u & 63;
+      const int g = uu >> lg;                               // block of the 2 len layer
+      int32_t* w = p + (u >> 6) * 256 + (g << (lg + 2)) + (uu & (len - 1));
+      const int32_t za = Q - zetas[(256 >> lg) - 1 - 2 * g];  // len blocks 2g, 2g + 1
+      const int32_t zb = Q - zetas[(256 >> lg) - 2 - 2 * g];
+      const int32_t zc = Q - zetas[(128 >> lg) - 1 - g];      // 2 len block g
+      int32_t a0 = w[0], a1 = w[len], a2 = w[2 * len], a3 = w[3 * len];
+      int32_t t = a0;
+      a0 = addq(t, a1);
+      a1 = montq(za, subq(t, a1));
+      t = a2;
+      a2 = addq(t, a3);
+      a3 = montq(zb, subq(t, a3));
+      t = a0;
+      a0 = addq(t, a2);
+      a2 = montq(zc, subq(t, a2));
+      t = a1;
+      a1 = addq(t, a3);
+      a3 = montq(zc, subq(t, a3));
+      if (lg == 6) {
+        a0 = montq(MONT_F, a0);
+        a1 = montq(MONT_F, a1);
+        a2 = montq(MONT_F, a2);
+        a3 = montq(MONT_F, a3);
+      }
+      w[0] = a0;
+      w[len] = a1;
+      w[2 * len] = a2;
+      w[3 * len] = a3;
     }
     __syncwarp();
   }
-  for (int t = lane; t < n * 256; t += 32) p[t] = montq(MONT_F, p[t]);
-  __syncwarp();
 }
 
 // Sign_internal (Alg. 7) of M' = 0 || 0 || pi_theta, rnd = {0}^32, for record
@@ -737,7 +786,7 @@ static __device__ __forceinline__ void sign_one(const SignArgs& a, SignSmem& S, 
       S.tmp[r][cidx] = yr[j];
     }
     __syncwarp();
-    ntt_w(&S.tmp[0][0], L, zetas, lane);
+    ntt_w<L>(&S.tmp[0][0], zetas, lane);
     for (int cc = lane; cc < 256; cc += 32)
       for (int i = 0; i < K; ++i) {
         int32_t acc = 0;
@@ -745,7 +794,7 @@ static __device__ __forceinline__ void sign_one(const SignArgs& a, SignSmem& S, 
         S.w[i][cc] = acc;
       }
     __syncwarp();
-    ntt_inv_w(&S.w[0][0], K, zetas, lane);
+    ntt_inv_w<K>(&S.w[0][0], zetas, lane);
     // w1Encode (Alg. 28): HighBits, 6 bits per coefficient, 4 coefficients -> 3 bytes
     for (int e = lane; e < K * 64; e += 32) {
       const int i = e >> 6, g4 = e & 63;
@@ -794,11 +843,11 @@ static __device__ __forceinline__ void sign_one(const SignArgs& a, SignSmem& S, 
       }
       __syncwarp();
     }
-    ntt_w(S.c, 1, zetas, lane);
+    ntt_w<1>(S.c, zetas, lane);
     // z = y + NTT^-1(c o s1); checked against gamma1 - beta
     for (int e = lane; e < L * 256; e += 32) S.tmp[e >> 8][e & 255] = montq(S.c[e & 255], key->s1[e >> 8][e & 255]);
     __syncwarp();
-    ntt_inv_w(&S.tmp[0][0], L, zetas, lane);
+    ntt_inv_w<L>(&S.tmp[0][0], zetas, lane);
     int bad = 0;
 #pragma unroll
     for (int j = 0; j < 32; ++j) {
@@ -811,7 +860,7 @@ static __device__ __forceinline__ void sign_one(const SignArgs& a, SignSmem& S, 
     // r0 = LowBits(w - c s2), checked against gamma2 - beta; w <- w - c s2
     for (int e = lane; e < K * 256; e += 32) S.tmp[e >> 8][e & 255] = montq(S.c[e & 255], key->s2[e >> 8][e & 255]);
     __syncwarp();
-    ntt_inv_w(&S.tmp[0][0], K, zetas, lane);
+    ntt_inv_w<K>(&S.tmp[0][0], zetas, lane);
     for (int e = lane; e < K * 256; e += 32) {
       const int32_t v = subq(S.w[e >> 8][e & 255], S.tmp[e >> 8][e & 255]);
       S.w[e >> 8][e & 255] = v;
@@ -823,7 +872,7 @@ static __device__ __forceinline__ void sign_one(const SignArgs& a, SignSmem& S, 
     // c t0; h = MakeHint(-ct0, w - cs2 + ct0); ||ct0|| < gamma2, #h <= omega
     for (int e = lane; e < K * 256; e += 32) S.tmp[e >> 8][e & 255] = montq(S.c[e & 255], key->t0[e >> 8][e & 255]);
     __syncwarp();
-    ntt_inv_w(&S.tmp[0][0], K, zetas, lane);
+    ntt_inv_w<K>(&S.tmp[0][0], zetas, lane);
     int cnt[K] = {0, 0, 0, 0};
     for (int e = lane; e < K * 256; e += 32) {
       const int32_t ct0 = S.tmp[e >> 8][e & 255];
