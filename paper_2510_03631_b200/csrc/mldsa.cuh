@@ -9,13 +9,14 @@
 //   mldsa_keygen_kernel  (1 CTA)   -- KeyGen_internal(xi) into an MldsaKey in
 //                                      global memory (A-hat, NTT(s1), NTT(s2),
 //                                      NTT(t0), K, tr, pk), once per bind call;
-//   mldsa_sign_kernel    (1 CTA per record) -- Sign_internal of pi_theta; the
-//                                      2420 signature bytes go to byte 597 of the
+//   mldsa_sign_kernel    (persistent warps, one record per warp at a time) --
+//                                      Sign_internal of pi_theta; the 2420
+//                                      signature bytes go to byte 597 of the
 //                                      record's 3024-byte staging row (16-byte
 //                                      aligned for the packing kernel).
-// The sponges run one per thread (byte-serial absorb / squeeze); polynomial
-// arithmetic runs across the CTA (256 threads: one coefficient or one NTT
-// butterfly per thread per step).
+// KeyGen's sponges run one per thread (byte-serial absorb / squeeze) and its
+// polynomial arithmetic across the CTA; the signer's sponges and NTTs are
+// warp-cooperative (see mldsa_sign_kernel).
 #pragma once
 #include <algorithm>
 #include <cstdint>
