@@ -231,13 +231,15 @@ __device__ __forceinline__ uint64_t rolv(uint64_t x, int s) { return s ? (x << s
 
 // Per-lane constants of the warp-cooperative round (lane i < 25 holds A[x + 5y];
 // lanes 25..31 shadow lane 0 and are never read).
-struct KLane {
+// Built once per CTA into a shared table (k_lane_tab) so a permutation call
+// loads them instead of re-deriving ~150 instructions of index arithmetic.
+struct alignas(16) KLane {
   int c1, c2, c4;   // A[x][y+1], A[x][y+2]-partner, A[x][y+4]: theta's column sum in 3 shuffles
   int xm1, xp1;     // C[x-1], C[x+1]
   int p0, p1, p2;   // pi sources of B[x][y], B[x+1][y], B[x+2][y] (chi reads them directly)
   int sw, rr;       // rho offset r[x][y] = 32 sw + rr
   uint64_t rcmask;  // lane 0: iota applies
-  __device__ __forceinline__ explicit KLane(int lane) {
+  __device__ __forceinline__ void init(int lane) {
     // rho offsets r[x][y] (FIPS 202 Table 2), indexed x + 5y
     constexpr uint32_t rho[25] = {0, 1, 62, 28, 27, 36, 44, 6, 55, 20, 3, 10, 43, 25, 39,
                                   41, 45, 15, 21, 8, 18, 2, 61, 56, 14};
@@ -298,8 +300,10 @@ __device__ __forceinline__ void keccak_warp_n(uint64_t (&a)[S], const KLane& k) 
   }
 }
 
+static __shared__ KLane k_lane_tab[32];
+
 static __device__ __noinline__ uint64_t keccak_warp(uint64_t a, int lane) {
-  const KLane k(lane);
+  const KLane k = k_lane_tab[lane];
   uint64_t st[1] = {a};
   keccak_warp_n<1>(st, k);
   return st[0];
@@ -314,27 +318,49 @@ static __device__ __noinline__ uint64_t keccak_warp(uint64_t a, int lane) {
 // instructions (the 25-lane layout above: 64 shuffles, ~120 ALU).
 // Lanes 20..31 compute on garbage and never store. `pis`: 200 words per warp.
 constexpr int KC_ROW = 22;  // pi buffer row stride in words (bank spread of the stores)
+// Per-lane constants of the column layout, built once per CTA (k_col_tab).
+struct alignas(16) KCol {
+  int sw[5], rr[5];  // rho offsets r[x][y] = 32 sw + rr of the lane's column x
+  int dst[5];        // pi destination word of A[x][y]: B[y][2x + 3y] at 22 Y + 5 s + X
+  int o0, o1, o2;    // row-0 words of columns x, x+1, x+2 of the lane's state
+  int xm1, xp1;      // C[x-1], C[x+1]
+  uint64_t rcm;      // column 0: iota applies
+  __device__ __forceinline__ void init(int lane) {
+    constexpr uint32_t rho[25] = {0, 1, 62, 28, 27, 36, 44, 6, 55, 20, 3, 10, 43, 25, 39,
+                                  41, 45, 15, 21, 8, 18, 2, 61, 56, 14};
+    // lanes 20..31 shadow state 3 (same words: their loads broadcast, no conflicts)
+    const int s = min(lane / 5, 3), x = lane % 5;
+    xm1 = 5 * s + (x + 4) % 5;
+    xp1 = 5 * s + (x + 1) % 5;
+    for (int y = 0; y < 5; ++y) {
+      const uint32_t r = rho[x + 5 * y];
+      sw[y] = r >= 32;
+      rr[y] = r & 31;
+      dst[y] = KC_ROW * ((2 * x + 3 * y) % 5) + 5 * s + y;
+    }
+    o0 = 5 * s + x;  // row Y at + 22 Y: a warp's loads hit consecutive words
+    o1 = 5 * s + (x + 1) % 5;
+    o2 = 5 * s + (x + 2) % 5;
+    rcm = x == 0 ? ~0ull : 0ull;
+  }
+};
+static __shared__ KCol k_col_tab[32];
+
 __device__ __forceinline__ void keccak_col4(uint64_t (&a)[5], uint64_t* pis, int lane) {
-  constexpr uint32_t rho[25] = {0, 1, 62, 28, 27, 36, 44, 6, 55, 20, 3, 10, 43, 25, 39,
-                                41, 45, 15, 21, 8, 18, 2, 61, 56, 14};
-  // lanes 20..31 shadow state 3 (same words: their loads broadcast, no conflicts)
-  const int s = min(lane / 5, 3), x = lane % 5;
-  const int xm1 = 5 * s + (x + 4) % 5, xp1 = 5 * s + (x + 1) % 5;
-  const bool st = lane < 20;
+  const KCol& kt = k_col_tab[lane];
   int sw[5], rr[5], dst[5];
 #pragma unroll
   for (int y = 0; y < 5; ++y) {
-    uint32_t r = 0;
-#pragma unroll
-    for (int i = 0; i < 5; ++i) r = i == x ? rho[i + 5 * y] : r;
-    sw[y] = r >= 32;
-    rr[y] = r & 31;
-    dst[y] = KC_ROW * ((2 * x + 3 * y) % 5) + 5 * s + y;  // B[y][2x + 3y]: word 22 Y + 5 s + X
+    sw[y] = kt.sw[y];
+    rr[y] = kt.rr[y];
+    dst[y] = kt.dst[y];
   }
-  const uint64_t* r0 = pis + 5 * s + x;  // row Y at + 22 Y: a warp's loads hit consecutive words
-  const uint64_t* r1 = pis + 5 * s + (x + 1) % 5;
-  const uint64_t* r2 = pis + 5 * s + (x + 2) % 5;
-  const uint64_t rcm = x == 0 ? ~0ull : 0ull;
+  const int xm1 = kt.xm1, xp1 = kt.xp1;
+  const uint64_t rcm = kt.rcm;
+  const bool st = lane < 20;
+  const uint64_t* r0 = pis + kt.o0;
+  const uint64_t* r1 = pis + kt.o1;
+  const uint64_t* r2 = pis + kt.o2;
 #pragma unroll 1
   for (int rd = 0; rd < 24; ++rd) {
     const uint64_t c = a[0] ^ a[1] ^ a[2] ^ a[3] ^ a[4];
@@ -944,6 +970,10 @@ static __global__ void __launch_bounds__(32 * WPB, 5) mldsa_sign_kernel(SignArgs
   __shared__ int32_t zetas[256];
   extern __shared__ __align__(16) uint8_t dsm[];
   fill_zetas(zetas);
+  if (threadIdx.x < 32) {
+    k_lane_tab[threadIdx.x].init(threadIdx.x);
+    k_col_tab[threadIdx.x].init(threadIdx.x);
+  }
   __syncthreads();
   for (int m = threadIdx.x; m < 256; m += blockDim.x) zetas[m] = mulq(zetas[m], MONT_R);  // Montgomery form
   __syncthreads();
