@@ -191,6 +191,34 @@ def test_signed_bind_ens_matches_oracle(cuda_ok):
     assert (got == want).all()
 
 
+def test_signed_bind_crosses_signing_chunks(cuda_ok):
+    """More records than one signing launch takes (64K): the persistent signer warps
+    draw records from a per-launch device counter, so the records at the chunk edges
+    and a random sample must equal the oracle's signed records (and verify under
+    OpenSSL's ML-DSA-44 when the package is present)."""
+    P = _P()
+    r, d = 70000, 3072
+    spec = synth.uniform_u8_np(31, (r, 560))
+    rng = np.random.default_rng(5)
+    picks = sorted(set([0, 1, 65535, 65536, 65537, r - 1] + [int(t) for t in rng.integers(0, r, 18)]))
+    with P.EnsServer(r, d) as s:
+        pk = s.puzzle_bind_hct(0, torch.from_numpy(spec).cuda(), 9, 20, 3, mldsa_seed=_XI)
+        Q = np.zeros((len(picks), (r + 7) // 8), np.uint8)
+        for i, t in enumerate(picks):
+            Q[i, t >> 3] = 1 << (t & 7)
+        got = s.answer_batch(Q).cpu().numpy()
+    for i, t in enumerate(picks):
+        want = O.puzzle_bind_hct_signed(spec[t:t + 1], t, 9, 20, 3, d, _XI)
+        assert (got[i] == want[0]).all(), t
+    try:
+        from cryptography.hazmat.primitives.asymmetric import mldsa as lib
+    except ImportError:
+        return
+    pub = lib.MLDSA44PublicKey.from_public_bytes(pk)
+    for i, t in enumerate(picks):
+        pub.verify(got[i, 597:3017].tobytes(), got[i, 560:597].tobytes())
+
+
 @pytest.mark.parametrize("seed", range(6))
 def test_bind_fuzz_geometries(cuda_ok, seed):
     """Random geometries (cells, channels, m, record size, row shard, bound theta
