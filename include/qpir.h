@@ -132,8 +132,11 @@ int qpir_db_write(qpir_ctx *ctx, uint64_t theta_begin, uint64_t n_records,
  * spectrum: n_records rows of spec_stride >= 560 bytes, host or device
  * (spectrum_len == n_records * spec_stride); requires rec_bytes >= 597 (>= 3017
  * when signing).
+ * Device memory owned by the context (kept for later calls): a host spectrum is
+ * staged in <= 64 MB chunks; signing stages up to 65536 signature rows of 3024
+ * bytes (198 MB) per launch, plus the expanded key (~29 KB).
  * Errors: QPIR_E_DIMENSION (range, lengths, stride, rec_bytes), QPIR_E_PARAM
- * (NULL spectrum).  Concurrency as qpir_db_write. */
+ * (NULL spectrum), QPIR_E_OOM / QPIR_E_CUDA.  Concurrency as qpir_db_write. */
 int qpir_puzzle_bind_hct(qpir_ctx *ctx, uint64_t theta_begin, uint64_t n_records,
                          const uint8_t *spectrum, uint64_t spec_stride,
                          uint64_t spectrum_len, uint64_t seed_psd, uint32_t kappa,
