@@ -668,7 +668,7 @@ static __device__ __noinline__ void ntt_w(int32_t* p, const int32_t* zetas, int 
 #pragma unroll 1
   for (int lg = 7; lg >= 1; lg -= 2) {  // layers (len, len / 2), len = 2^lg
     const int len = 1 << lg, h = len >> 1;
-#pragma unroll 2
+#pragma unroll 1
     for (int k = 0; k < 2 * N; ++k) {
       const int u = lane + 32 * k, uu = u & 63;
       const int grp = uu >> (lg - 1);                       // block of the len layer
@@ -704,7 +704,7 @@ static __device__ __noinline__ void ntt_inv_w(int32_t* p, const int32_t* zetas, 
 #pragma unroll 1
   for (int lg = 0; lg <= 6; lg += 2) {  // layers (len, 2 len), len = 2^lg
     const int len = 1 << lg;
-#pragma unroll 2
+#pragma unroll 1
     for (int k = 0; k < 2 * N; ++k) {
       const int u = lane + 32 * k, uu = u & 63;
       const int g = uu >> lg;                               // block of the 2 len layer
