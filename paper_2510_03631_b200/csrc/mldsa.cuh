@@ -140,84 +140,6 @@ struct Shake {
   }
 };
 
-// Register-resident sponge for the signing hot loop: the state stays in
-// registers (static indices only), message bytes are staged block by block in an
-// 8-byte aligned shared-memory scratch and absorbed / squeezed as 64-bit words
-// (the byte-serial Shake above keeps its state in local memory: one
-// read-modify-write per byte).
-static __device__ __forceinline__ void keccak_reg(uint64_t (&st)[25]) {
-  constexpr int rotc[24] = {1, 3, 6, 10, 15, 21, 28, 36, 45, 55, 2, 14, 27, 41, 56, 8, 25, 43, 62, 18, 39, 61, 20, 44};
-  constexpr int piln[24] = {10, 7, 11, 17, 18, 3, 5, 16, 8, 21, 24, 4, 15, 23, 19, 13, 12, 2, 20, 14, 22, 9, 6, 1};
-#pragma unroll 1
-  for (int r = 0; r < 24; ++r) {
-    uint64_t bc[5];
-#pragma unroll
-    for (int i = 0; i < 5; ++i) bc[i] = st[i] ^ st[i + 5] ^ st[i + 10] ^ st[i + 15] ^ st[i + 20];
-#pragma unroll
-    for (int i = 0; i < 5; ++i) {
-      const uint64_t t = bc[(i + 4) % 5] ^ rol64(bc[(i + 1) % 5], 1);
-#pragma unroll
-      for (int j = 0; j < 25; j += 5) st[j + i] ^= t;
-    }
-    uint64_t t = st[1];
-#pragma unroll
-    for (int i = 0; i < 24; ++i) {
-      const uint64_t b = st[piln[i]];
-      st[piln[i]] = rol64(t, rotc[i]);
-      t = b;
-    }
-#pragma unroll
-    for (int j = 0; j < 25; j += 5) {
-      uint64_t b[5];
-#pragma unroll
-      for (int i = 0; i < 5; ++i) b[i] = st[j + i];
-#pragma unroll
-      for (int i = 0; i < 5; ++i) st[j + i] ^= (~b[(i + 1) % 5]) & b[(i + 2) % 5];
-    }
-    st[0] ^= kRC[r];
-  }
-}
-
-template <int RATE>
-struct RSponge {
-  uint64_t a[25];
-  __device__ __forceinline__ void zero() {
-#pragma unroll
-    for (int i = 0; i < 25; ++i) a[i] = 0;
-  }
-  __device__ __forceinline__ void absorb_block(const uint8_t* blk) {  // 8-byte aligned
-#pragma unroll
-    for (int w = 0; w < RATE / 8; ++w) a[w] ^= reinterpret_cast<const uint64_t*>(blk)[w];
-    keccak_reg(a);
-  }
-  __device__ __forceinline__ void out_block(uint8_t* blk) const {  // RATE bytes of output
-#pragma unroll
-    for (int w = 0; w < RATE / 8; ++w) reinterpret_cast<uint64_t*>(blk)[w] = a[w];
-  }
-  __device__ __forceinline__ void next() { keccak_reg(a); }
-  // absorb p0 || p1 || p2 with the SHAKE padding (one thread; scratch: RATE bytes, 8-aligned)
-  __device__ void absorb_msg(const uint8_t* p0, int n0, const uint8_t* p1, int n1, const uint8_t* p2, int n2,
-                             uint8_t* scratch) {
-    const int total = n0 + n1 + n2;
-    for (int off = 0;; off += RATE) {
-      const int take = min(RATE, total - off);
-#pragma unroll
-      for (int w = 0; w < RATE / 8; ++w) reinterpret_cast<uint64_t*>(scratch)[w] = 0;
-      for (int i = 0; i < take; ++i) {
-        const int m = off + i;
-        scratch[i] = m < n0 ? p0[m] : m < n0 + n1 ? p1[m - n0] : p2[m - n0 - n1];
-      }
-      if (take < RATE) {
-        scratch[take] ^= 0x1F;
-        scratch[RATE - 1] ^= 0x80;
-        absorb_block(scratch);
-        return;
-      }
-      absorb_block(scratch);
-    }
-  }
-};
-
 // Warp-cooperative Keccak-f[1600]: lane i < 25 holds state word A[x + 5y]
 // (x = i % 5, y = i / 5); theta's column parities, pi's lane permutation and
 // chi's row neighbours move through warp shuffles (FIPS 202 Sec. 3.2 steps).
