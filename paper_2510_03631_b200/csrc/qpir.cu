@@ -959,6 +959,9 @@ static int answer_batch_impl(qpir_ctx* ctx, const uint32_t* Q, uint64_t B, uint6
     rc = ensure(ctx, (void**)&ar.acc64, &ar.acc64_bytes, (uint64_t)std::min(Bc, B) * g.ell_local * 8);
     if (rc) return rc;
   }
+  cudaStreamCaptureStatus cap_status = cudaStreamCaptureStatusNone;
+  CUDA_TRY(ctx, cudaStreamIsCapturing(st, &cap_status));
+  const bool capturing = cap_status != cudaStreamCaptureStatusNone;
   // exception lists: Poisson(m / p) entries per uniform query; cap ~ 4x the
   // mean + 64, an overflowed (adversarial) query falls back to a rescan
   const bool exc = two && p == 65537u;
@@ -977,8 +980,11 @@ static int answer_batch_impl(qpir_ctx* ctx, const uint32_t* Q, uint64_t B, uint6
     uint32_t* oc = out + b0 * g.ell_local;
     const uint64_t oe = (uint64_t)bc * g.ell_local;
     // 2 limbs: the split runs inside the GEMM (converter warps, mma.cuh) unless
-    // QPIR_FTR_FUSE=0 or the K-block is not 128 cells
-    const bool fuse = two && ctx->ftr_fuse && ctx->mma_gpb != 4;
+    // QPIR_FTR_FUSE=0, the K-block is not 128 cells, or the stream is being
+    // captured into a CUDA graph: the fused form's converter work counter and
+    // K-block epoch advance on the host per launch, so a replayed capture would
+    // wait forever on stale flags -- captures take the split-kernel form
+    const bool fuse = two && ctx->ftr_fuse && ctx->mma_gpb != 4 && !capturing;
     const uint64_t pM = p >= 2 ? ~0ull / p + 1 : 0;  // fastmod_u32 constant
     if (exc) CUDA_TRY(ctx, cudaMemsetAsync(exc_cnt, 0, (uint64_t)bc * 4, st));
     MmaJob cj;

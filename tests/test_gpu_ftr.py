@@ -118,6 +118,44 @@ def test_ftr_and_batches_back_to_back(cuda_ok):
                 assert (Pk.u32(out) == want).all()
 
 
+@pytest.mark.timeout(300, method="thread")  # a hang must end the process, not the box
+def test_ftr_captured_in_cuda_graph(cuda_ok):
+    """An FTR batch captured into a CUDA graph (after an eager call sized the
+    stream's scratch) replays exactly with the queries rewritten in place: the
+    library takes the split-kernel form under capture, because the fused form's
+    converter counter and K-block epochs advance on the host per launch (a
+    replayed fused capture would wait on stale flags)."""
+    Pk = _P()
+    r, s, B = 20000, 40, 64
+    rec = synth.uniform_u8_np(77, (r, s))
+    st = torch.cuda.Stream()
+    with Pk.FtrServer(r, s, records=rec) as srv:
+        Qd = torch.empty((B, r), dtype=torch.int32, device="cuda")
+        out = torch.empty((B, srv.server.ell_local), dtype=torch.int32, device="cuda")
+        with torch.cuda.stream(st):
+            srv.answer_batch(Qd.zero_(), out=out, stream=st)  # eager: fused form, sizes the arena
+        st.synchronize()
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g, stream=st, capture_error_mode="relaxed"):
+            srv.answer_batch(Qd, out=out, stream=st)
+        for rep in range(3):
+            Q = synth.uniform_u32_np(900 + rep, (B, r))
+            Q[rep, :50] = 65536  # residue 65536: the exception list
+            Qd.copy_(torch.from_numpy(Q.view(np.int32)))
+            torch.cuda.synchronize()
+            with torch.cuda.stream(st):
+                g.replay()
+            st.synchronize()
+            want = ((Q % P).astype(np.int64) @ rec.astype(np.int64)) % P
+            assert (Pk.u32(out) == want.astype(np.uint32)).all(), rep
+        # eager calls after the capture still take the fused form and stay exact
+        Q = synth.uniform_u32_np(999, (B, r))
+        res = srv.answer_batch(torch.from_numpy(Q.view(np.int32)).cuda(), stream=st)
+        st.synchronize()
+        got = Pk.u32(res)
+        assert (got == (((Q % P).astype(np.int64) @ rec.astype(np.int64)) % P).astype(np.uint32)).all()
+
+
 @pytest.mark.parametrize("l,t", [(5, 1), (7, 2), (9, 2)])
 def test_ftr_byzantine_responses_decoded(cuda_ok, l, t):
     """nu-Byzantine robustness (Lemma 1 proof P:1227):
