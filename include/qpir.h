@@ -174,7 +174,10 @@ int qpir_answer_batch(qpir_ctx *ctx, const uint32_t *Q, uint64_t B,
  * Internally the entries are reduced mod p first and split into 2 byte limbs
  * for p <= 65537 (the residue 65536 of p = 65537 is listed per query and added
  * back by the mod-p fixup), 3 for p <= 2^24, 4 otherwise: the cost falls with
- * p, the result does not depend on the path. */
+ * p, the result does not depend on the path.  The 2-limb split normally runs
+ * inside the GEMM (converter warps); on a stream that is being captured into a
+ * CUDA graph it runs as a separate kernel instead, so the captured work replays
+ * exactly (the fused form keeps per-launch state on the host). */
 int qpir_answer_batch_modp(qpir_ctx *ctx, const uint32_t *Q, uint64_t B,
                            uint64_t len_Q, uint32_t p, uint32_t *ans_local,
                            uint64_t len_ans, void *stream);
