@@ -762,7 +762,24 @@ static __device__ __forceinline__ void sign_one(const SignArgs& a, SignSmem& S, 
     {
       uint64_t h = 0;  // c~ = H(mu || w1Encode(w1), 32)
       uint8_t* sc = S.scratch[0];
-      wsp_absorb<136>(h, S.mu, 64, S.w1enc, K * 192, nullptr, 0, sc, lane);
+      {
+        // mu (8 words) || w1Encode (96 words) is word-aligned: each of the 7
+        // rate blocks is absorbed as 17 u64 loads, SHAKE padding on the words
+        constexpr int NW = (64 + K * 192) / 8, NB = NW / 17 + 1;
+        static_assert(NW % 17 != 0 && NB == 7, "mu || w1Encode: 6 full blocks + 2 words");
+        const uint64_t* mu64 = reinterpret_cast<const uint64_t*>(S.mu);
+        const uint64_t* w64 = reinterpret_cast<const uint64_t*>(S.w1enc);
+        for (int blk = 0; blk < NB; ++blk) {
+          if (lane < 17) {
+            const int m = 17 * blk + lane;
+            uint64_t v = m < 8 ? mu64[m] : m < NW ? w64[m - 8] : 0ull;
+            if (m == NW) v ^= 0x1Full;
+            if (blk == NB - 1 && lane == 16) v ^= 0x80ull << 56;
+            h ^= v;
+          }
+          h = keccak_warp(h, lane);
+        }
+      }
       wsp_out<136>(h, sc, lane);
       if (lane < 32) S.ctilde[lane] = sc[lane];
       __syncwarp();
@@ -869,15 +886,20 @@ static __device__ __forceinline__ void sign_one(const SignArgs& a, SignSmem& S, 
       for (int b = 0; b < 8; ++b) o[b] = (uint8_t)(lo >> (8 * b));
       o[8] = (uint8_t)hi;
     }
-    if (lane < K) {  // HintBitPack (Alg. 20): indices of poly `lane` after the previous polys'
+    {  // HintBitPack (Alg. 20): the indices of each poly's hints in increasing order,
+       // 32 coefficients per ballot, each hint's slot from the popcount below it
       uint8_t* hp = sig + 32 + L * 576;
       int index = 0;
-      for (int i = 0; i < lane; ++i) index += S.count[i];
-      for (int j = 0; j < 256; ++j)
-        if (S.w[lane][j]) hp[index++] = (uint8_t)j;
-      hp[OMEGA + lane] = (uint8_t)index;
-      if (lane == K - 1)
-        for (int k = index; k < OMEGA; ++k) hp[k] = 0;
+      for (int i = 0; i < K; ++i) {
+        for (int c = 0; c < 8; ++c) {
+          const bool hbit = S.w[i][32 * c + lane] != 0;
+          const uint32_t mk = __ballot_sync(0xffffffffu, hbit);
+          if (hbit) hp[index + __popc(mk & ((1u << lane) - 1u))] = (uint8_t)(32 * c + lane);
+          index += __popc(mk);
+        }
+        if (lane == 0) hp[OMEGA + i] = (uint8_t)index;
+      }
+      for (int k = index + lane; k < OMEGA; k += 32) hp[k] = 0;
     }
     return;
   }
