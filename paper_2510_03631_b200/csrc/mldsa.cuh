@@ -575,7 +575,8 @@ struct SignSmem {                   // per warp (y / z live in registers: 32 per
   alignas(8) uint8_t scratch[1][136];  // sponge block staging
   alignas(8) uint8_t mu[64];
   alignas(8) uint8_t rhopp[64];
-  uint8_t ctilde[32], msg[40], zeros[32];
+  alignas(8) uint8_t ctilde[32];
+  uint8_t msg[40], zeros[32];
   int count[K];
 };
 constexpr int WPB = 4;  // ~10 KB of shared memory per warp: 5 CTAs x 4 warps per SM
@@ -784,8 +785,11 @@ static __device__ __forceinline__ void sign_one(const SignArgs& a, SignSmem& S, 
       if (lane < 32) S.ctilde[lane] = sc[lane];
       __syncwarp();
       // SampleInBall (Alg. 29): lane 0 samples, the warp squeezes further blocks
-      uint64_t sb = 0;
-      wsp_absorb<136>(sb, S.ctilde, 32, nullptr, 0, nullptr, 0, sc, lane);
+      uint64_t sb = 0;  // H(c~): one block, c~ as 4 words, then the SHAKE padding
+      if (lane < 4) sb = reinterpret_cast<const uint64_t*>(S.ctilde)[lane];
+      if (lane == 4) sb = 0x1Full;
+      if (lane == 16) sb = 0x80ull << 56;
+      sb = keccak_warp(sb, lane);
       wsp_out<136>(sb, sc, lane);
       uint64_t hb = 0;
       for (int k = 0; k < 8; ++k) hb |= (uint64_t)sc[k] << (8 * k);
