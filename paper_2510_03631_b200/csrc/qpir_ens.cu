@@ -608,11 +608,12 @@ static int ens_batch_tc(qpir_ens_ctx* ctx, EnsArena& ar, const uint8_t* Qd, uint
     if (rc) return rc;
     unsigned long long* Qp = reinterpret_cast<unsigned long long*>(ar.Qb);
     {
-      const uint32_t gy = std::min<uint32_t>(rows64, 65535);
-      const uint32_t gz = (rows64 + gy - 1) / gy;
-      dim3 grid(ld / 128, gy, gz);
-      ens_share_pack_kernel<<<grid, 128, 0, st>>>(Qd, (uint32_t)B, ctx->r, (ctx->r + 7) / 8, Qp,
-                                                  rows64, ld);
+      const uint32_t tiles = (rows64 + 31) / 32;  // 32 K-blocks per CTA
+      const uint32_t gy = std::min<uint32_t>(tiles, 65535);
+      const uint32_t gz = (tiles + gy - 1) / gy;
+      dim3 grid(ld / 32, gy, gz);
+      ens_share_pack_kernel<<<grid, ESP_THREADS, 0, st>>>(Qd, (uint32_t)B, ctx->r, (ctx->r + 7) / 8, Qp,
+                                                          rows64, ld);
       ENS_LAUNCHED(ctx);
     }
     EnsMmaArgs a;
