@@ -512,14 +512,33 @@ struct ModpExceptions {
 // out[i] = acc[i] mod p (u64 -> u32), after the OUT_MODP* GEMM; with exception
 // lists, the missing terms 65536 * D[r][c] are added first (exact in u64).
 // out / acc are query-major [n][ld]: i = b * ld + r.
+// v mod p by Barrett with pB = floor(2^64 / p): the quotient estimate is exact or
+// one short, so one conditional subtraction (64-bit division runs as a software
+// routine on the GPU).
+__device__ __forceinline__ uint32_t mod_u64_barrett(unsigned long long v, uint32_t p,
+                                                    unsigned long long pB) {
+  const unsigned long long q = __umul64hi(v, pB);
+  unsigned long long r = v - q * p;
+  return (uint32_t)(r >= p ? r - p : r);
+}
+
 static __global__ void modp_fixup_kernel(const unsigned long long* __restrict__ acc,
                                          uint32_t* __restrict__ out, uint64_t n, uint32_t p,
                                          uint32_t ld, ModpExceptions ex) {
+  const unsigned long long pB = ~0ull / p;  // floor(2^64 / p) for p not a power of 2
+  const bool pow2 = (p & (p - 1)) == 0;
   for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
        i += (uint64_t)gridDim.x * blockDim.x) {
     unsigned long long v = acc[i];
     if (ex.cnt) {
-      const uint32_t b = (uint32_t)(i / ld), r = (uint32_t)(i % ld);
+      uint32_t b, r;
+      if (n <= 0xFFFFFFFFull) {  // 32-bit division (64-bit runs as a software routine)
+        b = (uint32_t)i / ld;
+        r = (uint32_t)i - b * ld;
+      } else {
+        b = (uint32_t)(i / ld);
+        r = (uint32_t)(i % ld);
+      }
       const uint32_t k = ex.cnt[b];
       if (k) {
         const uint8_t* Dr = ex.D + (size_t)(r >> 7) * ex.G * 2048 + (r & 127u) * 16u;
@@ -539,7 +558,7 @@ static __global__ void modp_fixup_kernel(const unsigned long long* __restrict__ 
         v += sum << 16;
       }
     }
-    out[i] = (uint32_t)(v % p);
+    out[i] = pow2 ? (uint32_t)(v & (p - 1)) : mod_u64_barrett(v, p, pB);
   }
 }
 }  // namespace qpir
